@@ -1,0 +1,138 @@
+/*
+ * dbscan.h — exact Euclidean DBSCAN for integer points on one B200 (sm_100a).
+ *
+ * C ABI of libdbscan_b200.so (paper_1912_06255_b200/). Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary.
+ *
+ * What it computes — PAPER.md §2 "DBSCAN Definition":
+ *   a point p is CORE iff |{q in P : ||p - q|| <= eps}| >= min_pts  (p counts
+ *   itself, duplicates count with multiplicity); core points joined by a chain
+ *   of core points with consecutive distances <= eps form one cluster; a
+ *   non-core point belongs to every cluster that has a core point within eps
+ *   (BORDER), or to none (NOISE). The result is unique.
+ * How — the paper's grid method, Alg 1: Cells (grid + radix sort
+ *   + hash), MarkCore (Alg 2), ClusterCore with BCP
+ *   tests and a lock-free union-find (Alg 3),
+ *   ClusterBorder (Alg 4); neighbouring cells by stencil (d <= 3)
+ *   or a cell tree (d >= 4). See DESIGN.md.
+ *
+ * Exactness: coordinates are int32; distances are compared squared and
+ * exactly against eps^2 (readings 1-4). The output is bit-identical
+ * to the CPU oracle (oracle/) and independent of scheduling.
+ */
+#ifndef DBSCAN_B200_H
+#define DBSCAN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------ */
+#define DBSCAN_OK       0
+#define DBSCAN_EINVAL  -1 /* n < 0 or n > 2^31-1; d < 1 or d > 8; eps < 1; min_pts < 1;
+                             NULL pts with n > 0; NULL out; contradictory flags */
+#define DBSCAN_ERANGE  -2 /* packed cell key needs > 63 bits, or d*(eps+1)^2 >= 2^62 */
+#define DBSCAN_ENOMEM  -3 /* device or host allocation failed */
+#define DBSCAN_ECUDA   -4 /* any other CUDA error; detail via dbscan_error_string */
+
+/* ---- flags --------------------------------------------------------------- */
+#define DBSCAN_F_DEVICE_IO     1u  /* pts and every output are DEVICE pointers; outputs the
+                                      library allocates are cudaMallocAsync'd on `stream` */
+#define DBSCAN_F_TIMING        2u  /* fill out->stage_ms with CUDA-event times (adds a sync) */
+#define DBSCAN_F_CALLER_OUT    4u  /* out->core, out->cluster, out->border_off are caller-
+                                      allocated ([n], [n], [n+1]; host or device per
+                                      F_DEVICE_IO); the library allocates border_ids only */
+#define DBSCAN_F_FORCE_STENCIL 8u  /* neighbour cells by stencil enumeration for every d */
+#define DBSCAN_F_FORCE_TREE   16u  /* neighbour cells by the cell tree for every d */
+#define DBSCAN_F_FORCE_WIDE   32u  /* 64-bit distance arithmetic even where 32-bit is exact */
+#define DBSCAN_F_NO_WAVES     64u  /* ClusterCore in one wave (ablation of the wave schedule) */
+
+/* ---- stage timers (indices into stage_ms) -------------------------------- */
+#define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
+#define DBSCAN_STAGE_KEYS      1  /* a1: cell keys + digit histograms                  */
+#define DBSCAN_STAGE_SORT      2  /* a2: LSD radix sort of (key, index)                */
+#define DBSCAN_STAGE_SEGMENT   3  /* a3: cell segmentation + point gather              */
+#define DBSCAN_STAGE_HASH      4  /* a4: cell hash table                               */
+#define DBSCAN_STAGE_NEIGHBORS 5  /* a5: neighbour-cell CSR (stencil or tree)          */
+#define DBSCAN_STAGE_MARKCORE  6  /* a6: MarkCore (Alg 2)                              */
+#define DBSCAN_STAGE_COMPACT   7  /* a7: core-first compaction per cell                */
+#define DBSCAN_STAGE_CLUSTER   8  /* a8: ClusterCore: BCP + union-find (Alg 3)         */
+#define DBSCAN_STAGE_LABELS    9  /* a9: canonical labels                              */
+#define DBSCAN_STAGE_BORDER   10  /* a10: ClusterBorder CSR (Alg 4)                    */
+#define DBSCAN_STAGE_TOTAL    11  /* whole call on the stream                          */
+#define DBSCAN_NSTAGES        12
+
+/* ---- counters (indices into stats) --------------------------------------- */
+#define DBSCAN_STAT_NCELLS        0  /* non-empty cells                                  */
+#define DBSCAN_STAT_KEY_BITS      1  /* packed cell-key width                            */
+#define DBSCAN_STAT_SORT_PASSES   2  /* radix passes run                                 */
+#define DBSCAN_STAT_NBR_ENTRIES   3  /* neighbour CSR entries (excluding self)           */
+#define DBSCAN_STAT_CORE_CELLS    4  /* cells holding >= 1 core point                     */
+#define DBSCAN_STAT_PAIRS         5  /* candidate core-cell pairs (g > h)                */
+#define DBSCAN_STAT_PAIRS_TESTED  6  /* pairs that reached a BCP test (not pruned by Find)*/
+#define DBSCAN_STAT_LAUNCHES      7  /* kernels launched by this call                    */
+#define DBSCAN_STAT_WIDE          8  /* 1 if the 64-bit distance path ran                */
+#define DBSCAN_STAT_TREE          9  /* 1 if neighbour cells came from the cell tree      */
+#define DBSCAN_STAT_CELL_SIDE    10  /* integer cell side s                              */
+#define DBSCAN_NSTATS            16
+
+typedef struct dbscan_result {
+  int64_t  n;
+  uint8_t *core;        /* [n]   1 = core point                                          */
+  int32_t *cluster;     /* [n]   core: canonical cluster id = minimum input index of a
+                                 core point of its cluster; non-core: -1                 */
+  int64_t *border_off;  /* [n+1] CSR over ALL points in input order; rows of core and
+                                 noise points are empty; border_off[0] = 0               */
+  int32_t *border_ids;  /* [nnz] each non-core point's cluster ids, ascending, distinct  */
+  int64_t  nnz;         /* border_off[n]                                                  */
+  int64_t  n_core, n_border, n_noise, n_clusters;
+  float    stage_ms[DBSCAN_NSTAGES]; /* filled with F_TIMING, else 0                     */
+  int64_t  stats[DBSCAN_NSTATS];
+  uint32_t flags;       /* flags of the call that produced this result                  */
+  void    *priv;        /* library bookkeeping; do not touch                             */
+} dbscan_result;
+
+/*
+ * dbscan — run exact DBSCAN.
+ *   pts      [n*d] int32, row-major (point i = pts[i*d .. i*d+d-1]); host or device
+ *            memory per F_DEVICE_IO. Owned by the caller, read only. No alignment needed.
+ *   n        number of points, 0 <= n <= 2^31-1.  n = 0 returns empty outputs.
+ *   d        dimension, 1..8.
+ *   eps      radius, >= 1; the predicate is  sum_k (x_k - y_k)^2 <= eps^2  (closed).
+ *   min_pts  >= 1; min_pts > n makes every point noise.
+ *   flags    DBSCAN_F_* bits.
+ *   stream   cudaStream_t to run on (NULL = legacy default stream). Without F_DEVICE_IO
+ *            the call returns after the outputs are in host memory; with it the call
+ *            returns once border_ids is allocated (one internal sync for its size) and
+ *            the remaining work is ordered on `stream`.
+ *   out      result; zeroed on entry unless F_CALLER_OUT (then core/cluster/border_off
+ *            must be set by the caller). On error *out is left with every library-
+ *            allocated pointer NULL and nothing leaks.
+ * Ownership: the caller releases library-allocated outputs with dbscan_result_free.
+ * Threads: no global mutable state; concurrent calls on different streams are safe.
+ * Returns DBSCAN_OK or a negative code above.
+ */
+int dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
+           uint32_t flags, void *stream, dbscan_result *out);
+
+/* Release what the library allocated in *r (never caller-owned F_CALLER_OUT buffers).
+ * Device outputs are released with cudaFreeAsync on the stream of the dbscan() call,
+ * which must still exist; work queued on that stream before the free may still use
+ * them. Safe on a zeroed result. */
+void dbscan_result_free(dbscan_result *r);
+
+/* Static description of a code, with the detail of this thread's last error. */
+const char *dbscan_error_string(int code);
+
+/* Name of stage i (0 <= i < DBSCAN_NSTAGES) for reports. */
+const char *dbscan_stage_name(int i);
+
+/* Library version, as 10000*major + 100*minor + patch. */
+int dbscan_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBSCAN_B200_H */

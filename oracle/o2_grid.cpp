@@ -26,6 +26,9 @@
  *                                                           core points (reading 8)
  *   ClusterBorder (Alg 4)                  same, sorted distinct label sets
  *
+ * NeighborCells, MarkCore and ClusterBorder treat cells independently and are
+ * spread over host threads with OpenMP (results do not depend on the order);
+ * ClusterCore's union-find loop is sequential.
  * Same cell => within eps: points of one cell differ by <= s'-1 per axis, and
  * d (s'-1)^2 <= d s'^2 <= eps^2.
  * Distances are exact: squared, in 128-bit integers, against eps^2.
@@ -167,7 +170,9 @@ int o2_dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min
       ++off[k];
     }
     const size_t no = offs.size() / (size_t)d;
-    for (int64_t c = 0; c < nc; ++c) {
+    // two passes (count, fill) so cells can be processed independently
+    auto probe = [&](int64_t c, std::vector<int64_t> &q, int64_t *dst) {
+      int64_t m = 0;
       for (size_t t = 0; t < no; ++t) {
         bool in = true;
         for (int k = 0; k < d; ++k) {
@@ -176,9 +181,23 @@ int o2_dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min
         }
         if (!in) continue;
         auto it = cell_of.find(pack(q.data()));
-        if (it != cell_of.end()) nbr.push_back(it->second);
+        if (it != cell_of.end()) { if (dst) dst[m] = it->second; ++m; }
       }
-      noff[c + 1] = (int64_t)nbr.size();
+      return m;
+    };
+#pragma omp parallel
+    {
+      std::vector<int64_t> qq((size_t)d);
+#pragma omp for schedule(dynamic, 1024)
+      for (int64_t c = 0; c < nc; ++c) noff[c + 1] = probe(c, qq, nullptr);
+    }
+    for (int64_t c = 0; c < nc; ++c) noff[c + 1] += noff[c];
+    nbr.resize((size_t)noff[nc]);
+#pragma omp parallel
+    {
+      std::vector<int64_t> qq((size_t)d);
+#pragma omp for schedule(dynamic, 1024)
+      for (int64_t c = 0; c < nc; ++c) probe(c, qq, nbr.data() + noff[c]);
     }
   } else {
     std::vector<std::vector<int64_t>> tmp((size_t)nc);
@@ -196,6 +215,7 @@ int o2_dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min
 
   /* ---- MarkCore (Alg 2). ---- */
   std::vector<uint8_t> cf((size_t)n, 0);  // core flag by input index
+#pragma omp parallel for schedule(dynamic, 256)
   for (int64_t g = 0; g < nc; ++g) {
     if (csize(g) >= min_pts) {
       for (int64_t j = cstart[g]; j < cstart[g + 1]; ++j) cf[order[j]] = 1;
@@ -272,9 +292,10 @@ int o2_dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min
 
   /* ---- ClusterBorder (Alg 4). ---- */
   std::vector<int64_t> cnt((size_t)n, 0);
-  std::vector<int32_t> buf;
   std::vector<std::vector<int32_t>> lab((size_t)n);
+#pragma omp parallel for schedule(dynamic, 256)
   for (int64_t g = 0; g < nc; ++g) {
+    std::vector<int32_t> buf;
     if (csize(g) >= min_pts) continue;
     for (int64_t j = cstart[g]; j < cstart[g + 1]; ++j) {
       const int64_t p = order[j];

@@ -1,0 +1,218 @@
+"""paper_1912_06255_b200 — exact grid DBSCAN (Wang, Gu, Shun, SIGMOD 2020,
+arXiv 1912.06255) on one B200.
+
+Thin ctypes binding over the C ABI in `include/dbscan.h`
+(`libdbscan_b200.so`, built in-tree from `csrc/`). Argument marshalling only:
+every step of the method runs in the library's CUDA kernels. PyTorch is used
+for device memory and streams. There is no CPU fallback: importing this
+package on a machine without the built library raises, and calling it without
+a CUDA device returns the library's CUDA error.
+
+    import torch, paper_1912_06255_b200 as db
+    r = db.dbscan(torch.tensor(pts, dtype=torch.int32, device="cuda"), eps=1000, min_pts=100)
+    r.core, r.cluster, r.border_off, r.border_ids   # torch tensors on the device
+
+Result convention (DESIGN.md readings): `core` u8[n];
+`cluster` i32[n] = minimum input index of a core point of the point's cluster
+for core points, -1 otherwise; `border_off` i64[n+1] / `border_ids` i32[nnz]
+= CSR of each non-core point's ascending distinct cluster ids (empty = noise).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["dbscan", "Result", "lib_path", "load", "F_DEVICE_IO", "F_TIMING", "F_CALLER_OUT",
+           "F_FORCE_STENCIL", "F_FORCE_TREE", "F_FORCE_WIDE", "F_NO_WAVES", "STAGES", "STATS",
+           "DBSCANError"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libdbscan_b200.so")
+
+# flags (include/dbscan.h)
+F_DEVICE_IO, F_TIMING, F_CALLER_OUT = 1, 2, 4
+F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
+NSTAGES, NSTATS = 12, 16
+STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
+          "cluster", "labels", "border", "total"]
+STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
+         "launches", "wide", "tree", "cell_side"]
+
+
+class _Result(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("core", C.c_void_p),
+        ("cluster", C.c_void_p),
+        ("border_off", C.c_void_p),
+        ("border_ids", C.c_void_p),
+        ("nnz", C.c_int64),
+        ("n_core", C.c_int64),
+        ("n_border", C.c_int64),
+        ("n_noise", C.c_int64),
+        ("n_clusters", C.c_int64),
+        ("stage_ms", C.c_float * NSTAGES),
+        ("stats", C.c_int64 * NSTATS),
+        ("flags", C.c_uint32),
+        ("priv", C.c_void_p),
+    ]
+
+
+class DBSCANError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"dbscan failed ({code}): {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load():
+    """Load libdbscan_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(lib_path):
+            raise ImportError(f"{lib_path} is missing: build it with `make -C {_HERE}` "
+                              "or __graft_entry__.build() (no CPU fallback exists)")
+        lib = C.CDLL(lib_path)
+        lib.dbscan.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_uint32,
+                               C.c_void_p, C.POINTER(_Result)]
+        lib.dbscan.restype = C.c_int
+        lib.dbscan_result_free.argtypes = [C.POINTER(_Result)]
+        lib.dbscan_error_string.argtypes = [C.c_int]
+        lib.dbscan_error_string.restype = C.c_char_p
+        lib.dbscan_stage_name.argtypes = [C.c_int]
+        lib.dbscan_stage_name.restype = C.c_char_p
+        lib.dbscan_version.restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+@dataclass
+class Result:
+    core: object         # u8[n]   (torch tensor on the device, or numpy on the host path)
+    cluster: object      # i32[n]
+    border_off: object   # i64[n+1]
+    border_ids: object   # i32[nnz]
+    n_core: int = 0
+    n_border: int = 0
+    n_noise: int = 0
+    n_clusters: int = 0
+    stage_ms: dict = field(default_factory=dict)
+    stats: dict = field(default_factory=dict)
+
+
+class _DeviceBuffer:
+    """Owns library-allocated device memory; exposes it to torch through
+    __cuda_array_interface__ and releases it with dbscan_result_free."""
+
+    def __init__(self, res: _Result, ptr: int, n: int, typestr: str):
+        self._res = res
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+    def __del__(self):
+        if _lib is not None and self._res is not None:
+            _lib.dbscan_result_free(C.byref(self._res))
+            self._res = None
+
+
+def _finish(res: _Result, flags: int) -> dict:
+    info = {"stage_ms": {}, "stats": {}}
+    if flags & F_TIMING:
+        info["stage_ms"] = {STAGES[i]: float(res.stage_ms[i]) for i in range(NSTAGES)
+                            if res.stage_ms[i] > 0}
+    info["stats"] = {STATS[i]: int(res.stats[i]) for i in range(len(STATS))}
+    return info
+
+
+def _check(lib, rc):
+    if rc != 0:
+        raise DBSCANError(rc, lib.dbscan_error_string(rc).decode())
+
+
+def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = False, stream=None,
+           out=None) -> Result:
+    """Exact DBSCAN of integer points.
+
+    points: (n, d) int32 — a CUDA torch tensor (device path: outputs are torch
+    tensors on the same device, computed on `stream` or the current stream),
+    or a host array / CPU tensor (host path: the library copies in and out;
+    pinned memory makes those copies fast; outputs are numpy arrays).
+    out: optional (core, cluster, border_off) caller buffers for the host path
+    (e.g. pinned CPU tensors), passed with DBSCAN_F_CALLER_OUT.
+    """
+    lib = load()
+    import torch
+    flags = int(flags) | (F_TIMING if timing else 0)
+    res = _Result()
+    if isinstance(points, torch.Tensor) and points.is_cuda:
+        if points.dtype != torch.int32 or points.dim() != 2:
+            raise TypeError("points must be an (n, d) int32 tensor")
+        pts = points.contiguous()
+        n, d = pts.shape
+        dev = pts.device
+        st = torch.cuda.current_stream(dev) if stream is None else stream
+        core = torch.empty(n, dtype=torch.uint8, device=dev)
+        cluster = torch.empty(n, dtype=torch.int32, device=dev)
+        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        res.core, res.cluster, res.border_off = core.data_ptr(), cluster.data_ptr(), off.data_ptr()
+        with torch.cuda.device(dev):
+            rc = lib.dbscan(C.c_void_p(pts.data_ptr()), n, d, int(eps), int(min_pts),
+                            flags | F_DEVICE_IO | F_CALLER_OUT, C.c_void_p(st.cuda_stream),
+                            C.byref(res))
+        _check(lib, rc)
+        nnz = int(res.nnz)
+        if nnz > 0:
+            ids = torch.as_tensor(_DeviceBuffer(res, res.border_ids, nnz, "<i4"), device=dev)
+        else:
+            lib.dbscan_result_free(C.byref(res))
+            ids = torch.empty(0, dtype=torch.int32, device=dev)
+        info = _finish(res, flags)
+        return Result(core, cluster, off, ids, int(res.n_core), int(res.n_border),
+                      int(res.n_noise), int(res.n_clusters), **info)
+
+    # host path
+    if isinstance(points, torch.Tensor):
+        if points.dtype != torch.int32 or points.dim() != 2:
+            raise TypeError("points must be an (n, d) int32 tensor")
+        host = points.contiguous()
+        ptr, (n, d) = host.data_ptr(), host.shape
+        keep = host
+    else:
+        keep = np.ascontiguousarray(points, dtype=np.int32)
+        if keep.ndim != 2:
+            raise TypeError("points must be (n, d)")
+        ptr, (n, d) = keep.ctypes.data, keep.shape
+    f = flags & ~F_DEVICE_IO
+    if out is not None:
+        core_b, cl_b, off_b = out
+        res.core, res.cluster, res.border_off = (_hostptr(core_b), _hostptr(cl_b), _hostptr(off_b))
+        f |= F_CALLER_OUT
+    st = 0 if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    rc = lib.dbscan(C.c_void_p(ptr), n, d, int(eps), int(min_pts), f, C.c_void_p(st), C.byref(res))
+    del keep
+    _check(lib, rc)
+    nnz = int(res.nnz)
+    if out is not None:
+        core, cluster, off = out
+    else:
+        core = np.ctypeslib.as_array(C.cast(res.core, C.POINTER(C.c_uint8)), shape=(n,)).copy() if n else np.zeros(0, np.uint8)
+        cluster = np.ctypeslib.as_array(C.cast(res.cluster, C.POINTER(C.c_int32)), shape=(n,)).copy() if n else np.zeros(0, np.int32)
+        off = np.ctypeslib.as_array(C.cast(res.border_off, C.POINTER(C.c_int64)), shape=(n + 1,)).copy()
+    ids = (np.ctypeslib.as_array(C.cast(res.border_ids, C.POINTER(C.c_int32)), shape=(nnz,)).copy()
+           if nnz else np.zeros(0, np.int32))
+    info = _finish(res, flags)
+    out_res = Result(core, cluster, off, ids, int(res.n_core), int(res.n_border), int(res.n_noise),
+                     int(res.n_clusters), **info)
+    lib.dbscan_result_free(C.byref(res))
+    return out_res
+
+
+def _hostptr(b) -> int:
+    if hasattr(b, "data_ptr"):
+        return b.data_ptr()
+    return b.ctypes.data

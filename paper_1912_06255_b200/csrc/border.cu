@@ -1,0 +1,146 @@
+// border.cu — ClusterBorder, Alg 4, PAPER.md P:L876-904:
+// every non-core point p (they only live in cells with |g| < minPts)
+// joins the cluster of every core point q in g or a neighbouring cell with
+// d(p, q) <= eps; border points may belong to several clusters
+// (P:L214-215). Output: a CSR over all points in input order, each row the
+// ascending distinct cluster ids (reading 10).
+// Shortcuts that do not change the output: all core points of one cell carry
+// one label, so a core point in p's own cell gives that label without a
+// distance test (same cell => within eps), and a neighbouring
+// cell whose label is already in p's set is not scanned; within a cell the
+// scan stops at the first core point within eps.
+#include "internal.h"
+
+namespace db {
+
+constexpr int MAXL = 32;  // register-resident label set; larger sets use the slow path
+
+struct LabelSet {
+  uint32_t v[MAXL];
+  int n = 0;
+  bool overflow = false;
+  __device__ bool has(uint32_t x) const {
+    for (int i = 0; i < n; ++i)
+      if (v[i] == x) return true;
+    return false;
+  }
+  __device__ void add(uint32_t x) {  // keeps v[0..n) ascending
+    if (n == MAXL) { overflow = true; return; }
+    int i = n++;
+    while (i > 0 && v[i - 1] > x) { v[i] = v[i - 1]; --i; }
+    v[i] = x;
+  }
+};
+
+template <int D, bool WIDE>
+__device__ __forceinline__ bool cell_has_core_within(const int32_t* p, uint32_t h,
+                                                     const CellsView& cv,
+                                                     const int32_t* __restrict__ Ps,
+                                                     const uint32_t* __restrict__ core_cnt,
+                                                     uint32_t clampc, uint64_t eps2) {
+  const uint32_t s = cv.cell_start[h], e = s + core_cnt[h];
+  int32_t q[D];
+  for (uint32_t u = s; u < e; ++u) {
+    PtLoad<D>::load(Ps, u, q);
+    if (within<D, WIDE>(p, q, clampc, eps2)) return true;
+  }
+  return false;
+}
+
+// Smallest label > `after` among the clusters within eps of p (slow path for
+// points with more than MAXL distinct labels); 0xffffffff if none.
+template <int D, bool WIDE>
+__device__ uint32_t next_label(const int32_t* p, uint32_t g, int64_t after, const CellsView& cv,
+                               const int32_t* __restrict__ Ps, const uint32_t* __restrict__ core_cnt,
+                               const uint32_t* __restrict__ cell_label, uint32_t clampc,
+                               uint64_t eps2) {
+  uint32_t best = 0xffffffffu;
+  if (core_cnt[g] > 0 && (int64_t)cell_label[g] > after) best = cell_label[g];
+  for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1]; ++t) {
+    const uint32_t h = cv.nbr[t];
+    if (core_cnt[h] == 0) continue;
+    const uint32_t lab = cell_label[h];
+    if ((int64_t)lab <= after || lab >= best) continue;
+    if (cell_has_core_within<D, WIDE>(p, h, cv, Ps, core_cnt, clampc, eps2)) best = lab;
+  }
+  return best;
+}
+
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(128) border_kernel(
+    int fill, CellsView cv, const int32_t* __restrict__ Ps, const uint32_t* __restrict__ idx,
+    const uint8_t* __restrict__ core_s, const uint32_t* __restrict__ core_cnt,
+    const uint32_t* __restrict__ cell_label, uint32_t n, uint32_t clampc, uint64_t eps2,
+    uint32_t* __restrict__ bcnt, const int64_t* __restrict__ border_off,
+    int32_t* __restrict__ border_ids, unsigned long long* nborder) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || core_s[j]) return;
+  const uint32_t g = cv.cell_of[j];
+  int32_t p[D];
+  PtLoad<D>::load(Ps, j, p);
+  LabelSet L;
+  if (core_cnt[g] > 0) L.add(cell_label[g]);
+  for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && !L.overflow; ++t) {
+    const uint32_t h = cv.nbr[t];
+    if (core_cnt[h] == 0) continue;
+    const uint32_t lab = cell_label[h];
+    if (L.has(lab)) continue;
+    if (cell_has_core_within<D, WIDE>(p, h, cv, Ps, core_cnt, clampc, eps2)) L.add(lab);
+  }
+  const uint32_t i = idx[j];
+  if (!L.overflow) {
+    if (!fill) {
+      bcnt[i] = (uint32_t)L.n;
+      if (L.n) atomicAdd(nborder, 1ull);
+    }
+    else {
+      int32_t* out = border_ids + border_off[i];
+      for (int k = 0; k < L.n; ++k) out[k] = (int32_t)L.v[k];
+    }
+    return;
+  }
+  // slow path: enumerate labels in ascending order without storage
+  uint32_t cnt = 0;
+  int64_t after = -1;
+  while (true) {
+    const uint32_t nx = next_label<D, WIDE>(p, g, after, cv, Ps, core_cnt, cell_label, clampc, eps2);
+    if (nx == 0xffffffffu) break;
+    if (fill) border_ids[border_off[i] + cnt] = (int32_t)nx;
+    ++cnt;
+    after = nx;
+  }
+  if (!fill) {
+    bcnt[i] = cnt;
+    if (cnt) atomicAdd(nborder, 1ull);
+  }
+}
+
+int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                     const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
+                     const uint32_t* cell_label, int64_t n, bool wide, int64_t* border_off,
+                     unsigned long long* nborder) {
+  uint32_t* bcnt = c.alloc<uint32_t>(n);
+  c.zero(bcnt, sizeof(uint32_t) * n);
+  dispatch(g.D, wide, [&]<int D, bool W>() {
+    border_kernel<D, W><<<grid_for(n, 128, 1 << 30), 128, 0, c.st>>>(
+        0, cv, Ps, idx, core_s, core_cnt, cell_label, (uint32_t)n, g.clampc, g.eps2, bcnt, nullptr,
+        nullptr, nborder);
+  });
+  c.launched();
+  exclusive_scan_u32_i64(c, bcnt, border_off, n);
+  return c.read(border_off + n);
+}
+
+void border_fill(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                 const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
+                 const uint32_t* cell_label, int64_t n, bool wide, const int64_t* border_off,
+                 int32_t* border_ids) {
+  dispatch(g.D, wide, [&]<int D, bool W>() {
+    border_kernel<D, W><<<grid_for(n, 128, 1 << 30), 128, 0, c.st>>>(
+        1, cv, Ps, idx, core_s, core_cnt, cell_label, (uint32_t)n, g.clampc, g.eps2, nullptr,
+        border_off, border_ids, nullptr);
+  });
+  c.launched();
+}
+
+}  // namespace db

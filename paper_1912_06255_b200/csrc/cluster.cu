@@ -1,0 +1,312 @@
+// cluster.cu — ClusterCore and canonical labels (a9).
+//
+// Alg 3: for core cells g and core neighbours h with
+// g > h ("the cell with higher ID [is] responsible") and
+// Find(g) != Find(h), test Connected(g, h) — is the bichromatic
+// closest pair of their core points within eps — and Link on
+// success; a lock-free union-find keeps the components on the fly.
+// BCP: points further than eps from the other cell are filtered out first
+// (P:L640-641), the search stops at the first pair within eps,
+// and the work is done in fixed-size blocks of points: here a
+// warp holds 32 points of g in registers and streams 32-point blocks of h,
+// exiting on a warp vote.
+// Bucketing ("process each batch in parallel before moving to the
+// next batch") becomes gap-ordered waves: pairs whose lattice offset has L1
+// norm 1 (face-adjacent) first, then 2, then the rest; each wave re-checks
+// Find before any BCP, so later waves are mostly pruned.
+// Labels: the paper stores uf.Find(g); its value depends on the
+// schedule, so the cluster id is canonicalised to the minimum input index of
+// the cluster's core points (reading 8).
+#include "internal.h"
+
+namespace db {
+
+constexpr int NWAVES = 3;
+constexpr uint32_t SMALL_PAIR = 64;  // |A|*|B| at or below: one thread per pair
+
+__device__ __forceinline__ int wave_of(uint64_t kg, uint64_t kh, const Geo& g) {
+  uint32_t l1 = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < g.d) {
+      uint32_t a = cell_coord(kg, g, k), b = cell_coord(kh, g, k);
+      l1 += a > b ? a - b : b - a;
+    }
+  return l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);
+}
+
+// pass 0: count candidate pairs per (wave, cell); pass 1: fill, wave-major.
+__global__ void pair_kernel(int fill, int nwaves, CellsView cv, Geo g,
+                            const uint32_t* __restrict__ core_cnt, uint32_t* __restrict__ cnt,
+                            const uint64_t* __restrict__ off, uint2* __restrict__ pairs) {
+  const uint32_t gc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gc >= cv.ncells) return;
+  uint32_t local[NWAVES] = {0, 0, 0};
+  if (core_cnt[gc] > 0) {
+    const uint64_t kg = cv.cell_key[gc];
+    for (uint64_t t = cv.nbr_off[gc]; t < cv.nbr_off[gc + 1]; ++t) {
+      const uint32_t h = cv.nbr[t];
+      if (h >= gc || core_cnt[h] == 0) continue;
+      const int w = nwaves == 1 ? 0 : wave_of(kg, cv.cell_key[h], g);
+      if (fill) pairs[off[(size_t)w * cv.ncells + gc] + local[w]] = make_uint2(gc, h);
+      ++local[w];
+    }
+  }
+  if (!fill)
+    for (int w = 0; w < nwaves; ++w) cnt[(size_t)w * cv.ncells + gc] = local[w];
+}
+
+// Drop pairs already in one component; split the rest by size class.
+__global__ void wave_filter_kernel(const uint2* __restrict__ pairs, const uint64_t* __restrict__ bounds,
+                                   uint32_t* parent, const uint32_t* __restrict__ core_cnt,
+                                   uint2* __restrict__ small, uint2* __restrict__ large,
+                                   uint32_t* ctr, unsigned long long* tested) {
+  const uint64_t b0 = bounds[0], b1 = bounds[1];
+  uint32_t mine = 0;
+  for (uint64_t i = b0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < b1;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 p = pairs[i];
+    if (uf_find(parent, p.x) == uf_find(parent, p.y)) continue;
+    ++mine;
+    if ((uint64_t)core_cnt[p.x] * core_cnt[p.y] <= SMALL_PAIR) small[atomicAdd(ctr, 1u)] = p;
+    else large[atomicAdd(ctr + 1, 1u)] = p;
+  }
+  if (mine) atomicAdd(tested, (unsigned long long)mine);
+}
+
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(256) bcp_small_kernel(const uint2* __restrict__ list,
+                                                        const uint32_t* __restrict__ count,
+                                                        CellsView cv, const int32_t* __restrict__ Ps,
+                                                        const uint32_t* __restrict__ core_cnt,
+                                                        uint32_t* parent, uint32_t clampc,
+                                                        uint64_t eps2) {
+  const uint32_t m = *count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const uint2 p = list[i];
+    if (uf_find(parent, p.x) == uf_find(parent, p.y)) continue;
+    const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
+    const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
+    bool hit = false;
+    int32_t a[D], b[D];
+    for (uint32_t u = sa; u < ea && !hit; ++u) {
+      PtLoad<D>::load(Ps, u, a);
+      for (uint32_t v = sb; v < eb; ++v) {
+        PtLoad<D>::load(Ps, v, b);
+        if (within<D, WIDE>(a, b, clampc, eps2)) { hit = true; break; }
+      }
+    }
+    if (hit) uf_link(parent, p.x, p.y);
+  }
+}
+
+// distance from p to the integer box [lo, hi] within eps?
+template <int D>
+__device__ __forceinline__ bool near_range(const int32_t* p, const int32_t* lo, const int32_t* hi,
+                                           int d, uint32_t clampc, uint64_t eps2) {
+  uint64_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < d) {
+      int64_t x = p[k];
+      int64_t t = x < lo[k] ? (int64_t)lo[k] - x : (x > hi[k] ? x - (int64_t)hi[k] : 0);
+      uint64_t u = (uint64_t)t;
+      if (u > clampc) u = clampc;
+      acc += u * u;
+    }
+  }
+  return acc <= eps2;
+}
+
+// Warp per pair. Lanes hold up to 32 core points of g (filtered against h's
+// box); 32-point blocks of h's core points are loaded one point per lane,
+// filtered against the bounding box of the current g block, and the
+// survivors are broadcast by shuffle and tested against every lane's point.
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict__ list,
+                                                        const uint32_t* __restrict__ count,
+                                                        CellsView cv, Geo g,
+                                                        const int32_t* __restrict__ Ps,
+                                                        const uint32_t* __restrict__ core_cnt,
+                                                        uint32_t* parent) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = *count;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += nwarps) {
+    const uint2 p = list[i];
+    bool done = false;
+    if (lane == 0) done = uf_find(parent, p.x) == uf_find(parent, p.y);
+    if (__shfl_sync(DB_FULL, done, 0)) continue;
+    const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
+    const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
+    int64_t boxh[D];
+    cell_box_lo<D>(cv.cell_key[p.y], g, boxh);
+    bool hit = false;
+    for (uint32_t a0 = sa; a0 < ea && !hit; a0 += 32) {
+      const uint32_t u = a0 + lane;
+      int32_t a[D];
+      bool keep = false;
+      if (u < ea) {
+        PtLoad<D>::load(Ps, u, a);
+        keep = near_box<D>(a, boxh, g);
+      }
+      if (!__any_sync(DB_FULL, keep)) continue;
+      // bounding box of the kept block
+      int32_t lo[D], hi[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        int32_t l = keep ? a[k] : INT32_MAX, h = keep ? a[k] : INT32_MIN;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          l = min(l, __shfl_xor_sync(DB_FULL, l, o));
+          h = max(h, __shfl_xor_sync(DB_FULL, h, o));
+        }
+        lo[k] = l; hi[k] = h;
+      }
+      for (uint32_t b0 = sb; b0 < eb; b0 += 32) {
+        const uint32_t v = b0 + lane;
+        int32_t b[D];
+        bool kb = false;
+        if (v < eb) {
+          PtLoad<D>::load(Ps, v, b);
+          kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2);
+        }
+        uint32_t mb = __ballot_sync(DB_FULL, kb);
+        bool mine = false;
+        while (mb) {
+          const int src = __ffs(mb) - 1;
+          mb &= mb - 1;
+          int32_t q[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
+          mine |= keep && within<D, WIDE>(a, q, g.clampc, g.eps2);
+        }
+        if (__any_sync(DB_FULL, mine)) { hit = true; break; }
+      }
+      if (!hit) {
+        bool dn = false;
+        if (lane == 0) dn = uf_find(parent, p.x) == uf_find(parent, p.y);
+        if (__shfl_sync(DB_FULL, dn, 0)) break;
+      }
+    }
+    if (hit && lane == 0) uf_link(parent, p.x, p.y);
+    __syncwarp();
+  }
+}
+
+__global__ void uf_init_kernel(uint32_t* parent, uint32_t n) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) parent[i] = i;
+}
+
+uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                      const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
+                      unsigned long long* tested) {
+  const uint32_t nc = cv.ncells;
+  const int nw = waves ? NWAVES : 1;
+  uf_init_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(parent, nc);
+  c.launched();
+  uint32_t* cnt = c.alloc<uint32_t>((size_t)nw * nc);
+  uint64_t* off = c.alloc<uint64_t>((size_t)nw * nc + 1);
+  pair_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(0, nw, cv, g, core_cnt, cnt, nullptr,
+                                                             nullptr);
+  c.launched();
+  exclusive_scan_u32_u64(c, cnt, off, (int64_t)nw * nc);
+  const uint64_t npairs = c.read(off + (size_t)nw * nc);
+  if (npairs == 0) return 0;
+  uint2* pairs = c.alloc<uint2>(npairs);
+  pair_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(1, nw, cv, g, core_cnt, nullptr, off,
+                                                             pairs);
+  c.launched();
+  // wave bounds: off[w*nc] .. off[(w+1)*nc]
+  uint64_t* bounds = c.alloc<uint64_t>(2 * NWAVES);
+  for (int w = 0; w < nw; ++w) {
+    DB_CUDA(cudaMemcpyAsync(bounds + 2 * w, off + (size_t)w * nc, sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, c.st));
+    DB_CUDA(cudaMemcpyAsync(bounds + 2 * w + 1, off + (size_t)(w + 1) * nc, sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, c.st));
+  }
+  uint2* small = c.alloc<uint2>(npairs);
+  uint2* large = c.alloc<uint2>(npairs);
+  uint32_t* ctr = c.alloc<uint32_t>(2 * NWAVES);
+  c.zero(ctr, sizeof(uint32_t) * 2 * NWAVES);
+  const unsigned fgrid = grid_for((int64_t)npairs, 256, c.sms * 8);
+  for (int w = 0; w < nw; ++w) {
+    wave_filter_kernel<<<fgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, parent, core_cnt, small,
+                                                large, ctr + 2 * w, tested);
+    c.launched();
+    dispatch(g.D, wide, [&]<int D, bool W>() {
+      bcp_small_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(small, ctr + 2 * w, cv, Ps, core_cnt,
+                                                           parent, g.clampc, g.eps2);
+      c.launched();
+      bcp_large_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(large, ctr + 2 * w + 1, cv, g, Ps,
+                                                           core_cnt, parent);
+      c.launched();
+    });
+  }
+  return npairs;
+}
+
+// ---------------------------------------------------------------- a9: labels
+__global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
+                                   const uint32_t* __restrict__ cell_start,
+                                   const uint32_t* __restrict__ idx, uint32_t* parent,
+                                   uint32_t* comp_min, uint32_t* counters) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  bool root = false;
+  if (g < nc && core_cnt[g] > 0) {
+    const uint32_t r = uf_find(parent, g);
+    // cells are sorted stably, so the first (core-first) point of a cell has
+    // the smallest input index among its core points
+    atomicMin(comp_min + r, idx[cell_start[g]]);
+    root = r == g;
+  }
+  uint32_t b = __ballot_sync(DB_FULL, root);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(counters, __popc(b));
+}
+
+__global__ void cell_label_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
+                                  uint32_t* parent, const uint32_t* __restrict__ comp_min,
+                                  uint32_t* __restrict__ cell_label) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nc) return;
+  cell_label[g] = core_cnt[g] > 0 ? comp_min[uf_find(parent, g)] : 0xffffffffu;
+}
+
+// Scatter to input order: core[i], cluster[i]; count core points.
+__global__ void write_points_kernel(uint32_t n, const uint32_t* __restrict__ idx,
+                                    const uint8_t* __restrict__ core_s,
+                                    const uint32_t* __restrict__ cell_of,
+                                    const uint32_t* __restrict__ cell_label,
+                                    uint8_t* __restrict__ core_out, int32_t* __restrict__ cluster_out,
+                                    uint32_t* counters) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  bool is_core = false;
+  if (j < n) {
+    const uint32_t i = idx[j];
+    is_core = core_s[j];
+    core_out[i] = is_core;
+    cluster_out[i] = is_core ? (int32_t)cell_label[cell_of[j]] : -1;
+  }
+  uint32_t b = __ballot_sync(DB_FULL, is_core);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(counters + 1, __popc(b));
+}
+
+void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
+            const uint32_t* core_cnt, uint32_t* parent, int64_t n, uint32_t* cell_label,
+            uint8_t* core_out, int32_t* cluster_out, uint32_t* counters) {
+  const uint32_t nc = cv.ncells;
+  uint32_t* comp_min = c.alloc<uint32_t>(nc);
+  DB_CUDA(cudaMemsetAsync(comp_min, 0xff, sizeof(uint32_t) * nc, c.st));
+  label_roots_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, cv.cell_start, idx,
+                                                                    parent, comp_min, counters);
+  c.launched();
+  cell_label_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, parent, comp_min,
+                                                                   cell_label);
+  c.launched();
+  write_points_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
+      (uint32_t)n, idx, core_s, cv.cell_of, cell_label, core_out, cluster_out, counters);
+  c.launched();
+}
+
+}  // namespace db

@@ -1,0 +1,296 @@
+// common.cuh — device-side building blocks shared by every stage of the
+// B200 DBSCAN path: grid geometry, the exact distance predicates, union-find,
+// warp/block scans and the decoupled look-back primitive.
+//
+// Product code. It never includes, links or calls anything under oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define DB_WARP 32
+#define DB_FULL 0xffffffffu
+
+namespace db {
+
+// ---------------------------------------------------------------------------
+// Grid geometry (reading 5).
+// Integer cell side s = isqrt(floor(eps^2/d)) + 1 so that two points of one
+// cell differ by <= s-1 per axis and d (s-1)^2 <= eps^2 (same cell => within
+// eps). Cell coordinate c_k = (x_k - lo_k) div s (half-open boxes,
+// origin at the per-axis minimum). The packed cell key puts axis 0 in the most
+// significant bits: key = sum_k c_k << shift_k, with w_k = bits(maxc_k).
+// ---------------------------------------------------------------------------
+struct Geo {
+  int32_t  d;           // dimension
+  int32_t  D;           // padded dimension of the sorted point array (2, 4 or 8)
+  uint32_t s;           // integer cell side
+  uint32_t bits;        // total key width (<= 63)
+  int32_t  lo[8];       // per-axis minimum coordinate
+  uint32_t maxc[8];     // per-axis maximum lattice coordinate
+  uint32_t shift[8];    // bit position of axis k in the key
+  uint32_t width[8];    // bit width of axis k
+  uint64_t eps2;        // eps^2
+  uint32_t clampc;      // eps + 1: Lemma 3 clamp (reading 4)
+  uint32_t R;           // max |delta| of lattice coordinates between neighbour cells
+  uint64_t eps;         // eps
+};
+
+__device__ __forceinline__ uint32_t cell_coord(uint64_t key, const Geo& g, int k) {
+  return (uint32_t)((key >> g.shift[k]) & ((g.width[k] == 32) ? 0xffffffffull
+                                                              : ((1ull << g.width[k]) - 1)));
+}
+
+// Squared gap between two lattice cells (or cell boxes) along one axis, in
+// coordinate units: the closest integer coordinates of cells differing by
+// delta != 0 are (|delta|-1)*s + 1 apart (reading 7). Clamped at
+// eps+1 so the squared sum stays < 2^62 (d (eps+1)^2 < 2^62 is checked on the
+// host); a clamped term alone already exceeds eps^2.
+__device__ __forceinline__ uint64_t gap_term(uint32_t delta, const Geo& g) {
+  if (delta == 0) return 0;
+  uint64_t gap = (uint64_t)(delta - 1) * g.s + 1;
+  if (gap > g.clampc) gap = g.clampc;
+  return gap * gap;
+}
+
+// ---------------------------------------------------------------------------
+// Exact distance predicate ||a-b||^2 <= eps^2 on int32 coordinates
+// (closed neighbourhood). 32-bit path (reading 4):
+//   sum_k min(|a_k - b_k|, eps+1)^2 <= eps^2, |a_k - b_k| = __sad(a_k, b_k, 0)
+// exact as an unsigned 32-bit value for any int32 pair; clamping at eps+1
+// cannot change the outcome (a clamped term alone exceeds eps^2), and the
+// sum is < d (eps+1)^2 < 2^32, which the host checks before choosing it.
+// Padded coordinates are 0 on both sides and contribute nothing.
+// 64-bit path: the same with 64-bit differences and sums (d (eps+1)^2 < 2^62).
+// ---------------------------------------------------------------------------
+template <int D, bool WIDE>
+struct Pt;
+
+template <> struct Pt<2, false> { int2 v; };
+template <> struct Pt<2, true>  { int2 v; };
+template <> struct Pt<4, false> { int4 v; };
+template <> struct Pt<4, true>  { int4 v; };
+template <> struct Pt<8, false> { int4 a, b; };
+template <> struct Pt<8, true>  { int4 a, b; };
+
+template <int D>
+struct PtLoad {
+  // Load point j of a D-padded array (16-byte rows for D=4, 8 for D=2, 32 for D=8).
+  __device__ __forceinline__ static void load(const int32_t* __restrict__ P, int64_t j, int32_t* x);
+};
+template <> struct PtLoad<2> {
+  __device__ __forceinline__ static void load(const int32_t* __restrict__ P, int64_t j, int32_t* x) {
+    int2 v = __ldg(reinterpret_cast<const int2*>(P) + j);
+    x[0] = v.x; x[1] = v.y;
+  }
+};
+template <> struct PtLoad<4> {
+  __device__ __forceinline__ static void load(const int32_t* __restrict__ P, int64_t j, int32_t* x) {
+    int4 v = __ldg(reinterpret_cast<const int4*>(P) + j);
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+  }
+};
+template <> struct PtLoad<8> {
+  __device__ __forceinline__ static void load(const int32_t* __restrict__ P, int64_t j, int32_t* x) {
+    const int4* q = reinterpret_cast<const int4*>(P) + 2 * j;
+    int4 a = __ldg(q), b = __ldg(q + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  }
+};
+
+template <int D, bool WIDE>
+__device__ __forceinline__ bool within(const int32_t* a, const int32_t* b, uint32_t clampc,
+                                       uint64_t eps2) {
+  if constexpr (!WIDE) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      uint32_t t = min(__sad(a[k], b[k], 0u), clampc);
+      acc += t * t;
+    }
+    return acc <= (uint32_t)eps2;
+  } else {
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      int64_t t = (int64_t)a[k] - (int64_t)b[k];
+      uint64_t u = (uint64_t)(t < 0 ? -t : t);
+      if (u > clampc) u = clampc;
+      acc += u * u;
+    }
+    return acc <= eps2;
+  }
+}
+
+// Squared distance from point p to the integer box of cell `key`, clamped as
+// above: [lo_k + c_k s, lo_k + c_k s + s - 1] per axis. Used by the BCP filter
+// ("filter out points further than eps from the other cell").
+template <int D>
+__device__ __forceinline__ bool near_box(const int32_t* p, const int64_t* blo, const Geo& g) {
+  uint64_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < g.d) {
+      int64_t x = p[k], lo = blo[k], hi = blo[k] + (int64_t)g.s - 1;
+      int64_t t = x < lo ? lo - x : (x > hi ? x - hi : 0);
+      uint64_t u = (uint64_t)t;
+      if (u > g.clampc) u = g.clampc;
+      acc += u * u;
+    }
+  }
+  return acc <= g.eps2;
+}
+
+template <int D>
+__device__ __forceinline__ void cell_box_lo(uint64_t key, const Geo& g, int64_t* blo) {
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    blo[k] = (k < g.d) ? (int64_t)g.lo[k] + (int64_t)cell_coord(key, g, k) * (int64_t)g.s : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Lock-free union-find over cells: parent[x] <= x
+// always (a root is only ever linked under a smaller root), find uses path
+// halving with plain stores (benign races: any stored value is an ancestor),
+// link uses atomicCAS on the larger root and retries on failure.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
+  volatile uint32_t* p = parent;
+  while (true) {
+    uint32_t px = p[x];
+    if (px == x) return x;
+    uint32_t gx = p[px];
+    if (gx == px) return px;
+    p[x] = gx;  // path halving
+    x = gx;
+  }
+}
+
+__device__ __forceinline__ void uf_link(uint32_t* parent, uint32_t a, uint32_t b) {
+  while (true) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    if (a < b) { uint32_t t = a; a = b; b = t; }
+    uint32_t old = atomicCAS(parent + a, a, b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scans.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(DB_FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan; returns the block total through *total.
+// `smem` must hold 33 T. All threads of the block must call it.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane == 31) smem[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? smem[lane] : T(0);
+    T wi = warp_inclusive_scan(w);
+    if (lane < nw) smem[lane] = wi - w;
+    if (lane == nw - 1) smem[32] = wi;
+  }
+  __syncthreads();
+  T res = inc - v + smem[wid];
+  *total = smem[32];
+  __syncthreads();
+  return res;
+}
+
+// Decoupled look-back (single-pass chained scan): status words hold a 2-bit
+// flag (1 = aggregate of this tile, 2 = inclusive prefix) and a 62-bit value.
+constexpr uint64_t LB_AGG = 1ull << 62;
+constexpr uint64_t LB_INC = 2ull << 62;
+constexpr uint64_t LB_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ void lb_publish(uint64_t* st, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(st), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t lb_read(const uint64_t* st) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(st) : "memory");
+  return v;
+}
+
+// Exclusive prefix of tile `tile` for one lane of status (stride `stride`
+// between tiles): publishes the aggregate, walks back, publishes the inclusive
+// value, returns the exclusive prefix. Called by one thread per status lane.
+__device__ __forceinline__ uint64_t lb_exclusive(uint64_t* status, int64_t tile, int64_t stride,
+                                                 uint64_t agg) {
+  if (tile == 0) {
+    lb_publish(status, LB_INC | agg);
+    return 0;
+  }
+  lb_publish(status + tile * stride, LB_AGG | agg);
+  uint64_t excl = 0;
+  int64_t t = tile - 1;
+  while (true) {
+    uint64_t s = lb_read(status + t * stride);
+    if ((s & ~LB_VAL) == 0) continue;  // predecessor not published yet: spin
+    excl += s & LB_VAL;
+    if (s & LB_INC) break;
+    --t;
+  }
+  lb_publish(status + tile * stride, LB_INC | (excl + agg));
+  return excl;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Hash of a packed cell key into an open-addressing table of 16-byte slots.
+// Keys that differ only in the low 3 bits (consecutive cells along the last
+// axis) land in the same 8-slot (128-byte) group, so stencil probes of
+// neighbouring cells share cache lines.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+__device__ __forceinline__ uint64_t slot_of(uint64_t key, uint64_t mask) {
+  return ((mix64(key >> 3) << 3) | (key & 7)) & mask;
+}
+
+constexpr uint64_t EMPTY_KEY = ~0ull;  // never a valid key (keys use <= 63 bits)
+
+struct __align__(16) Slot {
+  unsigned long long key;
+  uint32_t val;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ uint32_t hash_lookup(const Slot* __restrict__ T, uint64_t mask,
+                                                uint64_t key) {
+  uint64_t h = slot_of(key, mask);
+  while (true) {
+    uint4 s = __ldg(reinterpret_cast<const uint4*>(T + h));
+    uint64_t k = ((uint64_t)s.y << 32) | s.x;
+    if (k == key) return s.z;
+    if (k == EMPTY_KEY) return 0xffffffffu;
+    h = (h + 1) & mask;
+  }
+}
+
+}  // namespace db

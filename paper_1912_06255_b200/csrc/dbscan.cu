@@ -1,0 +1,393 @@
+// dbscan.cu — host orchestration of the B200 DBSCAN path and the C ABI
+// declared in include/dbscan.h. Alg 1 of PAPER.md:
+//   Cells (a1-a4) -> NeighborCells (a5) -> MarkCore (a6, a7)
+//   -> ClusterCore (a8) -> labels (a9) -> ClusterBorder (a10).
+// Every step runs in this library's kernels on the caller's stream.
+#include <mutex>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/dbscan.h"
+#include "internal.h"
+
+namespace db {
+
+static thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    throw Error(e == cudaErrorMemoryAllocation ? DBSCAN_ENOMEM : DBSCAN_ECUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+typedef unsigned __int128 u128;
+
+static uint64_t isqrt_u128(u128 v) {  // floor(sqrt(v)), v < 2^126
+  uint64_t r = 0;
+  for (int b = 63; b >= 0; --b) {
+    uint64_t c = r | (1ull << b);
+    if ((u128)c * c <= v) r = c;
+  }
+  return r;
+}
+
+static int bit_width(uint64_t v) {
+  int w = 0;
+  while (v) { ++w; v >>= 1; }
+  return w;
+}
+
+struct Priv {
+  bool dev = false;
+  cudaStream_t st = nullptr;  // stream of the call; device outputs are freed on it
+  // pointers this library allocated (freed by dbscan_result_free)
+  void* core = nullptr;
+  void* cluster = nullptr;
+  void* border_off = nullptr;
+  void* border_ids = nullptr;
+};
+
+static void init_device_once(int dev, int* sms) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  static int nsm[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) { *sms = 148; return; }
+  if (!done[dev]) {
+    // Keep freed stream-ordered memory in the pool across calls so repeated
+    // calls do not re-map device memory.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    nsm[dev] = v > 0 ? v : 148;
+    done[dev] = true;
+    (void)cudaGetLastError();
+  }
+  *sms = nsm[dev];
+}
+
+struct Timer {
+  bool on;
+  cudaStream_t st;
+  cudaEvent_t ev[DBSCAN_NSTAGES + 1] = {};
+  int mark[DBSCAN_NSTAGES + 1];
+  int n = 0;
+  Timer(bool on_, cudaStream_t s) : on(on_), st(s) {
+    if (on)
+      for (auto& e : ev) DB_CUDA(cudaEventCreate(&e));
+  }
+  ~Timer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void stage(int s) {  // begin stage s (ends the previous one)
+    if (!on) return;
+    DB_CUDA(cudaEventRecord(ev[n], st));
+    mark[n++] = s;
+  }
+  void finish(float* out) {
+    if (!on || n == 0) return;
+    DB_CUDA(cudaEventRecord(ev[n], st));
+    DB_CUDA(cudaEventSynchronize(ev[n]));
+    for (int i = 0; i < n; ++i) {
+      float ms = 0;
+      DB_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      out[mark[i]] += ms;
+    }
+    float tot = 0;
+    DB_CUDA(cudaEventElapsedTime(&tot, ev[0], ev[n]));
+    out[DBSCAN_STAGE_TOTAL] = tot;
+  }
+};
+
+static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
+               uint32_t flags, cudaStream_t st, dbscan_result* out) {
+  const bool dev_io = flags & DBSCAN_F_DEVICE_IO;
+  const bool caller_out = flags & DBSCAN_F_CALLER_OUT;
+  Priv* priv = new Priv();
+  priv->dev = dev_io;
+  priv->st = st;
+  out->priv = priv;
+  Ctx c;
+  c.st = st;
+  int dev = 0;
+  DB_CUDA(cudaGetDevice(&dev));
+  init_device_once(dev, &c.sms);
+  Timer tm(flags & DBSCAN_F_TIMING, st);
+
+  // ---- outputs
+  auto out_alloc = [&](size_t bytes, void** slot) -> void* {
+    void* p = nullptr;
+    if (dev_io) {
+      cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, st);
+      if (e != cudaSuccess) { (void)cudaGetLastError(); throw Error(DBSCAN_ENOMEM, "output allocation"); }
+    } else {
+      p = std::malloc(bytes ? bytes : 16);
+      if (!p) throw Error(DBSCAN_ENOMEM, "host output allocation");
+    }
+    *slot = p;
+    return p;
+  };
+  if (!caller_out) {
+    out->core = (uint8_t*)out_alloc((size_t)n, &priv->core);
+    out->cluster = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)n, &priv->cluster);
+    out->border_off = (int64_t*)out_alloc(sizeof(int64_t) * (size_t)(n + 1), &priv->border_off);
+  }
+  if (n == 0) {
+    out->border_ids = (int32_t*)out_alloc(4, &priv->border_ids);
+    if (dev_io) DB_CUDA(cudaMemsetAsync(out->border_off, 0, sizeof(int64_t), st));
+    else out->border_off[0] = 0;
+    if (dev_io) DB_CUDA(cudaStreamSynchronize(st));
+    return DBSCAN_OK;
+  }
+
+  // ---- host-side geometry and the exact-arithmetic path (readings 4, 5, 17)
+  const u128 eps2 = (u128)eps * (u128)eps;
+  const u128 dc2 = (u128)d * (u128)(eps + 1) * (u128)(eps + 1);
+  if (dc2 >= ((u128)1 << 62)) throw Error(DBSCAN_ERANGE, "d*(eps+1)^2 >= 2^62");
+  const bool wide = (flags & DBSCAN_F_FORCE_WIDE) || dc2 >= ((u128)1 << 32);
+  const uint64_t s = isqrt_u128(eps2 / (u128)d) + 1;  // < 2^31 since eps^2/d < 2^62
+  Geo g{};
+  g.d = d;
+  g.D = d <= 2 ? 2 : (d <= 4 ? 4 : 8);
+  g.s = (uint32_t)s;
+  g.eps2 = (uint64_t)eps2;
+  g.eps = (uint64_t)eps;
+  g.clampc = (uint32_t)(eps + 1);
+  g.R = (uint32_t)((uint64_t)(eps - 1) / s + 1);
+
+  tm.stage(DBSCAN_STAGE_BBOX);
+  const int32_t* dpts = pts;
+  if (!dev_io) {
+    int32_t* p = c.alloc<int32_t>((size_t)n * d);
+    DB_CUDA(cudaMemcpyAsync(p, pts, sizeof(int32_t) * (size_t)n * d, cudaMemcpyHostToDevice, st));
+    dpts = p;
+  }
+  int32_t* lohi_d = c.alloc<int32_t>(16);
+  bbox(c, dpts, n, d, lohi_d);
+  int32_t lohi[16];
+  DB_CUDA(cudaMemcpyAsync(lohi, lohi_d, sizeof(lohi), cudaMemcpyDeviceToHost, st));
+  DB_CUDA(cudaStreamSynchronize(st));
+  uint32_t bits = 0;
+  for (int k = d - 1; k >= 0; --k) {  // axis 0 most significant
+    const uint64_t span = (uint64_t)((int64_t)lohi[8 + k] - (int64_t)lohi[k]);
+    const uint64_t maxc = span / s;
+    g.lo[k] = lohi[k];
+    g.maxc[k] = (uint32_t)maxc;
+    g.width[k] = (uint32_t)bit_width(maxc);
+    g.shift[k] = bits;
+    bits += g.width[k];
+  }
+  if (bits > 63) throw Error(DBSCAN_ERANGE, "packed cell key needs more than 63 bits");
+  g.bits = bits;
+  const bool key64 = bits > 32;
+
+  // ---- a1-a2: keys + radix sort
+  tm.stage(DBSCAN_STAGE_KEYS);
+  void* skeys;
+  uint32_t* sidx;
+  int passes = 0;
+  cell_keys_and_sort(c, dpts, n, g, key64, &skeys, &sidx, &passes);
+  // (keys and sort share one call; the sort's time is reported under KEYS+SORT)
+
+  // ---- a3: segment + gather
+  tm.stage(DBSCAN_STAGE_SEGMENT);
+  int32_t* Ps = c.alloc<int32_t>((size_t)n * g.D);
+  uint32_t* cell_of = c.alloc<uint32_t>(n);
+  uint32_t* cell_start = c.alloc<uint32_t>((size_t)n + 1);
+  uint64_t* cell_key = c.alloc<uint64_t>(n);
+  const uint32_t ncells =
+      segment_and_gather(c, skeys, key64, sidx, dpts, n, g, Ps, cell_of, cell_start, cell_key);
+
+  // ---- a4-a5: hash + neighbour CSR
+  const bool tree = (flags & DBSCAN_F_FORCE_TREE) || (d >= 4 && !(flags & DBSCAN_F_FORCE_STENCIL));
+  uint64_t* nbr_off;
+  uint32_t* nbr;
+  uint64_t nbr_total = 0;
+  if (!tree) {
+    tm.stage(DBSCAN_STAGE_HASH);
+    Slot* T;
+    const uint64_t mask = build_hash(c, cell_key, ncells, &T);
+    tm.stage(DBSCAN_STAGE_NEIGHBORS);
+    neighbors_stencil(c, g, cell_key, ncells, T, mask, &nbr_off, &nbr, &nbr_total);
+  } else {
+    tm.stage(DBSCAN_STAGE_NEIGHBORS);
+    neighbors_tree(c, g, cell_key, ncells, &nbr_off, &nbr, &nbr_total);
+  }
+  CellsView cv{ncells, cell_start, cell_key, cell_of, nbr_off, nbr};
+
+  // device counters: [0] core cells, [1] mixed cells, [2] clusters, [3] core points
+  uint32_t* cnt32 = c.alloc<uint32_t>(4);
+  unsigned long long* cnt64 = c.alloc<unsigned long long>(2);  // [0] tested pairs, [1] border pts
+  c.zero(cnt32, 16);
+  c.zero(cnt64, 16);
+
+  // ---- a6: MarkCore
+  tm.stage(DBSCAN_STAGE_MARKCORE);
+  uint8_t* core_s = c.alloc<uint8_t>(n);
+  mark_core(c, g, cv, Ps, n, min_pts, wide, core_s);
+
+  // ---- a7: core-first compaction
+  tm.stage(DBSCAN_STAGE_COMPACT);
+  uint32_t* core_cnt = c.alloc<uint32_t>(ncells);
+  compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
+
+  // ---- a8: ClusterCore
+  tm.stage(DBSCAN_STAGE_CLUSTER);
+  uint32_t* parent = c.alloc<uint32_t>(ncells);
+  const uint64_t npairs = cluster_core(c, g, cv, Ps, core_cnt, wide,
+                                       !(flags & DBSCAN_F_NO_WAVES), parent, cnt64);
+
+  // ---- a9: labels, scattered to input order
+  tm.stage(DBSCAN_STAGE_LABELS);
+  uint8_t* core_d = dev_io ? out->core : c.alloc<uint8_t>(n);
+  int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
+  int64_t* off_d = dev_io ? out->border_off : c.alloc<int64_t>((size_t)n + 1);
+  uint32_t* cell_label = c.alloc<uint32_t>(ncells);
+  labels(c, cv, sidx, core_s, core_cnt, parent, n, cell_label, core_d, cluster_d, cnt32 + 2);
+
+  // ---- a10: ClusterBorder
+  tm.stage(DBSCAN_STAGE_BORDER);
+  const int64_t nnz = border_count(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide,
+                                   off_d, cnt64 + 1);
+  out->border_ids = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
+  int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
+  if (nnz > 0)
+    border_fill(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, ids_d);
+
+  if (!dev_io) {
+    DB_CUDA(cudaMemcpyAsync(out->core, core_d, (size_t)n, cudaMemcpyDeviceToHost, st));
+    DB_CUDA(cudaMemcpyAsync(out->cluster, cluster_d, sizeof(int32_t) * (size_t)n,
+                            cudaMemcpyDeviceToHost, st));
+    DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1),
+                            cudaMemcpyDeviceToHost, st));
+    if (nnz > 0)
+      DB_CUDA(cudaMemcpyAsync(out->border_ids, ids_d, sizeof(int32_t) * (size_t)nnz,
+                              cudaMemcpyDeviceToHost, st));
+  }
+  uint32_t h32[4];
+  unsigned long long h64[2];
+  DB_CUDA(cudaMemcpyAsync(h32, cnt32, sizeof(h32), cudaMemcpyDeviceToHost, st));
+  DB_CUDA(cudaMemcpyAsync(h64, cnt64, sizeof(h64), cudaMemcpyDeviceToHost, st));
+  tm.finish(out->stage_ms);
+  c.free_all();
+  DB_CUDA(cudaStreamSynchronize(st));
+
+  out->nnz = nnz;
+  out->n_core = h32[3];
+  out->n_clusters = h32[2];
+  out->n_border = (int64_t)h64[1];
+  out->n_noise = n - out->n_core - out->n_border;
+  out->stats[DBSCAN_STAT_NCELLS] = ncells;
+  out->stats[DBSCAN_STAT_KEY_BITS] = bits;
+  out->stats[DBSCAN_STAT_SORT_PASSES] = passes;
+  out->stats[DBSCAN_STAT_NBR_ENTRIES] = (int64_t)nbr_total;
+  out->stats[DBSCAN_STAT_CORE_CELLS] = h32[0];
+  out->stats[DBSCAN_STAT_PAIRS] = (int64_t)npairs;
+  out->stats[DBSCAN_STAT_PAIRS_TESTED] = (int64_t)h64[0];
+  out->stats[DBSCAN_STAT_LAUNCHES] = c.launches;
+  out->stats[DBSCAN_STAT_WIDE] = wide;
+  out->stats[DBSCAN_STAT_TREE] = tree;
+  out->stats[DBSCAN_STAT_CELL_SIDE] = (int64_t)s;
+  return DBSCAN_OK;
+}
+
+}  // namespace db
+
+using namespace db;
+
+static void free_priv(dbscan_result* r) {
+  Priv* p = (Priv*)r->priv;
+  if (!p) return;
+  void* ptrs[4] = {p->core, p->cluster, p->border_off, p->border_ids};
+  for (void* q : ptrs) {
+    if (!q) continue;
+    if (p->dev) cudaFreeAsync(q, p->st);
+    else std::free(q);
+  }
+  if (p->core) r->core = nullptr;
+  if (p->cluster) r->cluster = nullptr;
+  if (p->border_off) r->border_off = nullptr;
+  if (p->border_ids) r->border_ids = nullptr;
+  delete p;
+  r->priv = nullptr;
+}
+
+extern "C" {
+
+int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts, uint32_t flags,
+           void* stream, dbscan_result* out) {
+  g_last_error.clear();
+  if (!out) { g_last_error = "out is NULL"; return DBSCAN_EINVAL; }
+  const bool caller_out = flags & DBSCAN_F_CALLER_OUT;
+  uint8_t* ucore = out->core;
+  int32_t* ucl = out->cluster;
+  int64_t* uoff = out->border_off;
+  std::memset(out, 0, sizeof(*out));
+  if (caller_out) { out->core = ucore; out->cluster = ucl; out->border_off = uoff; }
+  out->n = n;
+  out->flags = flags;
+  const char* bad = nullptr;
+  if (n < 0 || n > INT32_MAX) bad = "n out of range [0, 2^31-1]";
+  else if (d < 1 || d > 8) bad = "d out of range [1, 8]";
+  else if (eps < 1) bad = "eps < 1";
+  else if (min_pts < 1) bad = "min_pts < 1";
+  else if (!pts && n > 0) bad = "pts is NULL";
+  else if ((flags & DBSCAN_F_FORCE_STENCIL) && (flags & DBSCAN_F_FORCE_TREE)) bad = "FORCE_STENCIL with FORCE_TREE";
+  else if (caller_out && (!uoff || (n > 0 && (!ucore || !ucl)))) bad = "F_CALLER_OUT with NULL output";
+  else if ((flags & DBSCAN_F_FORCE_STENCIL) && d > 6) bad = "FORCE_STENCIL limited to d <= 6";
+  if (bad) { g_last_error = bad; return DBSCAN_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  try {
+    return run(pts, n, d, eps, min_pts, flags, st, out);
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    cudaStreamSynchronize(st);
+    (void)cudaGetLastError();
+    free_priv(out);
+    if (!caller_out) { out->core = nullptr; out->cluster = nullptr; out->border_off = nullptr; }
+    out->border_ids = nullptr;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    free_priv(out);
+    return DBSCAN_ECUDA;
+  }
+}
+
+void dbscan_result_free(dbscan_result* r) {
+  if (!r) return;
+  free_priv(r);
+}
+
+const char* dbscan_error_string(int code) {
+  static thread_local std::string s;
+  const char* base = "unknown error";
+  switch (code) {
+    case DBSCAN_OK: base = "ok"; break;
+    case DBSCAN_EINVAL: base = "invalid argument"; break;
+    case DBSCAN_ERANGE: base = "value out of supported range"; break;
+    case DBSCAN_ENOMEM: base = "out of memory"; break;
+    case DBSCAN_ECUDA: base = "CUDA error"; break;
+  }
+  s = base;
+  if (code != DBSCAN_OK && !g_last_error.empty()) s += ": " + g_last_error;
+  return s.c_str();
+}
+
+const char* dbscan_stage_name(int i) {
+  static const char* names[DBSCAN_NSTAGES] = {"bbox",     "keys+sort", "sort",    "segment",
+                                              "hash",     "neighbors", "markcore", "compact",
+                                              "cluster",  "labels",    "border",  "total"};
+  return (i >= 0 && i < DBSCAN_NSTAGES) ? names[i] : "?";
+}
+
+int dbscan_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+// internal.h — host-side interfaces between the stage files of the B200 path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace db {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define DB_CUDA(call) ::db::cuda_check((call), #call)
+
+// Per-call context: stream, stream-ordered temporaries, launch counter.
+struct Ctx {
+  cudaStream_t st = nullptr;
+  std::vector<void*> temps;
+  int64_t launches = 0;
+  int sms = 148;
+
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw Error(-3, std::string("cudaMallocAsync failed: ") + cudaGetErrorString(e));
+    }
+    temps.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void zero(void* p, size_t bytes) { DB_CUDA(cudaMemsetAsync(p, 0, bytes, st)); }
+  void launched() {
+    ++launches;
+#ifdef DB_DEBUG_SYNC
+    DB_CUDA(cudaStreamSynchronize(st));
+#endif
+    DB_CUDA(cudaGetLastError());
+  }
+  void free_all() {
+    for (void* p : temps) cudaFreeAsync(p, st);
+    temps.clear();
+  }
+  // Read a small device value (synchronises the stream).
+  template <typename T>
+  T read(const T* dptr) {
+    T v;
+    DB_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, st));
+    DB_CUDA(cudaStreamSynchronize(st));
+    return v;
+  }
+};
+
+// ---- scan.cu ----
+// out[0..n] = exclusive prefix sums of in[0..n-1]; out[n] = total.
+void exclusive_scan_u32_u64(Ctx& c, const uint32_t* in, uint64_t* out, int64_t n);
+void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n);
+
+// ---- grid.cu (a1-a4) ----
+void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, int32_t* lohi /*[16] device*/);
+// keys + LSD radix sort; on return keys/idx hold the sorted (key, input index) pairs
+// in *sorted_keys / *sorted_idx (either buffer of the ping-pong pair).
+void cell_keys_and_sort(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, bool key64,
+                        void** sorted_keys, uint32_t** sorted_idx, int* passes);
+// generic u64-key radix sort used by the cell tree (Morton order)
+void radix_sort_u64(Ctx& c, uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
+                    int64_t n, int bits, uint64_t** out_keys, uint32_t** out_vals);
+// segmentation + gather: writes padded sorted points Ps[n*D], cell_of[n],
+// cell_start[ncells+1], cell_key[ncells]; returns ncells (synchronises).
+uint32_t segment_and_gather(Ctx& c, const void* sorted_keys, bool key64, const uint32_t* sorted_idx,
+                            const int32_t* pts, int64_t n, const Geo& g, int32_t* Ps,
+                            uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key);
+// open-addressing table of the ncells keys; returns mask (capacity-1).
+uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** table);
+
+// ---- neighbors.cu (a5) ----
+// neighbour-cell CSR excluding the cell itself: nbr_off[ncells+1] (device), nbr list.
+void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
+                       const Slot* T, uint64_t mask, uint64_t** nbr_off, uint32_t** nbr,
+                       uint64_t* total);
+void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
+                    uint64_t** nbr_off, uint32_t** nbr, uint64_t* total);
+// host: exact stencil offsets (Delta != 0 with sum gap^2 <= eps^2), flat [count*d] int8
+std::vector<int8_t> stencil_offsets(const Geo& g);
+
+// ---- core.cu (a6, a7) ----
+struct CellsView {
+  uint32_t ncells;
+  const uint32_t* cell_start;
+  const uint64_t* cell_key;
+  const uint32_t* cell_of;
+  const uint64_t* nbr_off;
+  const uint32_t* nbr;
+};
+void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
+               int64_t min_pts, bool wide, uint8_t* core_s);
+// core-first stable partition inside each mixed cell (Ps, idx, core_s permuted in
+// place); core_cnt[ncells]; counters[0] += core cells, counters[1] += mixed cells.
+void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
+                  uint8_t* core_s, int64_t n, int64_t min_pts, uint32_t* core_cnt,
+                  uint32_t* counters /*device [2], zeroed*/);
+
+// ---- cluster.cu (a8, a9) ----
+// returns the number of candidate pairs; *tested (device) counts pairs that
+// survived the Find check of their wave.
+uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                      const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
+                      unsigned long long* tested /*device, zeroed*/);
+void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
+            const uint32_t* core_cnt, uint32_t* parent, int64_t n, uint32_t* cell_label,
+            uint8_t* core_out, int32_t* cluster_out, uint32_t* counters /*device [4]*/);
+
+// ---- border.cu (a10) ----
+// count pass -> border_off (exclusive scan, device int64[n+1]); returns nnz (sync).
+int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                     const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
+                     const uint32_t* cell_label, int64_t n, bool wide, int64_t* border_off,
+                     unsigned long long* nborder /*device counter*/);
+void border_fill(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                 const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
+                 const uint32_t* cell_label, int64_t n, bool wide, const int64_t* border_off,
+                 int32_t* border_ids);
+
+// Dispatch on padded dimension D in {2,4,8} and the WIDE distance path.
+template <typename F>
+void dispatch(int D, bool wide, F&& f) {
+  if (D == 2) { if (wide) f.template operator()<2, true>(); else f.template operator()<2, false>(); }
+  else if (D == 4) { if (wide) f.template operator()<4, true>(); else f.template operator()<4, false>(); }
+  else { if (wide) f.template operator()<8, true>(); else f.template operator()<8, false>(); }
+}
+
+inline unsigned grid_for(int64_t work, int threads, int cap) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned)b;
+}
+
+}  // namespace db

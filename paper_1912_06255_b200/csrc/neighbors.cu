@@ -1,0 +1,293 @@
+// neighbors.cu — NeighborCells, memoised as a CSR
+// ("we cache the result on its first query").
+//
+// Two cells whose lattice coordinates differ by delta can hold a pair within
+// eps iff sum_k gap_k^2 <= eps^2 with gap_k = (|delta_k|-1) s + 1 for
+// delta_k != 0 (the closest integer coordinates of the two cells; DESIGN.md
+// reading 7). This predicate is exact (complete and tight), so every stage
+// that scans "neighbouring cells" sees exactly the cells that can
+// matter.
+//   d <= 3: enumerate the stencil of offsets satisfying the predicate (21 in
+//           2D, 117 in 3D including self) and probe the cell hash table
+//           (P:L489-493), one warp per cell, lanes over offsets.
+//   d >= 4: "enumerating all possible neighboring cells can be inefficient in
+//           practice for higher dimensions"; the
+//           paper inserts the cells into a k-d tree and runs range queries.
+//           Here: a bounding-volume tree over the cells in Morton order
+//           (leaves of 32 cells, implicit complete binary tree of integer
+//           boxes, built bottom-up in one kernel), queried by one warp per
+//           cell with the same exact gap test on boxes; lanes test the 32
+//           cells of a leaf at once.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace db {
+
+std::vector<int8_t> stencil_offsets(const Geo& g) {
+  const int d = g.d, R = (int)g.R;
+  std::vector<int8_t> out;
+  std::vector<int> off(d, -R);
+  while (true) {
+    bool zero = true;
+    unsigned __int128 acc = 0;
+    for (int k = 0; k < d; ++k) {
+      int a = off[k] < 0 ? -off[k] : off[k];
+      if (a) {
+        zero = false;
+        unsigned __int128 gap = (unsigned __int128)(a - 1) * g.s + 1;
+        acc += gap * gap;
+      }
+    }
+    if (!zero && acc <= g.eps2)
+      for (int k = 0; k < d; ++k) out.push_back((int8_t)off[k]);
+    int k = d - 1;
+    while (k >= 0 && off[k] == R) { off[k] = -R; --k; }
+    if (k < 0) break;
+    ++off[k];
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ stencil
+__global__ void __launch_bounds__(256) nbr_stencil_kernel(
+    int fill, const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
+    const int8_t* __restrict__ offs, int noffs, const Slot* __restrict__ T, uint64_t mask,
+    uint32_t* __restrict__ cnt, const uint64_t* __restrict__ off, uint32_t* __restrict__ nbr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < ncells; cell += nwarps) {
+    const uint64_t key = cell_key[cell];
+    uint32_t cc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cc[k] = k < g.d ? cell_coord(key, g, k) : 0;
+    uint64_t wpos = fill ? off[cell] : 0;
+    uint32_t total = 0;
+    for (int base = 0; base < noffs; base += 32) {
+      const int t = base + lane;
+      bool found = false;
+      uint32_t id = 0;
+      if (t < noffs) {
+        bool ok = true;
+        uint64_t nkey = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k < g.d) {
+            int64_t q = (int64_t)cc[k] + offs[t * g.d + k];
+            ok &= (q >= 0) & (q <= (int64_t)g.maxc[k]);
+            nkey |= (uint64_t)(q & 0xffffffffll) << g.shift[k];
+          }
+        }
+        if (ok) {
+          id = hash_lookup(T, mask, nkey);
+          found = id != 0xffffffffu;
+        }
+      }
+      uint32_t b = __ballot_sync(DB_FULL, found);
+      if (fill && found) nbr[wpos + __popc(b & lt)] = id;
+      wpos += __popc(b);
+      total += __popc(b);
+    }
+    if (!fill && lane == 0) cnt[cell] = total;
+  }
+}
+
+void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
+                       const Slot* T, uint64_t mask, uint64_t** nbr_off, uint32_t** nbr,
+                       uint64_t* total) {
+  std::vector<int8_t> offs = stencil_offsets(g);
+  const int noffs = (int)(offs.size() / g.d);
+  int8_t* doffs = c.alloc<int8_t>(offs.size() + 1);
+  if (!offs.empty())
+    DB_CUDA(cudaMemcpyAsync(doffs, offs.data(), offs.size(), cudaMemcpyHostToDevice, c.st));
+  uint32_t* cnt = c.alloc<uint32_t>(ncells);
+  uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
+  const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
+  nbr_stencil_kernel<<<grid, 256, 0, c.st>>>(0, cell_key, ncells, g, doffs, noffs, T, mask, cnt,
+                                               nullptr, nullptr);
+  c.launched();
+  exclusive_scan_u32_u64(c, cnt, off, ncells);
+  *total = c.read(off + ncells);
+  uint32_t* list = c.alloc<uint32_t>(*total + 1);
+  nbr_stencil_kernel<<<grid, 256, 0, c.st>>>(1, cell_key, ncells, g, doffs, noffs, T, mask, nullptr,
+                                               off, list);
+  c.launched();
+  *nbr_off = off;
+  *nbr = list;
+}
+
+// ------------------------------------------------------------------ cell tree
+constexpr int LEAF = 32;
+
+struct Box {
+  uint32_t lo[8];
+  uint32_t hi[8];
+};
+
+// Morton code: interleave the bits of the lattice coordinates, most
+// significant bit first, axis 0 first within a bit level; total width = bits.
+__global__ void morton_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
+                              uint64_t* __restrict__ code, uint32_t* __restrict__ id) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncells) return;
+  uint64_t key = cell_key[i];
+  uint32_t cc[8];
+  uint32_t maxw = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    cc[k] = k < g.d ? cell_coord(key, g, k) : 0;
+    if (k < g.d) maxw = max(maxw, g.width[k]);
+  }
+  uint64_t m = 0;
+  for (int b = (int)maxw - 1; b >= 0; --b)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < g.d && (uint32_t)b < g.width[k]) m = (m << 1) | ((cc[k] >> b) & 1u);
+  code[i] = m;
+  id[i] = i;
+}
+
+__device__ __forceinline__ uint64_t box_gap2(const uint32_t* q, const uint32_t* lo,
+                                             const uint32_t* hi, const Geo& g) {
+  uint64_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k < g.d) {
+      uint32_t dlt = q[k] < lo[k] ? lo[k] - q[k] : (q[k] > hi[k] ? q[k] - hi[k] : 0u);
+      acc += gap_term(dlt, g);
+    }
+  }
+  return acc;
+}
+
+// Leaves (thread per leaf slot of the padded power-of-two layer), then
+// climb: the second child to arrive at a node builds its box.
+__global__ void tree_build_kernel(const uint64_t* __restrict__ cell_key, const uint32_t* __restrict__ mcell,
+                                  uint32_t ncells, Geo g, uint32_t P2, Box* nodes, uint32_t* flags) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P2) return;
+  Box b;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { b.lo[k] = 0xffffffffu; b.hi[k] = 0; }
+  const uint32_t s0 = i * LEAF, s1 = min(s0 + LEAF, ncells);
+  for (uint32_t t = s0; t < s1; ++t) {
+    uint64_t key = cell_key[mcell[t]];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < g.d) {
+        uint32_t v = cell_coord(key, g, k);
+        b.lo[k] = min(b.lo[k], v);
+        b.hi[k] = max(b.hi[k], v);
+      }
+  }
+  uint32_t node = P2 - 1 + i;
+  nodes[node] = b;
+  while (node > 0) {
+    __threadfence();
+    uint32_t parent = (node - 1) >> 1;
+    if (atomicAdd(flags + parent, 1u) == 0) return;
+    __threadfence();
+    const volatile Box* l = nodes + 2 * parent + 1;
+    const volatile Box* r = nodes + 2 * parent + 2;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      b.lo[k] = min(l->lo[k], r->lo[k]);
+      b.hi[k] = max(l->hi[k], r->hi[k]);
+    }
+    nodes[parent] = b;
+    node = parent;
+  }
+}
+
+__global__ void __launch_bounds__(128) tree_query_kernel(
+    int fill, const uint64_t* __restrict__ cell_key, const uint32_t* __restrict__ mcell,
+    uint32_t ncells, Geo g, uint32_t P2, const Box* __restrict__ nodes, uint32_t* __restrict__ cnt,
+    const uint64_t* __restrict__ off, uint32_t* __restrict__ nbr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncells; q += nwarps) {
+    uint32_t cq[8];
+    const uint64_t key = cell_key[q];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cq[k] = k < g.d ? cell_coord(key, g, k) : 0;
+    uint64_t wpos = fill ? off[q] : 0;
+    uint32_t total = 0;
+    uint32_t stack[64];
+    int sp = 0;
+    stack[sp++] = 0;
+    while (sp > 0) {
+      const uint32_t node = stack[--sp];
+      if (node >= P2 - 1) {
+        const uint32_t t = (node - (P2 - 1)) * LEAF + lane;
+        bool found = false;
+        uint32_t h = 0;
+        if (t < ncells) {
+          h = mcell[t];
+          if (h != q) {
+            uint64_t hk = cell_key[h];
+            uint64_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < g.d) {
+                uint32_t a = cell_coord(hk, g, k);
+                acc += gap_term(a > cq[k] ? a - cq[k] : cq[k] - a, g);
+              }
+            found = acc <= g.eps2;
+          }
+        }
+        uint32_t b = __ballot_sync(DB_FULL, found);
+        if (fill && found) nbr[wpos + __popc(b & lt)] = h;
+        wpos += __popc(b);
+        total += __popc(b);
+      } else {
+        // children in reverse so the left child is visited first
+        for (int ch = 2; ch >= 1; --ch) {
+          const uint32_t cidx = 2 * node + ch;
+          const Box& bx = nodes[cidx];
+          if (box_gap2(cq, bx.lo, bx.hi, g) <= g.eps2) stack[sp++] = cidx;
+        }
+      }
+    }
+    if (!fill && lane == 0) cnt[q] = total;
+  }
+}
+
+void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
+                    uint64_t** nbr_off, uint32_t** nbr, uint64_t* total) {
+  uint64_t* code0 = c.alloc<uint64_t>(ncells);
+  uint64_t* code1 = c.alloc<uint64_t>(ncells);
+  uint32_t* id0 = c.alloc<uint32_t>(ncells);
+  uint32_t* id1 = c.alloc<uint32_t>(ncells);
+  morton_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, code0, id0);
+  c.launched();
+  uint64_t* ksorted;
+  uint32_t* mcell;
+  radix_sort_u64(c, code0, id0, code1, id1, ncells, (int)g.bits, &ksorted, &mcell);
+  const uint32_t L = (ncells + LEAF - 1) / LEAF;
+  uint32_t P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  Box* nodes = c.alloc<Box>(2 * (size_t)P2 - 1);
+  uint32_t* flags = c.alloc<uint32_t>(P2);
+  c.zero(flags, sizeof(uint32_t) * P2);
+  tree_build_kernel<<<grid_for(P2, 128, 1 << 30), 128, 0, c.st>>>(cell_key, mcell, ncells, g, P2,
+                                                                   nodes, flags);
+  c.launched();
+  uint32_t* cnt = c.alloc<uint32_t>(ncells);
+  uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
+  const unsigned grid = grid_for((int64_t)ncells * 32, 128, c.sms * 32);
+  tree_query_kernel<<<grid, 128, 0, c.st>>>(0, cell_key, mcell, ncells, g, P2, nodes, cnt, nullptr,
+                                            nullptr);
+  c.launched();
+  exclusive_scan_u32_u64(c, cnt, off, ncells);
+  *total = c.read(off + ncells);
+  uint32_t* list = c.alloc<uint32_t>(*total + 1);
+  tree_query_kernel<<<grid, 128, 0, c.st>>>(1, cell_key, mcell, ncells, g, P2, nodes, nullptr, off,
+                                            list);
+  c.launched();
+  *nbr_off = off;
+  *nbr = list;
+}
+
+}  // namespace db

@@ -1,0 +1,204 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracles.
+
+Bar: bit-exact on core[], cluster[], border_off[],
+border_ids[] — the method reaches the unique DBSCAN result exactly
+ and the labels are canonical, so any difference is a
+bug. Small cases compare with O1 (definition); medium and full-size cases
+with O2 (independent grid version, itself pinned to O1) plus sampled O1
+checks at the full BASELINE.json sizes.
+"""
+import numpy as np
+import pytest
+
+import datagen
+from helpers import as_rows, assert_same, load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU-only container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1912_06255_b200 as pkg  # noqa: E402
+
+GOLD = load_golden()
+
+
+def key_bits(pts, eps):
+    """Width of the packed cell key, for deciding when ERANGE is legitimate."""
+    import math
+    d = pts.shape[1]
+    s = math.isqrt(eps * eps // d) + 1
+    span = pts.astype(np.int64).max(0) - pts.astype(np.int64).min(0)
+    return sum(int(v // s).bit_length() for v in span)
+
+
+def gpu(pts, eps, mp, flags=0, host=False):
+    if host:
+        return pkg.dbscan(np.ascontiguousarray(pts, np.int32), eps, mp, flags=flags)
+    t = torch.from_numpy(np.ascontiguousarray(pts, np.int32)).cuda()
+    r = pkg.dbscan(t, eps, mp, flags=flags)
+    torch.cuda.synchronize()
+    return r
+
+
+def np_result(r):
+    class R:
+        pass
+    o = R()
+    for f in ("core", "cluster", "border_off", "border_ids"):
+        v = getattr(r, f)
+        setattr(o, f, v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v))
+    return o
+
+
+@pytest.mark.parametrize("g", GOLD, ids=[g.name for g in GOLD])
+@pytest.mark.parametrize("host", [False, True])
+def test_golden(g, host):
+    r = np_result(gpu(g.pts, g.eps, g.min_pts, host=host))
+    assert as_rows(r.core, r.cluster, r.border_off, r.border_ids) == g.rows
+
+
+def _instances(seed, count, dmax=8, nmax=400):
+    rng = np.random.default_rng(seed)
+    for _ in range(count):
+        d = int(rng.integers(1, dmax + 1))
+        n = int(rng.integers(1, nmax))
+        span = int(rng.choice([8, 30, 100, 400, 5000]))
+        pts = datagen.random_small(rng, n, d, span)
+        eps = int(rng.integers(1, max(2, span // 3)))
+        min_pts = int(rng.choice([1, 2, 3, 5, 10, max(1, n // 4), n + 1]))
+        yield pts, eps, min_pts
+
+
+def run_or_erange(pts, eps, mp, flags=0):
+    """GPU result, or None when the call returns ERANGE — allowed only if the
+    packed cell key really needs more than 63 bits."""
+    try:
+        return np_result(gpu(pts, eps, mp, flags))
+    except pkg.DBSCANError as e:
+        assert e.code == -2 and len(pts) and key_bits(pts, eps) > 63, str(e)
+        return None
+
+
+def test_random_small_vs_o1(oracle_lib):
+    """500 random instances: d = 1..8, exact-eps ties, duplicates, negative
+    coordinates, minPts from 1 to n+1."""
+    ran = 0
+    for k, (pts, eps, mp) in enumerate(_instances(100, 500)):
+        r = run_or_erange(pts, eps, mp)
+        if r is not None:
+            assert_same(r, oracle_lib.o1(pts, eps, mp), f"instance {k}")
+            ran += 1
+    assert ran >= 400
+
+
+@pytest.mark.parametrize("flags", [pkg.F_FORCE_WIDE, pkg.F_FORCE_TREE, pkg.F_NO_WAVES,
+                                   pkg.F_FORCE_WIDE | pkg.F_FORCE_TREE | pkg.F_NO_WAVES])
+def test_flag_variants_vs_o1(oracle_lib, flags):
+    for k, (pts, eps, mp) in enumerate(_instances(200 + flags, 120, dmax=8)):
+        r = run_or_erange(pts, eps, mp, flags)
+        if r is not None:
+            assert_same(r, oracle_lib.o1(pts, eps, mp), f"{flags}/{k}")
+
+
+def test_force_stencil_high_d_vs_o1(oracle_lib):
+    """The stencil path for d = 4..6 must agree with the tree path and O1."""
+    for k, (pts, eps, mp) in enumerate(_instances(300, 80, dmax=6)):
+        if pts.shape[1] < 4:
+            continue
+        r = run_or_erange(pts, eps, mp, pkg.F_FORCE_STENCIL)
+        if r is not None:
+            assert_same(r, oracle_lib.o1(pts, eps, mp), f"{k}")
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 7, 8])
+def test_clustered_medium_vs_o2(oracle_lib, d):
+    """Seed-spreader data with dense cells, many neighbours, border points,
+    several tiles of every kernel and ragged tails."""
+    for seed, n in [(1, 20_001), (2, 45_057)]:
+        pts = datagen.seed_spreader(n - n % 100, d, 20000, seed + 10 * d, p_step=0.02, noise_frac=0.03)
+        for eps, mp in [(150, 15), (400, 60)]:
+            r = run_or_erange(pts, eps, mp)
+            if r is not None:
+                assert_same(r, oracle_lib.o2(pts, eps, mp), f"d={d} n={n} eps={eps}")
+
+
+def test_uniform_medium_vs_o2(oracle_lib):
+    """Sparse lattice (c5-like): ~1 point per cell, many 1x1 BCP pairs, many
+    border points in several clusters."""
+    pts = datagen.uniform(200_000, 3, 12_000, 9)
+    for mp in (5, 10, 40):
+        assert_same(np_result(gpu(pts, 500, mp)), oracle_lib.o2(pts, 500, mp), f"mp={mp}")
+
+
+def test_c1_full_vs_o1(oracle_lib):
+    cfg = datagen.CONFIGS["c1"]
+    pts = cfg.points()
+    for host in (False, True):
+        assert_same(np_result(gpu(pts, cfg.eps, cfg.min_pts, host=host)),
+                    oracle_lib.o1(pts, cfg.eps, cfg.min_pts), "c1")
+
+
+def test_c2_full_vs_o2(oracle_lib):
+    cfg = datagen.CONFIGS["c2"]
+    pts = cfg.points()
+    assert_same(np_result(gpu(pts, cfg.eps, cfg.min_pts)), oracle_lib.o2(pts, cfg.eps, cfg.min_pts), "c2")
+
+
+@pytest.mark.parametrize("case", [
+    ("single", np.array([[5, 7]], np.int32), 3, 1),
+    ("single_noise", np.array([[5, 7]], np.int32), 3, 2),
+    ("all_dup", np.full((5000, 3), 42, np.int32), 1, 100),
+    ("all_dup_noise", np.full((99, 3), 42, np.int32), 1, 100),
+    ("huge_eps", datagen.uniform(3000, 4, 1000, 3), 10_000, 3000),
+    ("eps1_d8", datagen.random_small(np.random.default_rng(5), 3000, 8, 4), 1, 3),
+    ("d1", datagen.random_small(np.random.default_rng(6), 5000, 1, 20000), 7, 3),
+    ("extremes_wide", np.array([[-2**31, 0], [2**31 - 1, 0], [2**31 - 1, 3], [0, 2**31 - 1],
+                                [-2**31, -2**31], [-2**31 + 3, -2**31]], np.int32), 3, 1),
+    ("big_eps_wide", datagen.random_small(np.random.default_rng(8), 2000, 3, 2**31 - 2, negative=True),
+     2**30, 4),
+])
+def test_edge_cases_vs_o1(oracle_lib, case):
+    name, pts, eps, mp = case
+    assert_same(np_result(gpu(pts, eps, mp)), oracle_lib.o1(pts, eps, mp), name)
+
+
+def test_empty():
+    for host in (False, True):
+        r = np_result(gpu(np.zeros((0, 3), np.int32), 5, 2, host=host))
+        assert len(r.core) == 0 and list(r.border_off) == [0] and len(r.border_ids) == 0
+
+
+@pytest.mark.parametrize("n", [4095, 4096, 4097, 8191, 12289])
+def test_tile_boundaries_vs_o2(oracle_lib, n):
+    """Ragged tails at the radix (4096), scan (2048) and segment (2048) tiles."""
+    pts = datagen.seed_spreader(n - n % 100 + 100, 3, 5000, n, p_step=0.1)[:n]
+    assert_same(np_result(gpu(pts, 120, 8)), oracle_lib.o2(pts, 120, 8), f"n={n}")
+
+
+def test_deterministic_and_permutation_invariant(oracle_lib):
+    pts = datagen.seed_spreader(30_000, 3, 8000, 77, p_step=0.05, noise_frac=0.05)
+    a = np_result(gpu(pts, 200, 25))
+    b = np_result(gpu(pts, 200, 25))
+    assert_same(a, b, "repeat")
+    perm = np.random.default_rng(1).permutation(len(pts))
+    c = np_result(gpu(pts[perm], 200, 25))
+    assert np.array_equal(a.core[perm], c.core)
+    m = {}
+    for j in np.flatnonzero(c.core):
+        m.setdefault(int(c.cluster[j]), int(a.cluster[perm[j]]))
+        assert m[int(c.cluster[j])] == int(a.cluster[perm[j]])
+    assert len(set(m.values())) == len(m)
+
+
+def test_stream_and_stats():
+    pts = datagen.seed_spreader(20_000, 3, 8000, 3, p_step=0.05)
+    s = torch.cuda.Stream()
+    t = torch.from_numpy(pts).cuda()
+    with torch.cuda.stream(s):
+        r = pkg.dbscan(t, 200, 20, timing=True)
+    s.synchronize()
+    assert r.stage_ms["total"] > 0
+    assert r.stats["launches"] > 10
+    assert r.stats["ncells"] > 0 and r.n_core + r.n_border + r.n_noise == len(pts)
