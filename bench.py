@@ -1,0 +1,312 @@
+#!/usr/bin/env python3
+"""bench.py — end-to-end exact grid DBSCAN throughput on B200.
+
+Workload ("suite"): BASELINE.json configs[1..4] at full size — c2 (2D, 1M),
+c3 (3D, 10M), c4 5D and 7D (10M each), c5 3D uniform at minPts 10 and 10^4
+(10M each): 51M points per step over d = 2..7, the configurations the metric
+"points/sec end-to-end exact grid DBSCAN (10M pts, d=2-7)" is quoted on.
+configs[0] (10K points) is the oracle-sized parity case, not a bench line.
+
+One step = one dbscan() call per run, i.e. the whole hot path (SURVEY §8
+a1-a10) over every run's input. value = points processed / device time,
+inputs resident in HBM, outputs allocated by the call; L2 is flushed (256 MB
+write) before every run, outside the timed region. e2e = the same metric
+through the C ABI with pinned HOST buffers, H2D of the points and D2H of all
+outputs inside the timed region.
+
+Multi-GPU (torchrun): the method runs on one GPU (BASELINE north_star); each
+rank runs an independent replica of the suite ("replicas only", DESIGN.md
+§Multi-GPU), value = points of all ranks / max-over-ranks device time.
+
+--impl reference: the CPU oracle O2 (oracle/, the "simple CPU grid version")
+as it stands, on a bounded sample of the same runs (a 5% prefix of each run's
+points), timed on the host cores. It is a deliberately slow reference.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+
+METRIC = "points/sec end-to-end exact grid DBSCAN (10M pts, d=2–7); per-stage HBM GB/s"
+SUITE = ["c2", "c3", "c4_5d", "c4_7d", "c5_10", "c5_10k"]
+REF_FRACTION = 0.05
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- reference
+def run_reference(args):
+    """Time the CPU oracle O2 on a bounded sample of every run."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for name in SUITE:
+        cfg = datagen.CONFIGS[name]
+        pts = cfg.points()
+        k = max(1, int(len(pts) * REF_FRACTION))
+        samples.append((name, np.ascontiguousarray(pts[:k]), cfg.eps, cfg.min_pts))
+    oracle.build()
+    times = []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        for _, p, e, m in samples:
+            oracle.o2(p, e, m)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    npts = sum(len(s[1]) for s in samples)
+    total = sum(times)
+    value = npts * len(times) / total
+    cores = os.cpu_count()
+    sample = f"O2 CPU grid oracle on the first {REF_FRACTION:.0%} of each run's points ({npts} points/step)"
+    line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * total / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "suite: BASELINE configs[1..4] (c2,c3,c4_5d,c4_7d,c5 minPts 10 and 1e4)",
+                       "runs": SUITE, "sample": sample},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--runs", default=",".join(SUITE), help="comma list of runs (default: the suite)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="print per-run stage times to stderr")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_1912_06255_b200 as pkg
+    pkg.load()
+
+    runs = [r for r in args.runs.split(",") if r]
+    data = []
+    for name in runs:
+        cfg = datagen.CONFIGS[name]
+        pts = cfg.points()
+        data.append((name, cfg, torch.from_numpy(pts).to(dev), pts))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(timed):
+        ms, stages, launches, stats = [], [], 0, []
+        for name, cfg, t, _ in data:
+            flush.fill_(rank + 1)  # evict the inputs from L2 (outside the timed region)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = pkg.dbscan(t, cfg.eps, cfg.min_pts, timing=True)
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            stages.append(r.stage_ms)
+            stats.append(r.stats | {"n_core": r.n_core, "n_clusters": r.n_clusters, "n_border": r.n_border,
+                                    "nnz": int(r.border_ids.numel())})
+            launches += r.stats["launches"]
+            del r
+        return ms, stages, launches, stats
+
+    for _ in range(args.warmup):
+        one_step(False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    per_run_ms = [[] for _ in runs]
+    stage_acc = [dict() for _ in runs]
+    launches = 0
+    stats = None
+    for _ in range(args.steps):
+        ms, stages, l, stats = one_step(True)
+        launches += l
+        for i, m in enumerate(ms):
+            per_run_ms[i].append(m)
+            for k, v in stages[i].items():
+                stage_acc[i][k] = stage_acc[i].get(k, 0.0) + v
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    step_ms = [sum(per_run_ms[i][s] for i in range(len(runs))) for s in range(args.steps)]
+    total_ms = sum(step_ms)
+    if dist:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    npts_step = sum(c.n for _, c, _, _ in data)
+    value = npts_step * args.steps * world / (total_ms / 1000.0)
+
+    # ---- roofline: the radix sort (largest HBM consumer)
+    peak, peak_kind = load_peaks()
+    sort_bytes = 0.0
+    sort_ms = 0.0
+    for i, (name, cfg, t, _) in enumerate(data):
+        st = stats[i]
+        kb = 8 if st["key_bits"] > 32 else 4
+        # per pass: read + write (key, index) = 2*(kb+4) bytes per point
+        sort_bytes += st["sort_passes"] * 2 * (kb + 4) * cfg.n * args.steps
+        sort_ms += stage_acc[i].get("keys+sort", 0.0)
+    # keys kernel: read d*4 per point, write key+index
+    keys_bytes = sum((4 * c.d + (8 if stats[i]["key_bits"] > 32 else 4) + 4) * c.n
+                     for i, (_, c, _, _) in enumerate(data)) * args.steps
+    achieved = (sort_bytes + keys_bytes) / (sort_ms / 1000.0) / 1e9 if sort_ms > 0 else None
+    roofline = {"bound": "hbm", "kernel": "keys_kernel + radix_pass_kernel (stage keys+sort)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_kind": peak_kind,
+                "note": "algorithmic bytes: keys 4d+kb+4 per point; each LSD pass reads and writes (key,idx)"}
+
+    # ---- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        h2d = d2h = 0
+        for name, cfg, _, pts in data:
+            hp = torch.from_numpy(pts).pin_memory()
+            outs = (torch.empty(cfg.n, dtype=torch.uint8).pin_memory(),
+                    torch.empty(cfg.n, dtype=torch.int32).pin_memory(),
+                    torch.empty(cfg.n + 1, dtype=torch.int64).pin_memory())
+            host.append((cfg, hp, outs))
+        def e2e_step():
+            nonlocal h2d, d2h
+            t0 = time.perf_counter()
+            b_in = b_out = 0
+            for cfg, hp, outs in host:
+                r = pkg.dbscan(hp, cfg.eps, cfg.min_pts, out=outs, stream=stream)
+                b_in += hp.numel() * 4
+                b_out += cfg.n * (1 + 4 + 8) + 8 + 4 * len(r.border_ids)
+            h2d, d2h = b_in, b_out
+            return time.perf_counter() - t0
+        for _ in range(1):
+            e2e_step()
+        ts = [e2e_step() for _ in range(max(1, min(args.steps, 3)))]
+        e2e = {"value": npts_step * len(ts) / sum(ts), "unit": "points/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "timer": "host wall clock around blocking C-ABI calls"}
+
+    # ---- CPU baseline: the oracle as it stands, bounded sample (rank 0, N=1)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        npts = 0
+        for name, cfg, _, pts in data:
+            k = max(1, int(cfg.n * REF_FRACTION))
+            oracle.o2(np.ascontiguousarray(pts[:k]), cfg.eps, cfg.min_pts)
+            npts += k
+        dt = time.perf_counter() - t0
+        cpu = {"value": npts / dt, "unit": "points/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"O2 CPU grid oracle on the first {REF_FRACTION:.0%} of each run's points "
+                         f"({npts} points, {dt:.1f} s)"}
+
+    run_info = []
+    for i, (name, cfg, _, _) in enumerate(data):
+        m = statistics.median(per_run_ms[i])
+        run_info.append({"run": name, "n": cfg.n, "d": cfg.d, "eps": cfg.eps, "min_pts": cfg.min_pts,
+                         "ms_median": round(m, 4), "pts_per_s": cfg.n / (m / 1000.0),
+                         "stage_ms": {k: round(v / args.steps, 4) for k, v in stage_acc[i].items()},
+                         "stats": stats[i]})
+    line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "suite: BASELINE configs[1..4] (c2,c3,c4_5d,c4_7d,c5 minPts 10 and 1e4)",
+                       "runs": runs, "points_per_step": npts_step, "l2": "flushed (256 MB write) before every run",
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "runs": run_info}
+    if args.detail and rank == 0:
+        for ri in run_info:
+            print(ri["run"], ri["ms_median"], ri["stage_ms"], file=sys.stderr)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

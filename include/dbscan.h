@@ -54,7 +54,7 @@ extern "C" {
 #define DBSCAN_STAGE_KEYS      1  /* a1: cell keys + digit histograms                  */
 #define DBSCAN_STAGE_SORT      2  /* a2: LSD radix sort of (key, index)                */
 #define DBSCAN_STAGE_SEGMENT   3  /* a3: cell segmentation + point gather              */
-#define DBSCAN_STAGE_HASH      4  /* a4: cell hash table                               */
+#define DBSCAN_STAGE_HASH      4  /* a4: cell hash table (reported inside NEIGHBORS)     */
 #define DBSCAN_STAGE_NEIGHBORS 5  /* a5: neighbour-cell CSR (stencil or tree)          */
 #define DBSCAN_STAGE_MARKCORE  6  /* a6: MarkCore (Alg 2)                              */
 #define DBSCAN_STAGE_COMPACT   7  /* a7: core-first compaction per cell                */
@@ -76,6 +76,7 @@ extern "C" {
 #define DBSCAN_STAT_WIDE          8  /* 1 if the 64-bit distance path ran                */
 #define DBSCAN_STAT_TREE          9  /* 1 if neighbour cells came from the cell tree      */
 #define DBSCAN_STAT_CELL_SIDE    10  /* integer cell side s                              */
+#define DBSCAN_STAT_DENSE_DIR    11  /* 1 if cells were found through a dense directory   */
 #define DBSCAN_NSTATS            16
 
 typedef struct dbscan_result {

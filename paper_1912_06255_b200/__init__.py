@@ -39,7 +39,7 @@ NSTAGES, NSTATS = 12, 16
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
-         "launches", "wide", "tree", "cell_side"]
+         "launches", "wide", "tree", "cell_side", "dense_dir"]
 
 
 class _Result(C.Structure):

@@ -11,59 +11,146 @@
 
 namespace db {
 
-enum : uint8_t { CELL_DENSE = 0, CELL_COUNT = 1, CELL_NONCORE = 2 };
+enum : uint8_t { CELL_DENSE = 0, CELL_COUNT = 1, CELL_NONCORE = 2, CELL_COUNT_WARP = 3 };
+
+// Candidate points of one query (sum of neighbour-cell sizes) at or below this
+// are scanned by one thread; above it by one warp (SURVEY §8(a) a6 mapping).
+constexpr int64_t WARP_CANDIDATES = 32;
 
 __global__ void cell_class_kernel(CellsView cv, int64_t min_pts, uint8_t* __restrict__ cls) {
   uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= cv.ncells) return;
   const int64_t cnt = cv.cell_start[g + 1] - cv.cell_start[g];
   if (cnt >= min_pts) { cls[g] = CELL_DENSE; return; }
+  // upper bound |g| + sum_h |h|: below minPts no point of g can be core
   int64_t ub = cnt;
-  for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && ub < min_pts; ++t) {
+  const int64_t cap = cnt + max(min_pts, WARP_CANDIDATES + 1);
+  for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && ub < cap; ++t) {
     uint32_t h = cv.nbr[t];
     ub += cv.cell_start[h + 1] - cv.cell_start[h];
   }
-  cls[g] = ub >= min_pts ? CELL_COUNT : CELL_NONCORE;
+  if (ub < min_pts) cls[g] = CELL_NONCORE;
+  else cls[g] = (ub - cnt > WARP_CANDIDATES) ? CELL_COUNT_WARP : CELL_COUNT;
 }
 
-// Thread per sorted point. Threads of one warp are consecutive points of the
-// same or adjacent cells, so their neighbour-cell scans mostly read the same
-// points (broadcast loads through L1).
+// Thread per sorted point: dense / pruned cells are decided from the class;
+// queries with few candidates count in the thread; the others are queued for
+// the warp kernel.
 template <int D, bool WIDE>
 __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const uint8_t* __restrict__ cls,
                                                         const int32_t* __restrict__ Ps, uint32_t n,
                                                         int64_t min_pts, uint32_t clampc,
-                                                        uint64_t eps2, uint8_t* __restrict__ core_s) {
+                                                        uint64_t eps2, uint8_t* __restrict__ core_s,
+                                                        uint32_t* __restrict__ queue,
+                                                        uint32_t* __restrict__ qcount) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const uint32_t g = cv.cell_of[j];
-  const uint8_t c = cls[g];
-  if (c != CELL_COUNT) { core_s[j] = c == CELL_DENSE; return; }
-  int32_t p[D], q[D];
-  PtLoad<D>::load(Ps, j, p);
-  int64_t count = cv.cell_start[g + 1] - cv.cell_start[g];
-  for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && count < min_pts; ++t) {
-    const uint32_t h = cv.nbr[t];
-    const uint32_t e = cv.cell_start[h + 1];
-    for (uint32_t u = cv.cell_start[h]; u < e; ++u) {
-      PtLoad<D>::load(Ps, u, q);
-      count += within<D, WIDE>(p, q, clampc, eps2);
-      if (count >= min_pts) break;
+  bool enqueue = false;
+  if (j < n) {
+    const uint32_t g = cv.cell_of[j];
+    const uint8_t c = cls[g];
+    if (c == CELL_COUNT_WARP) {
+      enqueue = true;
+    } else if (c != CELL_COUNT) {
+      core_s[j] = c == CELL_DENSE;
+    } else {
+      int32_t p[D], q[D];
+      PtLoad<D>::load(Ps, j, p);
+      int64_t count = cv.cell_start[g + 1] - cv.cell_start[g];
+      for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && count < min_pts; ++t) {
+        const uint32_t h = cv.nbr[t];
+        const uint32_t e = cv.cell_start[h + 1];
+        for (uint32_t u = cv.cell_start[h]; u < e; ++u) {
+          PtLoad<D>::load(Ps, u, q);
+          count += within<D, WIDE>(p, q, clampc, eps2);
+          if (count >= min_pts) break;
+        }
+      }
+      core_s[j] = count >= min_pts;
     }
   }
-  core_s[j] = count >= min_pts;
+  // warp-aggregated append to the warp-kernel queue
+  const uint32_t b = __ballot_sync(DB_FULL, enqueue);
+  if (b) {
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(b) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(qcount, (uint32_t)__popc(b));
+    base = __shfl_sync(DB_FULL, base, leader);
+    if (enqueue) queue[base + __popc(b & lanemask_lt())] = j;
+  }
+}
+
+// Warp per queued query point. The candidates (points of the neighbouring
+// cells, 32 cells at a time) are flattened by a warp prefix sum over the cell
+// sizes; lane l tests candidate t0 + l, found by a 5-step binary search over
+// the lanes' exclusive offsets. Consecutive candidates of one cell are
+// consecutive points, so the loads coalesce. The count is warp-uniform, so
+// the exit at minPts is a uniform branch.
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+                                                             const uint32_t* __restrict__ queue,
+                                                             const uint32_t* __restrict__ qcount,
+                                                             int64_t min_pts, uint32_t clampc,
+                                                             uint64_t eps2, uint8_t* __restrict__ core_s) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = *qcount;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < m; w += nwarps) {
+    const uint32_t j = queue[w];
+    const uint32_t g = cv.cell_of[j];
+    int32_t p[D], q[D];
+    PtLoad<D>::load(Ps, j, p);
+    int64_t count = cv.cell_start[g + 1] - cv.cell_start[g];
+    const uint64_t nb1 = cv.nbr_off[g + 1];
+    for (uint64_t cb = cv.nbr_off[g]; cb < nb1 && count < min_pts; cb += 32) {
+      const uint64_t t = cb + lane;
+      uint32_t sz = 0, st = 0;
+      if (t < nb1) {
+        const uint32_t h = cv.nbr[t];
+        st = cv.cell_start[h];
+        sz = cv.cell_start[h + 1] - st;
+      }
+      const uint32_t incl = warp_inclusive_scan(sz);
+      const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
+      const uint32_t excl = incl - sz;
+      for (uint32_t t0 = 0; t0 < total && count < min_pts; t0 += 32) {
+        const uint32_t tt = t0 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const uint32_t e = __shfl_sync(DB_FULL, excl, lo + s);
+          if (e <= tt) lo += s;
+        }
+        const uint32_t ost = __shfl_sync(DB_FULL, st, lo);
+        const uint32_t oex = __shfl_sync(DB_FULL, excl, lo);
+        bool hit = false;
+        if (tt < total) {
+          PtLoad<D>::load(Ps, ost + (tt - oex), q);
+          hit = within<D, WIDE>(p, q, clampc, eps2);
+        }
+        count += __popc(__ballot_sync(DB_FULL, hit));
+      }
+    }
+    if (lane == 0) core_s[j] = count >= min_pts;
+  }
 }
 
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
                int64_t min_pts, bool wide, uint8_t* core_s) {
   uint8_t* cls = c.alloc<uint8_t>(cv.ncells);
+  uint32_t* queue = c.alloc<uint32_t>(n);
+  uint32_t* qcount = c.alloc<uint32_t>(1);
+  c.zero(qcount, sizeof(uint32_t));
   cell_class_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(cv, min_pts, cls);
   c.launched();
   dispatch(g.D, wide, [&]<int D, bool W>() {
     mark_core_kernel<D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
-        cv, cls, Ps, (uint32_t)n, min_pts, g.clampc, g.eps2, core_s);
+        cv, cls, Ps, (uint32_t)n, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
+    c.launched();
+    mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts,
+                                                               g.clampc, g.eps2, core_s);
+    c.launched();
   });
-  c.launched();
 }
 
 // ---------------------------------------------------------------- a7

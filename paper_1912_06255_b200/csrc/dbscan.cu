@@ -210,12 +210,10 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   uint64_t* nbr_off;
   uint32_t* nbr;
   uint64_t nbr_total = 0;
+  bool dense_dir = false;
   if (!tree) {
-    tm.stage(DBSCAN_STAGE_HASH);
-    Slot* T;
-    const uint64_t mask = build_hash(c, cell_key, ncells, &T);
     tm.stage(DBSCAN_STAGE_NEIGHBORS);
-    neighbors_stencil(c, g, cell_key, ncells, T, mask, &nbr_off, &nbr, &nbr_total);
+    neighbors_stencil(c, g, cell_key, ncells, n, &nbr_off, &nbr, &nbr_total, &dense_dir);
   } else {
     tm.stage(DBSCAN_STAGE_NEIGHBORS);
     neighbors_tree(c, g, cell_key, ncells, &nbr_off, &nbr, &nbr_total);
@@ -295,6 +293,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_WIDE] = wide;
   out->stats[DBSCAN_STAT_TREE] = tree;
   out->stats[DBSCAN_STAT_CELL_SIDE] = (int64_t)s;
+  out->stats[DBSCAN_STAT_DENSE_DIR] = dense_dir;
   return DBSCAN_OK;
 }
 

@@ -26,6 +26,7 @@ struct Ctx {
   std::vector<void*> temps;
   int64_t launches = 0;
   int sms = 148;
+  uint32_t* dense_dir = nullptr;  // dense cell directory, when built
 
   template <typename T>
   T* alloc(size_t count) {
@@ -86,9 +87,9 @@ uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** ta
 
 // ---- neighbors.cu (a5) ----
 // neighbour-cell CSR excluding the cell itself: nbr_off[ncells+1] (device), nbr list.
-void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
-                       const Slot* T, uint64_t mask, uint64_t** nbr_off, uint32_t** nbr,
-                       uint64_t* total);
+// d <= 3 (or forced): builds a dense cell directory or a hash table itself.
+void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells, int64_t n,
+                       uint64_t** nbr_off, uint32_t** nbr, uint64_t* total, bool* dense);
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
                     uint64_t** nbr_off, uint32_t** nbr, uint64_t* total);
 // host: exact stencil offsets (Delta != 0 with sum gap^2 <= eps^2), flat [count*d] int8

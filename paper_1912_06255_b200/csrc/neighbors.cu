@@ -9,7 +9,8 @@
 // matter.
 //   d <= 3: enumerate the stencil of offsets satisfying the predicate (21 in
 //           2D, 117 in 3D including self) and probe the cell hash table
-//           (P:L489-493), one warp per cell, lanes over offsets.
+//           (P:L489-493), one thread per cell, the warp's lanes being 32
+//           consecutive cells so that their probes coalesce.
 //   d >= 4: "enumerating all possible neighboring cells can be inefficient in
 //           practice for higher dimensions"; the
 //           paper inserts the cells into a k-d tree and runs range queries.
@@ -24,9 +25,12 @@
 
 namespace db {
 
+// Offsets delta != 0 with sum_k gap_k^2 <= eps^2, ordered by ascending squared
+// gap so that every CSR row lists the nearest cells first (the early exits of
+// MarkCore, BCP and ClusterBorder then fire sooner); ties lexicographic.
 std::vector<int8_t> stencil_offsets(const Geo& g) {
   const int d = g.d, R = (int)g.R;
-  std::vector<int8_t> out;
+  std::vector<std::pair<unsigned __int128, std::vector<int8_t>>> all;
   std::vector<int> off(d, -R);
   while (true) {
     bool zero = true;
@@ -39,80 +43,155 @@ std::vector<int8_t> stencil_offsets(const Geo& g) {
         acc += gap * gap;
       }
     }
-    if (!zero && acc <= g.eps2)
-      for (int k = 0; k < d; ++k) out.push_back((int8_t)off[k]);
+    if (!zero && acc <= g.eps2) all.push_back({acc, std::vector<int8_t>(off.begin(), off.end())});
     int k = d - 1;
     while (k >= 0 && off[k] == R) { off[k] = -R; --k; }
     if (k < 0) break;
     ++off[k];
   }
+  std::stable_sort(all.begin(), all.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<int8_t> out;
+  for (auto& e : all) out.insert(out.end(), e.second.begin(), e.second.end());
   return out;
 }
 
 // ------------------------------------------------------------------ stencil
+// Thread per cell, loop over the offsets: the 32 lanes of a warp are 32
+// consecutive cells in key order (mostly one column, consecutive last-axis
+// coordinates) probing the same offset, so their keys are consecutive too and
+// the locality-preserving slot hash (common.cuh) puts them in the same or
+// adjacent 128-byte slot groups: the probes of one warp instruction coalesce.
+// Each offset carries its packed key delta (sum_k delta_k << shift_k); the
+// per-axis range check keeps the two's-complement add exact.
+// DENSE: cells are looked up in a dense directory over the whole lattice
+// (chosen when the lattice has at most DENSE_PER_POINT cells per input point),
+// indexed like the key (axis 0 major), so a lookup is one coalesced load.
+constexpr int MAX_SMEM_OFFS = 2048;
+constexpr int64_t DENSE_PER_POINT = 8;
+
+struct Lattice {
+  uint64_t stride[3];
+};
+
+template <bool DENSE>
 __global__ void __launch_bounds__(256) nbr_stencil_kernel(
     int fill, const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
-    const int8_t* __restrict__ offs, int noffs, const Slot* __restrict__ T, uint64_t mask,
+    const int8_t* __restrict__ offs, const int64_t* __restrict__ delta, int noffs,
+    const Slot* __restrict__ T, uint64_t mask, const uint32_t* __restrict__ dir, Lattice lat,
     uint32_t* __restrict__ cnt, const uint64_t* __restrict__ off, uint32_t* __restrict__ nbr) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t lt = lanemask_lt();
-  for (uint32_t cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < ncells; cell += nwarps) {
-    const uint64_t key = cell_key[cell];
-    uint32_t cc[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) cc[k] = k < g.d ? cell_coord(key, g, k) : 0;
-    uint64_t wpos = fill ? off[cell] : 0;
-    uint32_t total = 0;
-    for (int base = 0; base < noffs; base += 32) {
-      const int t = base + lane;
-      bool found = false;
-      uint32_t id = 0;
-      if (t < noffs) {
-        bool ok = true;
-        uint64_t nkey = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (k < g.d) {
-            int64_t q = (int64_t)cc[k] + offs[t * g.d + k];
-            ok &= (q >= 0) & (q <= (int64_t)g.maxc[k]);
-            nkey |= (uint64_t)(q & 0xffffffffll) << g.shift[k];
-          }
-        }
-        if (ok) {
-          id = hash_lookup(T, mask, nkey);
-          found = id != 0xffffffffu;
-        }
-      }
-      uint32_t b = __ballot_sync(DB_FULL, found);
-      if (fill && found) nbr[wpos + __popc(b & lt)] = id;
-      wpos += __popc(b);
-      total += __popc(b);
-    }
-    if (!fill && lane == 0) cnt[cell] = total;
+  __shared__ int8_t s_off[MAX_SMEM_OFFS * 3];
+  __shared__ int64_t s_delta[MAX_SMEM_OFFS];
+  const bool smem = noffs <= MAX_SMEM_OFFS && g.d <= 3;
+  if (smem) {
+    for (int i = threadIdx.x; i < noffs * g.d; i += blockDim.x) s_off[i] = offs[i];
+    for (int i = threadIdx.x; i < noffs; i += blockDim.x) s_delta[i] = delta[i];
   }
+  __syncthreads();
+  const uint32_t cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= ncells) return;
+  const uint64_t key = cell_key[cell];
+  uint32_t cc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cc[k] = k < g.d ? cell_coord(key, g, k) : 0;
+  uint64_t base = key;
+  if constexpr (DENSE) {
+    base = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k < g.d) base += (uint64_t)cc[k] * lat.stride[k];
+  }
+  uint64_t wpos = fill ? off[cell] : 0;
+  uint32_t total = 0;
+  for (int t = 0; t < noffs; ++t) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < g.d) {
+        const int64_t q = (int64_t)cc[k] + (smem ? s_off[t * g.d + k] : offs[t * g.d + k]);
+        ok &= (q >= 0) & (q <= (int64_t)g.maxc[k]);
+      }
+    }
+    if (!ok) continue;
+    const uint64_t nkey = base + (uint64_t)(smem ? s_delta[t] : delta[t]);
+    uint32_t id;
+    if constexpr (DENSE) id = __ldg(dir + nkey);
+    else id = hash_lookup(T, mask, nkey);
+    if (id == 0xffffffffu) continue;
+    if (fill) nbr[wpos] = id;
+    ++wpos;
+    ++total;
+  }
+  if (!fill) cnt[cell] = total;
 }
 
-void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
-                       const Slot* T, uint64_t mask, uint64_t** nbr_off, uint32_t** nbr,
-                       uint64_t* total) {
+__global__ void dense_fill_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
+                                  Lattice lat, uint32_t* __restrict__ dir) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncells) return;
+  const uint64_t key = cell_key[i];
+  uint64_t lin = 0;
+  for (int k = 0; k < g.d; ++k) lin += (uint64_t)cell_coord(key, g, k) * lat.stride[k];
+  dir[lin] = i;
+}
+
+void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells, int64_t n,
+                       uint64_t** nbr_off, uint32_t** nbr, uint64_t* total, bool* dense_out) {
   std::vector<int8_t> offs = stencil_offsets(g);
   const int noffs = (int)(offs.size() / g.d);
+  // dense directory when the lattice is small relative to n (d <= 3 only)
+  Lattice lat{{0, 0, 0}};
+  bool dense = false;
+  if (g.d <= 3) {
+    unsigned __int128 vol = 1;
+    for (int k = g.d - 1; k >= 0; --k) {
+      lat.stride[k] = (uint64_t)vol;
+      vol *= (unsigned __int128)g.maxc[k] + 1;
+    }
+    dense = vol <= (unsigned __int128)(DENSE_PER_POINT * n + (1 << 20));
+    if (dense) {
+      const uint64_t volume = (uint64_t)vol;
+      uint32_t* dir = c.alloc<uint32_t>(volume);
+      DB_CUDA(cudaMemsetAsync(dir, 0xff, sizeof(uint32_t) * volume, c.st));
+      dense_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, lat, dir);
+      c.launched();
+      c.dense_dir = dir;
+    }
+  }
+  Slot* T = nullptr;
+  uint64_t mask = 0;
+  if (!dense) mask = build_hash(c, cell_key, ncells, &T);
+  *dense_out = dense;
+  std::vector<int64_t> delta((size_t)noffs + 1, 0);
+  for (int t = 0; t < noffs; ++t) {
+    int64_t dl = 0;
+    for (int k = 0; k < g.d; ++k)
+      dl += (int64_t)offs[(size_t)t * g.d + k] *
+            (dense ? (int64_t)lat.stride[k] : (int64_t)(1ull << g.shift[k]));
+    delta[t] = dl;
+  }
   int8_t* doffs = c.alloc<int8_t>(offs.size() + 1);
+  int64_t* ddelta = c.alloc<int64_t>(delta.size());
   if (!offs.empty())
     DB_CUDA(cudaMemcpyAsync(doffs, offs.data(), offs.size(), cudaMemcpyHostToDevice, c.st));
+  DB_CUDA(cudaMemcpyAsync(ddelta, delta.data(), sizeof(int64_t) * delta.size(), cudaMemcpyHostToDevice, c.st));
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
-  const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
-  nbr_stencil_kernel<<<grid, 256, 0, c.st>>>(0, cell_key, ncells, g, doffs, noffs, T, mask, cnt,
-                                               nullptr, nullptr);
-  c.launched();
+  const unsigned grid = grid_for(ncells, 256, 1 << 30);
+  auto launch = [&](int fill, uint32_t* list) {
+    if (dense)
+      nbr_stencil_kernel<true><<<grid, 256, 0, c.st>>>(fill, cell_key, ncells, g, doffs, ddelta, noffs,
+                                                         T, mask, c.dense_dir, lat, cnt, off, list);
+    else
+      nbr_stencil_kernel<false><<<grid, 256, 0, c.st>>>(fill, cell_key, ncells, g, doffs, ddelta, noffs,
+                                                          T, mask, nullptr, lat, cnt, off, list);
+    c.launched();
+  };
+  launch(0, nullptr);
   exclusive_scan_u32_u64(c, cnt, off, ncells);
   *total = c.read(off + ncells);
   uint32_t* list = c.alloc<uint32_t>(*total + 1);
-  nbr_stencil_kernel<<<grid, 256, 0, c.st>>>(1, cell_key, ncells, g, doffs, noffs, T, mask, nullptr,
-                                               off, list);
-  c.launched();
+  launch(1, list);
   *nbr_off = off;
   *nbr = list;
 }
@@ -254,6 +333,58 @@ __global__ void __launch_bounds__(128) tree_query_kernel(
   }
 }
 
+// Order each CSR row by ascending lattice gap to its cell (nearest first), a
+// block per row: bitonic sort of (scaled squared gap << 32 | id) in shared
+// memory. Rows longer than ROW_SORT_MAX stay in tree order (order only
+// affects how soon early exits fire, never the result).
+constexpr int ROW_SORT_MAX = 2048;
+
+__global__ void __launch_bounds__(256) sort_rows_kernel(const uint64_t* __restrict__ cell_key,
+                                                        uint32_t ncells, Geo g,
+                                                        const uint64_t* __restrict__ off,
+                                                        uint32_t* __restrict__ nbr) {
+  __shared__ unsigned long long sk[ROW_SORT_MAX];
+  for (uint32_t q = blockIdx.x; q < ncells; q += gridDim.x) {
+    const uint64_t b = off[q], e = off[q + 1];
+    const int len = (int)(e - b);
+    if (len < 2 || len > ROW_SORT_MAX) continue;
+    int P = 1;
+    while (P < len) P <<= 1;
+    const uint64_t kq = cell_key[q];
+    const float inv = 1.0f / (float)g.eps2;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      unsigned long long v = ~0ull;
+      if (i < len) {
+        const uint32_t h = nbr[b + i];
+        const uint64_t kh = cell_key[h];
+        uint64_t acc = 0;
+        for (int k = 0; k < g.d; ++k) {
+          const uint32_t x = cell_coord(kq, g, k), y = cell_coord(kh, g, k);
+          acc += gap_term(x > y ? x - y : y - x, g);
+        }
+        const uint32_t rank = (uint32_t)fminf((float)acc * inv * 2147483647.0f, 4294967295.0f);
+        v = ((unsigned long long)rank << 32) | h;
+      }
+      sk[i] = v;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long a = sk[i], c2 = sk[ixj];
+            const bool up = (i & k) == 0;
+            if ((a > c2) == up) { sk[i] = c2; sk[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) nbr[b + i] = (uint32_t)sk[i];
+    __syncthreads();
+  }
+}
+
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
                     uint64_t** nbr_off, uint32_t** nbr, uint64_t* total) {
   uint64_t* code0 = c.alloc<uint64_t>(ncells);
@@ -285,6 +416,8 @@ void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t nce
   uint32_t* list = c.alloc<uint32_t>(*total + 1);
   tree_query_kernel<<<grid, 128, 0, c.st>>>(1, cell_key, mcell, ncells, g, P2, nodes, nullptr, off,
                                             list);
+  c.launched();
+  sort_rows_kernel<<<grid_for(ncells, 1, c.sms * 8), 256, 0, c.st>>>(cell_key, ncells, g, off, list);
   c.launched();
   *nbr_off = off;
   *nbr = list;
