@@ -273,23 +273,36 @@ __global__ void cell_label_kernel(uint32_t nc, const uint32_t* __restrict__ core
   cell_label[g] = core_cnt[g] > 0 ? comp_min[uf_find(parent, g)] : 0xffffffffu;
 }
 
-// Scatter to input order: core[i], cluster[i]; count core points.
+// Scatter to input order: cluster[i] (one 4-byte store per point; a core flag
+// is implied by cluster >= 0); count core points.
 __global__ void write_points_kernel(uint32_t n, const uint32_t* __restrict__ idx,
                                     const uint8_t* __restrict__ core_s,
                                     const uint32_t* __restrict__ cell_of,
                                     const uint32_t* __restrict__ cell_label,
-                                    uint8_t* __restrict__ core_out, int32_t* __restrict__ cluster_out,
-                                    uint32_t* counters) {
+                                    int32_t* __restrict__ cluster_out, uint32_t* counters) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   bool is_core = false;
   if (j < n) {
-    const uint32_t i = idx[j];
     is_core = core_s[j];
-    core_out[i] = is_core;
-    cluster_out[i] = is_core ? (int32_t)cell_label[cell_of[j]] : -1;
+    cluster_out[idx[j]] = is_core ? (int32_t)cell_label[cell_of[j]] : -1;
   }
   uint32_t b = __ballot_sync(DB_FULL, is_core);
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(counters + 1, __popc(b));
+}
+
+// core[i] = cluster[i] >= 0, in input order (coalesced, 4 points per thread).
+__global__ void core_from_cluster_kernel(uint32_t n, const int32_t* __restrict__ cluster,
+                                         uint8_t* __restrict__ core) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t i = 4 * q;
+  if (i + 3 < n && (reinterpret_cast<uintptr_t>(core) & 3) == 0) {
+    const int4 v = reinterpret_cast<const int4*>(cluster)[q];
+    const uint32_t w = (uint32_t)(v.x >= 0) | ((uint32_t)(v.y >= 0) << 8) |
+                       ((uint32_t)(v.z >= 0) << 16) | ((uint32_t)(v.w >= 0) << 24);
+    reinterpret_cast<uint32_t*>(core)[q] = w;
+  } else {
+    for (uint32_t k = i; k < min(i + 4, n); ++k) core[k] = cluster[k] >= 0;
+  }
 }
 
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
@@ -305,7 +318,10 @@ void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* cor
                                                                    cell_label);
   c.launched();
   write_points_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
-      (uint32_t)n, idx, core_s, cv.cell_of, cell_label, core_out, cluster_out, counters);
+      (uint32_t)n, idx, core_s, cv.cell_of, cell_label, cluster_out, counters);
+  c.launched();
+  core_from_cluster_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, c.st>>>((uint32_t)n, cluster_out,
+                                                                                  core_out);
   c.launched();
 }
 

@@ -11,35 +11,18 @@
 
 namespace db {
 
-enum : uint8_t { CELL_DENSE = 0, CELL_COUNT = 1, CELL_NONCORE = 2, CELL_COUNT_WARP = 3 };
+// Candidate points of one query (sum of neighbour-cell sizes, ub[g]) at or
+// below this are scanned by one thread; above it by one warp.
+constexpr uint32_t WARP_CANDIDATES = 32;
 
-// Candidate points of one query (sum of neighbour-cell sizes) at or below this
-// are scanned by one thread; above it by one warp (SURVEY §8(a) a6 mapping).
-constexpr int64_t WARP_CANDIDATES = 32;
-
-__global__ void cell_class_kernel(CellsView cv, int64_t min_pts, uint8_t* __restrict__ cls) {
-  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= cv.ncells) return;
-  const int64_t cnt = cv.cell_start[g + 1] - cv.cell_start[g];
-  if (cnt >= min_pts) { cls[g] = CELL_DENSE; return; }
-  // upper bound |g| + sum_h |h|: below minPts no point of g can be core
-  int64_t ub = cnt;
-  const int64_t cap = cnt + max(min_pts, WARP_CANDIDATES + 1);
-  for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && ub < cap; ++t) {
-    uint32_t h = cv.nbr[t];
-    ub += cv.cell_start[h + 1] - cv.cell_start[h];
-  }
-  if (ub < min_pts) cls[g] = CELL_NONCORE;
-  else cls[g] = (ub - cnt > WARP_CANDIDATES) ? CELL_COUNT_WARP : CELL_COUNT;
-}
-
-// Thread per sorted point: dense / pruned cells are decided from the class;
-// queries with few candidates count in the thread; the others are queued for
-// the warp kernel.
+// Thread per sorted point. With cnt = |g| and ub = sum of the neighbours'
+// sizes (from the neighbour stage): cnt >= minPts -> core (dense cell);
+// cnt + ub < minPts -> not core without any distance test (the count can
+// only be lower); otherwise count, here if ub is small, else queue the point
+// for the warp kernel.
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const uint8_t* __restrict__ cls,
-                                                        const int32_t* __restrict__ Ps, uint32_t n,
-                                                        int64_t min_pts, uint32_t clampc,
+__global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+                                                        uint32_t n, int64_t min_pts, uint32_t clampc,
                                                         uint64_t eps2, uint8_t* __restrict__ core_s,
                                                         uint32_t* __restrict__ queue,
                                                         uint32_t* __restrict__ qcount) {
@@ -47,15 +30,18 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const uint
   bool enqueue = false;
   if (j < n) {
     const uint32_t g = cv.cell_of[j];
-    const uint8_t c = cls[g];
-    if (c == CELL_COUNT_WARP) {
+    const int64_t cnt = cv.cell_start[g + 1] - cv.cell_start[g];
+    const uint32_t ub = cv.ub[g];
+    if (cnt >= min_pts) {
+      core_s[j] = 1;
+    } else if (cnt + (int64_t)ub < min_pts) {
+      core_s[j] = 0;
+    } else if (ub > WARP_CANDIDATES) {
       enqueue = true;
-    } else if (c != CELL_COUNT) {
-      core_s[j] = c == CELL_DENSE;
     } else {
       int32_t p[D], q[D];
       PtLoad<D>::load(Ps, j, p);
-      int64_t count = cv.cell_start[g + 1] - cv.cell_start[g];
+      int64_t count = cnt;
       for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && count < min_pts; ++t) {
         const uint32_t h = cv.nbr[t];
         const uint32_t e = cv.cell_start[h + 1];
@@ -137,15 +123,12 @@ __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const
 
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
                int64_t min_pts, bool wide, uint8_t* core_s) {
-  uint8_t* cls = c.alloc<uint8_t>(cv.ncells);
   uint32_t* queue = c.alloc<uint32_t>(n);
   uint32_t* qcount = c.alloc<uint32_t>(1);
   c.zero(qcount, sizeof(uint32_t));
-  cell_class_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(cv, min_pts, cls);
-  c.launched();
   dispatch(g.D, wide, [&]<int D, bool W>() {
     mark_core_kernel<D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
-        cv, cls, Ps, (uint32_t)n, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
+        cv, Ps, (uint32_t)n, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
     c.launched();
     mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts,
                                                                g.clampc, g.eps2, core_s);

@@ -209,16 +209,15 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   const bool tree = (flags & DBSCAN_F_FORCE_TREE) || (d >= 4 && !(flags & DBSCAN_F_FORCE_STENCIL));
   uint64_t* nbr_off;
   uint32_t* nbr;
+  uint32_t* ub;
   uint64_t nbr_total = 0;
   bool dense_dir = false;
-  if (!tree) {
-    tm.stage(DBSCAN_STAGE_NEIGHBORS);
-    neighbors_stencil(c, g, cell_key, ncells, n, &nbr_off, &nbr, &nbr_total, &dense_dir);
-  } else {
-    tm.stage(DBSCAN_STAGE_NEIGHBORS);
-    neighbors_tree(c, g, cell_key, ncells, &nbr_off, &nbr, &nbr_total);
-  }
-  CellsView cv{ncells, cell_start, cell_key, cell_of, nbr_off, nbr};
+  tm.stage(DBSCAN_STAGE_NEIGHBORS);
+  if (!tree)
+    neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir);
+  else
+    neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total);
+  CellsView cv{ncells, cell_start, cell_key, cell_of, nbr_off, nbr, ub};
 
   // device counters: [0] core cells, [1] mixed cells, [2] clusters, [3] core points
   uint32_t* cnt32 = c.alloc<uint32_t>(4);
@@ -235,29 +234,42 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   tm.stage(DBSCAN_STAGE_COMPACT);
   uint32_t* core_cnt = c.alloc<uint32_t>(ncells);
   compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
+  const uint32_t core_cells = c.read(cnt32);
 
-  // ---- a8: ClusterCore
-  tm.stage(DBSCAN_STAGE_CLUSTER);
-  uint32_t* parent = c.alloc<uint32_t>(ncells);
-  const uint64_t npairs = cluster_core(c, g, cv, Ps, core_cnt, wide,
-                                       !(flags & DBSCAN_F_NO_WAVES), parent, cnt64);
-
-  // ---- a9: labels, scattered to input order
-  tm.stage(DBSCAN_STAGE_LABELS);
   uint8_t* core_d = dev_io ? out->core : c.alloc<uint8_t>(n);
   int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
   int64_t* off_d = dev_io ? out->border_off : c.alloc<int64_t>((size_t)n + 1);
-  uint32_t* cell_label = c.alloc<uint32_t>(ncells);
-  labels(c, cv, sidx, core_s, core_cnt, parent, n, cell_label, core_d, cluster_d, cnt32 + 2);
+  uint64_t npairs = 0;
+  int64_t nnz = 0;
+  if (core_cells == 0) {
+    // no core point: no cluster, every point is noise
+    tm.stage(DBSCAN_STAGE_LABELS);
+    DB_CUDA(cudaMemsetAsync(core_d, 0, (size_t)n, st));
+    DB_CUDA(cudaMemsetAsync(cluster_d, 0xff, sizeof(int32_t) * (size_t)n, st));
+    DB_CUDA(cudaMemsetAsync(off_d, 0, sizeof(int64_t) * (size_t)(n + 1), st));
+    out->border_ids = (int32_t*)out_alloc(4, &priv->border_ids);
+  } else {
+    // ---- a8: ClusterCore
+    tm.stage(DBSCAN_STAGE_CLUSTER);
+    uint32_t* parent = c.alloc<uint32_t>(ncells);
+    npairs = cluster_core(c, g, cv, Ps, core_cnt, wide, !(flags & DBSCAN_F_NO_WAVES), parent, cnt64);
 
-  // ---- a10: ClusterBorder
-  tm.stage(DBSCAN_STAGE_BORDER);
-  const int64_t nnz = border_count(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide,
-                                   off_d, cnt64 + 1);
-  out->border_ids = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
-  int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
-  if (nnz > 0)
-    border_fill(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, ids_d);
+    // ---- a9: labels, scattered to input order
+    tm.stage(DBSCAN_STAGE_LABELS);
+    uint32_t* cell_label = c.alloc<uint32_t>(ncells);
+    labels(c, cv, sidx, core_s, core_cnt, parent, n, cell_label, core_d, cluster_d, cnt32 + 2);
+
+    // ---- a10: ClusterBorder
+    tm.stage(DBSCAN_STAGE_BORDER);
+    nnz = border_count(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, cnt64 + 1);
+    out->border_ids = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
+    int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
+    if (nnz > 0)
+      border_fill(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, ids_d);
+    if (!dev_io && nnz > 0)
+      DB_CUDA(cudaMemcpyAsync(out->border_ids, ids_d, sizeof(int32_t) * (size_t)nnz,
+                              cudaMemcpyDeviceToHost, st));
+  }
 
   if (!dev_io) {
     DB_CUDA(cudaMemcpyAsync(out->core, core_d, (size_t)n, cudaMemcpyDeviceToHost, st));
@@ -265,9 +277,6 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
                             cudaMemcpyDeviceToHost, st));
     DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1),
                             cudaMemcpyDeviceToHost, st));
-    if (nnz > 0)
-      DB_CUDA(cudaMemcpyAsync(out->border_ids, ids_d, sizeof(int32_t) * (size_t)nnz,
-                              cudaMemcpyDeviceToHost, st));
   }
   uint32_t h32[4];
   unsigned long long h64[2];

@@ -27,6 +27,7 @@ struct Ctx {
   int64_t launches = 0;
   int sms = 148;
   uint32_t* dense_dir = nullptr;  // dense cell directory, when built
+  uint64_t dense_lat[3] = {0, 0, 0};
 
   template <typename T>
   T* alloc(size_t count) {
@@ -87,11 +88,14 @@ uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** ta
 
 // ---- neighbors.cu (a5) ----
 // neighbour-cell CSR excluding the cell itself: nbr_off[ncells+1] (device), nbr list.
+// Both build the CSR and ub[g] = sum of the neighbours' sizes (MarkCore bound).
 // d <= 3 (or forced): builds a dense cell directory or a hash table itself.
-void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells, int64_t n,
-                       uint64_t** nbr_off, uint32_t** nbr, uint64_t* total, bool* dense);
-void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
-                    uint64_t** nbr_off, uint32_t** nbr, uint64_t* total);
+void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
+                       uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,
+                       uint32_t** ub, uint64_t* total, bool* dense);
+void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
+                    uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub,
+                    uint64_t* total);
 // host: exact stencil offsets (Delta != 0 with sum gap^2 <= eps^2), flat [count*d] int8
 std::vector<int8_t> stencil_offsets(const Geo& g);
 
@@ -103,6 +107,7 @@ struct CellsView {
   const uint32_t* cell_of;
   const uint64_t* nbr_off;
   const uint32_t* nbr;
+  const uint32_t* ub;  // sum of neighbour-cell sizes (saturating)
 };
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
                int64_t min_pts, bool wide, uint8_t* core_s);

@@ -57,72 +57,122 @@ std::vector<int8_t> stencil_offsets(const Geo& g) {
 }
 
 // ------------------------------------------------------------------ stencil
-// Thread per cell, loop over the offsets: the 32 lanes of a warp are 32
-// consecutive cells in key order (mostly one column, consecutive last-axis
-// coordinates) probing the same offset, so their keys are consecutive too and
-// the locality-preserving slot hash (common.cuh) puts them in the same or
-// adjacent 128-byte slot groups: the probes of one warp instruction coalesce.
-// Each offset carries its packed key delta (sum_k delta_k << shift_k); the
-// per-axis range check keeps the two's-complement add exact.
-// DENSE: cells are looked up in a dense directory over the whole lattice
-// (chosen when the lattice has at most DENSE_PER_POINT cells per input point),
-// indexed like the key (axis 0 major), so a lookup is one coalesced load.
+// Offsets live in shared memory as {delta_0..2, packed key (or directory)
+// delta}. Two mappings:
+//  * thread per cell (many cells): the 32 lanes of a warp are 32 consecutive
+//    cells in key order (mostly one column, consecutive last-axis coordinates)
+//    probing the same offset, so their keys are consecutive and the probes of
+//    one warp instruction coalesce (locality-preserving slot hash, or the
+//    dense directory);
+//  * warp per cell (few cells, e.g. seed-spreader data): lanes over offsets,
+//    so a handful of cells still fill the machine.
+// DENSE: a directory over the lattice padded by R cells on every side (cell
+// id or ~0), indexed like the key (axis 0 major), chosen when the padded
+// lattice has at most DENSE_PER_POINT cells per point: one load per probe and
+// no range checks (out-of-range neighbours land in the padding).
+// The count pass also accumulates ub[g] = sum of the neighbours' sizes, the
+// MarkCore upper bound (core.cu), saturating at 2^32-1.
 constexpr int MAX_SMEM_OFFS = 2048;
 constexpr int64_t DENSE_PER_POINT = 8;
+constexpr uint32_t WARP_PER_CELL_BELOW = 1u << 15;
+
+struct __align__(16) StencilOff {
+  int8_t d[8];      // per-axis lattice offset
+  long long delta;  // packed-key (or padded directory) offset
+};
 
 struct Lattice {
   uint64_t stride[3];
 };
 
-template <bool DENSE>
-__global__ void __launch_bounds__(256) nbr_stencil_kernel(
-    int fill, const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
-    const int8_t* __restrict__ offs, const int64_t* __restrict__ delta, int noffs,
-    const Slot* __restrict__ T, uint64_t mask, const uint32_t* __restrict__ dir, Lattice lat,
-    uint32_t* __restrict__ cnt, const uint64_t* __restrict__ off, uint32_t* __restrict__ nbr) {
-  __shared__ int8_t s_off[MAX_SMEM_OFFS * 3];
-  __shared__ int64_t s_delta[MAX_SMEM_OFFS];
-  const bool smem = noffs <= MAX_SMEM_OFFS && g.d <= 3;
-  if (smem) {
-    for (int i = threadIdx.x; i < noffs * g.d; i += blockDim.x) s_off[i] = offs[i];
-    for (int i = threadIdx.x; i < noffs; i += blockDim.x) s_delta[i] = delta[i];
-  }
-  __syncthreads();
-  const uint32_t cell = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cell >= ncells) return;
-  const uint64_t key = cell_key[cell];
-  uint32_t cc[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) cc[k] = k < g.d ? cell_coord(key, g, k) : 0;
-  uint64_t base = key;
+template <int DIM, bool DENSE>
+__device__ __forceinline__ uint32_t probe(const StencilOff& o, const uint32_t* cc, uint64_t base,
+                                          const Geo& g, const Slot* __restrict__ T, uint64_t mask,
+                                          const uint32_t* __restrict__ dir) {
   if constexpr (DENSE) {
-    base = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if (k < g.d) base += (uint64_t)cc[k] * lat.stride[k];
-  }
-  uint64_t wpos = fill ? off[cell] : 0;
-  uint32_t total = 0;
-  for (int t = 0; t < noffs; ++t) {
+    return __ldg(dir + (base + (uint64_t)o.delta));
+  } else {
     bool ok = true;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (k < g.d) {
-        const int64_t q = (int64_t)cc[k] + (smem ? s_off[t * g.d + k] : offs[t * g.d + k]);
+    for (int k = 0; k < (DIM ? DIM : 8); ++k) {
+      if (DIM || k < g.d) {
+        const int64_t q = (int64_t)cc[k] + o.d[k];
         ok &= (q >= 0) & (q <= (int64_t)g.maxc[k]);
       }
     }
-    if (!ok) continue;
-    const uint64_t nkey = base + (uint64_t)(smem ? s_delta[t] : delta[t]);
-    uint32_t id;
-    if constexpr (DENSE) id = __ldg(dir + nkey);
-    else id = hash_lookup(T, mask, nkey);
-    if (id == 0xffffffffu) continue;
-    if (fill) nbr[wpos] = id;
-    ++wpos;
-    ++total;
+    if (!ok) return 0xffffffffu;
+    return hash_lookup(T, mask, base + (uint64_t)o.delta);
   }
-  if (!fill) cnt[cell] = total;
+}
+
+template <int DIM, bool DENSE, bool WARP>
+__global__ void __launch_bounds__(256) nbr_stencil_kernel(
+    int fill, const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
+    const StencilOff* __restrict__ offs, int noffs, const Slot* __restrict__ T, uint64_t mask,
+    const uint32_t* __restrict__ dir, Lattice lat, const uint32_t* __restrict__ cell_start,
+    uint32_t* __restrict__ cnt, uint32_t* __restrict__ ub, const uint64_t* __restrict__ off,
+    uint32_t* __restrict__ nbr) {
+  __shared__ StencilOff s_offs[MAX_SMEM_OFFS];
+  const bool in_smem = noffs <= MAX_SMEM_OFFS;
+  if (in_smem)
+    for (int i = threadIdx.x; i < noffs; i += blockDim.x) s_offs[i] = offs[i];
+  __syncthreads();
+  const StencilOff* O = in_smem ? s_offs : offs;
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = WARP ? (gridDim.x * blockDim.x) >> 5 : gridDim.x * blockDim.x;
+  uint32_t cell = WARP ? (blockIdx.x * blockDim.x + threadIdx.x) >> 5 : blockIdx.x * blockDim.x + threadIdx.x;
+  for (; cell < ncells; cell += stride) {
+    const uint64_t key = cell_key[cell];
+    uint32_t cc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cc[k] = (k < (DIM ? DIM : g.d)) ? cell_coord(key, g, k) : 0;
+    uint64_t base = key;
+    if constexpr (DENSE) {
+      base = 0;
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) base += (uint64_t)(cc[k] + g.R) * lat.stride[k];
+    }
+    uint64_t wpos = fill ? off[cell] : 0;
+    uint32_t total = 0;
+    uint64_t sum = 0;
+    if constexpr (WARP) {
+      const uint32_t lt = lanemask_lt();
+      for (int t0 = 0; t0 < noffs; t0 += 32) {
+        const int t = t0 + lane;
+        uint32_t id = 0xffffffffu;
+        if (t < noffs) id = probe<DIM, DENSE>(O[t], cc, base, g, T, mask, dir);
+        const bool found = id != 0xffffffffu;
+        const uint32_t b = __ballot_sync(DB_FULL, found);
+        if (fill) {
+          if (found) nbr[wpos + __popc(b & lt)] = id;
+        } else if (found) {
+          sum += cell_start[id + 1] - cell_start[id];
+        }
+        wpos += __popc(b);
+        total += __popc(b);
+      }
+      if (!fill) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(DB_FULL, sum, o);
+        if (lane == 0) {
+          cnt[cell] = total;
+          ub[cell] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+        }
+      }
+    } else {
+      for (int t = 0; t < noffs; ++t) {
+        const uint32_t id = probe<DIM, DENSE>(O[t], cc, base, g, T, mask, dir);
+        if (id == 0xffffffffu) continue;
+        if (fill) nbr[wpos++] = id;
+        else sum += cell_start[id + 1] - cell_start[id];
+        ++total;
+      }
+      if (!fill) {
+        cnt[cell] = total;
+        ub[cell] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+      }
+    }
+  }
 }
 
 __global__ void dense_fill_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
@@ -131,22 +181,23 @@ __global__ void dense_fill_kernel(const uint64_t* __restrict__ cell_key, uint32_
   if (i >= ncells) return;
   const uint64_t key = cell_key[i];
   uint64_t lin = 0;
-  for (int k = 0; k < g.d; ++k) lin += (uint64_t)cell_coord(key, g, k) * lat.stride[k];
+  for (int k = 0; k < g.d; ++k) lin += (uint64_t)(cell_coord(key, g, k) + g.R) * lat.stride[k];
   dir[lin] = i;
 }
 
-void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells, int64_t n,
-                       uint64_t** nbr_off, uint32_t** nbr, uint64_t* total, bool* dense_out) {
+void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
+                       uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,
+                       uint32_t** ub_out, uint64_t* total, bool* dense_out) {
   std::vector<int8_t> offs = stencil_offsets(g);
   const int noffs = (int)(offs.size() / g.d);
-  // dense directory when the lattice is small relative to n (d <= 3 only)
+  // dense directory when the padded lattice is small relative to n (d <= 3 only)
   Lattice lat{{0, 0, 0}};
   bool dense = false;
   if (g.d <= 3) {
     unsigned __int128 vol = 1;
     for (int k = g.d - 1; k >= 0; --k) {
       lat.stride[k] = (uint64_t)vol;
-      vol *= (unsigned __int128)g.maxc[k] + 1;
+      vol *= (unsigned __int128)g.maxc[k] + 1 + 2 * (unsigned __int128)g.R;
     }
     dense = vol <= (unsigned __int128)(DENSE_PER_POINT * n + (1 << 20));
     if (dense) {
@@ -156,35 +207,53 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t 
       dense_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, lat, dir);
       c.launched();
       c.dense_dir = dir;
+      c.dense_lat[0] = lat.stride[0]; c.dense_lat[1] = lat.stride[1]; c.dense_lat[2] = lat.stride[2];
     }
   }
   Slot* T = nullptr;
   uint64_t mask = 0;
   if (!dense) mask = build_hash(c, cell_key, ncells, &T);
   *dense_out = dense;
-  std::vector<int64_t> delta((size_t)noffs + 1, 0);
+  std::vector<StencilOff> so((size_t)noffs + 1);
   for (int t = 0; t < noffs; ++t) {
     int64_t dl = 0;
-    for (int k = 0; k < g.d; ++k)
-      dl += (int64_t)offs[(size_t)t * g.d + k] *
-            (dense ? (int64_t)lat.stride[k] : (int64_t)(1ull << g.shift[k]));
-    delta[t] = dl;
+    StencilOff& o = so[t];
+    for (int k = 0; k < 8; ++k) o.d[k] = 0;
+    for (int k = 0; k < g.d; ++k) {
+      const int8_t v = offs[(size_t)t * g.d + k];
+      o.d[k] = v;
+      dl += (int64_t)v * (dense ? (int64_t)lat.stride[k] : (int64_t)(1ull << g.shift[k]));
+    }
+    o.delta = dl;
   }
-  int8_t* doffs = c.alloc<int8_t>(offs.size() + 1);
-  int64_t* ddelta = c.alloc<int64_t>(delta.size());
-  if (!offs.empty())
-    DB_CUDA(cudaMemcpyAsync(doffs, offs.data(), offs.size(), cudaMemcpyHostToDevice, c.st));
-  DB_CUDA(cudaMemcpyAsync(ddelta, delta.data(), sizeof(int64_t) * delta.size(), cudaMemcpyHostToDevice, c.st));
+  StencilOff* doffs = c.alloc<StencilOff>(so.size());
+  DB_CUDA(cudaMemcpyAsync(doffs, so.data(), sizeof(StencilOff) * so.size(), cudaMemcpyHostToDevice, c.st));
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
+  uint32_t* ub = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
-  const unsigned grid = grid_for(ncells, 256, 1 << 30);
+  const bool warp = ncells < WARP_PER_CELL_BELOW;
+  const unsigned grid = warp ? grid_for((int64_t)ncells * 32, 256, 1 << 30) : grid_for(ncells, 256, 1 << 30);
   auto launch = [&](int fill, uint32_t* list) {
-    if (dense)
-      nbr_stencil_kernel<true><<<grid, 256, 0, c.st>>>(fill, cell_key, ncells, g, doffs, ddelta, noffs,
-                                                         T, mask, c.dense_dir, lat, cnt, off, list);
-    else
-      nbr_stencil_kernel<false><<<grid, 256, 0, c.st>>>(fill, cell_key, ncells, g, doffs, ddelta, noffs,
-                                                          T, mask, nullptr, lat, cnt, off, list);
+    auto go = [&](auto Dc, auto Dn, auto Wp) {
+      constexpr int DIM = decltype(Dc)::value;
+      constexpr bool DN = decltype(Dn)::value, WP = decltype(Wp)::value;
+      nbr_stencil_kernel<DIM, DN, WP><<<grid, 256, 0, c.st>>>(fill, cell_key, ncells, g, doffs, noffs, T,
+                                                              mask, c.dense_dir, lat, cell_start, cnt, ub,
+                                                              off, list);
+    };
+    using F = std::false_type;
+    using Tt = std::true_type;
+    auto by_mode = [&](auto Dc) {
+      if (dense) { if (warp) go(Dc, Tt(), Tt()); else go(Dc, Tt(), F()); }
+      else { if (warp) go(Dc, F(), Tt()); else go(Dc, F(), F()); }
+    };
+    if (g.d == 1) by_mode(std::integral_constant<int, 1>());
+    else if (g.d == 2) by_mode(std::integral_constant<int, 2>());
+    else if (g.d == 3) by_mode(std::integral_constant<int, 3>());
+    else {  // forced stencil, d >= 4: hash only, runtime d
+      if (warp) go(std::integral_constant<int, 0>(), F(), Tt());
+      else go(std::integral_constant<int, 0>(), F(), F());
+    }
     c.launched();
   };
   launch(0, nullptr);
@@ -194,6 +263,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t 
   launch(1, list);
   *nbr_off = off;
   *nbr = list;
+  *ub_out = ub;
 }
 
 // ------------------------------------------------------------------ cell tree
@@ -281,7 +351,8 @@ __global__ void tree_build_kernel(const uint64_t* __restrict__ cell_key, const u
 
 __global__ void __launch_bounds__(128) tree_query_kernel(
     int fill, const uint64_t* __restrict__ cell_key, const uint32_t* __restrict__ mcell,
-    uint32_t ncells, Geo g, uint32_t P2, const Box* __restrict__ nodes, uint32_t* __restrict__ cnt,
+    uint32_t ncells, Geo g, uint32_t P2, const Box* __restrict__ nodes,
+    const uint32_t* __restrict__ cell_start, uint32_t* __restrict__ cnt, uint32_t* __restrict__ ub,
     const uint64_t* __restrict__ off, uint32_t* __restrict__ nbr) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -293,6 +364,7 @@ __global__ void __launch_bounds__(128) tree_query_kernel(
     for (int k = 0; k < 8; ++k) cq[k] = k < g.d ? cell_coord(key, g, k) : 0;
     uint64_t wpos = fill ? off[q] : 0;
     uint32_t total = 0;
+    uint64_t sum = 0;
     uint32_t stack[64];
     int sp = 0;
     stack[sp++] = 0;
@@ -318,6 +390,7 @@ __global__ void __launch_bounds__(128) tree_query_kernel(
         }
         uint32_t b = __ballot_sync(DB_FULL, found);
         if (fill && found) nbr[wpos + __popc(b & lt)] = h;
+        if (!fill && found) sum += cell_start[h + 1] - cell_start[h];
         wpos += __popc(b);
         total += __popc(b);
       } else {
@@ -329,7 +402,14 @@ __global__ void __launch_bounds__(128) tree_query_kernel(
         }
       }
     }
-    if (!fill && lane == 0) cnt[q] = total;
+    if (!fill) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(DB_FULL, sum, o);
+      if (lane == 0) {
+        cnt[q] = total;
+        ub[q] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+      }
+    }
   }
 }
 
@@ -385,8 +465,9 @@ __global__ void __launch_bounds__(256) sort_rows_kernel(const uint64_t* __restri
   }
 }
 
-void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t ncells,
-                    uint64_t** nbr_off, uint32_t** nbr, uint64_t* total) {
+void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
+                    uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub_out,
+                    uint64_t* total) {
   uint64_t* code0 = c.alloc<uint64_t>(ncells);
   uint64_t* code1 = c.alloc<uint64_t>(ncells);
   uint32_t* id0 = c.alloc<uint32_t>(ncells);
@@ -406,21 +487,23 @@ void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, uint32_t nce
                                                                    nodes, flags);
   c.launched();
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
+  uint32_t* ub = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
   const unsigned grid = grid_for((int64_t)ncells * 32, 128, c.sms * 32);
-  tree_query_kernel<<<grid, 128, 0, c.st>>>(0, cell_key, mcell, ncells, g, P2, nodes, cnt, nullptr,
-                                            nullptr);
+  tree_query_kernel<<<grid, 128, 0, c.st>>>(0, cell_key, mcell, ncells, g, P2, nodes, cell_start, cnt,
+                                            ub, nullptr, nullptr);
   c.launched();
   exclusive_scan_u32_u64(c, cnt, off, ncells);
   *total = c.read(off + ncells);
   uint32_t* list = c.alloc<uint32_t>(*total + 1);
-  tree_query_kernel<<<grid, 128, 0, c.st>>>(1, cell_key, mcell, ncells, g, P2, nodes, nullptr, off,
-                                            list);
+  tree_query_kernel<<<grid, 128, 0, c.st>>>(1, cell_key, mcell, ncells, g, P2, nodes, cell_start,
+                                            nullptr, nullptr, off, list);
   c.launched();
   sort_rows_kernel<<<grid_for(ncells, 1, c.sms * 8), 256, 0, c.st>>>(cell_key, ncells, g, off, list);
   c.launched();
   *nbr_off = off;
   *nbr = list;
+  *ub_out = ub;
 }
 
 }  // namespace db
