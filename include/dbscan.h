@@ -48,6 +48,9 @@ extern "C" {
 #define DBSCAN_F_FORCE_TREE   16u  /* neighbour cells by the cell tree for every d */
 #define DBSCAN_F_FORCE_WIDE   32u  /* 64-bit distance arithmetic even where 32-bit is exact */
 #define DBSCAN_F_NO_WAVES     64u  /* ClusterCore in one wave (ablation of the wave schedule) */
+#define DBSCAN_F_NO_SPARSE   128u  /* never take the cell-centric sparse-lattice path         */
+#define DBSCAN_F_FORCE_SPARSE 256u /* take the sparse path whenever d <= 3 and the lattice
+                                      directory fits (otherwise it is chosen by occupancy)   */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
@@ -77,6 +80,7 @@ extern "C" {
 #define DBSCAN_STAT_TREE          9  /* 1 if neighbour cells came from the cell tree      */
 #define DBSCAN_STAT_CELL_SIDE    10  /* integer cell side s                              */
 #define DBSCAN_STAT_DENSE_DIR    11  /* 1 if cells were found through a dense directory   */
+#define DBSCAN_STAT_SPARSE       12  /* 1 if the cell-centric sparse-lattice path ran       */
 #define DBSCAN_NSTATS            16
 
 typedef struct dbscan_result {

@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
                                                         CellsView cv, Geo g,
                                                         const int32_t* __restrict__ Ps,
                                                         const uint32_t* __restrict__ core_cnt,
-                                                        uint32_t* parent) {
+                                                        uint32_t* parent, uint32_t cap) {
   const int lane = threadIdx.x & 31;
-  const uint32_t m = *count;
+  const uint32_t m = min(*count, cap);
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += nwarps) {
     const uint2 p = list[i];
@@ -199,13 +199,25 @@ __global__ void uf_init_kernel(uint32_t* parent, uint32_t n) {
   if (i < n) parent[i] = i;
 }
 
+void uf_init(Ctx& c, uint32_t* parent, uint32_t n) {
+  uf_init_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(parent, n);
+  c.launched();
+}
+
+void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
+               uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide) {
+  dispatch(g.D, wide, [&]<int D, bool W>() {
+    bcp_large_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap);
+  });
+  c.launched();
+}
+
 uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                       const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
                       unsigned long long* tested) {
   const uint32_t nc = cv.ncells;
   const int nw = waves ? NWAVES : 1;
-  uf_init_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(parent, nc);
-  c.launched();
+  uf_init(c, parent, nc);
   uint32_t* cnt = c.alloc<uint32_t>((size_t)nw * nc);
   uint64_t* off = c.alloc<uint64_t>((size_t)nw * nc + 1);
   pair_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(0, nw, cv, g, core_cnt, cnt, nullptr,
@@ -239,10 +251,8 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
       bcp_small_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(small, ctr + 2 * w, cv, Ps, core_cnt,
                                                            parent, g.clampc, g.eps2);
       c.launched();
-      bcp_large_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(large, ctr + 2 * w + 1, cv, g, Ps,
-                                                           core_cnt, parent);
-      c.launched();
     });
+    bcp_large(c, g, cv, Ps, core_cnt, parent, large, ctr + 2 * w + 1, (uint32_t)npairs, wide);
   }
   return npairs;
 }

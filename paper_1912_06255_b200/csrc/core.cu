@@ -199,11 +199,16 @@ void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
   core_count_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(cv, core_s, min_pts,
                                                                           core_cnt, mixed, counters);
   c.launched();
+  partition_mixed(c, g, cv, mixed, counters + 1, Ps, idx, core_s, n);
+}
+
+void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* mixed,
+                     const uint32_t* nmixed, int32_t* Ps, uint32_t* idx, uint8_t* core_s, int64_t n) {
   int32_t* sP = c.alloc<int32_t>((size_t)n * g.D);
   uint32_t* sI = c.alloc<uint32_t>(n);
   auto go = [&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
-    partition_kernel<D><<<c.sms * 4, 128, 0, c.st>>>(cv, mixed, counters + 1, Ps, idx, core_s, sP, sI);
+    partition_kernel<D><<<c.sms * 4, 128, 0, c.st>>>(cv, mixed, nmixed, Ps, idx, core_s, sP, sI);
   };
   if (g.D == 2) go(std::integral_constant<int, 2>());
   else if (g.D == 4) go(std::integral_constant<int, 4>());

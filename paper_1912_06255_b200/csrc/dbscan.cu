@@ -205,36 +205,54 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   const uint32_t ncells =
       segment_and_gather(c, skeys, key64, sidx, dpts, n, g, Ps, cell_of, cell_start, cell_key);
 
-  // ---- a4-a5: hash + neighbour CSR
+  // ---- regime: CSR path (neighbour lists) or the cell-centric sparse path
   const bool tree = (flags & DBSCAN_F_FORCE_TREE) || (d >= 4 && !(flags & DBSCAN_F_FORCE_STENCIL));
-  uint64_t* nbr_off;
-  uint32_t* nbr;
-  uint32_t* ub;
-  uint64_t nbr_total = 0;
-  bool dense_dir = false;
-  tm.stage(DBSCAN_STAGE_NEIGHBORS);
-  if (!tree)
-    neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir);
-  else
-    neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total);
-  CellsView cv{ncells, cell_start, cell_key, cell_of, nbr_off, nbr, ub};
+  const bool sparse = !tree && !(flags & DBSCAN_F_NO_SPARSE) && !(flags & DBSCAN_F_FORCE_STENCIL) &&
+                      sparse_applicable(g, n, ncells, flags & DBSCAN_F_FORCE_SPARSE);
+  const bool waves = !(flags & DBSCAN_F_NO_WAVES);
 
   // device counters: [0] core cells, [1] mixed cells, [2] clusters, [3] core points
   uint32_t* cnt32 = c.alloc<uint32_t>(4);
   unsigned long long* cnt64 = c.alloc<unsigned long long>(2);  // [0] tested pairs, [1] border pts
   c.zero(cnt32, 16);
   c.zero(cnt64, 16);
-
-  // ---- a6: MarkCore
-  tm.stage(DBSCAN_STAGE_MARKCORE);
   uint8_t* core_s = c.alloc<uint8_t>(n);
-  mark_core(c, g, cv, Ps, n, min_pts, wide, core_s);
-
-  // ---- a7: core-first compaction
-  tm.stage(DBSCAN_STAGE_COMPACT);
   uint32_t* core_cnt = c.alloc<uint32_t>(ncells);
-  compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
-  const uint32_t core_cells = c.read(cnt32);
+
+  uint64_t nbr_total = 0;
+  bool dense_dir = false;
+  CellsView cv{ncells, cell_start, cell_key, cell_of, nullptr, nullptr, nullptr};
+  SparseOut so;
+  struct SpGuard { SparseOut* o; ~SpGuard() { sparse_release(o); } } sp_guard{&so};
+  uint32_t core_cells = 0;
+  if (sparse) {
+    // ---- a4 + a6 + a7 on the rank directory
+    tm.stage(DBSCAN_STAGE_MARKCORE);
+    so.counters = c.alloc<uint32_t>(4);
+    c.zero(so.counters, 16);
+    sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, waves, &so);
+    core_cells = c.read(so.counters);
+  } else {
+    // ---- a4-a5: cell lookup + neighbour CSR (+ MarkCore bound ub)
+    uint64_t* nbr_off;
+    uint32_t* nbr;
+    uint32_t* ub;
+    tm.stage(DBSCAN_STAGE_NEIGHBORS);
+    if (!tree)
+      neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir);
+    else
+      neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total);
+    cv.nbr_off = nbr_off;
+    cv.nbr = nbr;
+    cv.ub = ub;
+    // ---- a6: MarkCore
+    tm.stage(DBSCAN_STAGE_MARKCORE);
+    mark_core(c, g, cv, Ps, n, min_pts, wide, core_s);
+    // ---- a7: core-first compaction
+    tm.stage(DBSCAN_STAGE_COMPACT);
+    compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
+    core_cells = c.read(cnt32);
+  }
 
   uint8_t* core_d = dev_io ? out->core : c.alloc<uint8_t>(n);
   int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
@@ -252,7 +270,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     // ---- a8: ClusterCore
     tm.stage(DBSCAN_STAGE_CLUSTER);
     uint32_t* parent = c.alloc<uint32_t>(ncells);
-    npairs = cluster_core(c, g, cv, Ps, core_cnt, wide, !(flags & DBSCAN_F_NO_WAVES), parent, cnt64);
+    if (sparse) sparse_cluster(c, g, cv, Ps, core_cnt, wide, waves, parent, cnt64, &so);
+    else npairs = cluster_core(c, g, cv, Ps, core_cnt, wide, waves, parent, cnt64);
 
     // ---- a9: labels, scattered to input order
     tm.stage(DBSCAN_STAGE_LABELS);
@@ -261,11 +280,14 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
 
     // ---- a10: ClusterBorder
     tm.stage(DBSCAN_STAGE_BORDER);
-    nnz = border_count(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, cnt64 + 1);
+    if (sparse) nnz = sparse_border(c, g, cell_label, n, wide, off_d, cnt64 + 1, &so);
+    else nnz = border_count(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, cnt64 + 1);
     out->border_ids = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
     int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
-    if (nnz > 0)
-      border_fill(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, ids_d);
+    if (nnz > 0) {
+      if (sparse) sparse_border_fill(c, g, wide, off_d, ids_d, &so);
+      else border_fill(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, ids_d);
+    }
     if (!dev_io && nnz > 0)
       DB_CUDA(cudaMemcpyAsync(out->border_ids, ids_d, sizeof(int32_t) * (size_t)nnz,
                               cudaMemcpyDeviceToHost, st));
@@ -295,7 +317,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_KEY_BITS] = bits;
   out->stats[DBSCAN_STAT_SORT_PASSES] = passes;
   out->stats[DBSCAN_STAT_NBR_ENTRIES] = (int64_t)nbr_total;
-  out->stats[DBSCAN_STAT_CORE_CELLS] = h32[0];
+  out->stats[DBSCAN_STAT_CORE_CELLS] = core_cells;
   out->stats[DBSCAN_STAT_PAIRS] = (int64_t)npairs;
   out->stats[DBSCAN_STAT_PAIRS_TESTED] = (int64_t)h64[0];
   out->stats[DBSCAN_STAT_LAUNCHES] = c.launches;
@@ -303,6 +325,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_TREE] = tree;
   out->stats[DBSCAN_STAT_CELL_SIDE] = (int64_t)s;
   out->stats[DBSCAN_STAT_DENSE_DIR] = dense_dir;
+  out->stats[DBSCAN_STAT_SPARSE] = sparse;
   return DBSCAN_OK;
 }
 

@@ -68,6 +68,15 @@ struct Ctx {
 // out[0..n] = exclusive prefix sums of in[0..n-1]; out[n] = total.
 void exclusive_scan_u32_u64(Ctx& c, const uint32_t* in, uint64_t* out, int64_t n);
 void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n);
+void exclusive_scan_u32_u32(Ctx& c, const uint32_t* in, uint32_t* out, int64_t n);
+
+// ---- radix.cu (a2) ----
+// LSD passes over the low `passes` 8-bit digits; hist = [passes][256] global digit
+// histograms; the sorted pairs end in *ko/*vo (one of the two buffers).
+void radix_sort_pairs_u32(Ctx& c, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t n,
+                          int passes, const uint32_t* hist, uint32_t** ko, uint32_t** vo);
+void radix_sort_pairs_u64(Ctx& c, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint32_t n,
+                          int passes, const uint32_t* hist, uint64_t** ko, uint32_t** vo);
 
 // ---- grid.cu (a1-a4) ----
 void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, int32_t* lohi /*[16] device*/);
@@ -117,7 +126,35 @@ void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
                   uint8_t* core_s, int64_t n, int64_t min_pts, uint32_t* core_cnt,
                   uint32_t* counters /*device [2], zeroed*/);
 
+// stable core-first partition of the listed cells (count on the device)
+void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* mixed,
+                     const uint32_t* nmixed, int32_t* Ps, uint32_t* idx, uint8_t* core_s, int64_t n);
+
+// ---- sparse.cu (cell-centric path for sparse lattices, d <= 3) ----
+constexpr uint64_t SPARSE_MEAN_PER_CELL = 4;  // n / ncells at or below: sparse path
+struct SparseOut {
+  uint32_t* counters = nullptr;  // device [4]: core cells, non-core cells, large pairs, mixed
+  void* stash = nullptr;         // kernel arguments kept between the stages
+};
+bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);
+// a4 + a6 + a7: rank directory, core flags, core-first compaction, core_cnt
+void sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
+                     uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
+                     bool waves, SparseOut* o);
+void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+                    const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
+                    unsigned long long* tested, SparseOut* o);
+int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, int64_t n, bool wide,
+                      int64_t* border_off, unsigned long long* nborder, SparseOut* o);
+void sparse_border_fill(Ctx& c, const Geo& g, bool wide, const int64_t* border_off,
+                        int32_t* border_ids, SparseOut* o);
+void sparse_release(SparseOut* o);
+
 // ---- cluster.cu (a8, a9) ----
+void uf_init(Ctx& c, uint32_t* parent, uint32_t n);
+// warp-per-pair BCP over list[0 .. min(*count, cap)) with Link on success
+void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
+               uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide);
 // returns the number of candidate pairs; *tested (device) counts pairs that
 // survived the Find check of their wave.
 uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,

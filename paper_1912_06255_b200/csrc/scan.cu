@@ -85,3 +85,9 @@ void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n)
 }
 
 }  // namespace db
+
+namespace db {
+void exclusive_scan_u32_u32(Ctx& c, const uint32_t* in, uint32_t* out, int64_t n) {
+  scan_impl<uint32_t>(c, in, out, n);
+}
+}  // namespace db

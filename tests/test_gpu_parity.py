@@ -94,7 +94,9 @@ def test_random_small_vs_o1(oracle_lib):
 
 
 @pytest.mark.parametrize("flags", [pkg.F_FORCE_WIDE, pkg.F_FORCE_TREE, pkg.F_NO_WAVES,
-                                   pkg.F_FORCE_WIDE | pkg.F_FORCE_TREE | pkg.F_NO_WAVES])
+                                   pkg.F_FORCE_WIDE | pkg.F_FORCE_TREE | pkg.F_NO_WAVES,
+                                   pkg.F_FORCE_SPARSE, pkg.F_NO_SPARSE,
+                                   pkg.F_FORCE_SPARSE | pkg.F_FORCE_WIDE | pkg.F_NO_WAVES])
 def test_flag_variants_vs_o1(oracle_lib, flags):
     for k, (pts, eps, mp) in enumerate(_instances(200 + flags, 120, dmax=8)):
         r = run_or_erange(pts, eps, mp, flags)
@@ -202,3 +204,16 @@ def test_stream_and_stats():
     assert r.stage_ms["total"] > 0
     assert r.stats["launches"] > 10
     assert r.stats["ncells"] > 0 and r.n_core + r.n_border + r.n_noise == len(pts)
+
+
+@pytest.mark.parametrize("flags", [0, pkg.F_NO_SPARSE])
+def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
+    """Both the cell-centric sparse path and the CSR path on sparse lattices
+    (1-8 points per cell), 1D-3D, with border points in several clusters."""
+    for d, n, hi, eps, mp in [(3, 150_000, 12_000, 500, 8), (2, 120_000, 30_000, 150, 5),
+                              (1, 50_000, 200_000, 3, 3), (3, 60_000, 4_000, 300, 20)]:
+        pts = datagen.uniform(n, d, hi, d + n)
+        r = gpu(pts, eps, mp, flags)
+        if flags == 0 and d == 3 and hi == 12_000:
+            assert r.stats["sparse"] == 1
+        assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"d={d} flags={flags}")
