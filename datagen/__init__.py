@@ -33,7 +33,8 @@ def sha256_prefix(pts: np.ndarray, k: int = 16) -> str:
 
 def seed_spreader(n: int, d: int, L: float, seed: int, p_step: float,
                   noise_frac: float = 0.0, radius: float = 100.0,
-                  shift: float = 50.0, per_step: int = 100) -> np.ndarray:
+                  shift: float = 50.0, per_step: int = 100,
+                  varden: bool = False) -> np.ndarray:
     """Gan-Tao style seed spreader (BASELINE.json configs[1..3]).
 
     Draw order: restart flags, segment starts, shifts,
@@ -41,6 +42,13 @@ def seed_spreader(n: int, d: int, L: float, seed: int, p_step: float,
     A spreader emits `per_step` points uniform in a ball of `radius` around
     its position, then moves `shift` in a uniformly random direction; with
     probability `p_step` per step it restarts at a uniform location.
+
+    varden=True gives SS-varden (variable-density clusters):
+    each walk segment scales its ball radius and shift by 2^j, j uniform in
+    {-1, 0, 1, 2}, so clusters differ 64x in density. The scales are drawn
+    after every other draw (the SS-simden draws are unchanged). The paper
+    names the generator (Gan and Tao's) but not its varden parameters; this
+    scaling is this build's stand-in.
     """
     rng = np.random.default_rng(seed)
     S = n // per_step
@@ -57,11 +65,19 @@ def seed_spreader(n: int, d: int, L: float, seed: int, p_step: float,
     first = np.flatnonzero(flags)                    # first step of each segment
     # inclusive sum within the segment: csum[t] - csum[first[seg]-1]
     base = np.where(first[:, None] > 0, csum[np.maximum(first - 1, 0)], 0.0)
-    pos = starts[seg] + (csum - base[seg])
     v = rng.standard_normal((n, d))
     v /= np.linalg.norm(v, axis=1, keepdims=True)
     u = rng.random(n)
-    pts = np.repeat(pos, per_step, axis=0) + (radius * u ** (1.0 / d))[:, None] * v
+    if varden:
+        scale = 2.0 ** rng.integers(-1, 3, size=n_seg)
+        sh = sh * scale[seg][:, None]
+        csum = np.cumsum(sh, axis=0)
+        base = np.where(first[:, None] > 0, csum[np.maximum(first - 1, 0)], 0.0)
+        r = radius * np.repeat(scale[seg], per_step)
+    else:
+        r = radius
+    pos = starts[seg] + (csum - base[seg])
+    pts = np.repeat(pos, per_step, axis=0) + (r * u ** (1.0 / d))[:, None] * v
     if noise_frac > 0:
         k = int(round(noise_frac * n))
         idx = rng.choice(n, k, replace=False)

@@ -66,15 +66,16 @@ __device__ uint32_t next_label(const int32_t* p, uint32_t g, int64_t after, cons
   return best;
 }
 
+// One non-core point j (sorted order): label set, then its CSR count (fill =
+// 0) or row (fill = 1). Returns whether it is a border point.
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(128) border_kernel(
-    int fill, CellsView cv, const int32_t* __restrict__ Ps, const uint32_t* __restrict__ idx,
-    const uint8_t* __restrict__ core_s, const uint32_t* __restrict__ core_cnt,
-    const uint32_t* __restrict__ cell_label, uint32_t n, uint32_t clampc, uint64_t eps2,
-    uint32_t* __restrict__ bcnt, const int64_t* __restrict__ border_off,
-    int32_t* __restrict__ border_ids, unsigned long long* nborder) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n || core_s[j]) return;
+__device__ __forceinline__ bool border_point(int fill, uint32_t j, const CellsView& cv,
+                                             const int32_t* __restrict__ Ps, const uint32_t* __restrict__ idx,
+                                             const uint32_t* __restrict__ core_cnt,
+                                             const uint32_t* __restrict__ cell_label, uint32_t clampc,
+                                             uint64_t eps2, uint32_t* __restrict__ bcnt,
+                                             const int64_t* __restrict__ border_off,
+                                             int32_t* __restrict__ border_ids) {
   const uint32_t g = cv.cell_of[j];
   int32_t p[D];
   PtLoad<D>::load(Ps, j, p);
@@ -91,13 +92,11 @@ __global__ void __launch_bounds__(128) border_kernel(
   if (!L.overflow) {
     if (!fill) {
       bcnt[i] = (uint32_t)L.n;
-      if (L.n) atomicAdd(nborder, 1ull);
-    }
-    else {
+    } else {
       int32_t* out = border_ids + border_off[i];
       for (int k = 0; k < L.n; ++k) out[k] = (int32_t)L.v[k];
     }
-    return;
+    return L.n > 0;
   }
   // slow path: enumerate labels in ascending order without storage
   uint32_t cnt = 0;
@@ -109,9 +108,24 @@ __global__ void __launch_bounds__(128) border_kernel(
     ++cnt;
     after = nx;
   }
+  if (!fill) bcnt[i] = cnt;
+  return cnt > 0;
+}
+
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(128) border_kernel(
+    int fill, CellsView cv, const int32_t* __restrict__ Ps, const uint32_t* __restrict__ idx,
+    const uint8_t* __restrict__ core_s, const uint32_t* __restrict__ core_cnt,
+    const uint32_t* __restrict__ cell_label, uint32_t n, uint32_t clampc, uint64_t eps2,
+    uint32_t* __restrict__ bcnt, const int64_t* __restrict__ border_off,
+    int32_t* __restrict__ border_ids, unsigned long long* nborder) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool is_border = j < n && !core_s[j] &&
+                         border_point<D, WIDE>(fill, j, cv, Ps, idx, core_cnt, cell_label, clampc, eps2,
+                                               bcnt, border_off, border_ids);
   if (!fill) {
-    bcnt[i] = cnt;
-    if (cnt) atomicAdd(nborder, 1ull);
+    const uint32_t nb = __syncthreads_count(is_border);  // one atomic per block
+    if (threadIdx.x == 0 && nb) atomicAdd(nborder, (unsigned long long)nb);
   }
 }
 

@@ -71,7 +71,7 @@ __global__ void wave_filter_kernel(const uint2* __restrict__ pairs, const uint64
     if ((uint64_t)core_cnt[p.x] * core_cnt[p.y] <= SMALL_PAIR) small[atomicAdd(ctr, 1u)] = p;
     else large[atomicAdd(ctr + 1, 1u)] = p;
   }
-  if (mine) atomicAdd(tested, (unsigned long long)mine);
+  block_add_u64(mine, tested);
 }
 
 template <int D, bool WIDE>
@@ -260,19 +260,31 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
 // ---------------------------------------------------------------- a9: labels
 __global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
                                    const uint32_t* __restrict__ cell_start,
-                                   const uint32_t* __restrict__ idx, uint32_t* parent,
+                                   const uint32_t* __restrict__ idx,
+                                   const uint32_t* __restrict__ cellmin, uint32_t* parent,
                                    uint32_t* comp_min, uint32_t* counters) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   bool root = false;
   if (g < nc && core_cnt[g] > 0) {
     const uint32_t r = uf_find(parent, g);
-    // cells are sorted stably, so the first (core-first) point of a cell has
-    // the smallest input index among its core points
-    atomicMin(comp_min + r, idx[cell_start[g]]);
+    const uint32_t s = cell_start[g], k = core_cnt[g];
+    uint32_t mn;
+    if (!cellmin) {
+      // stable sort + stable core-first partition: the first point of a cell
+      // has the smallest input index among its core points
+      mn = idx[s];
+    } else if (k == cell_start[g + 1] - s) {
+      mn = cellmin[g];  // all core: the cell's minimum
+    } else {
+      // mixed cell (fewer than minPts points): minimum over its core points
+      mn = 0xffffffffu;
+      for (uint32_t u = s; u < s + k; ++u) mn = min(mn, idx[u]);
+    }
+    atomicMin(comp_min + r, mn);
     root = r == g;
   }
-  uint32_t b = __ballot_sync(DB_FULL, root);
-  if ((threadIdx.x & 31) == 0 && b) atomicAdd(counters, __popc(b));
+  const uint32_t b = __syncthreads_count(root);  // one atomic per block, not per warp
+  if (threadIdx.x == 0 && b) atomicAdd(counters, b);
 }
 
 __global__ void cell_label_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
@@ -296,8 +308,8 @@ __global__ void write_points_kernel(uint32_t n, const uint32_t* __restrict__ idx
     is_core = core_s[j];
     cluster_out[idx[j]] = is_core ? (int32_t)cell_label[cell_of[j]] : -1;
   }
-  uint32_t b = __ballot_sync(DB_FULL, is_core);
-  if ((threadIdx.x & 31) == 0 && b) atomicAdd(counters + 1, __popc(b));
+  const uint32_t b = __syncthreads_count(is_core);  // one atomic per block, not per warp
+  if (threadIdx.x == 0 && b) atomicAdd(counters + 1, b);
 }
 
 // core[i] = cluster[i] >= 0, in input order (coalesced, 4 points per thread).
@@ -316,13 +328,14 @@ __global__ void core_from_cluster_kernel(uint32_t n, const int32_t* __restrict__
 }
 
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
-            const uint32_t* core_cnt, uint32_t* parent, int64_t n, uint32_t* cell_label,
+            const uint32_t* core_cnt, const uint32_t* cellmin, uint32_t* parent, int64_t n,
+            uint32_t* cell_label,
             uint8_t* core_out, int32_t* cluster_out, uint32_t* counters) {
   const uint32_t nc = cv.ncells;
   uint32_t* comp_min = c.alloc<uint32_t>(nc);
   DB_CUDA(cudaMemsetAsync(comp_min, 0xff, sizeof(uint32_t) * nc, c.st));
   label_roots_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, cv.cell_start, idx,
-                                                                    parent, comp_min, counters);
+                                                                    cellmin, parent, comp_min, counters);
   c.launched();
   cell_label_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, parent, comp_min,
                                                                    cell_label);

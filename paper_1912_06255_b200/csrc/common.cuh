@@ -253,6 +253,23 @@ __device__ __forceinline__ uint64_t lb_exclusive(uint64_t* status, int64_t tile,
   return excl;
 }
 
+// Add v over the whole block to *dst with ONE atomic (thread 0). Every thread
+// of the block must call it. Same-address atomics serialise in L2 (about one
+// per clock), so per-thread or per-warp counters over millions of items cost
+// hundreds of microseconds; per-block aggregation removes that.
+__device__ __forceinline__ void block_add_u64(unsigned long long v, unsigned long long* dst) {
+  __shared__ unsigned long long s_part[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(DB_FULL, v, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) t += s_part[w];
+    if (t) atomicAdd(dst, t);
+  }
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

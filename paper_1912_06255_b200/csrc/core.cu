@@ -160,8 +160,8 @@ __global__ void core_count_kernel(CellsView cv, const uint8_t* __restrict__ core
     core_cnt[g] = k;
     is_core_cell = k > 0;
   }
-  uint32_t b = __ballot_sync(DB_FULL, is_core_cell);
-  if ((threadIdx.x & 31) == 0 && b) atomicAdd(counters, __popc(b));
+  const uint32_t b = __syncthreads_count(is_core_cell);  // one atomic per block
+  if (threadIdx.x == 0 && b) atomicAdd(counters, b);
 }
 
 // Stable partition of one mixed cell: core points first, each group in its

@@ -169,9 +169,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     DB_CUDA(cudaMemcpyAsync(p, pts, sizeof(int32_t) * (size_t)n * d, cudaMemcpyHostToDevice, st));
     dpts = p;
   }
-  int32_t* lohi_d = c.alloc<int32_t>(16);
-  bbox(c, dpts, n, d, lohi_d);
-  int32_t lohi[16];
+  int32_t* lohi_d = c.alloc<int32_t>(17);
+  bbox(c, dpts, n, d, g.s, lohi_d);
+  int32_t lohi[17];
   DB_CUDA(cudaMemcpyAsync(lohi, lohi_d, sizeof(lohi), cudaMemcpyDeviceToHost, st));
   DB_CUDA(cudaStreamSynchronize(st));
   uint32_t bits = 0;
@@ -188,22 +188,31 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   g.bits = bits;
   const bool key64 = bits > 32;
 
-  // ---- a1-a2: keys + radix sort
+  // ---- a1-a4: group the points by cell. Few distinct cells: hash-table
+  // counting sort (group.cu); otherwise keys + LSD radix sort + segmentation.
   tm.stage(DBSCAN_STAGE_KEYS);
-  void* skeys;
-  uint32_t* sidx;
-  int passes = 0;
-  cell_keys_and_sort(c, dpts, n, g, key64, &skeys, &sidx, &passes);
-  // (keys and sort share one call; the sort's time is reported under KEYS+SORT)
-
-  // ---- a3: segment + gather
-  tm.stage(DBSCAN_STAGE_SEGMENT);
   int32_t* Ps = c.alloc<int32_t>((size_t)n * g.D);
   uint32_t* cell_of = c.alloc<uint32_t>(n);
   uint32_t* cell_start = c.alloc<uint32_t>((size_t)n + 1);
   uint64_t* cell_key = c.alloc<uint64_t>(n);
-  const uint32_t ncells =
-      segment_and_gather(c, skeys, key64, sidx, dpts, n, g, Ps, cell_of, cell_start, cell_key);
+  uint32_t* sidx = nullptr;
+  uint32_t* cellmin = nullptr;
+  uint32_t ncells = 0;
+  int passes = 0;
+  bool hash_group = false;
+  // the hash table (<= 2^20 slots) always fits n <= 2^19 cells; beyond that
+  // try it only if the sample saw repeated cells
+  const bool try_hash = !(flags & DBSCAN_F_RADIX_GROUP) && (n <= (1 << 19) || lohi[16] >= 16);
+  if (try_hash) {
+    sidx = c.alloc<uint32_t>(n);
+    hash_group = group_by_hash(c, dpts, n, g, Ps, sidx, cell_of, cell_start, cell_key, &cellmin, &ncells);
+  }
+  if (!hash_group) {
+    void* skeys;
+    cell_keys_and_sort(c, dpts, n, g, key64, &skeys, &sidx, &passes);
+    tm.stage(DBSCAN_STAGE_SEGMENT);
+    ncells = segment_and_gather(c, skeys, key64, sidx, dpts, n, g, Ps, cell_of, cell_start, cell_key);
+  }
 
   // ---- regime: CSR path (neighbour lists) or the cell-centric sparse path
   const bool tree = (flags & DBSCAN_F_FORCE_TREE) || (d >= 4 && !(flags & DBSCAN_F_FORCE_STENCIL));
@@ -276,7 +285,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     // ---- a9: labels, scattered to input order
     tm.stage(DBSCAN_STAGE_LABELS);
     uint32_t* cell_label = c.alloc<uint32_t>(ncells);
-    labels(c, cv, sidx, core_s, core_cnt, parent, n, cell_label, core_d, cluster_d, cnt32 + 2);
+    labels(c, cv, sidx, core_s, core_cnt, cellmin, parent, n, cell_label, core_d, cluster_d, cnt32 + 2);
 
     // ---- a10: ClusterBorder
     tm.stage(DBSCAN_STAGE_BORDER);
@@ -326,6 +335,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_CELL_SIDE] = (int64_t)s;
   out->stats[DBSCAN_STAT_DENSE_DIR] = dense_dir;
   out->stats[DBSCAN_STAT_SPARSE] = sparse;
+  out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group;
   return DBSCAN_OK;
 }
 

@@ -79,7 +79,9 @@ void radix_sort_pairs_u64(Ctx& c, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint
                           int passes, const uint32_t* hist, uint64_t** ko, uint32_t** vo);
 
 // ---- grid.cu (a1-a4) ----
-void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, int32_t* lohi /*[16] device*/);
+// lohi[0..7] per-axis minimum, [8..15] maximum, [16] sampled cell collisions
+// (see keys.cu) for the grouping choice; lohi must hold 17 int32.
+void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, uint32_t s, int32_t* lohi);
 // keys + LSD radix sort; on return keys/idx hold the sorted (key, input index) pairs
 // in *sorted_keys / *sorted_idx (either buffer of the ping-pong pair).
 void cell_keys_and_sort(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, bool key64,
@@ -92,6 +94,13 @@ void radix_sort_u64(Ctx& c, uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, 
 uint32_t segment_and_gather(Ctx& c, const void* sorted_keys, bool key64, const uint32_t* sorted_idx,
                             const int32_t* pts, int64_t n, const Geo& g, int32_t* Ps,
                             uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key);
+// counting-sort grouping through a hash table of the distinct keys (group.cu):
+// writes Ps, idx (input index per sorted position), cell_of, cell_start,
+// cell_key and *cellmin (minimum input index per cell); returns false (nothing
+// written) when the keys do not fit its table, and the caller sorts instead.
+bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int32_t* Ps, uint32_t* idx,
+                   uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key, uint32_t** cellmin,
+                   uint32_t* ncells);
 // open-addressing table of the ncells keys; returns mask (capacity-1).
 uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** table);
 
@@ -160,8 +169,11 @@ void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, con
 uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                       const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
                       unsigned long long* tested /*device, zeroed*/);
+// cellmin: minimum input index per cell (hash grouping; order inside a cell is
+// arbitrary), or NULL after the stable radix sort (first point = minimum).
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
-            const uint32_t* core_cnt, uint32_t* parent, int64_t n, uint32_t* cell_label,
+            const uint32_t* core_cnt, const uint32_t* cellmin, uint32_t* parent, int64_t n,
+            uint32_t* cell_label,
             uint8_t* core_out, int32_t* cluster_out, uint32_t* counters /*device [4]*/);
 
 // ---- border.cu (a10) ----

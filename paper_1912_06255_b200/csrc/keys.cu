@@ -18,6 +18,7 @@ __global__ void bbox_init_kernel(int32_t* lohi) {
   const int t = threadIdx.x;
   if (t < 8) lohi[t] = INT32_MAX;
   else if (t < 16) lohi[t] = INT32_MIN;
+  else if (t == 16) lohi[t] = 0;  // sampled cell collisions
 }
 
 // Thread per row (grid-stride); a warp reads 32 consecutive rows = 128*DD
@@ -72,14 +73,62 @@ static void by_dim(int d, F&& f) {
   }
 }
 
-void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, int32_t* lohi) {
+// Sampled cell collisions, an estimate of how many distinct cells there are
+// (it decides between the hash counting sort and the radix sort, DESIGN.md
+// §a2): S = min(n, 4096) evenly spaced points, cell coordinates taken from a
+// fixed origin (INT32_MIN; no bounding box needed, so this runs beside it),
+// hashed to 64 bits, sorted in shared memory; out = S - distinct. With m
+// equally likely cells about S^2 / 2m samples collide.
+constexpr int SAMPLE = 4096;
+
+template <int DD>
+__global__ void __launch_bounds__(1024) sample_collisions_kernel(const int32_t* __restrict__ pts, int64_t n,
+                                                                 uint32_t s, int32_t* out) {
+  __shared__ unsigned long long sk[SAMPLE];
+  const int S = (int)min((int64_t)SAMPLE, n);
+  for (int t = threadIdx.x; t < SAMPLE; t += blockDim.x) {
+    unsigned long long h = ~0ull;
+    if (t < S) {
+      const int64_t i = (int64_t)t * n / S;
+      h = 0x9e3779b97f4a7c15ull;
+#pragma unroll
+      for (int k = 0; k < DD; ++k) {
+        const uint32_t c = (uint32_t)(((int64_t)pts[i * DD + k] - (int64_t)INT32_MIN) / s);
+        h = mix64(h ^ (c + 0x632be59bd9b4e019ull + (h << 6)));
+      }
+      h >>= 1;  // below ~0 (padding)
+    }
+    sk[t] = h;
+  }
+  __syncthreads();
+  for (int kk = 2; kk <= SAMPLE; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < SAMPLE; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = sk[i], b = sk[ixj];
+          if ((a > b) == ((i & kk) == 0)) { sk[i] = b; sk[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  int dup = 0;
+  for (int i = threadIdx.x + 1; i < S; i += blockDim.x) dup += sk[i] == sk[i - 1];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dup += __shfl_xor_sync(DB_FULL, dup, o);
+  if ((threadIdx.x & 31) == 0 && dup) atomicAdd(out, dup);
+}
+
+void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, uint32_t s, int32_t* lohi) {
   bbox_init_kernel<<<1, 32, 0, c.st>>>(lohi);
   c.launched();
   by_dim(d, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
     bbox_kernel<DD><<<grid_for(n, 256, c.sms * 8), 256, 0, c.st>>>(pts, n, lohi);
+    c.launched();
+    sample_collisions_kernel<DD><<<1, 1024, 0, c.st>>>(pts, n, s, lohi + 16);
+    c.launched();
   });
-  c.launched();
 }
 
 // key = sum_k ((x_k - lo_k) div s) << shift_k; idx = input row; plus the

@@ -96,7 +96,8 @@ def test_random_small_vs_o1(oracle_lib):
 @pytest.mark.parametrize("flags", [pkg.F_FORCE_WIDE, pkg.F_FORCE_TREE, pkg.F_NO_WAVES,
                                    pkg.F_FORCE_WIDE | pkg.F_FORCE_TREE | pkg.F_NO_WAVES,
                                    pkg.F_FORCE_SPARSE, pkg.F_NO_SPARSE,
-                                   pkg.F_FORCE_SPARSE | pkg.F_FORCE_WIDE | pkg.F_NO_WAVES])
+                                   pkg.F_FORCE_SPARSE | pkg.F_FORCE_WIDE | pkg.F_NO_WAVES,
+                                   pkg.F_RADIX_GROUP, pkg.F_RADIX_GROUP | pkg.F_FORCE_SPARSE])
 def test_flag_variants_vs_o1(oracle_lib, flags):
     for k, (pts, eps, mp) in enumerate(_instances(200 + flags, 120, dmax=8)):
         r = run_or_erange(pts, eps, mp, flags)
@@ -114,14 +115,16 @@ def test_force_stencil_high_d_vs_o1(oracle_lib):
             assert_same(r, oracle_lib.o1(pts, eps, mp), f"{k}")
 
 
+@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP], ids=["hash", "radix"])
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 7, 8])
-def test_clustered_medium_vs_o2(oracle_lib, d):
+def test_clustered_medium_vs_o2(oracle_lib, d, grouping):
     """Seed-spreader data with dense cells, many neighbours, border points,
-    several tiles of every kernel and ragged tails."""
+    several tiles of every kernel and ragged tails; both groupings (hash
+    counting sort, LSD radix sort)."""
     for seed, n in [(1, 20_001), (2, 45_057)]:
         pts = datagen.seed_spreader(n - n % 100, d, 20000, seed + 10 * d, p_step=0.02, noise_frac=0.03)
         for eps, mp in [(150, 15), (400, 60)]:
-            r = run_or_erange(pts, eps, mp)
+            r = run_or_erange(pts, eps, mp, grouping)
             if r is not None:
                 assert_same(r, oracle_lib.o2(pts, eps, mp), f"d={d} n={n} eps={eps}")
 
@@ -172,11 +175,12 @@ def test_empty():
         assert len(r.core) == 0 and list(r.border_off) == [0] and len(r.border_ids) == 0
 
 
+@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP], ids=["hash", "radix"])
 @pytest.mark.parametrize("n", [4095, 4096, 4097, 8191, 12289])
-def test_tile_boundaries_vs_o2(oracle_lib, n):
+def test_tile_boundaries_vs_o2(oracle_lib, n, grouping):
     """Ragged tails at the radix (4096), scan (2048) and segment (2048) tiles."""
     pts = datagen.seed_spreader(n - n % 100 + 100, 3, 5000, n, p_step=0.1)[:n]
-    assert_same(np_result(gpu(pts, 120, 8)), oracle_lib.o2(pts, 120, 8), f"n={n}")
+    assert_same(np_result(gpu(pts, 120, 8, grouping)), oracle_lib.o2(pts, 120, 8), f"n={n}")
 
 
 def test_deterministic_and_permutation_invariant(oracle_lib):
@@ -206,7 +210,7 @@ def test_stream_and_stats():
     assert r.stats["ncells"] > 0 and r.n_core + r.n_border + r.n_noise == len(pts)
 
 
-@pytest.mark.parametrize("flags", [0, pkg.F_NO_SPARSE])
+@pytest.mark.parametrize("flags", [0, pkg.F_NO_SPARSE, pkg.F_RADIX_GROUP])
 def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
     """Both the cell-centric sparse path and the CSR path on sparse lattices
     (1-8 points per cell), 1D-3D, with border points in several clusters."""
@@ -214,6 +218,34 @@ def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
                               (1, 50_000, 200_000, 3, 3), (3, 60_000, 4_000, 300, 20)]:
         pts = datagen.uniform(n, d, hi, d + n)
         r = gpu(pts, eps, mp, flags)
-        if flags == 0 and d == 3 and hi == 12_000:
+        if flags != pkg.F_NO_SPARSE and d == 3 and hi == 12_000:
             assert r.stats["sparse"] == 1
+        assert r.stats["hash_group"] == (0 if flags & pkg.F_RADIX_GROUP else 1)
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"d={d} flags={flags}")
+
+
+def test_grouping_choice():
+    """Few cells: the hash counting sort groups the points; more distinct cells
+    than its 2^20-slot table holds (uniform 3D, 2M points, ~2M cells): it
+    gives up and the radix sort runs; both give the same result."""
+    few = datagen.seed_spreader(200_000, 3, 100_000, 5, p_step=0.01)
+    r = gpu(few, 1000, 50)
+    assert r.stats["hash_group"] == 1 and r.stats["sort_passes"] == 0
+    many = datagen.uniform(2_000_000, 3, 1_000_000, 6)
+    a = gpu(many, 3000, 3)
+    assert a.stats["hash_group"] == 0 and a.stats["sort_passes"] > 0
+    b = gpu(many, 3000, 3, pkg.F_RADIX_GROUP)
+    assert_same(np_result(a), np_result(b), "hash fallback vs radix")
+
+
+@pytest.mark.parametrize("d", [2, 3, 5, 7])
+def test_varden_and_sweeps_vs_o2(oracle_lib, d):
+    """SURVEY §8(f) f1 on the same kernels: SS-varden (variable-density
+    clusters) and eps / minPts sweeps at a size
+    the oracle finishes in seconds."""
+    L = 1e6 if d <= 3 else 1e5
+    pts = datagen.seed_spreader(40_000, d, L / 20, 40 + d, 0.02, varden=True, noise_frac=0.01)
+    for eps, mp in [(60, 10), (150, 10), (400, 10), (150, 3), (150, 60), (150, 400)]:
+        r = run_or_erange(pts, eps, mp)
+        if r is not None:
+            assert_same(r, oracle_lib.o2(pts, eps, mp), f"varden d={d} eps={eps} mp={mp}")
