@@ -52,7 +52,9 @@ extern "C" {
 #define DBSCAN_F_FORCE_SPARSE 256u /* take the sparse path whenever d <= 3 and the lattice
                                       directory fits (otherwise it is chosen by occupancy)   */
 #define DBSCAN_F_RADIX_GROUP 512u  /* group points by cell with the LSD radix sort only (never
-                                      the hash-table counting sort, which is tried first)    */
+                                      the hash-table or lattice counting sorts)              */
+#define DBSCAN_F_LATTICE_GROUP 1024u /* skip the hash counting sort: use the lattice counting
+                                      sort whenever d <= 3 and its lattice fits               */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
@@ -83,8 +85,8 @@ extern "C" {
 #define DBSCAN_STAT_CELL_SIDE    10  /* integer cell side s                              */
 #define DBSCAN_STAT_DENSE_DIR    11  /* 1 if cells were found through a dense directory   */
 #define DBSCAN_STAT_SPARSE       12  /* 1 if the cell-centric sparse-lattice path ran       */
-#define DBSCAN_STAT_HASH_GROUP   13  /* 1 if points were grouped by the hash counting sort
-                                        (0: LSD radix sort + segmentation)                   */
+#define DBSCAN_STAT_HASH_GROUP   13  /* grouping: 1 hash counting sort, 2 lattice counting sort,
+                                        0 LSD radix sort + segmentation                      */
 #define DBSCAN_NSTATS            16
 
 typedef struct dbscan_result {

@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = ["dbscan", "Result", "lib_path", "load", "F_DEVICE_IO", "F_TIMING", "F_CALLER_OUT",
            "F_FORCE_STENCIL", "F_FORCE_TREE", "F_FORCE_WIDE", "F_NO_WAVES", "F_NO_SPARSE",
-           "F_FORCE_SPARSE", "F_RADIX_GROUP", "STAGES", "STATS",
+           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "STAGES", "STATS",
            "DBSCANError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -36,7 +36,7 @@ lib_path = os.path.join(_HERE, "libdbscan_b200.so")
 # flags (include/dbscan.h)
 F_DEVICE_IO, F_TIMING, F_CALLER_OUT = 1, 2, 4
 F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
-F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP = 128, 256, 512
+F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP = 128, 256, 512, 1024
 NSTAGES, NSTATS = 12, 16
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]

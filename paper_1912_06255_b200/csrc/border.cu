@@ -76,7 +76,7 @@ __device__ __forceinline__ bool border_point(int fill, uint32_t j, const CellsVi
                                              uint64_t eps2, uint32_t* __restrict__ bcnt,
                                              const int64_t* __restrict__ border_off,
                                              int32_t* __restrict__ border_ids) {
-  const uint32_t g = cv.cell_of[j];
+  const uint32_t g = cv.cell_of[j];  // (the caller's cell; cell_of keeps this self-contained)
   int32_t p[D];
   PtLoad<D>::load(Ps, j, p);
   LabelSet L;
@@ -112,47 +112,56 @@ __device__ __forceinline__ bool border_point(int fill, uint32_t j, const CellsVi
   return cnt > 0;
 }
 
+// Warp per cell (grid-stride), lanes over the cell's non-core points, which
+// follow its core points (a7) and exist only in cells with |g| < minPts
+// (P:L883); cells without non-core points cost one load.
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(128) border_kernel(
+__global__ void __launch_bounds__(256) border_kernel(
     int fill, CellsView cv, const int32_t* __restrict__ Ps, const uint32_t* __restrict__ idx,
-    const uint8_t* __restrict__ core_s, const uint32_t* __restrict__ core_cnt,
-    const uint32_t* __restrict__ cell_label, uint32_t n, uint32_t clampc, uint64_t eps2,
-    uint32_t* __restrict__ bcnt, const int64_t* __restrict__ border_off,
+    const uint32_t* __restrict__ core_cnt, const uint32_t* __restrict__ cell_label, uint32_t clampc,
+    uint64_t eps2, uint32_t* __restrict__ bcnt, const int64_t* __restrict__ border_off,
     int32_t* __restrict__ border_ids, unsigned long long* nborder) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool is_border = j < n && !core_s[j] &&
-                         border_point<D, WIDE>(fill, j, cv, Ps, idx, core_cnt, cell_label, clampc, eps2,
-                                               bcnt, border_off, border_ids);
-  if (!fill) {
-    const uint32_t nb = __syncthreads_count(is_border);  // one atomic per block
-    if (threadIdx.x == 0 && nb) atomicAdd(nborder, (unsigned long long)nb);
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t nb = 0;
+  for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < cv.ncells; g += nwarps) {
+    const uint32_t e = cv.cell_start[g + 1];
+    for (uint32_t j = cv.cell_start[g] + core_cnt[g] + lane; j < e; j += 32)
+      nb += border_point<D, WIDE>(fill, j, cv, Ps, idx, core_cnt, cell_label, clampc, eps2, bcnt, border_off,
+                                  border_ids);
   }
+  if (!fill) block_add_u64(nb, nborder);
 }
 
+// Counts per non-core point (scattered to input order), then border_off =
+// exclusive scan over all points with core points read as 0 (cluster >= 0),
+// so the counts need no clearing; no border point at all: border_off = 0.
 int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                     const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
-                     const uint32_t* cell_label, int64_t n, bool wide, int64_t* border_off,
+                     const uint32_t* idx, const uint32_t* core_cnt, const uint32_t* cell_label,
+                     const int32_t* cluster, int64_t n, bool wide, int64_t* border_off,
                      unsigned long long* nborder) {
   uint32_t* bcnt = c.alloc<uint32_t>(n);
-  c.zero(bcnt, sizeof(uint32_t) * n);
+  const unsigned grid = grid_for((int64_t)cv.ncells * 32, 256, c.sms * 16);
   dispatch(g.D, wide, [&]<int D, bool W>() {
-    border_kernel<D, W><<<grid_for(n, 128, 1 << 30), 128, 0, c.st>>>(
-        0, cv, Ps, idx, core_s, core_cnt, cell_label, (uint32_t)n, g.clampc, g.eps2, bcnt, nullptr,
-        nullptr, nborder);
+    border_kernel<D, W><<<grid, 256, 0, c.st>>>(0, cv, Ps, idx, core_cnt, cell_label, g.clampc, g.eps2, bcnt,
+                                                nullptr, nullptr, nborder);
   });
   c.launched();
-  exclusive_scan_u32_i64(c, bcnt, border_off, n);
+  if (c.read(nborder) == 0) {
+    DB_CUDA(cudaMemsetAsync(border_off, 0, sizeof(int64_t) * (size_t)(n + 1), c.st));
+    return 0;
+  }
+  exclusive_scan_u32_i64_masked(c, bcnt, cluster, border_off, n);
   return c.read(border_off + n);
 }
 
 void border_fill(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                 const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
-                 const uint32_t* cell_label, int64_t n, bool wide, const int64_t* border_off,
-                 int32_t* border_ids) {
+                 const uint32_t* idx, const uint32_t* core_cnt, const uint32_t* cell_label, bool wide,
+                 const int64_t* border_off, int32_t* border_ids) {
+  const unsigned grid = grid_for((int64_t)cv.ncells * 32, 256, c.sms * 16);
   dispatch(g.D, wide, [&]<int D, bool W>() {
-    border_kernel<D, W><<<grid_for(n, 128, 1 << 30), 128, 0, c.st>>>(
-        1, cv, Ps, idx, core_s, core_cnt, cell_label, (uint32_t)n, g.clampc, g.eps2, nullptr,
-        border_off, border_ids, nullptr);
+    border_kernel<D, W><<<grid, 256, 0, c.st>>>(1, cv, Ps, idx, core_cnt, cell_label, g.clampc, g.eps2, nullptr,
+                                                border_off, border_ids, nullptr);
   });
   c.launched();
 }

@@ -36,24 +36,41 @@ __device__ __forceinline__ int wave_of(uint64_t kg, uint64_t kh, const Geo& g) {
 }
 
 // pass 0: count candidate pairs per (wave, cell); pass 1: fill, wave-major.
-__global__ void pair_kernel(int fill, int nwaves, CellsView cv, Geo g,
-                            const uint32_t* __restrict__ core_cnt, uint32_t* __restrict__ cnt,
-                            const uint64_t* __restrict__ off, uint2* __restrict__ pairs) {
-  const uint32_t gc = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gc >= cv.ncells) return;
-  uint32_t local[NWAVES] = {0, 0, 0};
-  if (core_cnt[gc] > 0) {
-    const uint64_t kg = cv.cell_key[gc];
-    for (uint64_t t = cv.nbr_off[gc]; t < cv.nbr_off[gc + 1]; ++t) {
-      const uint32_t h = cv.nbr[t];
-      if (h >= gc || core_cnt[h] == 0) continue;
-      const int w = nwaves == 1 ? 0 : wave_of(kg, cv.cell_key[h], g);
-      if (fill) pairs[off[(size_t)w * cv.ncells + gc] + local[w]] = make_uint2(gc, h);
-      ++local[w];
+// Warp per cell, lanes over its CSR row (rows hold up to ~10^3 cells in 7D),
+// ballots place each wave's pairs.
+__global__ void __launch_bounds__(256) pair_kernel(int fill, int nwaves, CellsView cv, Geo g,
+                                                   const uint32_t* __restrict__ core_cnt,
+                                                   uint32_t* __restrict__ cnt,
+                                                   const uint64_t* __restrict__ off,
+                                                   uint2* __restrict__ pairs) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t gc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gc < cv.ncells; gc += nwarps) {
+    uint32_t local[NWAVES] = {0, 0, 0};
+    if (core_cnt[gc] > 0) {
+      const uint64_t kg = cv.cell_key[gc];
+      const uint64_t r0 = cv.nbr_off[gc], r1 = cv.nbr_off[gc + 1];
+      for (uint64_t t0 = r0; t0 < r1; t0 += 32) {
+        const uint64_t t = t0 + lane;
+        int w = -1;
+        uint32_t h = 0;
+        if (t < r1) {
+          h = cv.nbr[t];
+          if (h < gc && core_cnt[h] > 0) w = nwaves == 1 ? 0 : wave_of(kg, cv.cell_key[h], g);
+        }
+#pragma unroll
+        for (int ww = 0; ww < NWAVES; ++ww) {
+          if (ww >= nwaves) break;
+          const uint32_t b = __ballot_sync(DB_FULL, w == ww);
+          if (fill && w == ww) pairs[off[(size_t)ww * cv.ncells + gc] + local[ww] + __popc(b & lt)] = make_uint2(gc, h);
+          local[ww] += __popc(b);
+        }
+      }
     }
+    if (!fill && lane == 0)
+      for (int w = 0; w < nwaves; ++w) cnt[(size_t)w * cv.ncells + gc] = local[w];
   }
-  if (!fill)
-    for (int w = 0; w < nwaves; ++w) cnt[(size_t)w * cv.ncells + gc] = local[w];
 }
 
 // Drop pairs already in one component; split the rest by size class.
@@ -220,15 +237,14 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
   uf_init(c, parent, nc);
   uint32_t* cnt = c.alloc<uint32_t>((size_t)nw * nc);
   uint64_t* off = c.alloc<uint64_t>((size_t)nw * nc + 1);
-  pair_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(0, nw, cv, g, core_cnt, cnt, nullptr,
-                                                             nullptr);
+  const unsigned pgrid = grid_for((int64_t)nc * 32, 256, c.sms * 16);
+  pair_kernel<<<pgrid, 256, 0, c.st>>>(0, nw, cv, g, core_cnt, cnt, nullptr, nullptr);
   c.launched();
   exclusive_scan_u32_u64(c, cnt, off, (int64_t)nw * nc);
   const uint64_t npairs = c.read(off + (size_t)nw * nc);
   if (npairs == 0) return 0;
   uint2* pairs = c.alloc<uint2>(npairs);
-  pair_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(1, nw, cv, g, core_cnt, nullptr, off,
-                                                             pairs);
+  pair_kernel<<<pgrid, 256, 0, c.st>>>(1, nw, cv, g, core_cnt, nullptr, off, pairs);
   c.launched();
   // wave bounds: off[w*nc] .. off[(w+1)*nc]
   uint64_t* bounds = c.alloc<uint64_t>(2 * NWAVES);
@@ -260,7 +276,7 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
 // ---------------------------------------------------------------- a9: labels
 __global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
                                    const uint32_t* __restrict__ cell_start,
-                                   const uint32_t* __restrict__ idx,
+                                   const uint32_t* __restrict__ idx, int min_mode,
                                    const uint32_t* __restrict__ cellmin, uint32_t* parent,
                                    uint32_t* comp_min, uint32_t* counters) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -269,14 +285,15 @@ __global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ cor
     const uint32_t r = uf_find(parent, g);
     const uint32_t s = cell_start[g], k = core_cnt[g];
     uint32_t mn;
-    if (!cellmin) {
+    if (min_mode == LABEL_MIN_FIRST) {
       // stable sort + stable core-first partition: the first point of a cell
       // has the smallest input index among its core points
       mn = idx[s];
-    } else if (k == cell_start[g + 1] - s) {
+    } else if (min_mode == LABEL_MIN_ARRAY && k == cell_start[g + 1] - s) {
       mn = cellmin[g];  // all core: the cell's minimum
     } else {
-      // mixed cell (fewer than minPts points): minimum over its core points
+      // mixed cell (fewer than minPts points), or any cell of the lattice
+      // counting sort (sparse cells): minimum over its core points
       mn = 0xffffffffu;
       for (uint32_t u = s; u < s + k; ++u) mn = min(mn, idx[u]);
     }
@@ -295,21 +312,48 @@ __global__ void cell_label_kernel(uint32_t nc, const uint32_t* __restrict__ core
   cell_label[g] = core_cnt[g] > 0 ? comp_min[uf_find(parent, g)] : 0xffffffffu;
 }
 
-// Scatter to input order: cluster[i] (one 4-byte store per point; a core flag
-// is implied by cluster >= 0); count core points.
-__global__ void write_points_kernel(uint32_t n, const uint32_t* __restrict__ idx,
-                                    const uint8_t* __restrict__ core_s,
-                                    const uint32_t* __restrict__ cell_of,
-                                    const uint32_t* __restrict__ cell_label,
-                                    int32_t* __restrict__ cluster_out, uint32_t* counters) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool is_core = false;
-  if (j < n) {
-    is_core = core_s[j];
-    cluster_out[idx[j]] = is_core ? (int32_t)cell_label[cell_of[j]] : -1;
+// Scatter the labels of core points to input order (cluster[] was set to -1
+// first). Core points are the first core_cnt[g] points of their cell (a7).
+// WARP: warp per cell, lanes over its core points (few, large cells);
+// otherwise thread per cell (many small cells). Counts core points.
+template <bool WARP>
+__global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const uint32_t* __restrict__ idx,
+                                                           const uint32_t* __restrict__ cell_start,
+                                                           const uint32_t* __restrict__ core_cnt,
+                                                           const uint32_t* __restrict__ cell_label,
+                                                           int32_t* __restrict__ cluster_out, uint32_t* counters) {
+  unsigned long long ncore = 0;
+  if (WARP) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < nc; g += nwarps) {
+      const uint32_t k = core_cnt[g];
+      if (!k) continue;
+      const int32_t lab = (int32_t)cell_label[g];
+      const uint32_t s = cell_start[g];
+      for (uint32_t u = s + lane; u < s + k; u += 32) cluster_out[idx[u]] = lab;
+      if (lane == 0) ncore += k;
+    }
+  } else {
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nc; g += gridDim.x * blockDim.x) {
+      const uint32_t k = core_cnt[g];
+      if (!k) continue;
+      const int32_t lab = (int32_t)cell_label[g];
+      const uint32_t s = cell_start[g];
+      for (uint32_t u = s; u < s + k; ++u) cluster_out[idx[u]] = lab;
+      ncore += k;
+    }
   }
-  const uint32_t b = __syncthreads_count(is_core);  // one atomic per block, not per warp
-  if (threadIdx.x == 0 && b) atomicAdd(counters + 1, b);
+  __shared__ unsigned long long s_part[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ncore += __shfl_xor_sync(DB_FULL, ncore, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = ncore;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w];
+    if (t) atomicAdd(counters + 1, (uint32_t)t);
+  }
 }
 
 // core[i] = cluster[i] >= 0, in input order (coalesced, 4 points per thread).
@@ -328,20 +372,26 @@ __global__ void core_from_cluster_kernel(uint32_t n, const int32_t* __restrict__
 }
 
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
-            const uint32_t* core_cnt, const uint32_t* cellmin, uint32_t* parent, int64_t n,
+            const uint32_t* core_cnt, int min_mode, const uint32_t* cellmin, uint32_t* parent, int64_t n,
             uint32_t* cell_label,
             uint8_t* core_out, int32_t* cluster_out, uint32_t* counters) {
   const uint32_t nc = cv.ncells;
   uint32_t* comp_min = c.alloc<uint32_t>(nc);
   DB_CUDA(cudaMemsetAsync(comp_min, 0xff, sizeof(uint32_t) * nc, c.st));
   label_roots_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, cv.cell_start, idx,
-                                                                    cellmin, parent, comp_min, counters);
+                                                                    min_mode, cellmin, parent, comp_min,
+                                                                    counters);
   c.launched();
   cell_label_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, parent, comp_min,
                                                                    cell_label);
   c.launched();
-  write_points_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
-      (uint32_t)n, idx, core_s, cv.cell_of, cell_label, cluster_out, counters);
+  DB_CUDA(cudaMemsetAsync(cluster_out, 0xff, sizeof(int32_t) * (size_t)n, c.st));
+  if ((int64_t)nc * 32 <= n)
+    write_points_kernel<true><<<grid_for((int64_t)nc * 32, 256, c.sms * 16), 256, 0, c.st>>>(
+        nc, idx, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
+  else
+    write_points_kernel<false><<<grid_for(nc, 256, c.sms * 16), 256, 0, c.st>>>(
+        nc, idx, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
   c.launched();
   core_from_cluster_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, c.st>>>((uint32_t)n, cluster_out,
                                                                                   core_out);

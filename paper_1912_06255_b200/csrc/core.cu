@@ -15,54 +15,56 @@ namespace db {
 // below this are scanned by one thread; above it by one warp.
 constexpr uint32_t WARP_CANDIDATES = 32;
 
-// Thread per sorted point. With cnt = |g| and ub = sum of the neighbours'
-// sizes (from the neighbour stage): cnt >= minPts -> core (dense cell);
-// cnt + ub < minPts -> not core without any distance test (the count can
-// only be lower); otherwise count, here if ub is small, else queue the point
-// for the warp kernel.
+// Warp per cell (grid-stride), lanes over its points. With cnt = |g| and
+// ub = sum of the neighbours' sizes (from the neighbour stage): cnt >= minPts
+// -> all core (dense cell); cnt + ub < minPts -> none core without any
+// distance test (the count can only be lower); otherwise count, in the lane
+// if ub is small, else queue the point for the warp kernel.
 template <int D, bool WIDE>
 __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int32_t* __restrict__ Ps,
-                                                        uint32_t n, int64_t min_pts, uint32_t clampc,
-                                                        uint64_t eps2, uint8_t* __restrict__ core_s,
+                                                        int64_t min_pts, uint32_t clampc, uint64_t eps2,
+                                                        uint8_t* __restrict__ core_s,
                                                         uint32_t* __restrict__ queue,
                                                         uint32_t* __restrict__ qcount) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool enqueue = false;
-  if (j < n) {
-    const uint32_t g = cv.cell_of[j];
-    const int64_t cnt = cv.cell_start[g + 1] - cv.cell_start[g];
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < cv.ncells; g += nwarps) {
+    const uint32_t s = cv.cell_start[g], e = cv.cell_start[g + 1];
+    const int64_t cnt = e - s;
     const uint32_t ub = cv.ub[g];
-    if (cnt >= min_pts) {
-      core_s[j] = 1;
-    } else if (cnt + (int64_t)ub < min_pts) {
-      core_s[j] = 0;
-    } else if (ub > WARP_CANDIDATES) {
-      enqueue = true;
-    } else {
-      int32_t p[D], q[D];
-      PtLoad<D>::load(Ps, j, p);
-      int64_t count = cnt;
-      for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && count < min_pts; ++t) {
-        const uint32_t h = cv.nbr[t];
-        const uint32_t e = cv.cell_start[h + 1];
-        for (uint32_t u = cv.cell_start[h]; u < e; ++u) {
-          PtLoad<D>::load(Ps, u, q);
-          count += within<D, WIDE>(p, q, clampc, eps2);
-          if (count >= min_pts) break;
-        }
-      }
-      core_s[j] = count >= min_pts;
+    if (cnt >= min_pts || cnt + (int64_t)ub < min_pts) {
+      const uint8_t v = cnt >= min_pts;
+      for (uint32_t u = s + lane; u < e; u += 32) core_s[u] = v;
+      continue;
     }
-  }
-  // warp-aggregated append to the warp-kernel queue
-  const uint32_t b = __ballot_sync(DB_FULL, enqueue);
-  if (b) {
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(b) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(qcount, (uint32_t)__popc(b));
-    base = __shfl_sync(DB_FULL, base, leader);
-    if (enqueue) queue[base + __popc(b & lanemask_lt())] = j;
+    for (uint32_t j0 = s; j0 < e; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool valid = j < e;
+      const bool enqueue = valid && ub > WARP_CANDIDATES;
+      if (valid && !enqueue) {
+        int32_t p[D], q[D];
+        PtLoad<D>::load(Ps, j, p);
+        int64_t count = cnt;
+        for (uint64_t t = cv.nbr_off[g]; t < cv.nbr_off[g + 1] && count < min_pts; ++t) {
+          const uint32_t h = cv.nbr[t];
+          const uint32_t he = cv.cell_start[h + 1];
+          for (uint32_t u = cv.cell_start[h]; u < he; ++u) {
+            PtLoad<D>::load(Ps, u, q);
+            count += within<D, WIDE>(p, q, clampc, eps2);
+            if (count >= min_pts) break;
+          }
+        }
+        core_s[j] = count >= min_pts;
+      }
+      // warp-aggregated append to the warp-kernel queue
+      const uint32_t b = __ballot_sync(DB_FULL, enqueue);
+      if (b) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(qcount, (uint32_t)__popc(b));
+        base = __shfl_sync(DB_FULL, base, 0);
+        if (enqueue) queue[base + __popc(b & lanemask_lt())] = j;
+      }
+    }
   }
 }
 
@@ -127,8 +129,8 @@ void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int
   uint32_t* qcount = c.alloc<uint32_t>(1);
   c.zero(qcount, sizeof(uint32_t));
   dispatch(g.D, wide, [&]<int D, bool W>() {
-    mark_core_kernel<D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
-        cv, Ps, (uint32_t)n, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
+    mark_core_kernel<D, W><<<grid_for((int64_t)cv.ncells * 32, 256, c.sms * 16), 256, 0, c.st>>>(
+        cv, Ps, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
     c.launched();
     mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts,
                                                                g.clampc, g.eps2, core_s);
@@ -139,11 +141,14 @@ void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int
 // ---------------------------------------------------------------- a7
 // core_cnt[g] = number of core points in g. Cells with |g| >= minPts are all
 // core; only cells with fewer points can be mixed.
-__global__ void core_count_kernel(CellsView cv, const uint8_t* __restrict__ core_s, int64_t min_pts,
-                                  uint32_t* __restrict__ core_cnt, uint32_t* __restrict__ mixed,
-                                  uint32_t* __restrict__ counters) {
-  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  bool is_core_cell = false;
+__global__ void __launch_bounds__(256) core_count_kernel(CellsView cv, const uint8_t* __restrict__ core_s,
+                                                         int64_t min_pts, uint32_t* __restrict__ core_cnt,
+                                                         uint32_t* __restrict__ mixed,
+                                                         uint32_t* __restrict__ counters) {
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_base;
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  bool is_core_cell = false, is_mixed = false;
   if (g < cv.ncells) {
     const uint32_t s = cv.cell_start[g], e = cv.cell_start[g + 1];
     uint32_t k;
@@ -152,16 +157,18 @@ __global__ void core_count_kernel(CellsView cv, const uint8_t* __restrict__ core
     } else {
       k = 0;
       for (uint32_t u = s; u < e; ++u) k += core_s[u];
-      if (k > 0 && k < e - s) {
-        uint32_t slot = atomicAdd(counters + 1, 1u);
-        mixed[slot] = g;
-      }
+      is_mixed = k > 0 && k < e - s;
     }
     core_cnt[g] = k;
     is_core_cell = k > 0;
   }
   const uint32_t b = __syncthreads_count(is_core_cell);  // one atomic per block
   if (threadIdx.x == 0 && b) atomicAdd(counters, b);
+  uint32_t nm;
+  const uint32_t ex = block_exclusive_scan<uint32_t>(is_mixed ? 1u : 0u, s_scan, &nm);
+  if (threadIdx.x == 0 && nm) s_base = atomicAdd(counters + 1, nm);
+  __syncthreads();
+  if (is_mixed) mixed[s_base + ex] = g;
 }
 
 // Stable partition of one mixed cell: core points first, each group in its

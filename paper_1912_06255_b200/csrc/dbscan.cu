@@ -200,23 +200,46 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   uint32_t ncells = 0;
   int passes = 0;
   bool hash_group = false;
+  bool key_ordered = true;  // cell ids follow key order (the radix path always)
   // the hash table (<= 2^20 slots) always fits n <= 2^19 cells; beyond that
   // try it only if the sample saw repeated cells
-  const bool try_hash = !(flags & DBSCAN_F_RADIX_GROUP) && (n <= (1 << 19) || lohi[16] >= 16);
+  const bool try_hash = !(flags & (DBSCAN_F_RADIX_GROUP | DBSCAN_F_LATTICE_GROUP)) &&
+                        (n <= (1 << 19) || lohi[16] >= 16);
   if (try_hash) {
     sidx = c.alloc<uint32_t>(n);
-    hash_group = group_by_hash(c, dpts, n, g, Ps, sidx, cell_of, cell_start, cell_key, &cellmin, &ncells);
+    const bool sparse_ok = d <= 3 && !(flags & (DBSCAN_F_NO_SPARSE | DBSCAN_F_FORCE_STENCIL | DBSCAN_F_FORCE_TREE));
+    const int sparse_mode = !sparse_ok ? 0 : ((flags & DBSCAN_F_FORCE_SPARSE) ? 2 : 1);
+    hash_group = group_by_hash(c, dpts, n, g, sparse_mode, Ps, sidx, cell_of, cell_start, cell_key, &cellmin,
+                               &ncells, &key_ordered);
   }
-  if (!hash_group) {
+  // many cells, d <= 3, small padded lattice: counting sort over the lattice
+  // (group.cu), which also yields the sparse path's rank directory and the
+  // largest cell for Alg 2's global bound
+  bool lat_group = false, no_core = false;
+  const uint4* lat_dir = nullptr;
+  if (!hash_group && !(flags & DBSCAN_F_RADIX_GROUP) && lattice_applicable(g, n)) {
+    if (!sidx) sidx = c.alloc<uint32_t>(n);
+    const uint64_t bound_cells = stencil_offsets(g).size() / (size_t)d + 1;
+    const int r = lattice_group(c, dpts, n, g, bound_cells, min_pts, Ps, sidx, cell_of, cell_start, cell_key,
+                                &lat_dir, &ncells);
+    lat_group = r == LAT_OK;
+    no_core = r == LAT_ALL_NOISE;
+  }
+  if (!hash_group && !lat_group && !no_core) {
     void* skeys;
     cell_keys_and_sort(c, dpts, n, g, key64, &skeys, &sidx, &passes);
     tm.stage(DBSCAN_STAGE_SEGMENT);
     ncells = segment_and_gather(c, skeys, key64, sidx, dpts, n, g, Ps, cell_of, cell_start, cell_key);
   }
+  // how a9 finds each cell's smallest core index: first point (stable radix
+  // sort + stable partition), per-cell minima (hash), or a scan of the cell's
+  // core points (lattice counting sort; sparse cells)
+  const int min_mode = hash_group ? LABEL_MIN_ARRAY : (lat_group ? LABEL_MIN_SCAN : LABEL_MIN_FIRST);
 
   // ---- regime: CSR path (neighbour lists) or the cell-centric sparse path
   const bool tree = (flags & DBSCAN_F_FORCE_TREE) || (d >= 4 && !(flags & DBSCAN_F_FORCE_STENCIL));
-  const bool sparse = !tree && !(flags & DBSCAN_F_NO_SPARSE) && !(flags & DBSCAN_F_FORCE_STENCIL) &&
+  const bool sparse = !no_core && !tree && key_ordered && !(flags & DBSCAN_F_NO_SPARSE) &&
+                      !(flags & DBSCAN_F_FORCE_STENCIL) &&
                       sparse_applicable(g, n, ncells, flags & DBSCAN_F_FORCE_SPARSE);
   const bool waves = !(flags & DBSCAN_F_NO_WAVES);
 
@@ -234,13 +257,14 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   SparseOut so;
   struct SpGuard { SparseOut* o; ~SpGuard() { sparse_release(o); } } sp_guard{&so};
   uint32_t core_cells = 0;
-  if (sparse) {
+  if (no_core) {
+    // Alg 2's global bound: no point can be core (nothing was grouped)
+  } else if (sparse) {
     // ---- a4 + a6 + a7 on the rank directory
     tm.stage(DBSCAN_STAGE_MARKCORE);
     so.counters = c.alloc<uint32_t>(4);
     c.zero(so.counters, 16);
-    sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, waves, &so);
-    core_cells = c.read(so.counters);
+    core_cells = sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, lat_dir, &so);
   } else {
     // ---- a4-a5: cell lookup + neighbour CSR (+ MarkCore bound ub)
     uint64_t* nbr_off;
@@ -250,7 +274,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     if (!tree)
       neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir);
     else
-      neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total);
+      neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total,
+                     !(flags & DBSCAN_F_FORCE_TREE));
     cv.nbr_off = nbr_off;
     cv.nbr = nbr;
     cv.ub = ub;
@@ -279,23 +304,24 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     // ---- a8: ClusterCore
     tm.stage(DBSCAN_STAGE_CLUSTER);
     uint32_t* parent = c.alloc<uint32_t>(ncells);
-    if (sparse) sparse_cluster(c, g, cv, Ps, core_cnt, wide, waves, parent, cnt64, &so);
+    if (sparse) sparse_cluster(c, g, cv, Ps, core_cnt, wide, parent, cnt64, &so);
     else npairs = cluster_core(c, g, cv, Ps, core_cnt, wide, waves, parent, cnt64);
 
     // ---- a9: labels, scattered to input order
     tm.stage(DBSCAN_STAGE_LABELS);
     uint32_t* cell_label = c.alloc<uint32_t>(ncells);
-    labels(c, cv, sidx, core_s, core_cnt, cellmin, parent, n, cell_label, core_d, cluster_d, cnt32 + 2);
+    labels(c, cv, sidx, core_s, core_cnt, min_mode, cellmin, parent, n, cell_label, core_d, cluster_d,
+           cnt32 + 2);
 
     // ---- a10: ClusterBorder
     tm.stage(DBSCAN_STAGE_BORDER);
-    if (sparse) nnz = sparse_border(c, g, cell_label, n, wide, off_d, cnt64 + 1, &so);
-    else nnz = border_count(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, cnt64 + 1);
+    if (sparse) nnz = sparse_border(c, g, cell_label, cluster_d, n, wide, off_d, cnt64 + 1, &so);
+    else nnz = border_count(c, g, cv, Ps, sidx, core_cnt, cell_label, cluster_d, n, wide, off_d, cnt64 + 1);
     out->border_ids = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
     int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
     if (nnz > 0) {
       if (sparse) sparse_border_fill(c, g, wide, off_d, ids_d, &so);
-      else border_fill(c, g, cv, Ps, sidx, core_s, core_cnt, cell_label, n, wide, off_d, ids_d);
+      else border_fill(c, g, cv, Ps, sidx, core_cnt, cell_label, wide, off_d, ids_d);
     }
     if (!dev_io && nnz > 0)
       DB_CUDA(cudaMemcpyAsync(out->border_ids, ids_d, sizeof(int32_t) * (size_t)nnz,
@@ -335,7 +361,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_CELL_SIDE] = (int64_t)s;
   out->stats[DBSCAN_STAT_DENSE_DIR] = dense_dir;
   out->stats[DBSCAN_STAT_SPARSE] = sparse;
-  out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group;
+  out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group ? 1 : (lat_group ? 2 : 0);
   return DBSCAN_OK;
 }
 
@@ -383,6 +409,7 @@ int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pt
   else if ((flags & DBSCAN_F_FORCE_STENCIL) && (flags & DBSCAN_F_FORCE_TREE)) bad = "FORCE_STENCIL with FORCE_TREE";
   else if (caller_out && (!uoff || (n > 0 && (!ucore || !ucl)))) bad = "F_CALLER_OUT with NULL output";
   else if ((flags & DBSCAN_F_FORCE_STENCIL) && d > 6) bad = "FORCE_STENCIL limited to d <= 6";
+  else if ((flags & DBSCAN_F_RADIX_GROUP) && (flags & DBSCAN_F_LATTICE_GROUP)) bad = "RADIX_GROUP with LATTICE_GROUP";
   if (bad) { g_last_error = bad; return DBSCAN_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   try {

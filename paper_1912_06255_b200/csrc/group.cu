@@ -215,9 +215,9 @@ static void by_dim_g(int d, F&& f) {
   }
 }
 
-bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int32_t* Ps, uint32_t* idx,
-                   uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key, uint32_t** cellmin_out,
-                   uint32_t* ncells_out) {
+bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int sparse_mode, int32_t* Ps,
+                   uint32_t* idx, uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key,
+                   uint32_t** cellmin_out, uint32_t* ncells_out, bool* ordered) {
   uint64_t cap = 1024;
   while (cap < 2ull * (uint64_t)n && cap < (1ull << 20)) cap <<= 1;
   const uint64_t magic = g.s > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + g.s - 1) / g.s) : 0;
@@ -241,8 +241,18 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int32_t*
   DB_CUDA(cudaStreamSynchronize(c.st));
   if (h2[0]) return false;  // too many cells for the table: radix path
   const uint32_t m = h2[1];
-  uint32_t* rank_slot = c.alloc<uint32_t>(m);
-  if (m <= RANK_SMALL) {
+  // Cell ids in key order are needed by the sparse path's rank directory
+  // (sparse_mode: 0 never, 1 if the lattice is sparse, 2 forced) and keep
+  // thread-per-cell hash probes coalesced when there are many cells; the
+  // CSR path over few cells takes any order (the table's).
+  const bool order = (sparse_mode == 2) || (sparse_mode == 1 && (uint64_t)n <= SPARSE_MEAN_PER_CELL * m) ||
+                     m > 32768;
+  uint32_t* rank_slot = list;
+  *ordered = order;
+  if (!order) {
+    // compaction order
+  } else if (m <= RANK_SMALL) {
+    rank_slot = c.alloc<uint32_t>(m);
     group_rank_kernel<<<grid_for(m, GR_THREADS, 1 << 30), GR_THREADS, 0, c.st>>>(T, list, m, rank_slot);
     c.launched();
   } else {
@@ -252,9 +262,7 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int32_t*
     group_keys_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(T, list, m, k0);
     c.launched();
     uint64_t* ko;
-    uint32_t* vo;
-    radix_sort_u64(c, k0, list, k1, v1, m, (int)g.bits, &ko, &vo);
-    DB_CUDA(cudaMemcpyAsync(rank_slot, vo, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, c.st));
+    radix_sort_u64(c, k0, list, k1, v1, m, (int)g.bits, &ko, &rank_slot);
   }
   uint32_t* cnt = c.alloc<uint32_t>(m);
   uint32_t* cellmin = c.alloc<uint32_t>(m);
@@ -272,6 +280,353 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int32_t*
   *cellmin_out = cellmin;
   *ncells_out = m;
   return true;
+}
+
+
+// ===========================================================================
+// Lattice counting sort (d <= 3, sparse lattices such as BASELINE configs[4]):
+// when the padded lattice has at most LAT_PER_POINT cells per point, count
+// the points of every lattice cell directly (packed 8-bit counters, L2
+// resident: 43 MB for c5), derive the rank directory, cell_start and cell_key
+// from the counts in linear order (= key order), and scatter each point to
+// cell_start[rank] + its slot. Two reads of the points and one scattered
+// write replace the key array, four radix passes and the gather. The largest
+// cell size falls out of the counts, so Alg 2's global bound (reading 13)
+// can declare every point non-core before any point is moved.
+// A cell with more than 255 points overflows its counter: the pass reports it
+// and the caller falls back to the radix sort.
+// ===========================================================================
+constexpr int LAT_THREADS = 256;
+
+template <int DD>
+__device__ __forceinline__ uint64_t point_lin(const int32_t* __restrict__ pts, uint32_t i, const Geo& g,
+                                              uint64_t magic, const uint64_t* stride, int32_t* x) {
+  uint64_t lin = 0;
+#pragma unroll
+  for (int k = 0; k < DD; ++k) {
+    x[k] = __ldg(pts + (uint64_t)i * DD + k);
+    const uint32_t off = (uint32_t)x[k] - (uint32_t)g.lo[k];
+    const uint32_t ck = magic ? (uint32_t)__umul64hi((uint64_t)off, magic) : off;
+    lin += (uint64_t)(ck + g.R) * stride[k];
+  }
+  return lin;
+}
+
+struct LatArgs {
+  Geo g;
+  uint64_t magic;
+  uint64_t stride[3];
+  uint64_t dims[3];    // padded lattice extent per axis
+  uint64_t words;      // 32-cell words
+  uint64_t smagic[3];  // ceil(2^64 / stride) (stride 1: 0 -> handled as identity below)
+  int small;           // padded lattice volume < 2^32: 32-bit coordinates by multiply-high
+};
+
+// pass 1: slot of every point in its lattice cell (8-bit packed counters)
+template <int DD>
+__global__ void __launch_bounds__(LAT_THREADS) lat_count_kernel(const int32_t* __restrict__ pts, uint32_t n,
+                                                                LatArgs L, uint32_t* __restrict__ cnt8,
+                                                                uint8_t* __restrict__ slot, uint32_t* overflow) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t x[DD];
+  const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, x);
+  const uint32_t sh = ((uint32_t)lin & 3u) * 8u;
+  const uint32_t old = (atomicAdd(cnt8 + (lin >> 2), 1u << sh) >> sh) & 255u;
+  if (old == 255u) *overflow = 1u;  // the add carried into the next counter
+  slot[i] = (uint8_t)old;
+}
+
+// pass 2a: per 32-cell word, occupancy bits and point count
+__global__ void __launch_bounds__(LAT_THREADS) lat_words_kernel(const uint32_t* __restrict__ cnt8, LatArgs L,
+                                                                uint32_t* __restrict__ bm,
+                                                                uint32_t* __restrict__ wcells,
+                                                                uint32_t* __restrict__ wpts, uint32_t* mx) {
+  const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint32_t m = 0;
+  if (w < L.words) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w + 1);
+    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t bits = 0, sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c = (v[q] >> (8 * k)) & 255u;
+        bits |= (uint32_t)(c != 0) << (4 * q + k);
+        sum += c;
+        m = max(m, c);
+      }
+    bm[w] = bits;
+    wcells[w] = __popc(bits);
+    wpts[w] = sum;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(DB_FULL, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(mx, m);
+}
+
+// pass 2b: cells in linear order: cell_start, cell_key, and the directory
+// entry {bits w, bits w+1, cells before w, 0} of the sparse path. The 32
+// counters of a word stay in registers; byte prefix sums by shifts; lattice
+// coordinates by multiply-high (exact for lin < 2^32, else 64-bit division).
+__global__ void __launch_bounds__(LAT_THREADS) lat_cells_kernel(const uint32_t* __restrict__ cnt8, LatArgs L,
+                                                                const uint32_t* __restrict__ bm,
+                                                                const uint32_t* __restrict__ cpre,
+                                                                const uint32_t* __restrict__ ppre,
+                                                                uint32_t* __restrict__ cell_start,
+                                                                uint64_t* __restrict__ cell_key,
+                                                                uint4* __restrict__ dir) {
+  const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (w >= L.words) return;
+  const uint32_t bits = bm[w];
+  dir[w] = make_uint4(bits, w + 1 < L.words ? bm[w + 1] : 0u, cpre[w], 0u);
+  if (!bits) return;
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w);
+  const uint4 b = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w + 1);
+  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  // excl[q]: points in counters 0 .. 4q-1 of the word; inside a u32 the byte
+  // prefix sums come from x * 0x01010101 (<= 4 * 255 would overflow a byte, so
+  // sum in 16-bit halves instead)
+  uint32_t excl[8];
+  uint32_t run = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    excl[q] = run;
+    run += (v[q] & 255u) + ((v[q] >> 8) & 255u) + ((v[q] >> 16) & 255u) + (v[q] >> 24);
+  }
+  uint32_t r = cpre[w];
+  const uint32_t p = ppre[w];
+  for (uint32_t bb = bits; bb; bb &= bb - 1) {
+    const int k = __ffs(bb) - 1;
+    const int q = k >> 2, sub = k & 3;
+    uint32_t before = excl[0];
+#pragma unroll
+    for (int qq = 1; qq < 8; ++qq)
+      if (qq == q) before = excl[qq];
+    uint32_t vq = v[0];
+#pragma unroll
+    for (int qq = 1; qq < 8; ++qq)
+      if (qq == q) vq = v[qq];
+    for (int s = 0; s < sub; ++s) before += (vq >> (8 * s)) & 255u;
+    const uint64_t lin = 32 * w + (uint64_t)k;
+    uint64_t key = 0;
+    if (L.small) {
+      uint32_t rem = (uint32_t)lin;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (ax < L.g.d) {
+          const uint32_t ca = L.smagic[ax] ? (uint32_t)__umul64hi((uint64_t)rem, L.smagic[ax]) : rem;
+          rem -= ca * (uint32_t)L.stride[ax];
+          key |= (uint64_t)(ca - L.g.R) << L.g.shift[ax];
+        }
+      }
+    } else {
+      uint64_t rem = lin;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (ax < L.g.d) {
+          const uint64_t ca = rem / L.stride[ax];
+          rem -= ca * L.stride[ax];
+          key |= (ca - L.g.R) << L.g.shift[ax];
+        }
+      }
+    }
+    cell_start[r] = p + before;
+    cell_key[r] = key;
+    ++r;
+  }
+}
+
+// pass 3: the permutation, in two steps so that no write is random.
+// Every point's final position pos = cell_start[rank] + slot is known; the
+// positions are split into buckets of BK_T consecutive positions.
+//  3a: a block takes BK_ITEMS consecutive points, ranks them by bucket in
+//      shared memory, reserves room in each bucket's staging range with one
+//      atomic per (block, bucket) and writes the records {pos, x, y, z} and
+//      the input index there (runs per bucket);
+//  3b: a block per bucket loads its BK_T records, places the points, input
+//      indices and cell ids in shared memory by pos - bucket start, and
+//      writes them out coalesced. cell_of is filled cell by cell from
+//      cell_start (the bucket's cells are one contiguous id range).
+constexpr int BK_T = 8192;           // positions per bucket (3b: 8192 x 24 B in shared memory)
+constexpr int BK_THREADS = 512;
+constexpr int BK_ITEMS = 8;          // 3a: 4096 points per block
+constexpr int BK_MAXB = 4096;        // buckets held by a 3a block's shared histogram
+
+template <int DD>
+__global__ void __launch_bounds__(BK_THREADS) lat_stage_kernel(const int32_t* __restrict__ pts, uint32_t n,
+                                                               LatArgs L, const uint4* __restrict__ dir,
+                                                               const uint8_t* __restrict__ slot,
+                                                               const uint32_t* __restrict__ cell_start,
+                                                               uint32_t nbk, uint32_t* __restrict__ bcur,
+                                                               uint4* __restrict__ rec, uint32_t* __restrict__ reci) {
+  __shared__ uint32_t hist[BK_MAXB];
+  for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS) hist[b] = 0;
+  __syncthreads();
+  const uint32_t i0 = blockIdx.x * (BK_THREADS * BK_ITEMS);
+  uint32_t pos[BK_ITEMS], lr[BK_ITEMS];
+  int32_t x[BK_ITEMS][3];
+#pragma unroll
+  for (int t = 0; t < BK_ITEMS; ++t) {
+    const uint32_t i = i0 + t * BK_THREADS + threadIdx.x;
+    pos[t] = 0xffffffffu;
+    if (i < n) {
+      int32_t xx[DD];
+      const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, xx);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) x[t][k] = k < DD ? xx[k] : 0;
+      const uint4 e = __ldg(dir + (lin >> 5));
+      const uint32_t rank = e.z + __popc(e.x & ((1u << ((uint32_t)lin & 31u)) - 1u));
+      pos[t] = cell_start[rank] + slot[i];
+      lr[t] = atomicAdd(hist + pos[t] / BK_T, 1u);
+    }
+  }
+  __syncthreads();
+  // reserve each touched bucket's room (hist[b] becomes the global base)
+  for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS)
+    if (hist[b]) hist[b] = atomicAdd(bcur + b, hist[b]);
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < BK_ITEMS; ++t) {
+    if (pos[t] == 0xffffffffu) continue;
+    const uint32_t b = pos[t] / BK_T;
+    const uint64_t o = (uint64_t)b * BK_T + hist[b] + lr[t];
+    rec[o] = make_uint4(pos[t], (uint32_t)x[t][0], (uint32_t)x[t][1], (uint32_t)x[t][2]);
+    reci[o] = i0 + t * BK_THREADS + threadIdx.x;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(1024) lat_place_kernel(uint32_t n, const uint4* __restrict__ rec,
+                                                         const uint32_t* __restrict__ reci,
+                                                         const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                                         int32_t* __restrict__ Ps, uint32_t* __restrict__ idx,
+                                                         uint32_t* __restrict__ cell_of) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  int4* sp = reinterpret_cast<int4*>(sm_raw);                        // [BK_T] points (x, y, z, 0)
+  uint32_t* si = reinterpret_cast<uint32_t*>(sp + BK_T);             // [BK_T] input index
+  uint32_t* sc = si + BK_T;                                          // [BK_T] cell id
+  const uint32_t base = blockIdx.x * BK_T;
+  const uint32_t cnt = min((uint32_t)BK_T, n - base);
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const uint4 r = rec[(uint64_t)base + t];
+    const uint32_t q = r.x - base;
+    sp[q] = make_int4((int32_t)r.y, (int32_t)r.z, (int32_t)r.w, 0);
+    si[q] = reci[(uint64_t)base + t];
+  }
+  // cells overlapping [base, base + cnt): ids first .. last, found by binary
+  // search (the last cell with start <= p); then a thread per cell fills
+  // its positions' cell ids
+  __shared__ uint32_t s_fl[2];
+  if (threadIdx.x < 2) {
+    const uint32_t p = threadIdx.x == 0 ? base : base + cnt - 1;
+    uint32_t lo = 0, hi = ncells - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (cell_start[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    s_fl[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  for (uint32_t r = s_fl[0] + threadIdx.x; r <= s_fl[1]; r += blockDim.x) {
+    const uint32_t lo = max(cell_start[r], base), hi = min(cell_start[r + 1], base + cnt);
+    for (uint32_t p = lo; p < hi; ++p) sc[p - base] = r;
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const int4 v = sp[t];
+    if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[base + t] = make_int2(v.x, v.y);
+    else reinterpret_cast<int4*>(Ps)[base + t] = v;
+    idx[base + t] = si[t];
+    cell_of[base + t] = sc[t];
+  }
+}
+
+bool lattice_applicable(const Geo& g, int64_t n) {
+  if (g.d > 3 || n == 0 || n > (int64_t)BK_MAXB * BK_T) return false;
+  unsigned __int128 vol = 1;
+  for (int k = 0; k < g.d; ++k) vol *= (unsigned __int128)g.maxc[k] + 1 + 2 * (unsigned __int128)g.R;
+  return vol <= (unsigned __int128)LAT_PER_POINT * (unsigned __int128)n + (1u << 20);
+}
+
+int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t min_pts_bound_cells,
+                  int64_t min_pts, int32_t* Ps, uint32_t* idx, uint32_t* cell_of, uint32_t* cell_start,
+                  uint64_t* cell_key, const uint4** dir_out, uint32_t* ncells_out) {
+  LatArgs L{};
+  L.g = g;
+  L.magic = g.s > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + g.s - 1) / g.s) : 0;
+  unsigned __int128 vol = 1;
+  for (int k = g.d - 1; k >= 0; --k) {
+    L.stride[k] = (uint64_t)vol;
+    L.dims[k] = (uint64_t)g.maxc[k] + 1 + 2 * (uint64_t)g.R;
+    vol *= L.dims[k];
+  }
+  L.words = ((uint64_t)vol + 31) / 32 + 1;
+  L.small = vol + 64 < ((unsigned __int128)1 << 32);
+  for (int k = 0; k < g.d; ++k)
+    L.smagic[k] = L.stride[k] > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + L.stride[k] - 1) / L.stride[k])
+                                  : 0;
+  uint32_t* cnt8 = c.alloc<uint32_t>(8 * L.words);
+  uint8_t* slot = c.alloc<uint8_t>(n);
+  uint32_t* flags = c.alloc<uint32_t>(2);  // [0] overflow, [1] largest cell
+  c.zero(cnt8, sizeof(uint32_t) * 8 * L.words);
+  c.zero(flags, 2 * sizeof(uint32_t));
+  const unsigned pgrid = grid_for(n, LAT_THREADS, 1 << 30);
+  auto by_d = [&](auto f) {
+    if (g.d == 1) f(std::integral_constant<int, 1>(), std::integral_constant<int, 2>());
+    else if (g.d == 2) f(std::integral_constant<int, 2>(), std::integral_constant<int, 2>());
+    else f(std::integral_constant<int, 3>(), std::integral_constant<int, 4>());
+  };
+  by_d([&](auto Dd, auto) {
+    constexpr int DD = decltype(Dd)::value;
+    lat_count_kernel<DD><<<pgrid, LAT_THREADS, 0, c.st>>>(pts, (uint32_t)n, L, cnt8, slot, flags);
+  });
+  c.launched();
+  uint32_t* bm = c.alloc<uint32_t>(L.words);
+  uint32_t* wcells = c.alloc<uint32_t>(L.words);
+  uint32_t* wpts = c.alloc<uint32_t>(L.words);
+  const unsigned wgrid = grid_for((int64_t)L.words, LAT_THREADS, 1 << 30);
+  lat_words_kernel<<<wgrid, LAT_THREADS, 0, c.st>>>(cnt8, L, bm, wcells, wpts, flags + 1);
+  c.launched();
+  uint32_t h[2];
+  DB_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, c.st));
+  DB_CUDA(cudaStreamSynchronize(c.st));
+  if (h[0]) return LAT_FALLBACK;
+  // Alg 2's count is at most (stencil cells) x (largest cell): below minPts,
+  // no point is core and nothing needs to be grouped (reading 13)
+  if ((uint64_t)h[1] * min_pts_bound_cells < (uint64_t)min_pts) return LAT_ALL_NOISE;
+  uint32_t* cpre = c.alloc<uint32_t>(L.words + 1);
+  uint32_t* ppre = c.alloc<uint32_t>(L.words + 1);
+  exclusive_scan_u32_u32(c, wcells, cpre, (int64_t)L.words);
+  exclusive_scan_u32_u32(c, wpts, ppre, (int64_t)L.words);
+  uint4* dir = c.alloc<uint4>(L.words);
+  lat_cells_kernel<<<wgrid, LAT_THREADS, 0, c.st>>>(cnt8, L, bm, cpre, ppre, cell_start, cell_key, dir);
+  c.launched();
+  const uint32_t ncells = c.read(cpre + L.words);
+  DB_CUDA(cudaMemcpyAsync(cell_start + ncells, ppre + L.words, sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.st));
+  // pass 3: stage by bucket of positions, then place bucket by bucket
+  const uint32_t nbk = (uint32_t)((n + BK_T - 1) / BK_T);
+  if (nbk > (uint32_t)BK_MAXB) throw Error(-4, "lattice sort: too many buckets");
+  uint32_t* bcur = c.alloc<uint32_t>(nbk);
+  uint4* rec = c.alloc<uint4>((size_t)nbk * BK_T);
+  uint32_t* reci = c.alloc<uint32_t>((size_t)nbk * BK_T);
+  c.zero(bcur, sizeof(uint32_t) * nbk);
+  const unsigned sgrid = (unsigned)((n + BK_THREADS * BK_ITEMS - 1) / (BK_THREADS * BK_ITEMS));
+  by_d([&](auto Dd, auto Dp) {
+    constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
+    lat_stage_kernel<DD><<<sgrid, BK_THREADS, 0, c.st>>>(pts, (uint32_t)n, L, dir, slot, cell_start, nbk, bcur,
+                                                         rec, reci);
+    c.launched();
+    const int smem = BK_T * (16 + 4 + 4);
+    DB_CUDA(cudaFuncSetAttribute(lat_place_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    lat_place_kernel<D><<<nbk, 1024, smem, c.st>>>((uint32_t)n, rec, reci, cell_start, ncells, Ps, idx, cell_of);
+    c.launched();
+  });
+  *dir_out = dir;
+  *ncells_out = ncells;
+  return LAT_OK;
 }
 
 }  // namespace db

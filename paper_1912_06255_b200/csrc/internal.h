@@ -69,6 +69,8 @@ struct Ctx {
 void exclusive_scan_u32_u64(Ctx& c, const uint32_t* in, uint64_t* out, int64_t n);
 void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n);
 void exclusive_scan_u32_u32(Ctx& c, const uint32_t* in, uint32_t* out, int64_t n);
+// same, with in[i] read as 0 where mask[i] >= 0 (in[i] is then never read)
+void exclusive_scan_u32_i64_masked(Ctx& c, const uint32_t* in, const int32_t* mask, int64_t* out, int64_t n);
 
 // ---- radix.cu (a2) ----
 // LSD passes over the low `passes` 8-bit digits; hist = [passes][256] global digit
@@ -98,9 +100,24 @@ uint32_t segment_and_gather(Ctx& c, const void* sorted_keys, bool key64, const u
 // writes Ps, idx (input index per sorted position), cell_of, cell_start,
 // cell_key and *cellmin (minimum input index per cell); returns false (nothing
 // written) when the keys do not fit its table, and the caller sorts instead.
-bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int32_t* Ps, uint32_t* idx,
-                   uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key, uint32_t** cellmin,
-                   uint32_t* ncells);
+// sparse_mode (whether the sparse path, which needs cell ids in key order,
+// may run): 0 no, 1 if the lattice turns out sparse, 2 forced.
+bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int sparse_mode, int32_t* Ps,
+                   uint32_t* idx, uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key,
+                   uint32_t** cellmin, uint32_t* ncells, bool* ordered /* ids in key order */);
+// lattice counting sort for d <= 3 when the padded lattice has at most
+// LAT_PER_POINT cells per point (group.cu): writes Ps, idx, cell_of,
+// cell_start, cell_key (cell ids in key order) and the sparse path's rank
+// directory (*dir, 16 B per 32 lattice cells). Returns LAT_OK; LAT_FALLBACK
+// (a cell has more than 255 points: nothing written, sort instead); or
+// LAT_ALL_NOISE when (largest cell) x bound_cells < min_pts (no core point is
+// possible; nothing written).
+constexpr uint64_t LAT_PER_POINT = 8;
+enum { LAT_OK = 0, LAT_FALLBACK = 1, LAT_ALL_NOISE = 2 };
+bool lattice_applicable(const Geo& g, int64_t n);
+int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t bound_cells, int64_t min_pts,
+                  int32_t* Ps, uint32_t* idx, uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key,
+                  const uint4** dir, uint32_t* ncells);
 // open-addressing table of the ncells keys; returns mask (capacity-1).
 uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** table);
 
@@ -111,9 +128,11 @@ uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** ta
 void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                        uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,
                        uint32_t** ub, uint64_t* total, bool* dense);
+// d >= 4: all-pairs over cells when there are few (<= 16384), else the cell tree
+// (allow_brute = false forces the tree).
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                     uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub,
-                    uint64_t* total);
+                    uint64_t* total, bool allow_brute);
 // host: exact stencil offsets (Delta != 0 with sum gap^2 <= eps^2), flat [count*d] int8
 std::vector<int8_t> stencil_offsets(const Geo& g);
 
@@ -146,15 +165,18 @@ struct SparseOut {
   void* stash = nullptr;         // kernel arguments kept between the stages
 };
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);
-// a4 + a6 + a7: rank directory, core flags, core-first compaction, core_cnt
-void sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
-                     uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
-                     bool waves, SparseOut* o);
+// a4 + a6 + a7 on the rank directories: core flags, core-first compaction,
+// core_cnt, the core-cell directory; returns the number of core cells (0 =
+// no core point, the caller takes the all-noise exit; synchronises).
+// dir: the rank directory from the lattice counting sort, or NULL (built here).
+uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
+                         uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
+                         const uint4* dir, SparseOut* o);
 void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                    const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
+                    const uint32_t* core_cnt, bool wide, uint32_t* parent,
                     unsigned long long* tested, SparseOut* o);
-int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, int64_t n, bool wide,
-                      int64_t* border_off, unsigned long long* nborder, SparseOut* o);
+int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const int32_t* cluster, int64_t n,
+                      bool wide, int64_t* border_off, unsigned long long* nborder, SparseOut* o);
 void sparse_border_fill(Ctx& c, const Geo& g, bool wide, const int64_t* border_off,
                         int32_t* border_ids, SparseOut* o);
 void sparse_release(SparseOut* o);
@@ -169,23 +191,25 @@ void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, con
 uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                       const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
                       unsigned long long* tested /*device, zeroed*/);
-// cellmin: minimum input index per cell (hash grouping; order inside a cell is
-// arbitrary), or NULL after the stable radix sort (first point = minimum).
+// Smallest core input index of a cell: its first point (stable radix sort and
+// stable partition), cellmin[] for all-core cells (hash grouping: order inside
+// a cell is arbitrary), or a scan of its core points (lattice counting sort).
+enum { LABEL_MIN_FIRST = 0, LABEL_MIN_ARRAY = 1, LABEL_MIN_SCAN = 2 };
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
-            const uint32_t* core_cnt, const uint32_t* cellmin, uint32_t* parent, int64_t n,
+            const uint32_t* core_cnt, int min_mode, const uint32_t* cellmin, uint32_t* parent, int64_t n,
             uint32_t* cell_label,
             uint8_t* core_out, int32_t* cluster_out, uint32_t* counters /*device [4]*/);
 
 // ---- border.cu (a10) ----
-// count pass -> border_off (exclusive scan, device int64[n+1]); returns nnz (sync).
+// count pass -> border_off (exclusive scan in input order, device int64[n+1],
+// core points read as 0 through cluster[] >= 0); returns nnz (synchronises).
 int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                     const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
-                     const uint32_t* cell_label, int64_t n, bool wide, int64_t* border_off,
-                     unsigned long long* nborder /*device counter*/);
+                     const uint32_t* idx, const uint32_t* core_cnt, const uint32_t* cell_label,
+                     const int32_t* cluster, int64_t n, bool wide, int64_t* border_off,
+                     unsigned long long* nborder /*device counter, zeroed*/);
 void border_fill(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                 const uint32_t* idx, const uint8_t* core_s, const uint32_t* core_cnt,
-                 const uint32_t* cell_label, int64_t n, bool wide, const int64_t* border_off,
-                 int32_t* border_ids);
+                 const uint32_t* idx, const uint32_t* core_cnt, const uint32_t* cell_label, bool wide,
+                 const int64_t* border_off, int32_t* border_ids);
 
 // Dispatch on padded dimension D in {2,4,8} and the WIDE distance path.
 template <typename F>

@@ -77,43 +77,37 @@ static void by_dim(int d, F&& f) {
 // (it decides between the hash counting sort and the radix sort, DESIGN.md
 // §a2): S = min(n, 4096) evenly spaced points, cell coordinates taken from a
 // fixed origin (INT32_MIN; no bounding box needed, so this runs beside it),
-// hashed to 64 bits, sorted in shared memory; out = S - distinct. With m
-// equally likely cells about S^2 / 2m samples collide.
+// hashed to a non-zero 32-bit fingerprint and inserted into a shared-memory
+// set; out = number of inserts that found their fingerprint already there.
+// With m equally likely cells about S^2 / 2m samples collide.
 constexpr int SAMPLE = 4096;
+constexpr int SAMPLE_SLOTS = 2 * SAMPLE;
 
 template <int DD>
 __global__ void __launch_bounds__(1024) sample_collisions_kernel(const int32_t* __restrict__ pts, int64_t n,
                                                                  uint32_t s, int32_t* out) {
-  __shared__ unsigned long long sk[SAMPLE];
-  const int S = (int)min((int64_t)SAMPLE, n);
-  for (int t = threadIdx.x; t < SAMPLE; t += blockDim.x) {
-    unsigned long long h = ~0ull;
-    if (t < S) {
-      const int64_t i = (int64_t)t * n / S;
-      h = 0x9e3779b97f4a7c15ull;
-#pragma unroll
-      for (int k = 0; k < DD; ++k) {
-        const uint32_t c = (uint32_t)(((int64_t)pts[i * DD + k] - (int64_t)INT32_MIN) / s);
-        h = mix64(h ^ (c + 0x632be59bd9b4e019ull + (h << 6)));
-      }
-      h >>= 1;  // below ~0 (padding)
-    }
-    sk[t] = h;
-  }
+  __shared__ uint32_t set[SAMPLE_SLOTS];
+  for (int t = threadIdx.x; t < SAMPLE_SLOTS; t += blockDim.x) set[t] = 0;
   __syncthreads();
-  for (int kk = 2; kk <= SAMPLE; kk <<= 1)
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < SAMPLE; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long a = sk[i], b = sk[ixj];
-          if ((a > b) == ((i & kk) == 0)) { sk[i] = b; sk[ixj] = a; }
-        }
-      }
-      __syncthreads();
-    }
+  const int S = (int)min((int64_t)SAMPLE, n);
   int dup = 0;
-  for (int i = threadIdx.x + 1; i < S; i += blockDim.x) dup += sk[i] == sk[i - 1];
+  for (int t = threadIdx.x; t < S; t += blockDim.x) {
+    const int64_t i = (int64_t)t * n / S;
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+#pragma unroll
+    for (int k = 0; k < DD; ++k) {
+      const uint32_t c = ((uint32_t)pts[i * DD + k] ^ 0x80000000u) / s;  // (x - INT32_MIN) / s
+      h = mix64(h ^ (c + 0x632be59bd9b4e019ull + (h << 6)));
+    }
+    const uint32_t f = (uint32_t)(h >> 32) | 1u;  // non-zero fingerprint
+    uint32_t slot = (uint32_t)h & (SAMPLE_SLOTS - 1);
+    while (true) {
+      const uint32_t prev = atomicCAS(set + slot, 0u, f);
+      if (prev == 0u) break;
+      if (prev == f) { ++dup; break; }
+      slot = (slot + 1) & (SAMPLE_SLOTS - 1);
+    }
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) dup += __shfl_xor_sync(DB_FULL, dup, o);
   if ((threadIdx.x & 31) == 0 && dup) atomicAdd(out, dup);

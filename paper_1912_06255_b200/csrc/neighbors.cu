@@ -266,6 +266,150 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
   *ub_out = ub;
 }
 
+// ------------------------------------------------------------ all-pairs cells
+// d >= 4 with few cells (the seed-spreader configs: 1.6K-4.7K cells): testing
+// every pair of cells with the exact gap predicate is cheaper than any tree
+// (4.7K^2 = 2.2e7 tests against ~10^2 tree-node visits x 32 lanes per query
+// with a per-warp stack). Warp per query cell, lanes over all cells, lattice
+// coordinates pre-decoded (cc[8] per cell), the squared gap per axis from a
+// shared table indexed by min(|delta|, R+1) (entry R+1 exceeds eps^2 on its
+// own). Rows come out in three classes of lattice L1 distance (1, 2, >= 3),
+// nearest class first, each in ascending cell id; the count pass records the
+// class sizes so that the fill pass places every entry in one sweep.
+constexpr uint32_t BRUTE_MAX_CELLS = 16384;
+constexpr int GT_MAX = 64;
+
+__global__ void decode_cells_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
+                                    uint32_t* __restrict__ cc) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncells) return;
+  const uint64_t key = cell_key[i];
+  uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+  uint32_t v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = k < g.d ? cell_coord(key, g, k) : 0u;
+  a = make_uint4(v[0], v[1], v[2], v[3]);
+  b = make_uint4(v[4], v[5], v[6], v[7]);
+  reinterpret_cast<uint4*>(cc)[2 * i] = a;
+  reinterpret_cast<uint4*>(cc)[2 * i + 1] = b;
+}
+
+template <int DD>
+__global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t* __restrict__ cc,
+                                                        uint32_t ncells, Geo g,
+                                                        const uint64_t* __restrict__ gtab_g, int gmax,
+                                                        const uint32_t* __restrict__ cell_start,
+                                                        uint32_t* __restrict__ ccount /*[3][ncells]*/,
+                                                        uint32_t* __restrict__ cnt, uint32_t* __restrict__ ub,
+                                                        const uint64_t* __restrict__ off,
+                                                        uint32_t* __restrict__ nbr) {
+  __shared__ unsigned long long gt[GT_MAX + 1];
+  for (int i = threadIdx.x; i <= gmax; i += blockDim.x) gt[i] = gtab_g[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint4* C = reinterpret_cast<const uint4*>(cc);
+  for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncells; q += nwarps) {
+    uint32_t cq[8];
+    {
+      const uint4 a = C[2 * q], b = C[2 * q + 1];
+      cq[0] = a.x; cq[1] = a.y; cq[2] = a.z; cq[3] = a.w; cq[4] = b.x; cq[5] = b.y; cq[6] = b.z; cq[7] = b.w;
+    }
+    uint64_t pos[3] = {0, 0, 0};
+    if (fill) {
+      pos[0] = off[q];
+      pos[1] = pos[0] + ccount[q];
+      pos[2] = pos[1] + ccount[ncells + q];
+    }
+    uint32_t n3[3] = {0, 0, 0};
+    uint64_t sum = 0;
+    for (uint32_t h0 = 0; h0 < ncells; h0 += 32) {
+      const uint32_t h = h0 + lane;
+      int cls = -1;
+      if (h < ncells && h != q) {
+        uint32_t ch[8];
+        const uint4 a = C[2 * h];
+        ch[0] = a.x; ch[1] = a.y; ch[2] = a.z; ch[3] = a.w;
+        if (DD > 4) {
+          const uint4 b = C[2 * h + 1];
+          ch[4] = b.x; ch[5] = b.y; ch[6] = b.z; ch[7] = b.w;
+        }
+        uint64_t acc = 0;
+        uint32_t l1 = 0;
+#pragma unroll
+        for (int k = 0; k < DD; ++k) {
+          const uint32_t dl = min(__usad(ch[k], cq[k], 0u), (uint32_t)gmax);
+          acc += gt[dl];
+          l1 += dl;
+        }
+        if (acc <= g.eps2) cls = l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t b = __ballot_sync(DB_FULL, cls == c);
+        if (fill && cls == c) nbr[pos[c] + __popc(b & lt)] = h;
+        pos[c] += __popc(b);
+        n3[c] += __popc(b);
+      }
+      if (!fill && cls >= 0) sum += cell_start[h + 1] - cell_start[h];
+    }
+    if (!fill) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(DB_FULL, sum, o);
+      if (lane == 0) {
+        cnt[q] = n3[0] + n3[1] + n3[2];
+        ccount[q] = n3[0];
+        ccount[ncells + q] = n3[1];
+        ub[q] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+      }
+    }
+  }
+}
+
+static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
+                            uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub_out,
+                            uint64_t* total) {
+  // squared gap per |delta| (u = |delta| clamped to R+1; entry R+1 > eps^2)
+  const int gmax = (int)g.R + 1;
+  if (gmax > GT_MAX || g.d < 4) return false;
+  std::vector<unsigned long long> gt((size_t)gmax + 1);
+  gt[0] = 0;
+  for (int i = 1; i <= (int)g.R; ++i) {
+    const unsigned long long gap = (unsigned long long)(i - 1) * g.s + 1;
+    gt[i] = gap * gap;
+  }
+  gt[gmax] = g.eps2 + 1;
+  unsigned long long* dgt = c.alloc<unsigned long long>(gt.size());
+  DB_CUDA(cudaMemcpyAsync(dgt, gt.data(), sizeof(unsigned long long) * gt.size(), cudaMemcpyHostToDevice, c.st));
+  uint32_t* cc = c.alloc<uint32_t>((size_t)ncells * 8);
+  decode_cells_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, cc);
+  c.launched();
+  uint32_t* ccount = c.alloc<uint32_t>(2 * (size_t)ncells);
+  uint32_t* cnt = c.alloc<uint32_t>(ncells);
+  uint32_t* ub = c.alloc<uint32_t>(ncells);
+  uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
+  const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
+  auto launch = [&](int fill, uint32_t* list) {
+    if (g.d <= 4)
+      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, ncells, g, (const uint64_t*)dgt, gmax, cell_start,
+                                                  ccount, cnt, ub, off, list);
+    else
+      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, ncells, g, (const uint64_t*)dgt, gmax, cell_start,
+                                                  ccount, cnt, ub, off, list);
+    c.launched();
+  };
+  launch(0, nullptr);
+  exclusive_scan_u32_u64(c, cnt, off, ncells);
+  *total = c.read(off + ncells);
+  uint32_t* list = c.alloc<uint32_t>(*total + 1);
+  launch(1, list);
+  *nbr_off = off;
+  *nbr = list;
+  *ub_out = ub;
+  return true;
+}
+
 // ------------------------------------------------------------------ cell tree
 constexpr int LEAF = 32;
 
@@ -467,7 +611,10 @@ __global__ void __launch_bounds__(256) sort_rows_kernel(const uint64_t* __restri
 
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                     uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub_out,
-                    uint64_t* total) {
+                    uint64_t* total, bool allow_brute) {
+  if (allow_brute && ncells <= BRUTE_MAX_CELLS &&
+      neighbors_brute(c, g, cell_key, cell_start, ncells, nbr_off, nbr, ub_out, total))
+    return;
   uint64_t* code0 = c.alloc<uint64_t>(ncells);
   uint64_t* code1 = c.alloc<uint64_t>(ncells);
   uint32_t* id0 = c.alloc<uint32_t>(ncells);

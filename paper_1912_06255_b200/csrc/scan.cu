@@ -10,8 +10,10 @@ constexpr int SC_THREADS = 256;
 constexpr int SC_ITEMS = 8;
 constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 
+// mask (optional): items with mask[i] >= 0 count as 0 (their in[i] is not read)
 template <typename TOut>
 __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __restrict__ in,
+                                                          const int32_t* __restrict__ mask,
                                                           TOut* __restrict__ out, int64_t n,
                                                           uint64_t* status, uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
@@ -26,7 +28,7 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
 #pragma unroll
   for (int i = 0; i < SC_ITEMS; ++i) {
     int64_t j = base + i * SC_THREADS + threadIdx.x;
-    s_in[i * SC_THREADS + threadIdx.x] = j < n ? in[j] : 0u;
+    s_in[i * SC_THREADS + threadIdx.x] = (j < n && !(mask && mask[j] >= 0)) ? in[j] : 0u;
   }
   __syncthreads();
   uint32_t v[SC_ITEMS];
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
 }
 
 template <typename TOut>
-static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n) {
+static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n, const int32_t* mask = nullptr) {
   if (n == 0) {
     c.zero(out, sizeof(TOut));
     return;
@@ -73,7 +75,7 @@ static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n) {
   uint32_t* ctr = c.alloc<uint32_t>(1);
   c.zero(status, sizeof(uint64_t) * tiles);
   c.zero(ctr, sizeof(uint32_t));
-  scan_kernel<TOut><<<(unsigned)tiles, SC_THREADS, 0, c.st>>>(in, out, n, status, ctr);
+  scan_kernel<TOut><<<(unsigned)tiles, SC_THREADS, 0, c.st>>>(in, mask, out, n, status, ctr);
   c.launched();
 }
 
@@ -82,6 +84,9 @@ void exclusive_scan_u32_u64(Ctx& c, const uint32_t* in, uint64_t* out, int64_t n
 }
 void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n) {
   scan_impl<int64_t>(c, in, out, n);
+}
+void exclusive_scan_u32_i64_masked(Ctx& c, const uint32_t* in, const int32_t* mask, int64_t* out, int64_t n) {
+  scan_impl<int64_t>(c, in, out, n, mask);
 }
 
 }  // namespace db

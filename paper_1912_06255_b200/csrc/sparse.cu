@@ -1,32 +1,42 @@
 // sparse.cu — the cell-centric path for sparse lattices (d <= 3, few points
 // per cell, e.g. BASELINE configs[4] "3D uniform fill": 8.9M cells of ~1.1
-// points). It computes exactly what the CSR path computes (rows a5-a10 of
+// points). It computes exactly what the CSR path computes (rows a4-a10 of
 // SURVEY §8(a)) but never materialises neighbour lists: with ~26 non-empty
 // neighbours of ~1 point per cell, building and re-reading a CSR costs more
 // than walking the stencil again.
 //
-//  * Cell lookup (a4): a rank directory over the lattice padded by R cells:
-//    an occupancy bitmap plus a per-32-cell exclusive prefix count (2 bits per
-//    lattice cell; L2-resident at these sizes). Cell ids follow key order,
-//    which is the lattice's linear order, so id = prefix[w] + popc(bits below).
+//  * Cell lookup (a4): a rank directory over the lattice padded by R cells.
+//    One 16-byte entry per 32 lattice cells holds that word of the occupancy
+//    bitmap, the next word and the number of occupied cells before it (L2
+//    resident: 21 MB for c5). Cell ids follow key order, which is the
+//    lattice's linear order, so one load answers "which cells of this run of
+//    up to 32 lattice cells exist, and what are their ids". The exact stencil
+//    (reading 7) is a union of COLUMNS, runs of consecutive cells
+//    along the last axis (25 in 3D, 5 in 2D); a column's cells have
+//    consecutive ids and their points are one contiguous range of Ps.
 //    Out-of-range neighbours land in the padding (no range checks).
-//  * MarkCore (a6, Alg 2): a thread per point probes every
-//    stencil offset without divergence (consecutive lanes probe adjacent
-//    directory words), lists the cells found in L1-resident local memory, then
-//    counts over those ~26 cells only, nearest first, stopping at minPts; a
-//    thread per cell then counts core points (a7) and mixed cells are
-//    partitioned core-first.
-//  * ClusterCore (a8, Alg 3): per wave (offsets of lattice L1 norm
-//    1, 2, >= 3, each with a negative linear offset so h < g, "g > h",
-//    P:L847-849), a warp takes 32 cells and, for each core cell among them,
-//    lanes probe the wave's offsets, skip pairs with equal Find, run small
-//    BCPs inline with early exit and queue large ones for the warp BCP kernel
+//  * MarkCore (a6, Alg 2): a warp per cell; lane c probes column
+//    c, a warp prefix sum flattens the columns' point ranges into one
+//    candidate list (nearest columns first), and for each point of the cell
+//    the lanes test 32 candidates at a time and count with a ballot, stopping
+//    at minPts. A cell with |g| >= minPts is all core.
+//  * a7: a thread per cell counts core points; mixed cells are partitioned
+//    core-first (core.cu); a second directory covers only the cells holding
+//    core points, with the list of those cells in linear order.
+//  * ClusterCore (a8, Alg 3): over the core cells, the lanes of a
+//    warp take (core cell g, back column) items — back columns hold the
+//    cells before g in linear order, so each pair is seen once, from its
+//    higher id ("g > h") — probe the core directory and test the
+//    core cells found: small BCPs directly (cheaper than the Finds that could
+//    prune them), larger ones after a Find check through the warp BCP kernel
 //    (cluster.cu).
-//  * ClusterBorder (a10, Alg 4): a thread per non-core point,
-//    the same two phases restricted to cells with core points, label sets of
-//    up to SP_MAXL in registers staged per sorted position; larger sets are
-//    enumerated without storage in ascending order.
+//  * ClusterBorder (a10, Alg 4): a thread per non-core point
+//    walks the stencil columns on the core directory (only cells with core
+//    points are visited), label sets of up to SP_MAXL in registers staged per
+//    sorted position; larger sets are enumerated without storage in
+//    ascending order.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 
 #include "internal.h"
@@ -34,14 +44,17 @@
 namespace db {
 
 constexpr int SP_MAXL = 4;
-constexpr int SP_MAX_OFFS = 1024;
+constexpr int SP_MAX_COLS = 32;  // lane per column in the MarkCore warp (3D: 25)
 constexpr uint32_t MISS = 0xffffffffu;
+constexpr uint32_t SP_SMALL = 64;
 
 struct SpArgs {
   Geo g;
   uint64_t stride[3];
-  const uint32_t* bm;
-  const uint32_t* pre;
+  const uint4* dir;          // all cells: {bits of word w, bits of w+1, cells before w, 0}
+  const uint4* cdir;         // cells with core points, same layout
+  const uint32_t* core_list; // cells with core points in linear order (rank in cdir -> id)
+  uint32_t ncore;
   const long long* coff;     // stencil columns: start offset (padded linear units), nearest first
   const uint32_t* cmask;     // stencil columns: (1 << width) - 1
   int ncols;
@@ -70,30 +83,22 @@ struct SpArgs {
   int64_t n;
 };
 
-__device__ __forceinline__ uint32_t rd_lookup(const uint32_t* __restrict__ bm,
-                                              const uint32_t* __restrict__ pre, uint64_t lin) {
-  const uint32_t w = __ldg(bm + (lin >> 5));
-  const uint32_t b = (uint32_t)lin & 31u;
-  if (!((w >> b) & 1u)) return MISS;
-  return __ldg(pre + (lin >> 5)) + __popc(w & ((1u << b) - 1u));
+// Cells of the lattice run start .. start+width-1 (mask = (1 << width) - 1,
+// width <= 32): returns how many exist; *id0 = the first one's id (rank).
+__device__ __forceinline__ uint32_t dir_probe(const uint4* __restrict__ dir, uint64_t start, uint32_t mask,
+                                              uint32_t* id0) {
+  const uint4 e = __ldg(dir + (start >> 5));
+  const uint32_t b0 = (uint32_t)start & 31u;
+  const uint32_t bits = __funnelshift_r(e.x, e.y, b0) & mask;
+  if (!bits) return 0;
+  *id0 = e.z + __popc(e.x & ((1u << b0) - 1u));
+  return __popc(bits);
 }
 
-// A stencil column: the lattice cells base + off .. base + off + width - 1,
-// consecutive along the last axis (the exact stencil is a union of such
-// columns). The cells present in it have consecutive ids (ids
-// follow the lattice's linear order), so one 64-bit window of the bitmap
-// gives how many there are and one prefix word gives the first id; their
-// points are one contiguous range of Ps. Returns the number of cells.
-__device__ __forceinline__ uint32_t col_probe(const uint32_t* __restrict__ bm,
-                                              const uint32_t* __restrict__ pre, uint64_t start,
-                                              uint32_t mask, uint32_t* id0) {
-  const uint64_t w0 = start >> 5;
-  const uint32_t b0 = (uint32_t)start & 31u;
-  const uint32_t lo = __ldg(bm + w0), hi = __ldg(bm + w0 + 1);
-  const uint32_t bits = __funnelshift_r(lo, hi, b0) & mask;
-  if (!bits) return 0;
-  *id0 = __ldg(pre + w0) + __popc(lo & ((1u << b0) - 1u));
-  return __popc(bits);
+// rank of an occupied lattice cell
+__device__ __forceinline__ uint32_t dir_rank(const uint4* __restrict__ dir, uint64_t lin) {
+  const uint4 e = __ldg(dir + (lin >> 5));
+  return e.z + __popc(e.x & ((1u << ((uint32_t)lin & 31u)) - 1u));
 }
 
 template <int DIM>
@@ -109,50 +114,46 @@ __device__ __forceinline__ void load_pt(const int32_t* __restrict__ Ps, uint32_t
   PtLoad<D>::load(Ps, j, x);
 }
 
-template <int D>
-__device__ __forceinline__ void shfl_pt(const int32_t* src, int from, int32_t* dst) {
+// ||p - q||^2 <= eps^2 over the first DIM coordinates (the padding is 0 on
+// both sides; skipping it saves an axis in 3D)
+template <int DIM, int D, bool WIDE>
+__device__ __forceinline__ bool within_dim(const int32_t* p, const int32_t* q, const Geo& g) {
+  int32_t a[D], b[D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) dst[k] = __shfl_sync(DB_FULL, src[k], from);
+  for (int k = 0; k < D; ++k) { a[k] = k < DIM ? p[k] : 0; b[k] = k < DIM ? q[k] : 0; }
+  return within<D, WIDE>(a, b, g.clampc, g.eps2);
 }
 
-// Flattened candidates of one batch: lane l owns cell (st_l, sz_l); candidate
-// tt lives in the lane o with excl_o <= tt < excl_o + sz_o.
-struct Batch {
-  uint32_t st, excl, total;
-};
-
-__device__ __forceinline__ Batch make_batch(uint32_t st, uint32_t sz) {
-  const uint32_t incl = warp_inclusive_scan(sz);
-  Batch b;
-  b.st = st;
-  b.excl = incl - sz;
-  b.total = __shfl_sync(DB_FULL, incl, 31);
-  return b;
-}
-
-// owner lane and point index of candidate tt (all lanes call; tt may be >= total)
-__device__ __forceinline__ uint32_t batch_point(const Batch& b, uint32_t tt, int* owner) {
-  int lo = 0;
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const uint32_t e = __shfl_sync(DB_FULL, b.excl, lo + s);
-    if (e <= tt) lo += s;
-  }
-  *owner = lo;
-  const uint32_t ost = __shfl_sync(DB_FULL, b.st, lo);
-  const uint32_t oex = __shfl_sync(DB_FULL, b.excl, lo);
-  return ost + (tt - oex);
-}
-
-// ------------------------------------------------------------- directory
-__global__ void rd_set_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, SpArgs a,
-                              uint32_t* bm) {
+// ------------------------------------------------------------- directories
+__global__ void dir_set_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, SpArgs a,
+                               const uint32_t* __restrict__ only_if /* core_cnt or NULL */, uint32_t* bm) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ncells) return;
+  if (i >= ncells || (only_if && only_if[i] == 0)) return;
   const uint64_t key = cell_key[i];
   uint64_t lin = 0;
   for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
   atomicOr(bm + (lin >> 5), 1u << (lin & 31));
+}
+
+__global__ void popc_kernel(const uint32_t* __restrict__ bm, uint64_t words, uint32_t* __restrict__ cnt) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < words) cnt[i] = __popc(bm[i]);
+}
+
+__global__ void dir_pack_kernel(const uint32_t* __restrict__ bm, const uint32_t* __restrict__ pre, uint64_t words,
+                                uint4* __restrict__ dir) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < words) dir[i] = make_uint4(bm[i], i + 1 < words ? bm[i + 1] : 0u, pre[i], 0u);
+}
+
+// core_list[rank in cdir] = cell id, for every cell holding core points
+__global__ void core_list_kernel(SpArgs a, uint32_t* __restrict__ core_list) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.ncells || a.core_cnt[g] == 0) return;
+  uint64_t lin = 0;
+  const uint64_t key = a.cell_key[g];
+  for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
+  core_list[dir_rank(a.cdir, lin)] = g;
 }
 
 // largest cell size (block max, one atomic per block)
@@ -172,23 +173,78 @@ __global__ void __launch_bounds__(256) cell_max_kernel(const uint32_t* __restric
   }
 }
 
-__global__ void popc_kernel(const uint32_t* __restrict__ bm, uint64_t words, uint32_t* __restrict__ cnt) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i < words) cnt[i] = __popc(bm[i]);
-}
-
 // ------------------------------------------------------------ MarkCore (a6)
-// Thread per sorted point (Alg 2): a dense cell (|g| >= minPts)
-// is all core; otherwise count the points within eps over the
-// stencil columns, nearest column first, stopping at minPts. The own cell
-// lies in the central column and is counted by the same test (same cell =>
-// within eps, so the test always passes there; p counts itself).
-// Consecutive lanes hold consecutive sorted points (mostly one cell or its
-// last-axis neighbours), so their column probes and point loads coalesce.
-constexpr int SP_MAX_COLS = 64;
-
+// Warp per cell (grid-stride). A dense cell (|g| >= minPts) is all core
+// (P:L579-582). Otherwise lane c probes stencil column c (nearest columns
+// first), a warp prefix sum flattens the columns' point ranges, and for each
+// point p of the cell the lanes test candidates 32 at a time, counting with a
+// ballot and stopping once count >= minPts. The own cell lies in the central
+// column and passes the same test (same cell => within eps); p counts itself
+// (P:L585). The first 32 candidates are loaded once per cell and reused by
+// every point of the cell.
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a) {
+  const int lane = threadIdx.x & 31;
+  long long my_off = 0;
+  uint32_t my_mask = 0;
+  if (lane < a.ncols) { my_off = a.coff[lane]; my_mask = a.cmask[lane]; }
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < a.ncells; g += nwarps) {
+    const uint32_t s = a.cell_start[g], e = a.cell_start[g + 1];
+    if ((int64_t)(e - s) >= a.min_pts) {  // dense cell
+      for (uint32_t u = s + lane; u < e; u += 32) a.core_s[u] = 1;
+      continue;
+    }
+    const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
+    uint32_t st = 0, sz = 0;
+    if (lane < a.ncols) {
+      uint32_t id0;
+      const uint32_t nc = dir_probe(a.dir, base + (uint64_t)my_off, my_mask, &id0);
+      if (nc) { st = a.cell_start[id0]; sz = a.cell_start[id0 + nc] - st; }
+    }
+    const uint32_t incl = warp_inclusive_scan(sz);
+    const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
+    const uint32_t excl = incl - sz;
+    // candidate tt -> owner lane (largest lane with excl <= tt) -> point index
+    auto cand = [&](uint32_t tt) -> uint32_t {
+      int lo = 0;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const uint32_t ex = __shfl_sync(DB_FULL, excl, lo + o);
+        if (ex <= tt) lo += o;
+      }
+      return __shfl_sync(DB_FULL, st, lo) + (tt - __shfl_sync(DB_FULL, excl, lo));
+    };
+    int32_t q0[D];
+    const bool v0 = (uint32_t)lane < total;
+    {
+      const uint32_t u = cand((uint32_t)lane);
+      if (v0) load_pt<D>(a.Ps, u, q0);
+    }
+    for (uint32_t j = s; j < e; ++j) {
+      int32_t p[D];
+      load_pt<D>(a.Ps, j, p);
+      int64_t count = __popc(__ballot_sync(DB_FULL, v0 && within_dim<DIM, D, WIDE>(p, q0, a.g)));
+      for (uint32_t t0 = 32; t0 < total && count < a.min_pts; t0 += 32) {
+        const uint32_t tt = t0 + lane;
+        const uint32_t u = cand(tt);
+        bool hit = false;
+        if (tt < total) {
+          int32_t q[D];
+          load_pt<D>(a.Ps, u, q);
+          hit = within_dim<DIM, D, WIDE>(p, q, a.g);
+        }
+        count += __popc(__ballot_sync(DB_FULL, hit));
+      }
+      if (lane == 0) a.core_s[j] = count >= a.min_pts;
+    }
+  }
+}
+
+// Thread per sorted point (variant 1): nested loops over the stencil columns
+// (nearest first) and their point ranges, stopping at minPts.
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(256) sp_core_thread_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
@@ -204,17 +260,112 @@ __global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a) {
   int64_t count = 0;
   for (int c = 0; c < a.ncols && count < a.min_pts; ++c) {
     uint32_t id0;
-    const uint32_t nc = col_probe(a.bm, a.pre, base + (uint64_t)s_off[c], s_mask[c], &id0);
+    const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
     if (!nc) continue;
     const uint32_t ue = a.cell_start[id0 + nc];
     for (uint32_t u = a.cell_start[id0]; u < ue; ++u) {
       int32_t q[D];
       load_pt<D>(a.Ps, u, q);
-      count += within<D, WIDE>(p, q, a.g.clampc, a.g.eps2);
+      count += within_dim<DIM, D, WIDE>(p, q, a.g);
       if (count >= a.min_pts) break;
     }
   }
   a.core_s[j] = count >= a.min_pts;
+}
+
+// Thread per sorted point (variant 2): one flat loop over the point's
+// candidates; when the current column's range is exhausted the thread probes
+// forward to the next non-empty column. Every iteration tests at most one
+// candidate, so the lanes of a warp stay in step (the nested loops diverge
+// on the per-column range lengths).
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(256) sp_core_flat_kernel(SpArgs a) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  __syncthreads();
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  const uint32_t g = a.cell_of[j];
+  const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
+  if ((int64_t)m >= a.min_pts) { a.core_s[j] = 1; return; }  // dense cell
+  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
+  int32_t p[D];
+  load_pt<D>(a.Ps, j, p);
+  uint32_t count = 0;
+  const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
+  uint32_t u = 0, ue = 0;
+  int c = 0;
+  while (count < need) {
+    if (u == ue) {
+      uint32_t nc = 0, id0 = 0;
+      while (c < a.ncols && nc == 0) {
+        nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+        ++c;
+      }
+      if (!nc) break;
+      u = a.cell_start[id0];
+      ue = a.cell_start[id0 + nc];
+    }
+    int32_t q[D];
+    load_pt<D>(a.Ps, u, q);
+    count += within_dim<DIM, D, WIDE>(p, q, a.g);
+    ++u;
+  }
+  a.core_s[j] = count >= need;
+}
+
+// Thread per sorted point (variant 3), two phases through shared memory:
+// (1) every lane probes all stencil columns in lock step and appends the
+//     non-empty ones' point ranges to its own list (shared memory, one
+//     column-major slot per lane: no bank conflicts);
+// (2) one flat loop over the point's candidates: each iteration tests one
+//     candidate per lane, stepping to the next listed range when one is
+//     exhausted, stopping at minPts. The lanes stay in step except for the
+//     ranges' ends (the nested loops diverge on every range length).
+constexpr int SPC_THREADS = 256;
+
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(SPC_THREADS) sp_core_2p_kernel(SpArgs a) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  extern __shared__ uint2 s_rng[];  // [ncols][SPC_THREADS] {start, end}
+  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  __syncthreads();
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  const uint32_t g = a.cell_of[j];
+  const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
+  if ((int64_t)m >= a.min_pts) { a.core_s[j] = 1; return; }  // dense cell
+  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
+  int nf = 0;
+  for (int c = 0; c < a.ncols; ++c) {
+    uint32_t id0;
+    const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+    if (nc) {
+      s_rng[nf * SPC_THREADS + threadIdx.x] = make_uint2(a.cell_start[id0], a.cell_start[id0 + nc]);
+      ++nf;
+    }
+  }
+  int32_t p[D];
+  load_pt<D>(a.Ps, j, p);
+  const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
+  uint32_t count = 0, u = 0, ue = 0;
+  int f = 0;
+  while (count < need) {
+    if (u == ue) {
+      if (f == nf) break;
+      const uint2 r = s_rng[f * SPC_THREADS + threadIdx.x];
+      u = r.x;
+      ue = r.y;
+      ++f;
+    }
+    int32_t q[D];
+    load_pt<D>(a.Ps, u, q);
+    count += within_dim<DIM, D, WIDE>(p, q, a.g);
+    ++u;
+  }
+  a.core_s[j] = count >= need;
 }
 
 // Thread per cell: core count (a7); mixed cells are listed for the partition.
@@ -231,32 +382,29 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
     core_cell = k > 0;
     mixed = k > 0 && k < m;
   }
+  __shared__ uint32_t s_scan[33];
+  __shared__ uint32_t s_base;
   const uint32_t cb = __syncthreads_count(core_cell);
   if (threadIdx.x == 0 && cb) atomicAdd(a.counters + 0, cb);
-  const uint32_t mb = __ballot_sync(DB_FULL, mixed);
-  if (mb) {
-    const int lane = threadIdx.x & 31, leader = __ffs(mb) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(a.counters + 3, (uint32_t)__popc(mb));
-    base = __shfl_sync(DB_FULL, base, leader);
-    if (mixed) a.mixed_list[base + __popc(mb & lanemask_lt())] = g;
-  }
+  uint32_t nm;
+  const uint32_t ex = block_exclusive_scan<uint32_t>(mixed ? 1u : 0u, s_scan, &nm);
+  if (threadIdx.x == 0 && nm) s_base = atomicAdd(a.counters + 3, nm);  // one atomic per block
+  __syncthreads();
+  if (mixed) a.mixed_list[s_base + ex] = g;
 }
 
 // ---------------------------------------------------------- ClusterCore (a8)
-// One pass over the "back" stencil columns (cells h before g in the lattice's
-// linear order, i.e. h < g: "the cell with higher ID checks").
-// A warp takes 32 consecutive cells; its lanes then run over the (core cell,
-// back column) items of the chunk. For a core cell h found in a column:
+// Over the core cells (core_list, linear order): a warp takes 32 of them and
+// its lanes run over the (core cell g, back column) items; each probes the
+// core directory and tests the core cells h found (h < g in linear order:
+// every pair once):
 //  * small pairs (|A| |B| <= SP_SMALL core points; ~1x1 on sparse lattices):
 //    the BCP test itself is cheaper than the two Finds that could prune it,
 //    so it runs directly (early exit at the first pair within eps,
 //    P:L642-644) and Links on success;
 //  * larger pairs are skipped if Find(g) == Find(h) and queued
 //    for the warp BCP kernel (cluster.cu), which re-checks Find first.
-constexpr uint32_t SP_SMALL = 64;
-
-template <int DIM, int D, bool WIDE>
+template <int DIM, int D, bool WIDE, bool BY_CELLS>
 __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
@@ -266,22 +414,30 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   uint32_t mine = 0;
-  for (uint32_t c0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; c0 < a.ncells;
-       c0 += nwarps * 32) {
-    const uint32_t gl = c0 + lane;
-    const uint32_t kl = gl < a.ncells ? a.core_cnt[gl] : 0;
-    const uint32_t cm = __ballot_sync(DB_FULL, kl > 0);
-    const uint32_t items = (uint32_t)__popc(cm) * (uint32_t)nb;
+  // BY_CELLS: chunks of 32 consecutive cells, the core ones found by a ballot;
+  // else chunks of 32 consecutive core cells from core_list
+  const uint32_t limit = BY_CELLS ? a.ncells : a.ncore;
+  for (uint32_t r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < limit; r0 += nwarps * 32) {
+    uint32_t cm = 0xffffffffu, k;
+    if (BY_CELLS) {
+      const uint32_t gl = r0 + lane;
+      cm = __ballot_sync(DB_FULL, gl < a.ncells && a.core_cnt[gl] > 0);
+      k = __popc(cm);
+    } else {
+      k = min(32u, a.ncore - r0);
+    }
+    const uint32_t items = k * (uint32_t)nb;
     for (uint32_t it = lane; it < items; it += 32) {
       const uint32_t ci = it / nb, col = it - ci * nb;
-      const uint32_t g = c0 + (uint32_t)(__fns(cm, 0, ci + 1));
-      const uint32_t kg = a.core_cnt[g];
+      const uint32_t g = BY_CELLS ? r0 + (uint32_t)__fns(cm, 0, ci + 1) : a.core_list[r0 + ci];
       const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
       uint32_t id0;
-      const uint32_t nc = col_probe(a.bm, a.pre, base + (uint64_t)s_off[col], s_mask[col], &id0);
-      for (uint32_t h = id0; h < id0 + nc; ++h) {
+      const uint32_t nc = dir_probe(a.cdir, base + (uint64_t)s_off[col], s_mask[col], &id0);
+      if (!nc) continue;
+      const uint32_t kg = a.core_cnt[g], sg = a.cell_start[g];
+      for (uint32_t r = id0; r < id0 + nc; ++r) {
+        const uint32_t h = a.core_list[r];
         const uint32_t kh = a.core_cnt[h];
-        if (kh == 0) continue;
         if ((uint64_t)kg * kh > SP_SMALL) {
           if (uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
           const uint32_t slot = atomicAdd(a.counters + 2, 1u);
@@ -289,7 +445,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
           // list full: test the pair here (correct, only slower)
         }
         ++mine;
-        const uint32_t sg = a.cell_start[g], sh = a.cell_start[h];
+        const uint32_t sh = a.cell_start[h];
         bool hit = false;
         for (uint32_t u = sg; u < sg + kg && !hit; ++u) {
           int32_t p[D];
@@ -297,7 +453,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
           for (uint32_t v = sh; v < sh + kh; ++v) {
             int32_t q[D];
             load_pt<D>(a.Ps, v, q);
-            if (within<D, WIDE>(p, q, a.g.clampc, a.g.eps2)) { hit = true; break; }
+            if (within_dim<DIM, D, WIDE>(p, q, a.g)) { hit = true; break; }
           }
         }
         if (hit) uf_link(a.parent, g, h);
@@ -308,15 +464,15 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
 }
 
 // --------------------------------------------------------- ClusterBorder (a10)
-// Does cell h hold a core point within eps of p? Core points are first in
+// Does core cell h hold a core point within eps of p? Core points are first in
 // their cell (a7), so they are Ps[cell_start[h] .. + core_cnt[h]).
-template <int D, bool WIDE>
-__device__ __forceinline__ bool sp_core_within(const SpArgs& a, const int32_t* p, uint32_t h, uint32_t kh) {
-  const uint32_t sh = a.cell_start[h];
+template <int DIM, int D, bool WIDE>
+__device__ __forceinline__ bool sp_core_within(const SpArgs& a, const int32_t* p, uint32_t h) {
+  const uint32_t sh = a.cell_start[h], kh = a.core_cnt[h];
   for (uint32_t v = sh; v < sh + kh; ++v) {
     int32_t q[D];
     load_pt<D>(a.Ps, v, q);
-    if (within<D, WIDE>(p, q, a.g.clampc, a.g.eps2)) return true;
+    if (within_dim<DIM, D, WIDE>(p, q, a.g)) return true;
   }
   return false;
 }
@@ -329,24 +485,23 @@ __device__ uint32_t sp_next_label(const SpArgs& a, const long long* s_off, const
   uint32_t best = MISS;
   for (int c = 0; c < a.ncols; ++c) {
     uint32_t id0;
-    const uint32_t nc = col_probe(a.bm, a.pre, base + (uint64_t)s_off[c], s_mask[c], &id0);
-    for (uint32_t h = id0; h < id0 + nc; ++h) {
-      const uint32_t kh = a.core_cnt[h];
-      if (kh == 0) continue;
+    const uint32_t nc = dir_probe(a.cdir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+    for (uint32_t r = id0; r < id0 + nc; ++r) {
+      const uint32_t h = a.core_list[r];
       const uint32_t lab = a.cell_label[h];
       if ((int64_t)lab <= after || lab >= best) continue;
-      if (h == g || sp_core_within<D, WIDE>(a, p, h, kh)) best = lab;
+      if (h == g || sp_core_within<DIM, D, WIDE>(a, p, h)) best = lab;
     }
   }
   return best;
 }
 
 // Thread per sorted non-core point (Alg 4): walk the stencil
-// columns nearest first; for each cell with core points whose label is not
-// yet in the set, scan its core points until one is within eps. The own cell
-// gives its label with no distance test (same cell => within eps,
-// P:L400-403). Up to SP_MAXL labels live in registers (unused = ~0, sorted
-// by a 4-input network at the end) and are staged per sorted position for the
+// columns nearest first on the core directory; for each core cell whose label
+// is not yet in the set, scan its core points until one is within eps. The
+// own cell gives its label with no distance test (same cell => within eps,
+// P:L400-403). Up to SP_MAXL labels live in registers (unused = ~0, sorted by
+// a 4-input network at the end) and are staged per sorted position for the
 // fill pass; larger sets are enumerated without storage in ascending order.
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_kernel(SpArgs a) {
@@ -366,13 +521,12 @@ __global__ void __launch_bounds__(256) sp_border_kernel(SpArgs a) {
     bool ovf = false;
     for (int c = 0; c < a.ncols && !ovf; ++c) {
       uint32_t id0;
-      const uint32_t nc = col_probe(a.bm, a.pre, base + (uint64_t)s_off[c], s_mask[c], &id0);
-      for (uint32_t h = id0; h < id0 + nc; ++h) {
-        const uint32_t kh = a.core_cnt[h];
-        if (kh == 0) continue;
+      const uint32_t nc = dir_probe(a.cdir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+      for (uint32_t r = id0; r < id0 + nc; ++r) {
+        const uint32_t h = a.core_list[r];
         const uint32_t lab = a.cell_label[h];
         if (lab == L0 || lab == L1 || lab == L2 || lab == L3) continue;
-        if (h != g && !sp_core_within<D, WIDE>(a, p, h, kh)) continue;
+        if (h != g && !sp_core_within<DIM, D, WIDE>(a, p, h)) continue;
         if (nl == 0) L0 = lab;
         else if (nl == 1) L1 = lab;
         else if (nl == 2) L2 = lab;
@@ -404,6 +558,99 @@ __global__ void __launch_bounds__(256) sp_border_kernel(SpArgs a) {
         after = nx;
       }
       a.tmp_n[j] = 0xff;
+    }
+    a.bcnt[a.idx[j]] = cnt;
+    bord = cnt > 0;
+  }
+  const uint32_t nb = __syncthreads_count(bord);
+  if (threadIdx.x == 0 && nb) atomicAdd(a.nborder, (unsigned long long)nb);
+}
+
+// Core-centric ClusterBorder (variant 1, default). Alg 4 asks, for every
+// non-core point p, which clusters have a core point within eps of p
+// (P:L876-904). On a sparse lattice most stencil cells of p hold no core
+// point (c5: 8% of points are core), so the search runs from the other side:
+// a thread per core cell h walks h's stencil columns on the directory of all
+// cells and tests every non-core point p found against h's core points; on a
+// hit it adds label(h) to p's label set, a lock-free set of SP_MAXL slots
+// (atomicCAS into the first slot that is empty or already holds the label;
+// slots fill in order, so a label appears once). A point whose set overflows
+// is flagged and enumerated later without storage (sp_next_label). The
+// relation "core point q within eps of p" is symmetric, so both sides find
+// the same pairs; p's own cell is h's centre column.
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  __syncthreads();
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < a.ncore; r += gridDim.x * blockDim.x) {
+    const uint32_t h = a.core_list[r];
+    const uint32_t sh = a.cell_start[h], kh = a.core_cnt[h];
+    const uint32_t lab = a.cell_label[h];
+    const uint64_t base = cell_lin<DIM>(a.cell_key[h], a);
+    for (int c = 0; c < a.ncols; ++c) {
+      uint32_t id0;
+      const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+      if (!nc) continue;
+      const uint32_t ue = a.cell_start[id0 + nc];
+      for (uint32_t u = a.cell_start[id0]; u < ue; ++u) {
+        if (a.core_s[u]) continue;
+        int32_t p[D];
+        load_pt<D>(a.Ps, u, p);
+        bool hit = false;
+        for (uint32_t v = sh; v < sh + kh && !hit; ++v) {
+          int32_t q[D];
+          load_pt<D>(a.Ps, v, q);
+          hit = within_dim<DIM, D, WIDE>(p, q, a.g);
+        }
+        if (!hit) continue;
+        uint32_t* L = a.tmp_lab + (size_t)u * SP_MAXL;
+        bool placed = false;
+#pragma unroll
+        for (int t = 0; t < SP_MAXL; ++t) {
+          const uint32_t old = atomicCAS(L + t, MISS, lab);
+          if (old == MISS || old == lab) { placed = true; break; }
+        }
+        if (!placed) a.tmp_n[u] = 0xff;  // overflow: enumerate later
+      }
+    }
+  }
+}
+
+// Thread per sorted non-core point: sort its label set (4-input network),
+// count it into bcnt (input order), or count an overflowed set by the
+// storage-free ascending enumeration.
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  __syncthreads();
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  bool bord = false;
+  if (j < a.n && !a.core_s[j]) {
+    uint32_t cnt;
+    if (a.tmp_n[j] != 0xff) {
+      uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
+      auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
+      cs(v.x, v.y); cs(v.z, v.w); cs(v.x, v.z); cs(v.y, v.w); cs(v.y, v.z);
+      cnt = (v.x != MISS) + (v.y != MISS) + (v.z != MISS) + (v.w != MISS);
+      if (cnt > 1) *reinterpret_cast<uint4*>(a.tmp_lab + (size_t)j * SP_MAXL) = v;
+      a.tmp_n[j] = (uint8_t)cnt;
+    } else {
+      const uint32_t g = a.cell_of[j];
+      const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
+      int32_t p[D];
+      load_pt<D>(a.Ps, j, p);
+      int64_t after = -1;
+      cnt = 0;
+      while (true) {
+        const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
+        if (nx == MISS) break;
+        ++cnt;
+        after = nx;
+      }
     }
     a.bcnt[a.idx[j]] = cnt;
     bord = cnt > 0;
@@ -460,108 +707,90 @@ static unsigned __int128 padded_volume(const Geo& g) {
   return vol;
 }
 
+// Stencil columns: the offsets (and self) grouped by all but
+// the last axis; each group is |delta_last| <= m, one column of width 2m + 1.
+// Returns {squared gap of the prefix, {start offset, mask}} nearest first;
+// *back gets the columns of cells before the centre in linear order.
+typedef std::vector<std::pair<unsigned __int128, std::pair<long long, uint32_t>>> Cols;
+static Cols stencil_columns(const Geo& g, const uint64_t* stride, Cols* back) {
+  const std::vector<int8_t> offs = stencil_offsets(g);
+  const int noffs = (int)(offs.size() / g.d);
+  std::map<std::vector<int>, int> colm;
+  colm[std::vector<int>(g.d > 1 ? g.d - 1 : 0, 0)] = 0;
+  for (int t = 0; t < noffs; ++t) {
+    std::vector<int> pfx(offs.begin() + (size_t)t * g.d, offs.begin() + (size_t)t * g.d + g.d - 1);
+    const int v = offs[(size_t)t * g.d + g.d - 1];
+    int& mm = colm[pfx];
+    mm = std::max(mm, v < 0 ? -v : v);
+  }
+  Cols cols;
+  back->clear();
+  for (auto& [pfx, mm] : colm) {
+    int first = 0;  // sign of the first non-zero prefix component
+    for (int v : pfx)
+      if (v) { first = v < 0 ? -1 : 1; break; }
+    unsigned __int128 gap = 0;
+    long long off = -(long long)mm;
+    for (int k = 0; k + 1 < g.d; ++k) {
+      const int v = pfx[k] < 0 ? -pfx[k] : pfx[k];
+      if (v) { const unsigned __int128 gg = (unsigned __int128)(v - 1) * g.s + 1; gap += gg * gg; }
+      off += (long long)pfx[k] * (long long)stride[k];
+    }
+    const uint32_t full = (uint32_t)((1ull << (2 * mm + 1)) - 1);
+    cols.push_back({gap, {off, full}});
+    if (first < 0) back->push_back({gap, {off, full}});
+    else if (first == 0 && mm > 0) back->push_back({gap, {off, (uint32_t)((1ull << mm) - 1)}});
+  }
+  auto by_gap = [](const auto& x, const auto& y) { return x.first < y.first; };
+  std::stable_sort(cols.begin(), cols.end(), by_gap);
+  std::stable_sort(back->begin(), back->end(), by_gap);
+  return cols;
+}
+
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced) {
   if (g.d > 3) return false;
-  // 2 bits per lattice cell: keep the directory within ~32 bytes per point
+  // 4 bits per lattice cell (two directories of 16 B per 32 cells): keep them
+  // within ~64 bytes per point
   if (padded_volume(g) > (unsigned __int128)128 * n + (1u << 24)) return false;
-  if (stencil_offsets(g).size() / g.d + 1 > (size_t)SP_MAX_OFFS) return false;
+  uint64_t stride[3] = {0, 0, 0};
+  unsigned __int128 vol = 1;
+  for (int k = g.d - 1; k >= 0; --k) {
+    stride[k] = (uint64_t)vol;
+    vol *= (unsigned __int128)g.maxc[k] + 1 + 2 * (unsigned __int128)g.R;
+  }
+  Cols back;
+  if (stencil_columns(g, stride, &back).size() > (size_t)SP_MAX_COLS) return false;
   if (forced) return true;
   return (uint64_t)n <= (uint64_t)SPARSE_MEAN_PER_CELL * ncells;
 }
 
-void sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
-                     uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
-                     bool waves, SparseOut* o) {
-  (void)waves;
+// Build a directory over the padded lattice for every cell (only_if = NULL)
+// or the cells with only_if[g] > 0.
+static uint4* build_dir(Ctx& c, const SpArgs& a, uint64_t words, const uint32_t* only_if) {
+  uint32_t* bm = c.alloc<uint32_t>(words);
+  uint32_t* wcnt = c.alloc<uint32_t>(words);
+  uint32_t* pre = c.alloc<uint32_t>(words + 1);
+  uint4* dir = c.alloc<uint4>(words);
+  c.zero(bm, sizeof(uint32_t) * words);
+  dir_set_kernel<<<grid_for(a.ncells, 256, 1 << 30), 256, 0, c.st>>>(a.cell_key, a.ncells, a, only_if, bm);
+  c.launched();
+  popc_kernel<<<grid_for((int64_t)words, 256, 1 << 30), 256, 0, c.st>>>(bm, words, wcnt);
+  c.launched();
+  exclusive_scan_u32_u32(c, wcnt, pre, (int64_t)words);
+  dir_pack_kernel<<<grid_for((int64_t)words, 256, 1 << 30), 256, 0, c.st>>>(bm, pre, words, dir);
+  c.launched();
+  return dir;
+}
+
+uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
+                         uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
+                         const uint4* dir, SparseOut* o) {
   SpArgs a{};
   a.g = g;
   unsigned __int128 vol = 1;
   for (int k = g.d - 1; k >= 0; --k) {
     a.stride[k] = (uint64_t)vol;
     vol *= (unsigned __int128)g.maxc[k] + 1 + 2 * (unsigned __int128)g.R;
-  }
-  // stencil offsets in padded linear units, nearest first; back offsets per wave
-  std::vector<int8_t> offs = stencil_offsets(g);
-  const int noffs = (int)(offs.size() / g.d);
-  // Global MarkCore bound (Alg 2's count can never exceed the points of the
-  // stencil cells, reading 13): if (stencil cells) x (largest cell) < minPts
-  // no point can be core and the caller takes the all-noise exit.
-  if ((uint64_t)min_pts > (uint64_t)noffs + 1) {
-    uint32_t* mx = c.alloc<uint32_t>(1);
-    c.zero(mx, sizeof(uint32_t));
-    cell_max_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(cv.cell_start, cv.ncells, mx);
-    c.launched();
-    const uint64_t bound = (uint64_t)c.read(mx) * (uint64_t)(noffs + 1);
-    if (bound < (uint64_t)min_pts) return;  // counters[0] (core cells) stays 0
-  }
-  // rank directory
-  const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
-  uint32_t* bm = c.alloc<uint32_t>(words);
-  uint32_t* wcnt = c.alloc<uint32_t>(words);
-  uint32_t* pre = c.alloc<uint32_t>(words + 1);
-  c.zero(bm, sizeof(uint32_t) * words);
-  a.bm = bm;
-  a.pre = pre;
-  rd_set_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(cv.cell_key, cv.ncells, a, bm);
-  c.launched();
-  popc_kernel<<<grid_for((int64_t)words, 256, 1 << 30), 256, 0, c.st>>>(bm, words, wcnt);
-  c.launched();
-  exclusive_scan_u32_u32(c, wcnt, pre, (int64_t)words);
-  // stencil columns: group the offsets (and self) by all but the last axis;
-  // each group is |delta_last| <= m, one column of width 2m + 1
-  {
-    std::map<std::vector<int>, int> colm;
-    std::vector<int> zero(g.d > 1 ? g.d - 1 : 0, 0);
-    colm[zero] = 0;
-    for (int t = 0; t < noffs; ++t) {
-      std::vector<int> pfx(offs.begin() + (size_t)t * g.d, offs.begin() + (size_t)t * g.d + g.d - 1);
-      const int v = offs[(size_t)t * g.d + g.d - 1];
-      int& mm = colm[pfx];
-      mm = std::max(mm, v < 0 ? -v : v);
-    }
-    std::vector<std::pair<unsigned __int128, std::pair<long long, uint32_t>>> cols, bcols;
-    for (auto& [pfx, mm] : colm) {
-      int first = 0;  // sign of the first non-zero prefix component
-      for (int v : pfx)
-        if (v) { first = v < 0 ? -1 : 1; break; }
-      unsigned __int128 gap = 0;
-      long long off = -(long long)mm;
-      for (int k = 0; k + 1 < g.d; ++k) {
-        const int v = pfx[k] < 0 ? -pfx[k] : pfx[k];
-        if (v) { const unsigned __int128 gg = (unsigned __int128)(v - 1) * g.s + 1; gap += gg * gg; }
-        off += (long long)pfx[k] * (long long)a.stride[k];
-      }
-      cols.push_back({gap, {off, (uint32_t)((1ull << (2 * mm + 1)) - 1)}});
-      // back columns: every cell precedes g in linear order (prefix < 0), or
-      // the cells below g in its own column
-      if (first < 0) bcols.push_back({gap, {off, (uint32_t)((1ull << (2 * mm + 1)) - 1)}});
-      else if (first == 0 && mm > 0) bcols.push_back({gap, {off, (uint32_t)((1ull << mm) - 1)}});
-    }
-    std::stable_sort(bcols.begin(), bcols.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
-    std::stable_sort(cols.begin(), cols.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
-    if ((int)cols.size() > SP_MAX_COLS) throw Error(-4, "sparse path: too many stencil columns");
-    std::vector<long long> co;
-    std::vector<uint32_t> cm;
-    for (auto& e : cols) { co.push_back(e.second.first); cm.push_back(e.second.second); }
-    long long* dco = c.alloc<long long>(co.size());
-    uint32_t* dcm = c.alloc<uint32_t>(cm.size());
-    DB_CUDA(cudaMemcpyAsync(dco, co.data(), sizeof(long long) * co.size(), cudaMemcpyHostToDevice, c.st));
-    DB_CUDA(cudaMemcpyAsync(dcm, cm.data(), sizeof(uint32_t) * cm.size(), cudaMemcpyHostToDevice, c.st));
-    a.coff = dco;
-    a.cmask = dcm;
-    a.ncols = (int)cols.size();
-    std::vector<long long> bo;
-    std::vector<uint32_t> bmk;
-    for (auto& e : bcols) { bo.push_back(e.second.first); bmk.push_back(e.second.second); }
-    bo.push_back(0);
-    bmk.push_back(0);
-    long long* dbo = c.alloc<long long>(bo.size());
-    uint32_t* dbm = c.alloc<uint32_t>(bmk.size());
-    DB_CUDA(cudaMemcpyAsync(dbo, bo.data(), sizeof(long long) * bo.size(), cudaMemcpyHostToDevice, c.st));
-    DB_CUDA(cudaMemcpyAsync(dbm, bmk.data(), sizeof(uint32_t) * bmk.size(), cudaMemcpyHostToDevice, c.st));
-    a.bcoff = dbo;
-    a.bcmask = dbm;
-    a.nbcols = (int)bcols.size();
   }
   a.ncells = cv.ncells;
   a.cell_start = cv.cell_start;
@@ -574,55 +803,135 @@ void sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uin
   a.min_pts = min_pts;
   a.n = n;
   a.counters = o->counters;  // [4], zeroed by the caller
-  a.mixed_list = c.alloc<uint32_t>(cv.ncells);
+  Cols back;
+  const Cols cols = stencil_columns(g, a.stride, &back);
+  if ((int)cols.size() > SP_MAX_COLS) throw Error(-4, "sparse path: too many stencil columns");
+  // Global MarkCore bound (Alg 2's count can never exceed the points of the
+  // stencil cells, reading 13): if (stencil cells) x (largest cell) < minPts
+  // no point can be core and the caller takes the all-noise exit.
+  uint64_t stencil_cells = 0;
+  for (auto& e : cols) stencil_cells += (uint64_t)__builtin_popcount(e.second.second);
+  if (!dir && (uint64_t)min_pts > stencil_cells) {  // (the lattice sort checked it already)
+    uint32_t* mx = c.alloc<uint32_t>(1);
+    c.zero(mx, sizeof(uint32_t));
+    cell_max_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(cv.cell_start, cv.ncells, mx);
+    c.launched();
+    if ((uint64_t)c.read(mx) * stencil_cells < (uint64_t)min_pts) return 0;  // no core point
+  }
+  auto upload = [&](const Cols& cs, const long long** off, const uint32_t** mask) {
+    std::vector<long long> co;
+    std::vector<uint32_t> cm;
+    for (auto& e : cs) { co.push_back(e.second.first); cm.push_back(e.second.second); }
+    co.push_back(0);
+    cm.push_back(0);
+    long long* dco = c.alloc<long long>(co.size());
+    uint32_t* dcm = c.alloc<uint32_t>(cm.size());
+    DB_CUDA(cudaMemcpyAsync(dco, co.data(), sizeof(long long) * co.size(), cudaMemcpyHostToDevice, c.st));
+    DB_CUDA(cudaMemcpyAsync(dcm, cm.data(), sizeof(uint32_t) * cm.size(), cudaMemcpyHostToDevice, c.st));
+    *off = dco;
+    *mask = dcm;
+  };
+  upload(cols, &a.coff, &a.cmask);
+  a.ncols = (int)cols.size();
+  upload(back, &a.bcoff, &a.bcmask);
+  a.nbcols = (int)back.size();
+  // a4: directory of all cells
+  const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
+  a.dir = dir ? dir : build_dir(c, a, words, nullptr);
+  // a6: MarkCore (variant chosen by DBSCAN_SP_CORE for measurements: 0 warp
+  // per cell, 1 thread per point nested, 2 thread per point flat)
+  static const int variant = getenv("DBSCAN_SP_CORE") ? atoi(getenv("DBSCAN_SP_CORE")) : 1;
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
-    sp_core_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+    if (variant == 0)
+      sp_core_kernel<DIM, D, W><<<grid_for((int64_t)cv.ncells * 32, 256, c.sms * 32), 256, 0, c.st>>>(a);
+    else if (variant == 1)
+      sp_core_thread_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+    else if (variant == 3) {
+      const int smem = (int)(sizeof(uint2) * SPC_THREADS * a.ncols);
+      DB_CUDA(cudaFuncSetAttribute(sp_core_2p_kernel<DIM, D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      sp_core_2p_kernel<DIM, D, W><<<grid_for(n, SPC_THREADS, 1 << 30), SPC_THREADS, smem, c.st>>>(a);
+    }
+    else
+      sp_core_flat_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
   });
   c.launched();
+  // a7: core counts, core-first partition of mixed cells
+  a.mixed_list = c.alloc<uint32_t>(cv.ncells);
   sp_cells_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(a);
   c.launched();
   partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, Ps, idx, core_s, n);
+  // directory of the cells holding core points, and their list in linear order
+  a.cdir = build_dir(c, a, words, core_cnt);
+  uint32_t* core_list = c.alloc<uint32_t>(cv.ncells);
+  a.core_list = core_list;
+  core_list_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(a, core_list);
+  c.launched();
+  a.ncore = c.read(a.counters);
   o->stash = new SpArgs(a);
+  return a.ncore;
 }
 
 void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                    const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
+                    const uint32_t* core_cnt, bool wide, uint32_t* parent,
                     unsigned long long* tested, SparseOut* o) {
-  (void)waves;  // one pass: small pairs are tested without Find (see sp_pairs_kernel)
   SpArgs& a = *(SpArgs*)o->stash;
   a.parent = parent;
-  a.large_cap = cv.ncells + 4096;
+  a.large_cap = a.ncore + 4096;
   a.large = c.alloc<uint2>(a.large_cap);
   uf_init(c, parent, cv.ncells);
-  const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
-  c.zero(a.counters + 2, sizeof(uint32_t));
-  by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
-    constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
-    constexpr bool W = decltype(Wd)::value;
-    sp_pairs_kernel<DIM, D, W><<<grid, 256, 0, c.st>>>(a, tested);
-  });
-  c.launched();
-  bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
+  if (a.nbcols > 0 && a.ncore > 0) {
+    static const int variant = getenv("DBSCAN_SP_PAIRS") ? atoi(getenv("DBSCAN_SP_PAIRS")) : 1;
+    const uint32_t units = variant ? cv.ncells : a.ncore;
+    const unsigned grid = grid_for(((int64_t)units + 31) / 32 * 32, 256, c.sms * 16);
+    c.zero(a.counters + 2, sizeof(uint32_t));
+    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
+      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
+      constexpr bool W = decltype(Wd)::value;
+      if (variant) sp_pairs_kernel<DIM, D, W, true><<<grid, 256, 0, c.st>>>(a, tested);
+      else sp_pairs_kernel<DIM, D, W, false><<<grid, 256, 0, c.st>>>(a, tested);
+    });
+    c.launched();
+    bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
+  }
 }
 
-int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, int64_t n, bool wide,
-                      int64_t* border_off, unsigned long long* nborder, SparseOut* o) {
+int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const int32_t* cluster, int64_t n,
+                      bool wide, int64_t* border_off, unsigned long long* nborder, SparseOut* o) {
   SpArgs& a = *(SpArgs*)o->stash;
   a.cell_label = cell_label;
   a.bcnt = c.alloc<uint32_t>(n);
   a.tmp_lab = c.alloc<uint32_t>((size_t)n * SP_MAXL);
   a.tmp_n = c.alloc<uint8_t>(n);
   a.nborder = nborder;
-  c.zero(a.bcnt, sizeof(uint32_t) * n);
-  by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
-    constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
-    constexpr bool W = decltype(Wd)::value;
-    sp_border_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
-  });
-  c.launched();
-  exclusive_scan_u32_i64(c, a.bcnt, border_off, n);
+  static const int variant = getenv("DBSCAN_SP_BORDER") ? atoi(getenv("DBSCAN_SP_BORDER")) : 1;
+  if (variant == 1) {
+    // core-centric: label sets of SP_MAXL slots per sorted point, empty = ~0
+    DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
+    c.zero(a.tmp_n, (size_t)n);
+    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
+      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
+      constexpr bool W = decltype(Wd)::value;
+      sp_border_emit_kernel<DIM, D, W><<<grid_for(a.ncore, 256, c.sms * 16), 256, 0, c.st>>>(a);
+      c.launched();
+      sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+      c.launched();
+    });
+  } else {
+    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
+      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
+      constexpr bool W = decltype(Wd)::value;
+      sp_border_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+    });
+    c.launched();
+  }
+  if (c.read(nborder) == 0) {
+    DB_CUDA(cudaMemsetAsync(border_off, 0, sizeof(int64_t) * (size_t)(n + 1), c.st));
+    return 0;
+  }
+  // counts exist for non-core points only; core points (cluster >= 0) read as 0
+  exclusive_scan_u32_i64_masked(c, a.bcnt, cluster, border_off, n);
   return c.read(border_off + n);
 }
 

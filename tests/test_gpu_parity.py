@@ -97,7 +97,9 @@ def test_random_small_vs_o1(oracle_lib):
                                    pkg.F_FORCE_WIDE | pkg.F_FORCE_TREE | pkg.F_NO_WAVES,
                                    pkg.F_FORCE_SPARSE, pkg.F_NO_SPARSE,
                                    pkg.F_FORCE_SPARSE | pkg.F_FORCE_WIDE | pkg.F_NO_WAVES,
-                                   pkg.F_RADIX_GROUP, pkg.F_RADIX_GROUP | pkg.F_FORCE_SPARSE])
+                                   pkg.F_RADIX_GROUP, pkg.F_RADIX_GROUP | pkg.F_FORCE_SPARSE,
+                                   pkg.F_LATTICE_GROUP, pkg.F_LATTICE_GROUP | pkg.F_FORCE_SPARSE,
+                                   pkg.F_LATTICE_GROUP | pkg.F_NO_SPARSE])
 def test_flag_variants_vs_o1(oracle_lib, flags):
     for k, (pts, eps, mp) in enumerate(_instances(200 + flags, 120, dmax=8)):
         r = run_or_erange(pts, eps, mp, flags)
@@ -115,7 +117,7 @@ def test_force_stencil_high_d_vs_o1(oracle_lib):
             assert_same(r, oracle_lib.o1(pts, eps, mp), f"{k}")
 
 
-@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP], ids=["hash", "radix"])
+@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP, pkg.F_LATTICE_GROUP], ids=["hash", "radix", "lattice"])
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 7, 8])
 def test_clustered_medium_vs_o2(oracle_lib, d, grouping):
     """Seed-spreader data with dense cells, many neighbours, border points,
@@ -175,7 +177,7 @@ def test_empty():
         assert len(r.core) == 0 and list(r.border_off) == [0] and len(r.border_ids) == 0
 
 
-@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP], ids=["hash", "radix"])
+@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP, pkg.F_LATTICE_GROUP], ids=["hash", "radix", "lattice"])
 @pytest.mark.parametrize("n", [4095, 4096, 4097, 8191, 12289])
 def test_tile_boundaries_vs_o2(oracle_lib, n, grouping):
     """Ragged tails at the radix (4096), scan (2048) and segment (2048) tiles."""
@@ -210,7 +212,8 @@ def test_stream_and_stats():
     assert r.stats["ncells"] > 0 and r.n_core + r.n_border + r.n_noise == len(pts)
 
 
-@pytest.mark.parametrize("flags", [0, pkg.F_NO_SPARSE, pkg.F_RADIX_GROUP])
+@pytest.mark.parametrize("flags", [0, pkg.F_NO_SPARSE, pkg.F_RADIX_GROUP, pkg.F_LATTICE_GROUP,
+                                   pkg.F_LATTICE_GROUP | pkg.F_NO_SPARSE])
 def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
     """Both the cell-centric sparse path and the CSR path on sparse lattices
     (1-8 points per cell), 1D-3D, with border points in several clusters."""
@@ -218,16 +221,21 @@ def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
                               (1, 50_000, 200_000, 3, 3), (3, 60_000, 4_000, 300, 20)]:
         pts = datagen.uniform(n, d, hi, d + n)
         r = gpu(pts, eps, mp, flags)
-        if flags != pkg.F_NO_SPARSE and d == 3 and hi == 12_000:
+        if not (flags & pkg.F_NO_SPARSE) and d == 3 and hi == 12_000:
             assert r.stats["sparse"] == 1
-        assert r.stats["hash_group"] == (0 if flags & pkg.F_RADIX_GROUP else 1)
+        expect = 0 if flags & pkg.F_RADIX_GROUP else (2 if flags & pkg.F_LATTICE_GROUP else 1)
+        if expect == 2 and r.stats["hash_group"] == 0:
+            pass  # lattice too large for the counting sort (d=1 span): radix
+        else:
+            assert r.stats["hash_group"] == expect
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"d={d} flags={flags}")
 
 
 def test_grouping_choice():
-    """Few cells: the hash counting sort groups the points; more distinct cells
-    than its 2^20-slot table holds (uniform 3D, 2M points, ~2M cells): it
-    gives up and the radix sort runs; both give the same result."""
+    """Few cells: the hash counting sort groups the points; many distinct
+    cells (uniform 3D, 2M points, ~2M cells) on a lattice too large to count
+    over: the radix sort runs; on a small lattice: the lattice counting sort;
+    all give the same result."""
     few = datagen.seed_spreader(200_000, 3, 100_000, 5, p_step=0.01)
     r = gpu(few, 1000, 50)
     assert r.stats["hash_group"] == 1 and r.stats["sort_passes"] == 0
@@ -236,6 +244,23 @@ def test_grouping_choice():
     assert a.stats["hash_group"] == 0 and a.stats["sort_passes"] > 0
     b = gpu(many, 3000, 3, pkg.F_RADIX_GROUP)
     assert_same(np_result(a), np_result(b), "hash fallback vs radix")
+    dense = datagen.uniform(2_000_000, 3, 40_000, 7)
+    c = gpu(dense, 300, 4)
+    assert c.stats["hash_group"] == 2 and c.stats["sparse"] == 1
+    assert_same(np_result(c), np_result(gpu(dense, 300, 4, pkg.F_RADIX_GROUP)), "lattice vs radix")
+    # Alg 2's global bound: no point can reach minPts, nothing is grouped
+    e = gpu(dense, 300, 5000)
+    assert e.n_core == 0 and e.stats["ncells"] == 0 and e.n_noise == len(dense)
+
+
+def test_lattice_overflow_falls_back():
+    """More than 255 points in one lattice cell overflows its 8-bit counter:
+    the radix sort takes over with the same result."""
+    pts = datagen.uniform(300_000, 2, 3000, 8)
+    pts[:400] = pts[0]
+    r = gpu(pts, 20, 3, pkg.F_LATTICE_GROUP)
+    assert r.stats["hash_group"] == 0
+    assert_same(np_result(r), np_result(gpu(pts, 20, 3, pkg.F_RADIX_GROUP)), "overflow fallback")
 
 
 @pytest.mark.parametrize("d", [2, 3, 5, 7])
