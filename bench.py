@@ -43,6 +43,22 @@ SUITE = ["c2", "c3", "c4_5d", "c4_7d", "c5_10", "c5_10k"]
 REF_FRACTION = 0.05
 
 
+# int32 issue peak: 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz = 37.2 T
+# lane-instructions/s; a 3D distance test is ~10 int32 SASS instructions
+# (3 x VABSDIFF/VIMNMX/IMAD + compare): ~3.7e12 tests/s
+INT_TESTS_PEAK = 148 * 4 * 32 * 1.965e9 / 10
+
+
+def load_traffic():
+    """Per-launch DRAM bytes (read + write) from the committed ncu --set full
+    summary (profiles/r1_traffic.json), or {} when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -63,13 +79,19 @@ class ClockSampler:
         self.rows = []
         self.proc = None
 
-    def start(self):
+    def start(self, wait_s=3.0):
+        """Start sampling and wait for the first sample, so that the timed
+        region that follows is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < wait_s:
+                time.sleep(0.01)
+            self.rows.clear()
         except Exception:
             self.proc = None
 
@@ -190,6 +212,14 @@ def main():
             del r
         return ms, stages, launches, stats
 
+    # algorithmic work of the sparse MarkCore: one counting run per run (untimed)
+    work_tests = {}
+    for name, cfg, t, _ in data:
+        r = pkg.dbscan(t, cfg.eps, cfg.min_pts, flags=pkg.F_COUNT_WORK)
+        if r.stats.get("markcore_tests"):
+            work_tests[name] = r.stats["markcore_tests"]
+        del r
+    torch.cuda.synchronize()
     for _ in range(args.warmup):
         one_step(False)
     if dist:
@@ -221,25 +251,55 @@ def main():
     npts_step = sum(c.n for _, c, _, _ in data)
     value = npts_step * args.steps * world / (total_ms / 1000.0)
 
-    # ---- roofline: the radix sort (largest HBM consumer)
+    # ---- rooflines. Stage times come from CUDA events the
+    # library records on the launching stream (F_TIMING); algorithmic work per
+    # run from the run's shape and, for the sparse MarkCore, from one counting
+    # run (F_COUNT_WORK) outside the timed region.
     peak, peak_kind = load_peaks()
-    sort_bytes = 0.0
-    sort_ms = 0.0
+    traffic = load_traffic()
+    stage_tot = {}
+    for i in range(len(runs)):
+        for k, v in stage_acc[i].items():
+            if k != "total":
+                stage_tot[k] = stage_tot.get(k, 0.0) + v
+    rooflines = []
+    # grouping (a2-a4): the largest HBM stage; algorithmic bytes = read the
+    # points twice + write the padded sorted points, index and cell id, plus
+    # the cell table (12 B per cell); the radix path adds its key passes
+    g_bytes = g_ms = 0.0
     for i, (name, cfg, t, _) in enumerate(data):
         st = stats[i]
-        kb = 8 if st["key_bits"] > 32 else 4
-        # per pass: read + write (key, index) = 2*(kb+4) bytes per point
-        sort_bytes += st["sort_passes"] * 2 * (kb + 4) * cfg.n * args.steps
-        sort_ms += stage_acc[i].get("keys+sort", 0.0)
-    # keys kernel: read d*4 per point, write key+index
-    keys_bytes = sum((4 * c.d + (8 if stats[i]["key_bits"] > 32 else 4) + 4) * c.n
-                     for i, (_, c, _, _) in enumerate(data)) * args.steps
-    achieved = (sort_bytes + keys_bytes) / (sort_ms / 1000.0) / 1e9 if sort_ms > 0 else None
-    roofline = {"bound": "hbm", "kernel": "keys_kernel + radix_pass_kernel (stage keys+sort)",
-                "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "peak_kind": peak_kind,
-                "note": "algorithmic bytes: keys 4d+kb+4 per point; each LSD pass reads and writes (key,idx)"}
+        D = 2 if cfg.d <= 2 else (4 if cfg.d <= 4 else 8)
+        by = (8 * cfg.d + 4 * D + 8) * cfg.n + 12 * st["ncells"]
+        if st["hash_group"] == 0 and st["sort_passes"]:
+            kb = 8 if st["key_bits"] > 32 else 4
+            by += (kb + 4) * cfg.n + st["sort_passes"] * 2 * (kb + 4) * cfg.n
+        g_bytes += by * args.steps
+        g_ms += stage_acc[i].get("keys+sort", 0.0) + stage_acc[i].get("segment", 0.0)
+    if g_ms > 0:
+        ach = g_bytes / (g_ms / 1e3) / 1e9
+        rooflines.append({"stage": "a2-a4 grouping", "bound": "hbm",
+                          "kernel": "group_count/group_scatter (hash), lat_* (lattice), radix_pass+segment",
+                          "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                          "traffic": traffic.get("grouping"),
+                          "traffic_note": "DRAM bytes per call of the grouping kernels by run, ncu --set full (cold L2)",
+                          "peak_kind": peak_kind,
+                          "ms_share": g_ms / max(1e-9, sum(stage_tot.values())),
+                          "note": "algorithmic bytes: 8d+4D+8 per point + 12 per cell (+ key passes on the radix path)"})
+    # sparse MarkCore (a6): int32 ALU issue bound; tests per second
+    for i, (name, cfg, t, _) in enumerate(data):
+        if stats[i]["sparse"] and work_tests.get(name):
+            ms = stage_acc[i].get("markcore", 0.0) / args.steps
+            if ms <= 0:
+                continue
+            ach = work_tests[name] / (ms / 1e3) / 1e12
+            tp = INT_TESTS_PEAK / 1e12
+            rooflines.append({"stage": f"a6 MarkCore ({name})", "bound": "alu", "kernel": "sp_core_kernel",
+                              "achieved": ach, "peak": tp, "unit": "T distance tests/s", "frac": ach / tp,
+                              "traffic": traffic.get("sp_core_kernel"), "peak_kind": "derived (DESIGN.md §8)",
+                              "ms_share": ms * args.steps / max(1e-9, sum(stage_tot.values())),
+                              "tests_per_launch": work_tests[name]})
+    roofline = max(rooflines, key=lambda r: r["ms_share"]) if rooflines else None
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None
@@ -250,7 +310,8 @@ def main():
             hp = torch.from_numpy(pts).pin_memory()
             outs = (torch.empty(cfg.n, dtype=torch.uint8).pin_memory(),
                     torch.empty(cfg.n, dtype=torch.int32).pin_memory(),
-                    torch.empty(cfg.n + 1, dtype=torch.int64).pin_memory())
+                    torch.empty(cfg.n + 1, dtype=torch.int64).pin_memory(),
+                    torch.empty(cfg.n, dtype=torch.int32).pin_memory())
             host.append((cfg, hp, outs))
         def e2e_step():
             nonlocal h2d, d2h
@@ -297,7 +358,8 @@ def main():
             "config": {"workload": "suite: BASELINE configs[1..4] (c2,c3,c4_5d,c4_7d,c5 minPts 10 and 1e4)",
                        "runs": runs, "points_per_step": npts_step, "l2": "flushed (256 MB write) before every run",
                        "parallelism": "replicas" if world > 1 else "single GPU"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "rooflines": rooflines, "stage_ms_per_step": {k: round(v / args.steps, 4) for k, v in stage_tot.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "runs": run_info}
     if args.detail and rank == 0:
         for ri in run_info:

@@ -43,7 +43,9 @@ extern "C" {
 #define DBSCAN_F_TIMING        2u  /* fill out->stage_ms with CUDA-event times (adds a sync) */
 #define DBSCAN_F_CALLER_OUT    4u  /* out->core, out->cluster, out->border_off are caller-
                                       allocated ([n], [n], [n+1]; host or device per
-                                      F_DEVICE_IO); the library allocates border_ids only */
+                                      F_DEVICE_IO). out->border_ids may also be set, with
+                                      its capacity (elements) in out->nnz: it is used when
+                                      the result fits, else the library allocates one    */
 #define DBSCAN_F_FORCE_STENCIL 8u  /* neighbour cells by stencil enumeration for every d */
 #define DBSCAN_F_FORCE_TREE   16u  /* neighbour cells by the cell tree for every d */
 #define DBSCAN_F_FORCE_WIDE   32u  /* 64-bit distance arithmetic even where 32-bit is exact */
@@ -55,6 +57,8 @@ extern "C" {
                                       the hash-table or lattice counting sorts)              */
 #define DBSCAN_F_LATTICE_GROUP 1024u /* skip the hash counting sort: use the lattice counting
                                       sort whenever d <= 3 and its lattice fits               */
+#define DBSCAN_F_COUNT_WORK  2048u /* count the sparse MarkCore's distance tests into
+                                      stats[DBSCAN_STAT_MARKCORE_TESTS] (measurement runs)   */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
@@ -87,6 +91,7 @@ extern "C" {
 #define DBSCAN_STAT_SPARSE       12  /* 1 if the cell-centric sparse-lattice path ran       */
 #define DBSCAN_STAT_HASH_GROUP   13  /* grouping: 1 hash counting sort, 2 lattice counting sort,
                                         0 LSD radix sort + segmentation                      */
+#define DBSCAN_STAT_MARKCORE_TESTS 14 /* distance tests of the sparse MarkCore (F_COUNT_WORK)  */
 #define DBSCAN_NSTATS            16
 
 typedef struct dbscan_result {

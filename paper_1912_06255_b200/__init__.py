@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = ["dbscan", "Result", "lib_path", "load", "F_DEVICE_IO", "F_TIMING", "F_CALLER_OUT",
            "F_FORCE_STENCIL", "F_FORCE_TREE", "F_FORCE_WIDE", "F_NO_WAVES", "F_NO_SPARSE",
-           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "STAGES", "STATS",
+           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "F_COUNT_WORK", "STAGES", "STATS",
            "DBSCANError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -36,12 +36,12 @@ lib_path = os.path.join(_HERE, "libdbscan_b200.so")
 # flags (include/dbscan.h)
 F_DEVICE_IO, F_TIMING, F_CALLER_OUT = 1, 2, 4
 F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
-F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP = 128, 256, 512, 1024
+F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP, F_COUNT_WORK = 128, 256, 512, 1024, 2048
 NSTAGES, NSTATS = 12, 16
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
-         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group"]
+         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests"]
 
 
 class _Result(C.Structure):
@@ -144,8 +144,9 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
     tensors on the same device, computed on `stream` or the current stream),
     or a host array / CPU tensor (host path: the library copies in and out;
     pinned memory makes those copies fast; outputs are numpy arrays).
-    out: optional (core, cluster, border_off) caller buffers for the host path
-    (e.g. pinned CPU tensors), passed with DBSCAN_F_CALLER_OUT.
+    out: optional (core, cluster, border_off[, border_ids]) caller buffers for
+    the host path (e.g. pinned CPU tensors), passed with DBSCAN_F_CALLER_OUT;
+    border_ids is used when the result fits it (returned as a prefix view).
     """
     lib = load()
     import torch
@@ -190,9 +191,14 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
             raise TypeError("points must be (n, d)")
         ptr, (n, d) = keep.ctypes.data, keep.shape
     f = flags & ~F_DEVICE_IO
+    ids_b = None
     if out is not None:
-        core_b, cl_b, off_b = out
+        core_b, cl_b, off_b = out[:3]
         res.core, res.cluster, res.border_off = (_hostptr(core_b), _hostptr(cl_b), _hostptr(off_b))
+        if len(out) > 3 and out[3] is not None:
+            ids_b = out[3]
+            res.border_ids = _hostptr(ids_b)
+            res.nnz = len(ids_b)
         f |= F_CALLER_OUT
     st = 0 if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
     rc = lib.dbscan(C.c_void_p(ptr), n, d, int(eps), int(min_pts), f, C.c_void_p(st), C.byref(res))
@@ -200,13 +206,16 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
     _check(lib, rc)
     nnz = int(res.nnz)
     if out is not None:
-        core, cluster, off = out
+        core, cluster, off = out[:3]
     else:
         core = np.ctypeslib.as_array(C.cast(res.core, C.POINTER(C.c_uint8)), shape=(n,)).copy() if n else np.zeros(0, np.uint8)
         cluster = np.ctypeslib.as_array(C.cast(res.cluster, C.POINTER(C.c_int32)), shape=(n,)).copy() if n else np.zeros(0, np.int32)
         off = np.ctypeslib.as_array(C.cast(res.border_off, C.POINTER(C.c_int64)), shape=(n + 1,)).copy()
-    ids = (np.ctypeslib.as_array(C.cast(res.border_ids, C.POINTER(C.c_int32)), shape=(nnz,)).copy()
-           if nnz else np.zeros(0, np.int32))
+    if ids_b is not None and res.border_ids == _hostptr(ids_b):
+        ids = ids_b[:nnz]
+    else:
+        ids = (np.ctypeslib.as_array(C.cast(res.border_ids, C.POINTER(C.c_int32)), shape=(nnz,)).copy()
+               if nnz else np.zeros(0, np.int32))
     info = _finish(res, flags)
     out_res = Result(core, cluster, off, ids, int(res.n_core), int(res.n_border), int(res.n_noise),
                      int(res.n_clusters), **info)

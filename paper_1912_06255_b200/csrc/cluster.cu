@@ -274,14 +274,22 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
 }
 
 // ---------------------------------------------------------------- a9: labels
-__global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
+// Cells are t = 0..nc-1, or list[t] when a list of the cells with core
+// points is given (sparse lattices: 733K of 8.9M cells on c5).
+__device__ __forceinline__ uint32_t cell_at(const uint32_t* __restrict__ list, uint32_t t) {
+  return list ? list[t] : t;
+}
+
+__global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ list,
+                                   const uint32_t* __restrict__ core_cnt,
                                    const uint32_t* __restrict__ cell_start,
                                    const uint32_t* __restrict__ idx, int min_mode,
                                    const uint32_t* __restrict__ cellmin, uint32_t* parent,
                                    uint32_t* comp_min, uint32_t* counters) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = t < nc ? cell_at(list, t) : 0;
   bool root = false;
-  if (g < nc && core_cnt[g] > 0) {
+  if (t < nc && core_cnt[g] > 0) {
     const uint32_t r = uf_find(parent, g);
     const uint32_t s = cell_start[g], k = core_cnt[g];
     uint32_t mn;
@@ -304,45 +312,56 @@ __global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ cor
   if (threadIdx.x == 0 && b) atomicAdd(counters, b);
 }
 
-__global__ void cell_label_kernel(uint32_t nc, const uint32_t* __restrict__ core_cnt,
-                                  uint32_t* parent, const uint32_t* __restrict__ comp_min,
-                                  uint32_t* __restrict__ cell_label) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= nc) return;
+__global__ void cell_label_kernel(uint32_t nc, const uint32_t* __restrict__ list,
+                                  const uint32_t* __restrict__ core_cnt, uint32_t* parent,
+                                  const uint32_t* __restrict__ comp_min, uint32_t* __restrict__ cell_label) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc) return;
+  const uint32_t g = cell_at(list, t);
   cell_label[g] = core_cnt[g] > 0 ? comp_min[uf_find(parent, g)] : 0xffffffffu;
 }
 
-// Scatter the labels of core points to input order (cluster[] was set to -1
-// first). Core points are the first core_cnt[g] points of their cell (a7).
-// WARP: warp per cell, lanes over its core points (few, large cells);
-// otherwise thread per cell (many small cells). Counts core points.
-template <bool WARP>
-__global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const uint32_t* __restrict__ idx,
+// Scatter the labels to input order (a9). Core points are the first
+// core_cnt[g] points of their cell (a7).
+//  * per position (few large cells): thread per sorted position, -1 for
+//    non-core points, so cluster[] needs no clearing; 10^7 independent
+//    threads hide the latency of the idx load before each scattered store;
+//  * per cell (many small cells, or the list of cells holding core points):
+//    cluster[] was set to -1 first and only core points are written (8% of
+//    the points on c5).
+__global__ void __launch_bounds__(256) write_positions_kernel(uint32_t n, const uint32_t* __restrict__ idx,
+                                                              const uint32_t* __restrict__ cell_of,
+                                                              const uint32_t* __restrict__ cell_start,
+                                                              const uint32_t* __restrict__ core_cnt,
+                                                              const uint32_t* __restrict__ cell_label,
+                                                              int32_t* __restrict__ cluster_out,
+                                                              uint32_t* counters) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  bool is_core = false;
+  if (j < n) {
+    const uint32_t g = cell_of[j];
+    is_core = j - cell_start[g] < core_cnt[g];
+    cluster_out[idx[j]] = is_core ? (int32_t)cell_label[g] : -1;
+  }
+  const uint32_t b = __syncthreads_count(is_core);  // one atomic per block
+  if (threadIdx.x == 0 && b) atomicAdd(counters + 1, b);
+}
+
+__global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const uint32_t* __restrict__ list,
+                                                           const uint32_t* __restrict__ idx,
                                                            const uint32_t* __restrict__ cell_start,
                                                            const uint32_t* __restrict__ core_cnt,
                                                            const uint32_t* __restrict__ cell_label,
                                                            int32_t* __restrict__ cluster_out, uint32_t* counters) {
   unsigned long long ncore = 0;
-  if (WARP) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < nc; g += nwarps) {
-      const uint32_t k = core_cnt[g];
-      if (!k) continue;
-      const int32_t lab = (int32_t)cell_label[g];
-      const uint32_t s = cell_start[g];
-      for (uint32_t u = s + lane; u < s + k; u += 32) cluster_out[idx[u]] = lab;
-      if (lane == 0) ncore += k;
-    }
-  } else {
-    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nc; g += gridDim.x * blockDim.x) {
-      const uint32_t k = core_cnt[g];
-      if (!k) continue;
-      const int32_t lab = (int32_t)cell_label[g];
-      const uint32_t s = cell_start[g];
-      for (uint32_t u = s; u < s + k; ++u) cluster_out[idx[u]] = lab;
-      ncore += k;
-    }
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += gridDim.x * blockDim.x) {
+    const uint32_t g = cell_at(list, t);
+    const uint32_t k = core_cnt[g];
+    if (!k) continue;
+    const int32_t lab = (int32_t)cell_label[g];
+    const uint32_t s = cell_start[g];
+    for (uint32_t u = s; u < s + k; ++u) cluster_out[idx[u]] = lab;
+    ncore += k;
   }
   __shared__ unsigned long long s_part[32];
 #pragma unroll
@@ -352,7 +371,7 @@ __global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const ui
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w];
-    if (t) atomicAdd(counters + 1, (uint32_t)t);
+    if (t) atomicAdd(counters + 1, (uint32_t)t);  // core points (< 2^31)
   }
 }
 
@@ -372,26 +391,28 @@ __global__ void core_from_cluster_kernel(uint32_t n, const int32_t* __restrict__
 }
 
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
-            const uint32_t* core_cnt, int min_mode, const uint32_t* cellmin, uint32_t* parent, int64_t n,
-            uint32_t* cell_label,
+            const uint32_t* core_cnt, int min_mode, const uint32_t* cellmin, const uint32_t* core_list,
+            uint32_t ncore, uint32_t* parent, int64_t n, uint32_t* cell_label,
             uint8_t* core_out, int32_t* cluster_out, uint32_t* counters) {
   const uint32_t nc = cv.ncells;
+  const uint32_t m = core_list ? ncore : nc;  // cells the kernels visit
   uint32_t* comp_min = c.alloc<uint32_t>(nc);
   DB_CUDA(cudaMemsetAsync(comp_min, 0xff, sizeof(uint32_t) * nc, c.st));
-  label_roots_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, cv.cell_start, idx,
+  label_roots_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(m, core_list, core_cnt, cv.cell_start, idx,
                                                                     min_mode, cellmin, parent, comp_min,
                                                                     counters);
   c.launched();
-  cell_label_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(nc, core_cnt, parent, comp_min,
-                                                                   cell_label);
+  cell_label_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(m, core_list, core_cnt, parent, comp_min,
+                                                                  cell_label);
   c.launched();
-  DB_CUDA(cudaMemsetAsync(cluster_out, 0xff, sizeof(int32_t) * (size_t)n, c.st));
-  if ((int64_t)nc * 32 <= n)
-    write_points_kernel<true><<<grid_for((int64_t)nc * 32, 256, c.sms * 16), 256, 0, c.st>>>(
-        nc, idx, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
-  else
-    write_points_kernel<false><<<grid_for(nc, 256, c.sms * 16), 256, 0, c.st>>>(
-        nc, idx, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
+  if (!core_list && (int64_t)nc * 32 <= n) {
+    write_positions_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
+        (uint32_t)n, idx, cv.cell_of, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
+  } else {
+    DB_CUDA(cudaMemsetAsync(cluster_out, 0xff, sizeof(int32_t) * (size_t)n, c.st));
+    write_points_kernel<<<grid_for(m, 256, c.sms * 16), 256, 0, c.st>>>(
+        m, core_list, idx, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
+  }
   c.launched();
   core_from_cluster_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, c.st>>>((uint32_t)n, cluster_out,
                                                                                   core_out);

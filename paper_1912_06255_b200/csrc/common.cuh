@@ -55,13 +55,14 @@ __device__ __forceinline__ uint64_t gap_term(uint32_t delta, const Geo& g) {
 
 // ---------------------------------------------------------------------------
 // Exact distance predicate ||a-b||^2 <= eps^2 on int32 coordinates
-// (closed neighbourhood). 32-bit path (reading 4):
-//   sum_k min(|a_k - b_k|, eps+1)^2 <= eps^2, |a_k - b_k| = __sad(a_k, b_k, 0)
-// exact as an unsigned 32-bit value for any int32 pair; clamping at eps+1
-// cannot change the outcome (a clamped term alone exceeds eps^2), and the
-// sum is < d (eps+1)^2 < 2^32, which the host checks before choosing it.
+// (closed neighbourhood). Every caller compares points of cells
+// at most R apart per axis (stencil / neighbour cells), so |a_k - b_k| <=
+// (R+1)s - 1. 32-bit path (reading 4): sum_k |a_k - b_k|^2 <= eps^2
+// with |a_k - b_k| = __sad(a_k, b_k, 0), exact in uint32 because the host
+// chooses it only when d ((R+1)s - 1)^2 < 2^32.
 // Padded coordinates are 0 on both sides and contribute nothing.
-// 64-bit path: the same with 64-bit differences and sums (d (eps+1)^2 < 2^62).
+// 64-bit path: 64-bit differences clamped at eps+1 (Lemma 3: a clamped term
+// alone exceeds eps^2) and 64-bit sums (d (eps+1)^2 < 2^62).
 // ---------------------------------------------------------------------------
 template <int D, bool WIDE>
 struct Pt;
@@ -106,7 +107,7 @@ __device__ __forceinline__ bool within(const int32_t* a, const int32_t* b, uint3
     uint32_t acc = 0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      uint32_t t = min(__sad(a[k], b[k], 0u), clampc);
+      const uint32_t t = __sad(a[k], b[k], 0u);
       acc += t * t;
     }
     return acc <= (uint32_t)eps2;

@@ -106,8 +106,17 @@ struct Timer {
   }
 };
 
+// Host-path copies of finished outputs run on a side stream (one per thread
+// and device), overlapping the remaining stages on the call's stream.
+static cudaStream_t side_stream(int dev) {
+  static thread_local cudaStream_t s[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!s[dev]) DB_CUDA(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking));
+  return s[dev];
+}
+
 static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
-               uint32_t flags, cudaStream_t st, dbscan_result* out) {
+               uint32_t flags, cudaStream_t st, dbscan_result* out, int32_t* uids, int64_t ucap) {
   const bool dev_io = flags & DBSCAN_F_DEVICE_IO;
   const bool caller_out = flags & DBSCAN_F_CALLER_OUT;
   Priv* priv = new Priv();
@@ -120,6 +129,12 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   DB_CUDA(cudaGetDevice(&dev));
   init_device_once(dev, &c.sms);
   Timer tm(flags & DBSCAN_F_TIMING, st);
+  c.stage_fn = [](void* t, int s) { static_cast<Timer*>(t)->stage(s); };
+  c.stage_obj = &tm;
+  if (flags & DBSCAN_F_COUNT_WORK) {
+    c.work = c.alloc<unsigned long long>(4);
+    c.zero(c.work, 4 * sizeof(unsigned long long));
+  }
 
   // ---- outputs
   auto out_alloc = [&](size_t bytes, void** slot) -> void* {
@@ -139,8 +154,13 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     out->cluster = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)n, &priv->cluster);
     out->border_off = (int64_t*)out_alloc(sizeof(int64_t) * (size_t)(n + 1), &priv->border_off);
   }
+  // border_ids: the caller's buffer (F_CALLER_OUT with capacity) when it fits
+  auto ids_alloc = [&](int64_t nnz) -> int32_t* {
+    if (caller_out && uids && nnz <= ucap) return uids;
+    return (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
+  };
   if (n == 0) {
-    out->border_ids = (int32_t*)out_alloc(4, &priv->border_ids);
+    out->border_ids = ids_alloc(0);
     if (dev_io) DB_CUDA(cudaMemsetAsync(out->border_off, 0, sizeof(int64_t), st));
     else out->border_off[0] = 0;
     if (dev_io) DB_CUDA(cudaStreamSynchronize(st));
@@ -151,8 +171,14 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   const u128 eps2 = (u128)eps * (u128)eps;
   const u128 dc2 = (u128)d * (u128)(eps + 1) * (u128)(eps + 1);
   if (dc2 >= ((u128)1 << 62)) throw Error(DBSCAN_ERANGE, "d*(eps+1)^2 >= 2^62");
-  const bool wide = (flags & DBSCAN_F_FORCE_WIDE) || dc2 >= ((u128)1 << 32);
   const uint64_t s = isqrt_u128(eps2 / (u128)d) + 1;  // < 2^31 since eps^2/d < 2^62
+  // 32-bit distance path (reading 4): every distance test compares
+  // points of cells at most R apart per axis, so |a_k - b_k| <= (R+1)s - 1;
+  // if d ((R+1)s - 1)^2 < 2^32 the plain squared sum is exact in uint32.
+  const uint64_t Rr = (uint64_t)(eps - 1) / s + 1;
+  const u128 span = (u128)(Rr + 1) * s - 1;
+  const bool wide = (flags & DBSCAN_F_FORCE_WIDE) || dc2 >= ((u128)1 << 32) ||
+                    (u128)d * span * span >= ((u128)1 << 32);
   Geo g{};
   g.d = d;
   g.D = d <= 2 ? 2 : (d <= 4 ? 4 : 8);
@@ -288,6 +314,20 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     core_cells = c.read(cnt32);
   }
 
+  cudaStream_t side = nullptr;
+  struct Ev {
+    cudaEvent_t e = nullptr;
+    ~Ev() { if (e) cudaEventDestroy(e); }
+  } evl, evs;
+  cudaEvent_t ev_labels = nullptr, ev_side = nullptr;
+  bool side_used = false;
+  if (!dev_io) {
+    side = side_stream(dev);
+    DB_CUDA(cudaEventCreateWithFlags(&evl.e, cudaEventDisableTiming));
+    DB_CUDA(cudaEventCreateWithFlags(&evs.e, cudaEventDisableTiming));
+    ev_labels = evl.e;
+    ev_side = evs.e;
+  }
   uint8_t* core_d = dev_io ? out->core : c.alloc<uint8_t>(n);
   int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
   int64_t* off_d = dev_io ? out->border_off : c.alloc<int64_t>((size_t)n + 1);
@@ -299,7 +339,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     DB_CUDA(cudaMemsetAsync(core_d, 0, (size_t)n, st));
     DB_CUDA(cudaMemsetAsync(cluster_d, 0xff, sizeof(int32_t) * (size_t)n, st));
     DB_CUDA(cudaMemsetAsync(off_d, 0, sizeof(int64_t) * (size_t)(n + 1), st));
-    out->border_ids = (int32_t*)out_alloc(4, &priv->border_ids);
+    out->border_ids = ids_alloc(0);
   } else {
     // ---- a8: ClusterCore
     tm.stage(DBSCAN_STAGE_CLUSTER);
@@ -310,14 +350,29 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     // ---- a9: labels, scattered to input order
     tm.stage(DBSCAN_STAGE_LABELS);
     uint32_t* cell_label = c.alloc<uint32_t>(ncells);
-    labels(c, cv, sidx, core_s, core_cnt, min_mode, cellmin, parent, n, cell_label, core_d, cluster_d,
-           cnt32 + 2);
+    labels(c, cv, sidx, core_s, core_cnt, min_mode, cellmin, sparse ? so.core_list : nullptr, so.ncore, parent,
+           n, cell_label, core_d, cluster_d, cnt32 + 2);
+
+    // host path: core flags and labels are final; copy them out on the side
+    // stream while ClusterBorder runs
+    if (!dev_io) {
+      DB_CUDA(cudaEventRecord(ev_labels, st));
+      DB_CUDA(cudaStreamWaitEvent(side, ev_labels, 0));
+      DB_CUDA(cudaMemcpyAsync(out->core, core_d, (size_t)n, cudaMemcpyDeviceToHost, side));
+      DB_CUDA(cudaMemcpyAsync(out->cluster, cluster_d, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost,
+                              side));
+      side_used = true;
+    }
 
     // ---- a10: ClusterBorder
     tm.stage(DBSCAN_STAGE_BORDER);
     if (sparse) nnz = sparse_border(c, g, cell_label, cluster_d, n, wide, off_d, cnt64 + 1, &so);
     else nnz = border_count(c, g, cv, Ps, sidx, core_cnt, cell_label, cluster_d, n, wide, off_d, cnt64 + 1);
-    out->border_ids = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
+    // (border_count synchronised the stream: border_off is final)
+    if (!dev_io)
+      DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost,
+                              side));
+    out->border_ids = ids_alloc(nnz);
     int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
     if (nnz > 0) {
       if (sparse) sparse_border_fill(c, g, wide, off_d, ids_d, &so);
@@ -328,15 +383,21 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
                               cudaMemcpyDeviceToHost, st));
   }
 
-  if (!dev_io) {
+  if (!dev_io && !side_used) {
     DB_CUDA(cudaMemcpyAsync(out->core, core_d, (size_t)n, cudaMemcpyDeviceToHost, st));
     DB_CUDA(cudaMemcpyAsync(out->cluster, cluster_d, sizeof(int32_t) * (size_t)n,
                             cudaMemcpyDeviceToHost, st));
     DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1),
                             cudaMemcpyDeviceToHost, st));
   }
+  if (side_used) {  // the temporaries stay alive until the side copies are done
+    DB_CUDA(cudaEventRecord(ev_side, side));
+    DB_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+  }
   uint32_t h32[4];
   unsigned long long h64[2];
+  unsigned long long hw[4] = {0, 0, 0, 0};
+  if (c.work) DB_CUDA(cudaMemcpyAsync(hw, c.work, sizeof(hw), cudaMemcpyDeviceToHost, st));
   DB_CUDA(cudaMemcpyAsync(h32, cnt32, sizeof(h32), cudaMemcpyDeviceToHost, st));
   DB_CUDA(cudaMemcpyAsync(h64, cnt64, sizeof(h64), cudaMemcpyDeviceToHost, st));
   tm.finish(out->stage_ms);
@@ -362,6 +423,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_DENSE_DIR] = dense_dir;
   out->stats[DBSCAN_STAT_SPARSE] = sparse;
   out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group ? 1 : (lat_group ? 2 : 0);
+  out->stats[DBSCAN_STAT_MARKCORE_TESTS] = (int64_t)hw[0];
   return DBSCAN_OK;
 }
 
@@ -396,6 +458,8 @@ int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pt
   uint8_t* ucore = out->core;
   int32_t* ucl = out->cluster;
   int64_t* uoff = out->border_off;
+  int32_t* uids = caller_out ? out->border_ids : nullptr;  // optional, capacity in out->nnz
+  const int64_t ucap = caller_out && uids ? out->nnz : 0;
   std::memset(out, 0, sizeof(*out));
   if (caller_out) { out->core = ucore; out->cluster = ucl; out->border_off = uoff; }
   out->n = n;
@@ -413,14 +477,15 @@ int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pt
   if (bad) { g_last_error = bad; return DBSCAN_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   try {
-    return run(pts, n, d, eps, min_pts, flags, st, out);
+    return run(pts, n, d, eps, min_pts, flags, st, out, uids, ucap);
   } catch (const Error& e) {
     g_last_error = e.what();
-    cudaStreamSynchronize(st);
+    cudaDeviceSynchronize();  // the call's stream and its side stream
     (void)cudaGetLastError();
     free_priv(out);
     if (!caller_out) { out->core = nullptr; out->cluster = nullptr; out->border_off = nullptr; }
     out->border_ids = nullptr;
+    out->nnz = 0;
     return e.code;
   } catch (const std::exception& e) {
     g_last_error = e.what();

@@ -80,8 +80,17 @@ __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* 
     const bool valid = i < n;
     int32_t x[DD];
     const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
-    const uint32_t peers = __match_any_sync(DB_FULL, key);
-    if (!valid || (peers & lanemask_lt()) != 0) continue;  // one leader per distinct key
+    // clustered data: usually one key for the whole warp (no match needed)
+    const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
+    const uint32_t vmask = __ballot_sync(DB_FULL, valid);
+    uint32_t peers;
+    if (__all_sync(DB_FULL, !valid || key == k0)) {
+      if (lane != 0 || !valid) continue;
+      peers = vmask;
+    } else {
+      peers = __match_any_sync(DB_FULL, key);
+      if (!valid || (peers & lanemask_lt()) != 0) continue;  // one leader per distinct key
+    }
     uint64_t h = gslot(key, mask);
     int probe = 0;
     while (true) {
@@ -174,7 +183,8 @@ __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
         h = (h + 1) & mask;  // present: inserted by the count pass
       }
     }
-    const uint32_t peers = __match_any_sync(DB_FULL, id);
+    const uint32_t id0 = __shfl_sync(DB_FULL, id, 0);
+    const uint32_t peers = __all_sync(DB_FULL, id == id0) ? DB_FULL : __match_any_sync(DB_FULL, id);
     const int leader = __ffs(peers) - 1;
     uint32_t base = 0;
     if (valid && lane == leader) {

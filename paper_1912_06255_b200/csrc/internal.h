@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/dbscan.h"
 #include "common.cuh"
 
 namespace db {
@@ -23,6 +24,14 @@ void cuda_check(cudaError_t e, const char* what);
 // Per-call context: stream, stream-ordered temporaries, launch counter.
 struct Ctx {
   cudaStream_t st = nullptr;
+  // stage timer hook (begin stage s; no-op without F_TIMING) and optional
+  // work counters (F_COUNT_WORK: device [4] u64, see DBSCAN_STAT_*_TESTS)
+  void (*stage_fn)(void*, int) = nullptr;
+  void* stage_obj = nullptr;
+  unsigned long long* work = nullptr;
+  void stage(int s) {
+    if (stage_fn) stage_fn(stage_obj, s);
+  }
   std::vector<void*> temps;
   int64_t launches = 0;
   int sms = 148;
@@ -54,6 +63,7 @@ struct Ctx {
     for (void* p : temps) cudaFreeAsync(p, st);
     temps.clear();
   }
+  ~Ctx() { free_all(); }  // error paths (the success path frees explicitly)
   // Read a small device value (synchronises the stream).
   template <typename T>
   T read(const T* dptr) {
@@ -163,6 +173,8 @@ constexpr uint64_t SPARSE_MEAN_PER_CELL = 4;  // n / ncells at or below: sparse 
 struct SparseOut {
   uint32_t* counters = nullptr;  // device [4]: core cells, non-core cells, large pairs, mixed
   void* stash = nullptr;         // kernel arguments kept between the stages
+  const uint32_t* core_list = nullptr;  // cells holding core points, linear order
+  uint32_t ncore = 0;
 };
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);
 // a4 + a6 + a7 on the rank directories: core flags, core-first compaction,
@@ -195,9 +207,11 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
 // stable partition), cellmin[] for all-core cells (hash grouping: order inside
 // a cell is arbitrary), or a scan of its core points (lattice counting sort).
 enum { LABEL_MIN_FIRST = 0, LABEL_MIN_ARRAY = 1, LABEL_MIN_SCAN = 2 };
+// core_list (optional): the ncore cells holding core points; the kernels then
+// visit only those (cell_label of other cells is left unset: never read).
 void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* core_s,
-            const uint32_t* core_cnt, int min_mode, const uint32_t* cellmin, uint32_t* parent, int64_t n,
-            uint32_t* cell_label,
+            const uint32_t* core_cnt, int min_mode, const uint32_t* cellmin, const uint32_t* core_list,
+            uint32_t ncore, uint32_t* parent, int64_t n, uint32_t* cell_label,
             uint8_t* core_out, int32_t* cluster_out, uint32_t* counters /*device [4]*/);
 
 // ---- border.cu (a10) ----

@@ -36,7 +36,6 @@
 //    sorted position; larger sets are enumerated without storage in
 //    ascending order.
 #include <algorithm>
-#include <cstdlib>
 #include <map>
 
 #include "internal.h"
@@ -174,198 +173,58 @@ __global__ void __launch_bounds__(256) cell_max_kernel(const uint32_t* __restric
 }
 
 // ------------------------------------------------------------ MarkCore (a6)
-// Warp per cell (grid-stride). A dense cell (|g| >= minPts) is all core
-// (P:L579-582). Otherwise lane c probes stencil column c (nearest columns
-// first), a warp prefix sum flattens the columns' point ranges, and for each
-// point p of the cell the lanes test candidates 32 at a time, counting with a
-// ballot and stopping once count >= minPts. The own cell lies in the central
-// column and passes the same test (same cell => within eps); p counts itself
-// (P:L585). The first 32 candidates are loaded once per cell and reused by
-// every point of the cell.
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a) {
-  const int lane = threadIdx.x & 31;
-  long long my_off = 0;
-  uint32_t my_mask = 0;
-  if (lane < a.ncols) { my_off = a.coff[lane]; my_mask = a.cmask[lane]; }
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < a.ncells; g += nwarps) {
-    const uint32_t s = a.cell_start[g], e = a.cell_start[g + 1];
-    if ((int64_t)(e - s) >= a.min_pts) {  // dense cell
-      for (uint32_t u = s + lane; u < e; u += 32) a.core_s[u] = 1;
-      continue;
-    }
-    const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-    uint32_t st = 0, sz = 0;
-    if (lane < a.ncols) {
-      uint32_t id0;
-      const uint32_t nc = dir_probe(a.dir, base + (uint64_t)my_off, my_mask, &id0);
-      if (nc) { st = a.cell_start[id0]; sz = a.cell_start[id0 + nc] - st; }
-    }
-    const uint32_t incl = warp_inclusive_scan(sz);
-    const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
-    const uint32_t excl = incl - sz;
-    // candidate tt -> owner lane (largest lane with excl <= tt) -> point index
-    auto cand = [&](uint32_t tt) -> uint32_t {
-      int lo = 0;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const uint32_t ex = __shfl_sync(DB_FULL, excl, lo + o);
-        if (ex <= tt) lo += o;
-      }
-      return __shfl_sync(DB_FULL, st, lo) + (tt - __shfl_sync(DB_FULL, excl, lo));
-    };
-    int32_t q0[D];
-    const bool v0 = (uint32_t)lane < total;
-    {
-      const uint32_t u = cand((uint32_t)lane);
-      if (v0) load_pt<D>(a.Ps, u, q0);
-    }
-    for (uint32_t j = s; j < e; ++j) {
+// Thread per sorted point (Alg 2): a dense cell (|g| >= minPts)
+// is all core; otherwise count the points within eps over the
+// stencil columns, nearest column first, stopping at minPts. The own cell
+// lies in the central column and passes the same test (same cell => within
+// eps; p counts itself). Consecutive lanes hold consecutive sorted
+// points (mostly one cell or its last-axis neighbours), so their column
+// probes and point loads hit the same lines. The range loop is unrolled by U:
+// U candidate loads in flight per thread, ceil(max range / U) iterations per
+// column for the warp. Measured alternatives on c5: a warp per
+// cell (latency-bound), a flat or two-phase per-point loop, U = 4, and
+// symmetric counting with atomics were all slower.
+// COUNT (F_COUNT_WORK, measurement runs only): distance tests, summed into
+// work[0] with one atomic per block.
+template <int DIM, int D, bool WIDE, int U, bool COUNT>
+__global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, unsigned long long* work) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  __syncthreads();
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t tests = 0;
+  if (j < a.n) {
+    const uint32_t g = a.cell_of[j];
+    const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
+    if ((int64_t)m >= a.min_pts) {
+      a.core_s[j] = 1;  // dense cell
+    } else {
+      const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
       int32_t p[D];
       load_pt<D>(a.Ps, j, p);
-      int64_t count = __popc(__ballot_sync(DB_FULL, v0 && within_dim<DIM, D, WIDE>(p, q0, a.g)));
-      for (uint32_t t0 = 32; t0 < total && count < a.min_pts; t0 += 32) {
-        const uint32_t tt = t0 + lane;
-        const uint32_t u = cand(tt);
-        bool hit = false;
-        if (tt < total) {
-          int32_t q[D];
-          load_pt<D>(a.Ps, u, q);
-          hit = within_dim<DIM, D, WIDE>(p, q, a.g);
+      const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
+      uint32_t count = 0;
+      for (int c = 0; c < a.ncols && count < need; ++c) {
+        uint32_t id0;
+        const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+        if (!nc) continue;
+        const uint32_t ue = a.cell_start[id0 + nc];
+        for (uint32_t u = a.cell_start[id0]; u < ue && count < need; u += U) {
+          int32_t q[U][D];
+#pragma unroll
+          for (int k = 0; k < U; ++k)
+            if (u + k < ue) load_pt<D>(a.Ps, u + k, q[k]);
+#pragma unroll
+          for (int k = 0; k < U; ++k)
+            if (u + k < ue) count += within_dim<DIM, D, WIDE>(p, q[k], a.g);
+          if (COUNT) tests += min((uint32_t)U, ue - u);
         }
-        count += __popc(__ballot_sync(DB_FULL, hit));
       }
-      if (lane == 0) a.core_s[j] = count >= a.min_pts;
+      a.core_s[j] = count >= need;
     }
   }
-}
-
-// Thread per sorted point (variant 1): nested loops over the stencil columns
-// (nearest first) and their point ranges, stopping at minPts.
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_core_thread_kernel(SpArgs a) {
-  __shared__ long long s_off[SP_MAX_COLS];
-  __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
-  __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n) return;
-  const uint32_t g = a.cell_of[j];
-  const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
-  if ((int64_t)m >= a.min_pts) { a.core_s[j] = 1; return; }  // dense cell
-  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-  int32_t p[D];
-  load_pt<D>(a.Ps, j, p);
-  int64_t count = 0;
-  for (int c = 0; c < a.ncols && count < a.min_pts; ++c) {
-    uint32_t id0;
-    const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
-    if (!nc) continue;
-    const uint32_t ue = a.cell_start[id0 + nc];
-    for (uint32_t u = a.cell_start[id0]; u < ue; ++u) {
-      int32_t q[D];
-      load_pt<D>(a.Ps, u, q);
-      count += within_dim<DIM, D, WIDE>(p, q, a.g);
-      if (count >= a.min_pts) break;
-    }
-  }
-  a.core_s[j] = count >= a.min_pts;
-}
-
-// Thread per sorted point (variant 2): one flat loop over the point's
-// candidates; when the current column's range is exhausted the thread probes
-// forward to the next non-empty column. Every iteration tests at most one
-// candidate, so the lanes of a warp stay in step (the nested loops diverge
-// on the per-column range lengths).
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_core_flat_kernel(SpArgs a) {
-  __shared__ long long s_off[SP_MAX_COLS];
-  __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
-  __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n) return;
-  const uint32_t g = a.cell_of[j];
-  const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
-  if ((int64_t)m >= a.min_pts) { a.core_s[j] = 1; return; }  // dense cell
-  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-  int32_t p[D];
-  load_pt<D>(a.Ps, j, p);
-  uint32_t count = 0;
-  const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
-  uint32_t u = 0, ue = 0;
-  int c = 0;
-  while (count < need) {
-    if (u == ue) {
-      uint32_t nc = 0, id0 = 0;
-      while (c < a.ncols && nc == 0) {
-        nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
-        ++c;
-      }
-      if (!nc) break;
-      u = a.cell_start[id0];
-      ue = a.cell_start[id0 + nc];
-    }
-    int32_t q[D];
-    load_pt<D>(a.Ps, u, q);
-    count += within_dim<DIM, D, WIDE>(p, q, a.g);
-    ++u;
-  }
-  a.core_s[j] = count >= need;
-}
-
-// Thread per sorted point (variant 3), two phases through shared memory:
-// (1) every lane probes all stencil columns in lock step and appends the
-//     non-empty ones' point ranges to its own list (shared memory, one
-//     column-major slot per lane: no bank conflicts);
-// (2) one flat loop over the point's candidates: each iteration tests one
-//     candidate per lane, stepping to the next listed range when one is
-//     exhausted, stopping at minPts. The lanes stay in step except for the
-//     ranges' ends (the nested loops diverge on every range length).
-constexpr int SPC_THREADS = 256;
-
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(SPC_THREADS) sp_core_2p_kernel(SpArgs a) {
-  __shared__ long long s_off[SP_MAX_COLS];
-  __shared__ uint32_t s_mask[SP_MAX_COLS];
-  extern __shared__ uint2 s_rng[];  // [ncols][SPC_THREADS] {start, end}
-  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
-  __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n) return;
-  const uint32_t g = a.cell_of[j];
-  const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
-  if ((int64_t)m >= a.min_pts) { a.core_s[j] = 1; return; }  // dense cell
-  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-  int nf = 0;
-  for (int c = 0; c < a.ncols; ++c) {
-    uint32_t id0;
-    const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
-    if (nc) {
-      s_rng[nf * SPC_THREADS + threadIdx.x] = make_uint2(a.cell_start[id0], a.cell_start[id0 + nc]);
-      ++nf;
-    }
-  }
-  int32_t p[D];
-  load_pt<D>(a.Ps, j, p);
-  const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
-  uint32_t count = 0, u = 0, ue = 0;
-  int f = 0;
-  while (count < need) {
-    if (u == ue) {
-      if (f == nf) break;
-      const uint2 r = s_rng[f * SPC_THREADS + threadIdx.x];
-      u = r.x;
-      ue = r.y;
-      ++f;
-    }
-    int32_t q[D];
-    load_pt<D>(a.Ps, u, q);
-    count += within_dim<DIM, D, WIDE>(p, q, a.g);
-    ++u;
-  }
-  a.core_s[j] = count >= need;
+  if (COUNT) block_add_u64(tests, work);
 }
 
 // Thread per cell: core count (a7); mixed cells are listed for the partition.
@@ -378,7 +237,7 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
     if ((int64_t)m >= a.min_pts) k = m;
     else
       for (uint32_t u = s; u < e; ++u) k += a.core_s[u];
-    a.core_cnt[g] = k;
+  a.core_cnt[g] = k;
     core_cell = k > 0;
     mixed = k > 0 && k < m;
   }
@@ -496,124 +355,55 @@ __device__ uint32_t sp_next_label(const SpArgs& a, const long long* s_off, const
   return best;
 }
 
-// Thread per sorted non-core point (Alg 4): walk the stencil
-// columns nearest first on the core directory; for each core cell whose label
-// is not yet in the set, scan its core points until one is within eps. The
-// own cell gives its label with no distance test (same cell => within eps,
-// P:L400-403). Up to SP_MAXL labels live in registers (unused = ~0, sorted by
-// a 4-input network at the end) and are staged per sorted position for the
-// fill pass; larger sets are enumerated without storage in ascending order.
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_border_kernel(SpArgs a) {
-  __shared__ long long s_off[SP_MAX_COLS];
-  __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
-  __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool bord = false;
-  if (j < a.n && !a.core_s[j]) {
-    const uint32_t g = a.cell_of[j];
-    const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-    int32_t p[D];
-    load_pt<D>(a.Ps, j, p);
-    uint32_t L0 = MISS, L1 = MISS, L2 = MISS, L3 = MISS;
-    int nl = 0;
-    bool ovf = false;
-    for (int c = 0; c < a.ncols && !ovf; ++c) {
-      uint32_t id0;
-      const uint32_t nc = dir_probe(a.cdir, base + (uint64_t)s_off[c], s_mask[c], &id0);
-      for (uint32_t r = id0; r < id0 + nc; ++r) {
-        const uint32_t h = a.core_list[r];
-        const uint32_t lab = a.cell_label[h];
-        if (lab == L0 || lab == L1 || lab == L2 || lab == L3) continue;
-        if (h != g && !sp_core_within<DIM, D, WIDE>(a, p, h)) continue;
-        if (nl == 0) L0 = lab;
-        else if (nl == 1) L1 = lab;
-        else if (nl == 2) L2 = lab;
-        else if (nl == 3) L3 = lab;
-        else { ovf = true; break; }
-        ++nl;
-      }
-    }
-    uint32_t cnt;
-    if (!ovf) {
-      auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
-      cs(L0, L1); cs(L2, L3); cs(L0, L2); cs(L1, L3); cs(L1, L2);
-      if (nl) {
-        uint32_t* dst = a.tmp_lab + (size_t)j * SP_MAXL;
-        dst[0] = L0;
-        if (nl > 1) dst[1] = L1;
-        if (nl > 2) dst[2] = L2;
-        if (nl > 3) dst[3] = L3;
-      }
-      a.tmp_n[j] = (uint8_t)nl;
-      cnt = (uint32_t)nl;
-    } else {
-      int64_t after = -1;
-      cnt = 0;
-      while (true) {
-        const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
-        if (nx == MISS) break;
-        ++cnt;
-        after = nx;
-      }
-      a.tmp_n[j] = 0xff;
-    }
-    a.bcnt[a.idx[j]] = cnt;
-    bord = cnt > 0;
-  }
-  const uint32_t nb = __syncthreads_count(bord);
-  if (threadIdx.x == 0 && nb) atomicAdd(a.nborder, (unsigned long long)nb);
-}
-
-// Core-centric ClusterBorder (variant 1, default). Alg 4 asks, for every
-// non-core point p, which clusters have a core point within eps of p
-// (P:L876-904). On a sparse lattice most stencil cells of p hold no core
-// point (c5: 8% of points are core), so the search runs from the other side:
-// a thread per core cell h walks h's stencil columns on the directory of all
-// cells and tests every non-core point p found against h's core points; on a
-// hit it adds label(h) to p's label set, a lock-free set of SP_MAXL slots
+// Core-centric ClusterBorder. Alg 4 asks, for every non-core point p, which
+// clusters have a core point within eps of p. On a sparse
+// lattice most stencil cells of p hold no core point (c5: 8% of points are
+// core), so the search runs from the other side: a thread per (core cell h,
+// stencil column) item probes the column on the directory of all cells and
+// tests every non-core point p found against h's core points; on a hit it
+// adds label(h) to p's label set, a lock-free set of SP_MAXL slots
 // (atomicCAS into the first slot that is empty or already holds the label;
 // slots fill in order, so a label appears once). A point whose set overflows
-// is flagged and enumerated later without storage (sp_next_label). The
-// relation "core point q within eps of p" is symmetric, so both sides find
-// the same pairs; p's own cell is h's centre column.
+// is flagged and enumerated later without storage (sp_next_label). "Core
+// point within eps" is symmetric, so both sides find the same pairs; p's own
+// cell is h's centre column (same cell => within eps, the test passes).
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
   __syncthreads();
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < a.ncore; r += gridDim.x * blockDim.x) {
+  const uint64_t items = (uint64_t)a.ncore * (uint64_t)a.ncols;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < items;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(t / (uint32_t)a.ncols), c = (uint32_t)(t - (uint64_t)r * a.ncols);
     const uint32_t h = a.core_list[r];
+    const uint64_t base = cell_lin<DIM>(a.cell_key[h], a);
+    uint32_t id0;
+    const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+    if (!nc) continue;
     const uint32_t sh = a.cell_start[h], kh = a.core_cnt[h];
     const uint32_t lab = a.cell_label[h];
-    const uint64_t base = cell_lin<DIM>(a.cell_key[h], a);
-    for (int c = 0; c < a.ncols; ++c) {
-      uint32_t id0;
-      const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
-      if (!nc) continue;
-      const uint32_t ue = a.cell_start[id0 + nc];
-      for (uint32_t u = a.cell_start[id0]; u < ue; ++u) {
-        if (a.core_s[u]) continue;
-        int32_t p[D];
-        load_pt<D>(a.Ps, u, p);
-        bool hit = false;
-        for (uint32_t v = sh; v < sh + kh && !hit; ++v) {
-          int32_t q[D];
-          load_pt<D>(a.Ps, v, q);
-          hit = within_dim<DIM, D, WIDE>(p, q, a.g);
-        }
-        if (!hit) continue;
-        uint32_t* L = a.tmp_lab + (size_t)u * SP_MAXL;
-        bool placed = false;
-#pragma unroll
-        for (int t = 0; t < SP_MAXL; ++t) {
-          const uint32_t old = atomicCAS(L + t, MISS, lab);
-          if (old == MISS || old == lab) { placed = true; break; }
-        }
-        if (!placed) a.tmp_n[u] = 0xff;  // overflow: enumerate later
+    const uint32_t ue = a.cell_start[id0 + nc];
+    for (uint32_t u = a.cell_start[id0]; u < ue; ++u) {
+      if (a.core_s[u]) continue;
+      int32_t p[D];
+      load_pt<D>(a.Ps, u, p);
+      bool hit = false;
+      for (uint32_t v = sh; v < sh + kh && !hit; ++v) {
+        int32_t q[D];
+        load_pt<D>(a.Ps, v, q);
+        hit = within_dim<DIM, D, WIDE>(p, q, a.g);
       }
+      if (!hit) continue;
+      uint32_t* L = a.tmp_lab + (size_t)u * SP_MAXL;
+      bool placed = false;
+#pragma unroll
+      for (int k = 0; k < SP_MAXL; ++k) {
+        const uint32_t old = atomicCAS(L + k, MISS, lab);
+        if (old == MISS || old == lab) { placed = true; break; }
+      }
+      if (!placed) a.tmp_n[u] = 0xff;  // overflow: enumerate later
     }
   }
 }
@@ -652,7 +442,7 @@ __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
         after = nx;
       }
     }
-    a.bcnt[a.idx[j]] = cnt;
+    if (cnt) a.bcnt[a.idx[j]] = cnt;  // bcnt was cleared: only border points scatter
     bord = cnt > 0;
   }
   const uint32_t nb = __syncthreads_count(bord);
@@ -838,26 +628,19 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   // a4: directory of all cells
   const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
   a.dir = dir ? dir : build_dir(c, a, words, nullptr);
-  // a6: MarkCore (variant chosen by DBSCAN_SP_CORE for measurements: 0 warp
-  // per cell, 1 thread per point nested, 2 thread per point flat)
-  static const int variant = getenv("DBSCAN_SP_CORE") ? atoi(getenv("DBSCAN_SP_CORE")) : 1;
+  // a6: MarkCore, thread per point over the stencil columns (U = 2)
+  c.stage(DBSCAN_STAGE_MARKCORE);
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
-    if (variant == 0)
-      sp_core_kernel<DIM, D, W><<<grid_for((int64_t)cv.ncells * 32, 256, c.sms * 32), 256, 0, c.st>>>(a);
-    else if (variant == 1)
-      sp_core_thread_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
-    else if (variant == 3) {
-      const int smem = (int)(sizeof(uint2) * SPC_THREADS * a.ncols);
-      DB_CUDA(cudaFuncSetAttribute(sp_core_2p_kernel<DIM, D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      sp_core_2p_kernel<DIM, D, W><<<grid_for(n, SPC_THREADS, 1 << 30), SPC_THREADS, smem, c.st>>>(a);
-    }
+    if (c.work)
+      sp_core_kernel<DIM, D, W, 2, true><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, c.work);
     else
-      sp_core_flat_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+      sp_core_kernel<DIM, D, W, 2, false><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr);
   });
   c.launched();
   // a7: core counts, core-first partition of mixed cells
+  c.stage(DBSCAN_STAGE_COMPACT);
   a.mixed_list = c.alloc<uint32_t>(cv.ncells);
   sp_cells_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(a);
   c.launched();
@@ -870,6 +653,8 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   c.launched();
   a.ncore = c.read(a.counters);
   o->stash = new SpArgs(a);
+  o->core_list = core_list;
+  o->ncore = a.ncore;
   return a.ncore;
 }
 
@@ -882,15 +667,12 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   a.large = c.alloc<uint2>(a.large_cap);
   uf_init(c, parent, cv.ncells);
   if (a.nbcols > 0 && a.ncore > 0) {
-    static const int variant = getenv("DBSCAN_SP_PAIRS") ? atoi(getenv("DBSCAN_SP_PAIRS")) : 1;
-    const uint32_t units = variant ? cv.ncells : a.ncore;
-    const unsigned grid = grid_for(((int64_t)units + 31) / 32 * 32, 256, c.sms * 16);
+    const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
     c.zero(a.counters + 2, sizeof(uint32_t));
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
-      if (variant) sp_pairs_kernel<DIM, D, W, true><<<grid, 256, 0, c.st>>>(a, tested);
-      else sp_pairs_kernel<DIM, D, W, false><<<grid, 256, 0, c.st>>>(a, tested);
+      sp_pairs_kernel<DIM, D, W, true><<<grid, 256, 0, c.st>>>(a, tested);
     });
     c.launched();
     bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
@@ -905,33 +687,24 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   a.tmp_lab = c.alloc<uint32_t>((size_t)n * SP_MAXL);
   a.tmp_n = c.alloc<uint8_t>(n);
   a.nborder = nborder;
-  static const int variant = getenv("DBSCAN_SP_BORDER") ? atoi(getenv("DBSCAN_SP_BORDER")) : 1;
-  if (variant == 1) {
-    // core-centric: label sets of SP_MAXL slots per sorted point, empty = ~0
-    DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
-    c.zero(a.tmp_n, (size_t)n);
-    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
-      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
-      constexpr bool W = decltype(Wd)::value;
-      sp_border_emit_kernel<DIM, D, W><<<grid_for(a.ncore, 256, c.sms * 16), 256, 0, c.st>>>(a);
-      c.launched();
-      sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
-      c.launched();
-    });
-  } else {
-    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
-      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
-      constexpr bool W = decltype(Wd)::value;
-      sp_border_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
-    });
+  // core-centric: label sets of SP_MAXL slots per sorted point, empty = ~0
+  DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
+  c.zero(a.bcnt, sizeof(uint32_t) * (size_t)n);
+  c.zero(a.tmp_n, (size_t)n);
+  by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
+    constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
+    constexpr bool W = decltype(Wd)::value;
+    sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * a.ncols, 256, c.sms * 32), 256, 0, c.st>>>(a);
     c.launched();
-  }
+    sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+    c.launched();
+  });
   if (c.read(nborder) == 0) {
     DB_CUDA(cudaMemsetAsync(border_off, 0, sizeof(int64_t) * (size_t)(n + 1), c.st));
     return 0;
   }
-  // counts exist for non-core points only; core points (cluster >= 0) read as 0
-  exclusive_scan_u32_i64_masked(c, a.bcnt, cluster, border_off, n);
+  (void)cluster;
+  exclusive_scan_u32_i64(c, a.bcnt, border_off, n);
   return c.read(border_off + n);
 }
 

@@ -274,3 +274,19 @@ def test_varden_and_sweeps_vs_o2(oracle_lib, d):
         r = run_or_erange(pts, eps, mp)
         if r is not None:
             assert_same(r, oracle_lib.o2(pts, eps, mp), f"varden d={d} eps={eps} mp={mp}")
+
+
+def test_host_path_caller_buffers(oracle_lib):
+    """Host path with caller-owned (pinned) output buffers, border_ids
+    included: used when the result fits, else the library allocates; both
+    equal the oracle (the side-stream copies overlap ClusterBorder)."""
+    pts = datagen.uniform(60_000, 3, 4_000, 31)
+    o = oracle_lib.o2(pts, 300, 20)
+    n = len(pts)
+    for cap in (n, 1):
+        outs = (torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
+                torch.empty(n + 1, dtype=torch.int64).pin_memory(), torch.empty(cap, dtype=torch.int32).pin_memory())
+        r = pkg.dbscan(torch.from_numpy(pts).pin_memory(), 300, 20, out=outs)
+        got = np_result(r)
+        assert len(got.border_ids) == int(got.border_off[-1])
+        assert_same(got, o, f"cap={cap}")

@@ -11,3 +11,11 @@ ncu --set full --clock-control none --import-source on -k "regex:$rx" -c "$cnt" 
 python tools/ncu_table.py "/tmp/$name.ncu-rep" > "gpurun_out/${name}_table.txt" 2>&1
 ncu -i "/tmp/$name.ncu-rep" --page raw --csv > "gpurun_out/${name}_raw.csv" 2>&1
 ncu -i "/tmp/$name.ncu-rep" --page details > "gpurun_out/${name}_details.txt" 2>&1
+# optional 6th argument: kernel-name regex whose per-source-line counters to export
+if [ $# -ge 6 ]; then
+  ncu -i "/tmp/$name.ncu-rep" --page source --csv --print-source sass --kernel-name "regex:$6" \
+      > "gpurun_out/${name}_sass.csv" 2>&1
+  ncu -i "/tmp/$name.ncu-rep" --page source --csv --print-source cuda --kernel-name "regex:$6" \
+      > "gpurun_out/${name}_src.csv" 2>&1
+  gzip -f "gpurun_out/${name}_sass.csv"
+fi
