@@ -129,6 +129,14 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   DB_CUDA(cudaGetDevice(&dev));
   init_device_once(dev, &c.sms);
   Timer tm(flags & DBSCAN_F_TIMING, st);
+  struct Evs {
+    cudaEvent_t e[4] = {};
+    ~Evs() { for (auto x : e) if (x) cudaEventDestroy(x); }
+  } evs;
+  for (auto& x : evs.e) DB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  c.side = side_stream(dev);
+  c.fork_ev = evs.e[0];
+  c.join_ev = evs.e[1];
   c.stage_fn = [](void* t, int s) { static_cast<Timer*>(t)->stage(s); };
   c.stage_obj = &tm;
   if (flags & DBSCAN_F_COUNT_WORK) {
@@ -314,20 +322,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     core_cells = c.read(cnt32);
   }
 
-  cudaStream_t side = nullptr;
-  struct Ev {
-    cudaEvent_t e = nullptr;
-    ~Ev() { if (e) cudaEventDestroy(e); }
-  } evl, evs;
-  cudaEvent_t ev_labels = nullptr, ev_side = nullptr;
+  cudaStream_t side = c.side;
+  cudaEvent_t ev_labels = evs.e[2], ev_side = evs.e[3];
   bool side_used = false;
-  if (!dev_io) {
-    side = side_stream(dev);
-    DB_CUDA(cudaEventCreateWithFlags(&evl.e, cudaEventDisableTiming));
-    DB_CUDA(cudaEventCreateWithFlags(&evs.e, cudaEventDisableTiming));
-    ev_labels = evl.e;
-    ev_side = evs.e;
-  }
   uint8_t* core_d = dev_io ? out->core : c.alloc<uint8_t>(n);
   int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
   int64_t* off_d = dev_io ? out->border_off : c.alloc<int64_t>((size_t)n + 1);

@@ -29,6 +29,18 @@ struct Ctx {
   void (*stage_fn)(void*, int) = nullptr;
   void* stage_obj = nullptr;
   unsigned long long* work = nullptr;
+  // a second stream for independent work (set by the caller with two events
+  // for the fork and the join)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  void fork() {  // side waits for everything queued on st so far
+    DB_CUDA(cudaEventRecord(fork_ev, st));
+    DB_CUDA(cudaStreamWaitEvent(side, fork_ev, 0));
+  }
+  void join() {  // st waits for everything queued on side so far
+    DB_CUDA(cudaEventRecord(join_ev, side));
+    DB_CUDA(cudaStreamWaitEvent(st, join_ev, 0));
+  }
   void stage(int s) {
     if (stage_fn) stage_fn(stage_obj, s);
   }

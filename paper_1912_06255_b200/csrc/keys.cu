@@ -118,10 +118,12 @@ void bbox(Ctx& c, const int32_t* pts, int64_t n, int d, uint32_t s, int32_t* loh
   c.launched();
   by_dim(d, [&](auto Dc) {
     constexpr int DD = decltype(Dc)::value;
+    c.fork();  // the one-block sample runs beside the bounding box
+    sample_collisions_kernel<DD><<<1, 1024, 0, c.side>>>(pts, n, s, lohi + 16);
+    c.launched();
     bbox_kernel<DD><<<grid_for(n, 256, c.sms * 8), 256, 0, c.st>>>(pts, n, lohi);
     c.launched();
-    sample_collisions_kernel<DD><<<1, 1024, 0, c.st>>>(pts, n, s, lohi + 16);
-    c.launched();
+    c.join();
   });
 }
 

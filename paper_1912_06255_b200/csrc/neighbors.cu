@@ -273,9 +273,12 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
 // with a per-warp stack). Warp per query cell, lanes over all cells, lattice
 // coordinates pre-decoded (cc[8] per cell), the squared gap per axis from a
 // shared table indexed by min(|delta|, R+1) (entry R+1 exceeds eps^2 on its
-// own). Rows come out in three classes of lattice L1 distance (1, 2, >= 3),
-// nearest class first, each in ascending cell id; the count pass records the
-// class sizes so that the fill pass places every entry in one sweep.
+// own). Cells are bucketed by their axis-0 coordinate first (counting sort),
+// so a query scans only the buckets c0 - R .. c0 + R (seed-spreader cells sit
+// in ~10 walk clusters: ~1/15 of the cells). Rows come out in three classes
+// of lattice L1 distance (1, 2, >= 3), nearest class first; the count pass
+// records the class sizes so that the fill pass places every entry in one
+// sweep.
 constexpr uint32_t BRUTE_MAX_CELLS = 16384;
 constexpr int GT_MAX = 64;
 
@@ -294,8 +297,29 @@ __global__ void decode_cells_kernel(const uint64_t* __restrict__ cell_key, uint3
   reinterpret_cast<uint4*>(cc)[2 * i + 1] = b;
 }
 
+__global__ void iota_kernel(uint32_t* __restrict__ v, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+__global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t* __restrict__ bcnt) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ncells) atomicAdd(bcnt + cc[8 * (size_t)i], 1u);
+}
+
+__global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells,
+                                   const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcur,
+                                   uint32_t* __restrict__ order) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncells) return;
+  const uint32_t b = cc[8 * (size_t)i];
+  order[bstart[b] + atomicAdd(bcur + b, 1u)] = i;
+}
+
 template <int DD>
 __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t* __restrict__ cc,
+                                                        const uint32_t* __restrict__ order,
+                                                        const uint32_t* __restrict__ bstart, uint32_t maxb,
                                                         uint32_t ncells, Geo g,
                                                         const uint64_t* __restrict__ gtab_g, int gmax,
                                                         const uint32_t* __restrict__ cell_start,
@@ -324,10 +348,14 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     }
     uint32_t n3[3] = {0, 0, 0};
     uint64_t sum = 0;
-    for (uint32_t h0 = 0; h0 < ncells; h0 += 32) {
-      const uint32_t h = h0 + lane;
+    const uint32_t c0 = maxb ? cq[0] : 0u;  // maxb = 0: a single bucket
+    const uint32_t blo = c0 > g.R ? c0 - g.R : 0u, bhi = min(maxb, c0 + g.R);
+    const uint32_t t1 = bstart[bhi + 1];
+    for (uint32_t t0 = bstart[blo]; t0 < t1; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      const uint32_t h = t < t1 ? order[t] : 0u;
       int cls = -1;
-      if (h < ncells && h != q) {
+      if (t < t1 && h != q) {
         uint32_t ch[8];
         const uint4 a = C[2 * h];
         ch[0] = a.x; ch[1] = a.y; ch[2] = a.z; ch[3] = a.w;
@@ -385,6 +413,26 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   uint32_t* cc = c.alloc<uint32_t>((size_t)ncells * 8);
   decode_cells_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, cc);
   c.launched();
+  // axis-0 buckets (one bucket if the axis is too long to bucket cheaply)
+  const uint32_t maxb = (uint64_t)g.maxc[0] < 4ull * ncells + 1024 ? g.maxc[0] : 0u;
+  uint32_t* bcnt = c.alloc<uint32_t>((size_t)maxb + 2);
+  uint32_t* bstart = c.alloc<uint32_t>((size_t)maxb + 2);
+  uint32_t* order = c.alloc<uint32_t>(ncells);
+  c.zero(bcnt, sizeof(uint32_t) * ((size_t)maxb + 2));
+  if (maxb) {
+    bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, bcnt);
+    c.launched();
+    exclusive_scan_u32_u32(c, bcnt, bstart, (int64_t)maxb + 1);
+    c.zero(bcnt, sizeof(uint32_t) * ((size_t)maxb + 2));
+    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, bstart, bcnt, order);
+    c.launched();
+  } else {
+    // one bucket: every cell (cc[0] is then clamped by maxb = 0 -> buckets 0..0)
+    const uint32_t h2[2] = {0u, ncells};
+    DB_CUDA(cudaMemcpyAsync(bstart, h2, sizeof(h2), cudaMemcpyHostToDevice, c.st));
+    iota_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(order, ncells);
+    c.launched();
+  }
   uint32_t* ccount = c.alloc<uint32_t>(2 * (size_t)ncells);
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
   uint32_t* ub = c.alloc<uint32_t>(ncells);
@@ -392,11 +440,11 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
   auto launch = [&](int fill, uint32_t* list) {
     if (g.d <= 4)
-      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, ncells, g, (const uint64_t*)dgt, gmax, cell_start,
-                                                  ccount, cnt, ub, off, list);
+      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, ncells, g, (const uint64_t*)dgt,
+                                                  gmax, cell_start, ccount, cnt, ub, off, list);
     else
-      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, ncells, g, (const uint64_t*)dgt, gmax, cell_start,
-                                                  ccount, cnt, ub, off, list);
+      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, ncells, g, (const uint64_t*)dgt,
+                                                  gmax, cell_start, ccount, cnt, ub, off, list);
     c.launched();
   };
   launch(0, nullptr);

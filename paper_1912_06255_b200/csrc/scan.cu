@@ -6,11 +6,14 @@
 
 namespace db {
 
-constexpr int SC_THREADS = 256;
-constexpr int SC_ITEMS = 8;
+constexpr int SC_THREADS = 512;
+constexpr int SC_ITEMS = 16;  // consecutive items per thread: 4 x 16-byte loads
 constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 
 // mask (optional): items with mask[i] >= 0 count as 0 (their in[i] is not read)
+// Thread t of a tile owns items [16t, 16t + 16): vector loads and stores
+// straight from registers (a warp's 4 loads / 8 stores of 16 B cover whole
+// sectors), the tile total is published as the aggregate before the look-back.
 template <typename TOut>
 __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __restrict__ in,
                                                           const int32_t* __restrict__ mask,
@@ -19,49 +22,64 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_scan[33];
   __shared__ uint64_t s_pref;
-  __shared__ uint32_t s_in[SC_TILE];
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
-  const int64_t base = tile * SC_TILE;
-  // coalesced load through shared memory, then blocked per-thread sums
-#pragma unroll
-  for (int i = 0; i < SC_ITEMS; ++i) {
-    int64_t j = base + i * SC_THREADS + threadIdx.x;
-    s_in[i * SC_THREADS + threadIdx.x] = (j < n && !(mask && mask[j] >= 0)) ? in[j] : 0u;
-  }
-  __syncthreads();
+  const int64_t j0 = tile * SC_TILE + (int64_t)threadIdx.x * SC_ITEMS;
   uint32_t v[SC_ITEMS];
+  const bool full = j0 + SC_ITEMS <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                    (!mask || (reinterpret_cast<uintptr_t>(mask) & 15) == 0);
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS / 4; ++q) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(in + j0) + q);
+      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+      if (mask) {
+        const int4 m = __ldg(reinterpret_cast<const int4*>(mask + j0) + q);
+        if (m.x >= 0) v[4 * q] = 0;
+        if (m.y >= 0) v[4 * q + 1] = 0;
+        if (m.z >= 0) v[4 * q + 2] = 0;
+        if (m.w >= 0) v[4 * q + 3] = 0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; ++i) {
+      const int64_t j = j0 + i;
+      v[i] = (j < n && !(mask && mask[j] >= 0)) ? in[j] : 0u;
+    }
+  }
   uint64_t sum = 0;
 #pragma unroll
-  for (int i = 0; i < SC_ITEMS; ++i) { v[i] = s_in[threadIdx.x * SC_ITEMS + i]; sum += v[i]; }
+  for (int i = 0; i < SC_ITEMS; ++i) sum += v[i];
   uint64_t tot;
-  uint64_t ex = block_exclusive_scan<uint64_t>(sum, s_scan, &tot);
+  const uint64_t ex = block_exclusive_scan<uint64_t>(sum, s_scan, &tot);
   if (threadIdx.x == 0) s_pref = lb_exclusive(status, tile, 1, tot);
   __syncthreads();
   uint64_t run = s_pref + ex;
-  // write back through shared memory for coalescing (two halves for 64-bit outputs)
-  TOut* s_out = reinterpret_cast<TOut*>(s_in);  // reuse: SC_TILE*4 bytes
-  constexpr int PER = (int)(sizeof(uint32_t) * SC_TILE / sizeof(TOut));  // outputs per round
   TOut o[SC_ITEMS];
 #pragma unroll
   for (int i = 0; i < SC_ITEMS; ++i) { o[i] = (TOut)run; run += v[i]; }
-  __syncthreads();
-  for (int r = 0; r < SC_TILE / PER; ++r) {
-    const int lo = r * PER;
+  constexpr int PER16 = 16 / sizeof(TOut);  // outputs per 16-byte store
+  const bool ofull = j0 + SC_ITEMS <= n && (reinterpret_cast<uintptr_t>(out + j0) & 15) == 0;
+  if (ofull) {
 #pragma unroll
-    for (int i = 0; i < SC_ITEMS; ++i) {
-      int li = threadIdx.x * SC_ITEMS + i;
-      if (li >= lo && li < lo + PER) s_out[li - lo] = o[i];
+    for (int q = 0; q < SC_ITEMS / PER16; ++q) {
+      uint4 w;
+      if constexpr (PER16 == 4) {
+        w = make_uint4((uint32_t)o[4 * q], (uint32_t)o[4 * q + 1], (uint32_t)o[4 * q + 2], (uint32_t)o[4 * q + 3]);
+      } else {
+        const uint64_t a = (uint64_t)o[2 * q], b = (uint64_t)o[2 * q + 1];
+        w = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+      }
+      reinterpret_cast<uint4*>(out + j0)[q] = w;
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < PER; t += SC_THREADS) {
-      int64_t j = base + lo + t;
-      if (j < n) out[j] = s_out[t];
-    }
-    __syncthreads();
+  } else {
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; ++i)
+      if (j0 + i < n) out[j0 + i] = o[i];
   }
-  if ((n - 1) / SC_TILE == tile && threadIdx.x == SC_THREADS - 1) out[n] = (TOut)run;  // total
+  if (j0 < n && j0 + SC_ITEMS >= n) out[n] = (TOut)run;  // total (the thread holding item n-1)
 }
 
 template <typename TOut>

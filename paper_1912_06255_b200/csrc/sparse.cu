@@ -71,6 +71,7 @@ struct SpArgs {
   int64_t min_pts;
   uint32_t* counters;        // [0] core cells, [1] unused, [2] large pairs, [3] mixed cells
   uint32_t* mixed_list;
+  uint32_t* core_tmp;        // cells with core points, unordered (count in counters[0])
   const uint32_t* cell_label;
   uint32_t* parent;
   uint2* large;
@@ -124,14 +125,18 @@ __device__ __forceinline__ bool within_dim(const int32_t* p, const int32_t* q, c
 }
 
 // ------------------------------------------------------------- directories
+// every cell (list = NULL), or the cells list[0 .. *count) (grid-stride)
 __global__ void dir_set_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, SpArgs a,
-                               const uint32_t* __restrict__ only_if /* core_cnt or NULL */, uint32_t* bm) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ncells || (only_if && only_if[i] == 0)) return;
-  const uint64_t key = cell_key[i];
-  uint64_t lin = 0;
-  for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
-  atomicOr(bm + (lin >> 5), 1u << (lin & 31));
+                               const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
+                               uint32_t* bm) {
+  const uint32_t m = list ? *count : ncells;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+    const uint32_t i = list ? list[t] : t;
+    const uint64_t key = cell_key[i];
+    uint64_t lin = 0;
+    for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
+    atomicOr(bm + (lin >> 5), 1u << (lin & 31));
+  }
 }
 
 __global__ void popc_kernel(const uint32_t* __restrict__ bm, uint64_t words, uint32_t* __restrict__ cnt) {
@@ -146,13 +151,16 @@ __global__ void dir_pack_kernel(const uint32_t* __restrict__ bm, const uint32_t*
 }
 
 // core_list[rank in cdir] = cell id, for every cell holding core points
+// (from the unordered list core_tmp[0 .. counters[0]))
 __global__ void core_list_kernel(SpArgs a, uint32_t* __restrict__ core_list) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.ncells || a.core_cnt[g] == 0) return;
-  uint64_t lin = 0;
-  const uint64_t key = a.cell_key[g];
-  for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
-  core_list[dir_rank(a.cdir, lin)] = g;
+  const uint32_t m = a.counters[0];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+    const uint32_t g = a.core_tmp[t];
+    uint64_t lin = 0;
+    const uint64_t key = a.cell_key[g];
+    for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
+    core_list[dir_rank(a.cdir, lin)] = g;
+  }
 }
 
 // largest cell size (block max, one atomic per block)
@@ -241,14 +249,18 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
     core_cell = k > 0;
     mixed = k > 0 && k < m;
   }
+  // core cells (unordered, for the core directory) and mixed cells (for the
+  // partition) are appended with one atomic per block each
   __shared__ uint32_t s_scan[33];
-  __shared__ uint32_t s_base;
-  const uint32_t cb = __syncthreads_count(core_cell);
-  if (threadIdx.x == 0 && cb) atomicAdd(a.counters + 0, cb);
+  __shared__ uint32_t s_base, s_cbase;
+  uint32_t nc;
+  const uint32_t cx = block_exclusive_scan<uint32_t>(core_cell ? 1u : 0u, s_scan, &nc);
+  if (threadIdx.x == 0 && nc) s_cbase = atomicAdd(a.counters + 0, nc);
   uint32_t nm;
   const uint32_t ex = block_exclusive_scan<uint32_t>(mixed ? 1u : 0u, s_scan, &nm);
-  if (threadIdx.x == 0 && nm) s_base = atomicAdd(a.counters + 3, nm);  // one atomic per block
+  if (threadIdx.x == 0 && nm) s_base = atomicAdd(a.counters + 3, nm);
   __syncthreads();
+  if (core_cell) a.core_tmp[s_cbase + cx] = g;
   if (mixed) a.mixed_list[s_base + ex] = g;
 }
 
@@ -554,15 +566,16 @@ bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced) {
   return (uint64_t)n <= (uint64_t)SPARSE_MEAN_PER_CELL * ncells;
 }
 
-// Build a directory over the padded lattice for every cell (only_if = NULL)
-// or the cells with only_if[g] > 0.
-static uint4* build_dir(Ctx& c, const SpArgs& a, uint64_t words, const uint32_t* only_if) {
+// Build a directory over the padded lattice for every cell (list = NULL) or
+// the cells list[0 .. *count).
+static uint4* build_dir(Ctx& c, const SpArgs& a, uint64_t words, const uint32_t* list,
+                        const uint32_t* count) {
   uint32_t* bm = c.alloc<uint32_t>(words);
   uint32_t* wcnt = c.alloc<uint32_t>(words);
   uint32_t* pre = c.alloc<uint32_t>(words + 1);
   uint4* dir = c.alloc<uint4>(words);
   c.zero(bm, sizeof(uint32_t) * words);
-  dir_set_kernel<<<grid_for(a.ncells, 256, 1 << 30), 256, 0, c.st>>>(a.cell_key, a.ncells, a, only_if, bm);
+  dir_set_kernel<<<grid_for(a.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a.cell_key, a.ncells, a, list, count, bm);
   c.launched();
   popc_kernel<<<grid_for((int64_t)words, 256, 1 << 30), 256, 0, c.st>>>(bm, words, wcnt);
   c.launched();
@@ -627,7 +640,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.nbcols = (int)back.size();
   // a4: directory of all cells
   const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
-  a.dir = dir ? dir : build_dir(c, a, words, nullptr);
+  a.dir = dir ? dir : build_dir(c, a, words, nullptr, nullptr);
   // a6: MarkCore, thread per point over the stencil columns (U = 2)
   c.stage(DBSCAN_STAGE_MARKCORE);
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
@@ -642,14 +655,15 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   // a7: core counts, core-first partition of mixed cells
   c.stage(DBSCAN_STAGE_COMPACT);
   a.mixed_list = c.alloc<uint32_t>(cv.ncells);
+  a.core_tmp = c.alloc<uint32_t>(cv.ncells);
   sp_cells_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(a);
   c.launched();
   partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, Ps, idx, core_s, n);
   // directory of the cells holding core points, and their list in linear order
-  a.cdir = build_dir(c, a, words, core_cnt);
+  a.cdir = build_dir(c, a, words, a.core_tmp, a.counters);
   uint32_t* core_list = c.alloc<uint32_t>(cv.ncells);
   a.core_list = core_list;
-  core_list_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(a, core_list);
+  core_list_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a, core_list);
   c.launched();
   a.ncore = c.read(a.counters);
   o->stash = new SpArgs(a);
