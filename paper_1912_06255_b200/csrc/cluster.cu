@@ -73,50 +73,6 @@ __global__ void __launch_bounds__(256) pair_kernel(int fill, int nwaves, CellsVi
   }
 }
 
-// Drop pairs already in one component; split the rest by size class.
-__global__ void wave_filter_kernel(const uint2* __restrict__ pairs, const uint64_t* __restrict__ bounds,
-                                   uint32_t* parent, const uint32_t* __restrict__ core_cnt,
-                                   uint2* __restrict__ small, uint2* __restrict__ large,
-                                   uint32_t* ctr, unsigned long long* tested) {
-  const uint64_t b0 = bounds[0], b1 = bounds[1];
-  uint32_t mine = 0;
-  for (uint64_t i = b0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < b1;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint2 p = pairs[i];
-    if (uf_find(parent, p.x) == uf_find(parent, p.y)) continue;
-    ++mine;
-    if ((uint64_t)core_cnt[p.x] * core_cnt[p.y] <= SMALL_PAIR) small[atomicAdd(ctr, 1u)] = p;
-    else large[atomicAdd(ctr + 1, 1u)] = p;
-  }
-  block_add_u64(mine, tested);
-}
-
-template <int D, bool WIDE>
-__global__ void __launch_bounds__(256) bcp_small_kernel(const uint2* __restrict__ list,
-                                                        const uint32_t* __restrict__ count,
-                                                        CellsView cv, const int32_t* __restrict__ Ps,
-                                                        const uint32_t* __restrict__ core_cnt,
-                                                        uint32_t* parent, uint32_t clampc,
-                                                        uint64_t eps2) {
-  const uint32_t m = *count;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const uint2 p = list[i];
-    if (uf_find(parent, p.x) == uf_find(parent, p.y)) continue;
-    const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
-    const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
-    bool hit = false;
-    int32_t a[D], b[D];
-    for (uint32_t u = sa; u < ea && !hit; ++u) {
-      PtLoad<D>::load(Ps, u, a);
-      for (uint32_t v = sb; v < eb; ++v) {
-        PtLoad<D>::load(Ps, v, b);
-        if (within<D, WIDE>(a, b, clampc, eps2)) { hit = true; break; }
-      }
-    }
-    if (hit) uf_link(parent, p.x, p.y);
-  }
-}
-
 // distance from p to the integer box [lo, hi] within eps?
 template <int D>
 __device__ __forceinline__ bool near_range(const int32_t* p, const int32_t* lo, const int32_t* hi,
@@ -135,10 +91,70 @@ __device__ __forceinline__ bool near_range(const int32_t* p, const int32_t* lo, 
   return acc <= eps2;
 }
 
-// Warp per pair. Lanes hold up to 32 core points of g (filtered against h's
-// box); 32-point blocks of h's core points are loaded one point per lane,
-// filtered against the bounding box of the current g block, and the
-// survivors are broadcast by shuffle and tested against every lane's point.
+// Warp-cooperative BCP of one pair (warp-uniform arguments and result).
+// Lanes hold up to 32 core points of g (filtered against h's box);
+// 32-point blocks of h's core points are loaded one point per lane, filtered
+// against the bounding box of the current g block, and the survivors are
+// broadcast by shuffle and tested against every lane's point; the first pair
+// within eps ends the search. Between g blocks, a Find check
+// stops early when another warp has connected the pair meanwhile.
+template <int D, bool WIDE>
+__device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32_t* __restrict__ Ps,
+                         const uint32_t* __restrict__ core_cnt, uint32_t* parent) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
+  const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
+  int64_t boxh[D];
+  cell_box_lo<D>(cv.cell_key[p.y], g, boxh);
+  for (uint32_t a0 = sa; a0 < ea; a0 += 32) {
+    const uint32_t u = a0 + lane;
+    int32_t a[D];
+    bool keep = false;
+    if (u < ea) {
+      PtLoad<D>::load(Ps, u, a);
+      keep = near_box<D>(a, boxh, g);
+    }
+    if (!__any_sync(DB_FULL, keep)) continue;
+    // bounding box of the kept block
+    int32_t lo[D], hi[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      int32_t l = keep ? a[k] : INT32_MAX, h = keep ? a[k] : INT32_MIN;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        l = min(l, __shfl_xor_sync(DB_FULL, l, o));
+        h = max(h, __shfl_xor_sync(DB_FULL, h, o));
+      }
+      lo[k] = l; hi[k] = h;
+    }
+    for (uint32_t b0 = sb; b0 < eb; b0 += 32) {
+      const uint32_t v = b0 + lane;
+      int32_t b[D];
+      bool kb = false;
+      if (v < eb) {
+        PtLoad<D>::load(Ps, v, b);
+        kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2);
+      }
+      uint32_t mb = __ballot_sync(DB_FULL, kb);
+      bool mine = false;
+      while (mb) {
+        const int src = __ffs(mb) - 1;
+        mb &= mb - 1;
+        int32_t q[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
+        mine |= keep && within<D, WIDE>(a, q, g.clampc, g.eps2);
+      }
+      if (__any_sync(DB_FULL, mine)) return true;
+    }
+    bool dn = false;
+    if (lane == 0) dn = uf_find(parent, p.x) == uf_find(parent, p.y);
+    if (__shfl_sync(DB_FULL, dn, 0)) return false;
+  }
+  return false;
+}
+
+// Warp per pair over list[0 .. min(*count, cap)) (the sparse path's queue).
 template <int D, bool WIDE>
 __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict__ list,
                                                         const uint32_t* __restrict__ count,
@@ -154,61 +170,62 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
     bool done = false;
     if (lane == 0) done = uf_find(parent, p.x) == uf_find(parent, p.y);
     if (__shfl_sync(DB_FULL, done, 0)) continue;
-    const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
-    const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
-    int64_t boxh[D];
-    cell_box_lo<D>(cv.cell_key[p.y], g, boxh);
-    bool hit = false;
-    for (uint32_t a0 = sa; a0 < ea && !hit; a0 += 32) {
-      const uint32_t u = a0 + lane;
-      int32_t a[D];
-      bool keep = false;
-      if (u < ea) {
-        PtLoad<D>::load(Ps, u, a);
-        keep = near_box<D>(a, boxh, g);
-      }
-      if (!__any_sync(DB_FULL, keep)) continue;
-      // bounding box of the kept block
-      int32_t lo[D], hi[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        int32_t l = keep ? a[k] : INT32_MAX, h = keep ? a[k] : INT32_MIN;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          l = min(l, __shfl_xor_sync(DB_FULL, l, o));
-          h = max(h, __shfl_xor_sync(DB_FULL, h, o));
-        }
-        lo[k] = l; hi[k] = h;
-      }
-      for (uint32_t b0 = sb; b0 < eb; b0 += 32) {
-        const uint32_t v = b0 + lane;
-        int32_t b[D];
-        bool kb = false;
-        if (v < eb) {
-          PtLoad<D>::load(Ps, v, b);
-          kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2);
-        }
-        uint32_t mb = __ballot_sync(DB_FULL, kb);
-        bool mine = false;
-        while (mb) {
-          const int src = __ffs(mb) - 1;
-          mb &= mb - 1;
-          int32_t q[D];
-#pragma unroll
-          for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
-          mine |= keep && within<D, WIDE>(a, q, g.clampc, g.eps2);
-        }
-        if (__any_sync(DB_FULL, mine)) { hit = true; break; }
-      }
-      if (!hit) {
-        bool dn = false;
-        if (lane == 0) dn = uf_find(parent, p.x) == uf_find(parent, p.y);
-        if (__shfl_sync(DB_FULL, dn, 0)) break;
-      }
-    }
+    const bool hit = warp_bcp<D, WIDE>(p, cv, g, Ps, core_cnt, parent);
     if (hit && lane == 0) uf_link(parent, p.x, p.y);
     __syncwarp();
   }
+}
+
+// One wave of ClusterCore (Alg 3), first half: the lanes of a warp take 32
+// pairs of the wave, drop those already connected (Find), test
+// the small ones (|A| |B| <= SMALL_PAIR core points) each in its lane (Link on
+// success) and queue the large ones for bcp_large_kernel (a warp per pair),
+// with one atomic per warp.
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(256) wave_kernel(const uint2* __restrict__ pairs,
+                                                   const uint64_t* __restrict__ bounds, CellsView cv, Geo g,
+                                                   const int32_t* __restrict__ Ps,
+                                                   const uint32_t* __restrict__ core_cnt, uint32_t* parent,
+                                                   uint2* __restrict__ large, uint32_t* __restrict__ nlarge,
+                                                   unsigned long long* tested) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t b0 = bounds[0], b1 = bounds[1];
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  uint32_t mine = 0;
+  for (uint64_t c0 = b0 + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; c0 < b1;
+       c0 += nwarps * 32) {
+    const uint64_t i = c0 + lane;
+    uint2 p = make_uint2(0, 0);
+    bool need = false, small = false;
+    if (i < b1) {
+      p = pairs[i];
+      need = uf_find(parent, p.x) != uf_find(parent, p.y);
+      small = need && (uint64_t)core_cnt[p.x] * core_cnt[p.y] <= SMALL_PAIR;
+    }
+    mine += need;
+    const uint32_t lm = __ballot_sync(DB_FULL, need && !small);
+    if (lm) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(nlarge, (uint32_t)__popc(lm));
+      base = __shfl_sync(DB_FULL, base, 0);
+      if (need && !small) large[base + __popc(lm & lanemask_lt())] = p;
+    }
+    if (small) {
+      const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
+      const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
+      bool hit = false;
+      int32_t a[D], q[D];
+      for (uint32_t u = sa; u < ea && !hit; ++u) {
+        PtLoad<D>::load(Ps, u, a);
+        for (uint32_t v = sb; v < eb; ++v) {
+          PtLoad<D>::load(Ps, v, q);
+          if (within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
+        }
+      }
+      if (hit) uf_link(parent, p.x, p.y);
+    }
+  }
+  block_add_u64(mine, tested);
 }
 
 __global__ void uf_init_kernel(uint32_t* parent, uint32_t n) {
@@ -229,24 +246,24 @@ void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, con
   c.launched();
 }
 
-uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
-                      const uint32_t* core_cnt, bool wide, bool waves, uint32_t* parent,
-                      unsigned long long* tested) {
+void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
+                  bool wide, bool waves, uint64_t nbr_total, uint32_t* parent, unsigned long long* tested,
+                  unsigned long long* npairs_out) {
   const uint32_t nc = cv.ncells;
   const int nw = waves ? NWAVES : 1;
   uf_init(c, parent, nc);
+  if (nbr_total == 0) return;
   uint32_t* cnt = c.alloc<uint32_t>((size_t)nw * nc);
   uint64_t* off = c.alloc<uint64_t>((size_t)nw * nc + 1);
   const unsigned pgrid = grid_for((int64_t)nc * 32, 256, c.sms * 16);
   pair_kernel<<<pgrid, 256, 0, c.st>>>(0, nw, cv, g, core_cnt, cnt, nullptr, nullptr);
   c.launched();
   exclusive_scan_u32_u64(c, cnt, off, (int64_t)nw * nc);
-  const uint64_t npairs = c.read(off + (size_t)nw * nc);
-  if (npairs == 0) return 0;
-  uint2* pairs = c.alloc<uint2>(npairs);
+  // at most one pair per CSR entry: no host read of the pair count is needed
+  uint2* pairs = c.alloc<uint2>(nbr_total);
   pair_kernel<<<pgrid, 256, 0, c.st>>>(1, nw, cv, g, core_cnt, nullptr, off, pairs);
   c.launched();
-  // wave bounds: off[w*nc] .. off[(w+1)*nc]
+  // wave w: pairs[off[w*nc] .. off[(w+1)*nc]), bounds kept on the device
   uint64_t* bounds = c.alloc<uint64_t>(2 * NWAVES);
   for (int w = 0; w < nw; ++w) {
     DB_CUDA(cudaMemcpyAsync(bounds + 2 * w, off + (size_t)w * nc, sizeof(uint64_t),
@@ -254,23 +271,19 @@ uint64_t cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* 
     DB_CUDA(cudaMemcpyAsync(bounds + 2 * w + 1, off + (size_t)(w + 1) * nc, sizeof(uint64_t),
                             cudaMemcpyDeviceToDevice, c.st));
   }
-  uint2* small = c.alloc<uint2>(npairs);
-  uint2* large = c.alloc<uint2>(npairs);
-  uint32_t* ctr = c.alloc<uint32_t>(2 * NWAVES);
-  c.zero(ctr, sizeof(uint32_t) * 2 * NWAVES);
-  const unsigned fgrid = grid_for((int64_t)npairs, 256, c.sms * 8);
+  DB_CUDA(cudaMemcpyAsync(npairs_out, off + (size_t)nw * nc, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c.st));
+  uint2* large = c.alloc<uint2>(nbr_total);
+  uint32_t* nlarge = c.alloc<uint32_t>(NWAVES);
+  c.zero(nlarge, sizeof(uint32_t) * NWAVES);
+  const unsigned wgrid = grid_for((int64_t)(nbr_total / 2 + 32), 256, c.sms * 8);
   for (int w = 0; w < nw; ++w) {
-    wave_filter_kernel<<<fgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, parent, core_cnt, small,
-                                                large, ctr + 2 * w, tested);
-    c.launched();
     dispatch(g.D, wide, [&]<int D, bool W>() {
-      bcp_small_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(small, ctr + 2 * w, cv, Ps, core_cnt,
-                                                           parent, g.clampc, g.eps2);
-      c.launched();
+      wave_kernel<D, W><<<wgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, cv, g, Ps, core_cnt, parent, large,
+                                                 nlarge + w, tested);
     });
-    bcp_large(c, g, cv, Ps, core_cnt, parent, large, ctr + 2 * w + 1, (uint32_t)npairs, wide);
+    c.launched();
+    bcp_large(c, g, cv, Ps, core_cnt, parent, large, nlarge + w, (uint32_t)nbr_total, wide);
   }
-  return npairs;
 }
 
 // ---------------------------------------------------------------- a9: labels

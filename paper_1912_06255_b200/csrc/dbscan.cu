@@ -279,9 +279,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
 
   // device counters: [0] core cells, [1] mixed cells, [2] clusters, [3] core points
   uint32_t* cnt32 = c.alloc<uint32_t>(4);
-  unsigned long long* cnt64 = c.alloc<unsigned long long>(2);  // [0] tested pairs, [1] border pts
+  unsigned long long* cnt64 = c.alloc<unsigned long long>(3);  // [0] tested pairs, [1] border pts, [2] pairs
   c.zero(cnt32, 16);
-  c.zero(cnt64, 16);
+  c.zero(cnt64, 24);
   uint8_t* core_s = c.alloc<uint8_t>(n);
   uint32_t* core_cnt = c.alloc<uint32_t>(ncells);
 
@@ -328,7 +328,6 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   uint8_t* core_d = dev_io ? out->core : c.alloc<uint8_t>(n);
   int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
   int64_t* off_d = dev_io ? out->border_off : c.alloc<int64_t>((size_t)n + 1);
-  uint64_t npairs = 0;
   int64_t nnz = 0;
   if (core_cells == 0) {
     // no core point: no cluster, every point is noise
@@ -342,7 +341,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     tm.stage(DBSCAN_STAGE_CLUSTER);
     uint32_t* parent = c.alloc<uint32_t>(ncells);
     if (sparse) sparse_cluster(c, g, cv, Ps, core_cnt, wide, parent, cnt64, &so);
-    else npairs = cluster_core(c, g, cv, Ps, core_cnt, wide, waves, parent, cnt64);
+    else cluster_core(c, g, cv, Ps, core_cnt, wide, waves, nbr_total, parent, cnt64, cnt64 + 2);
 
     // ---- a9: labels, scattered to input order
     tm.stage(DBSCAN_STAGE_LABELS);
@@ -392,7 +391,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     DB_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   }
   uint32_t h32[4];
-  unsigned long long h64[2];
+  unsigned long long h64[3];
   unsigned long long hw[4] = {0, 0, 0, 0};
   if (c.work) DB_CUDA(cudaMemcpyAsync(hw, c.work, sizeof(hw), cudaMemcpyDeviceToHost, st));
   DB_CUDA(cudaMemcpyAsync(h32, cnt32, sizeof(h32), cudaMemcpyDeviceToHost, st));
@@ -411,7 +410,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_SORT_PASSES] = passes;
   out->stats[DBSCAN_STAT_NBR_ENTRIES] = (int64_t)nbr_total;
   out->stats[DBSCAN_STAT_CORE_CELLS] = core_cells;
-  out->stats[DBSCAN_STAT_PAIRS] = (int64_t)npairs;
+  out->stats[DBSCAN_STAT_PAIRS] = (int64_t)h64[2];
   out->stats[DBSCAN_STAT_PAIRS_TESTED] = (int64_t)h64[0];
   out->stats[DBSCAN_STAT_LAUNCHES] = c.launches;
   out->stats[DBSCAN_STAT_WIDE] = wide;
