@@ -59,6 +59,9 @@ extern "C" {
                                       sort whenever d <= 3 and its lattice fits               */
 #define DBSCAN_F_COUNT_WORK  2048u /* count the sparse MarkCore's distance tests into
                                       stats[DBSCAN_STAT_MARKCORE_TESTS] (measurement runs)   */
+#define DBSCAN_F_QUADTREE    4096u /* our-exact-qt: MarkCore's
+                                      RangeCount on cells with >= 256 points traverses a
+                                      per-cell tree instead of scanning (CSR path)           */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
@@ -92,6 +95,7 @@ extern "C" {
 #define DBSCAN_STAT_HASH_GROUP   13  /* grouping: 1 hash counting sort, 2 lattice counting sort,
                                         0 LSD radix sort + segmentation                      */
 #define DBSCAN_STAT_MARKCORE_TESTS 14 /* distance tests of the sparse MarkCore (F_COUNT_WORK)  */
+#define DBSCAN_STAT_QT_NODES     15  /* tree nodes built with F_QUADTREE                         */
 #define DBSCAN_NSTATS            16
 
 typedef struct dbscan_result {

@@ -123,8 +123,124 @@ __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const
   }
 }
 
+// Tree variant of the warp kernel (row f2, our-exact-qt): neighbour cells
+// with a tree are searched by a traversal of their tree instead
+// of a scan: a node whose box is out of reach is skipped, a node whose box
+// lies inside the eps-ball adds its count with no distance test (exact), a
+// leaf's 32 points are tested by the lanes. Cells without a tree are scanned
+// as in mark_core_warp_kernel. Decisions are warp-uniform.
+constexpr uint32_t QT_MIN_CELL = 256;  // = QT_MIN in qtree.cu
+
+template <int D>
+__device__ __forceinline__ void box_dist2(const int32_t* p, const int32_t* __restrict__ bx, const Geo& g,
+                                          uint64_t* dmin, uint64_t* dmax) {
+  uint64_t mn = 0, mx = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < g.d) {
+      const int64_t x = p[k], lo = bx[k], hi = bx[D + k];
+      uint64_t a = (uint64_t)(x < lo ? lo - x : (x > hi ? x - hi : 0));
+      uint64_t b = (uint64_t)max(x - lo, hi - x);
+      if (a > g.clampc) a = g.clampc;
+      if (b > g.clampc) b = g.clampc;
+      mn += a * a;
+      mx += b * b;
+    }
+  }
+  *dmin = mn;
+  *dmax = mx;
+}
+
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(256) mark_core_qt_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+                                                           const uint32_t* __restrict__ queue,
+                                                           const uint32_t* __restrict__ qcount, int64_t min_pts,
+                                                           Geo g, QTrees qt, uint8_t* __restrict__ core_s) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = *qcount;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < m; w += nwarps) {
+    const uint32_t j = queue[w];
+    const uint32_t gc = cv.cell_of[j];
+    int32_t p[D], q[D];
+    PtLoad<D>::load(Ps, j, p);
+    int64_t count = cv.cell_start[gc + 1] - cv.cell_start[gc];
+    const uint64_t nb1 = cv.nbr_off[gc + 1];
+    for (uint64_t cb = cv.nbr_off[gc]; cb < nb1 && count < min_pts; cb += 32) {
+      const uint64_t t = cb + lane;
+      uint32_t sz = 0, st = 0, h = 0;
+      bool tree = false;
+      if (t < nb1) {
+        h = cv.nbr[t];
+        st = cv.cell_start[h];
+        sz = cv.cell_start[h + 1] - st;
+        tree = sz >= QT_MIN_CELL;
+        if (tree) sz = 0;
+      }
+      // cells without a tree: flattened scan
+      const uint32_t incl = warp_inclusive_scan(sz);
+      const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
+      const uint32_t excl = incl - sz;
+      for (uint32_t t0 = 0; t0 < total && count < min_pts; t0 += 32) {
+        const uint32_t tt = t0 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const uint32_t e = __shfl_sync(DB_FULL, excl, lo + s);
+          if (e <= tt) lo += s;
+        }
+        const uint32_t ost = __shfl_sync(DB_FULL, st, lo);
+        const uint32_t oex = __shfl_sync(DB_FULL, excl, lo);
+        bool hit = false;
+        if (tt < total) {
+          PtLoad<D>::load(Ps, ost + (tt - oex), q);
+          hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
+        }
+        count += __popc(__ballot_sync(DB_FULL, hit));
+      }
+      // cells with a tree: one traversal each
+      uint32_t tm = __ballot_sync(DB_FULL, tree);
+      while (tm && count < min_pts) {
+        const int src = __ffs(tm) - 1;
+        tm &= tm - 1;
+        const uint32_t hc = __shfl_sync(DB_FULL, h, src);
+        const uint32_t s0 = cv.cell_start[hc], e0 = cv.cell_start[hc + 1];
+        uint32_t L = (e0 - s0 + 31) / 32, P2 = 1;
+        while (P2 < L) P2 <<= 1;
+        const uint64_t base = qt.node_off[hc];
+        uint32_t stack[64];
+        int sp = 0;
+        stack[sp++] = 0;
+        while (sp > 0 && count < min_pts) {
+          const uint32_t node = stack[--sp];
+          if (node >= P2 - 1) {  // leaf: lanes test its points
+            const uint32_t u = s0 + (node - (P2 - 1)) * 32 + lane;
+            bool hit = false;
+            if (u < e0) {
+              PtLoad<D>::load(Ps, u, q);
+              hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
+            }
+            count += __popc(__ballot_sync(DB_FULL, hit));
+            continue;
+          }
+          for (uint32_t ch = 2 * node + 2; ch >= 2 * node + 1; --ch) {  // left child on top
+            const uint32_t nc = qt.cnt[base + ch];
+            if (nc == 0) continue;
+            uint64_t dmin, dmax;
+            box_dist2<D>(p, qt.box + (base + ch) * 2 * D, g, &dmin, &dmax);
+            if (dmin > g.eps2) continue;
+            if (dmax <= g.eps2) { count += nc; continue; }  // box inside the ball
+            stack[sp++] = ch;
+          }
+        }
+      }
+    }
+    if (lane == 0) core_s[j] = count >= min_pts;
+  }
+}
+
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
-               int64_t min_pts, bool wide, uint8_t* core_s) {
+               int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt) {
   uint32_t* queue = c.alloc<uint32_t>(n);
   uint32_t* qcount = c.alloc<uint32_t>(1);
   c.zero(qcount, sizeof(uint32_t));
@@ -132,8 +248,11 @@ void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int
     mark_core_kernel<D, W><<<grid_for((int64_t)cv.ncells * 32, 256, c.sms * 16), 256, 0, c.st>>>(
         cv, Ps, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
     c.launched();
-    mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts,
-                                                               g.clampc, g.eps2, core_s);
+    if (qt && qt->nodes)
+      mark_core_qt_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts, g, *qt, core_s);
+    else
+      mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts,
+                                                                 g.clampc, g.eps2, core_s);
     c.launched();
   });
 }

@@ -268,7 +268,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   // how a9 finds each cell's smallest core index: first point (stable radix
   // sort + stable partition), per-cell minima (hash), or a scan of the cell's
   // core points (lattice counting sort; sparse cells)
-  const int min_mode = hash_group ? LABEL_MIN_ARRAY : (lat_group ? LABEL_MIN_SCAN : LABEL_MIN_FIRST);
+  int min_mode = hash_group ? LABEL_MIN_ARRAY : (lat_group ? LABEL_MIN_SCAN : LABEL_MIN_FIRST);
+  QTrees qtrees;
 
   // ---- regime: CSR path (neighbour lists) or the cell-centric sparse path
   const bool tree = (flags & DBSCAN_F_FORCE_TREE) || (d >= 4 && !(flags & DBSCAN_F_FORCE_STENCIL));
@@ -313,9 +314,14 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     cv.nbr_off = nbr_off;
     cv.nbr = nbr;
     cv.ub = ub;
+    // ---- row f2 (our-exact-qt): per-cell range-count trees for big cells
+    if (flags & DBSCAN_F_QUADTREE) {
+      build_qtrees(c, g, cv, Ps, sidx, n, &qtrees);
+      if (min_mode == LABEL_MIN_FIRST) min_mode = LABEL_MIN_SCAN;  // cells are no longer stable
+    }
     // ---- a6: MarkCore
     tm.stage(DBSCAN_STAGE_MARKCORE);
-    mark_core(c, g, cv, Ps, n, min_pts, wide, core_s);
+    mark_core(c, g, cv, Ps, n, min_pts, wide, core_s, &qtrees);
     // ---- a7: core-first compaction
     tm.stage(DBSCAN_STAGE_COMPACT);
     compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
@@ -420,6 +426,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_SPARSE] = sparse;
   out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group ? 1 : (lat_group ? 2 : 0);
   out->stats[DBSCAN_STAT_MARKCORE_TESTS] = (int64_t)hw[0];
+  out->stats[DBSCAN_STAT_QT_NODES] = (int64_t)qtrees.nodes;
   return DBSCAN_OK;
 }
 

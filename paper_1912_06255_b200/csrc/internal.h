@@ -168,8 +168,20 @@ struct CellsView {
   const uint32_t* nbr;
   const uint32_t* ub;  // sum of neighbour-cell sizes (saturating)
 };
+// Per-cell range-count trees (qtree.cu, row f2): cells with >= QT_MIN points;
+// node_off[c] = first node of cell c's implicit binary tree (heap order),
+// box[node] = {lo[D], hi[D]} of its points, cnt[node] = their number.
+struct QTrees {
+  const uint64_t* node_off = nullptr;
+  const int32_t* box = nullptr;
+  const uint32_t* cnt = nullptr;
+  uint64_t nodes = 0;
+};
+// Orders the points of tree cells by Morton code inside the cell (Ps, idx
+// permuted within each cell) and builds the trees.
+void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx, int64_t n, QTrees* qt);
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
-               int64_t min_pts, bool wide, uint8_t* core_s);
+               int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt = nullptr);
 // core-first stable partition inside each mixed cell (Ps, idx, core_s permuted in
 // place); core_cnt[ncells]; counters[0] += core cells, counters[1] += mixed cells.
 void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,

@@ -1,0 +1,241 @@
+// qtree.cu — per-cell trees for RangeCount (the paper's
+// our-exact-qt: PAPER.md §"Range Counting").
+//
+// The paper divides each cell (side eps/sqrt(d)) recursively into 2^d
+// sub-cells until they are empty or small, each node storing its point count
+// (P:L960-967), builds the trees in parallel by integer-sorting the points of
+// a node by sub-cell, and answers RangeCount(p, eps, h) by a
+// traversal that descends only into sub-cells intersecting the eps-ball of p
+// and counts points explicitly at the leaves.
+//
+// GPU form (DESIGN.md §5 f2): the points of every cell with at least QT_MIN
+// points are ordered by the Morton code of their position inside the cell
+// (B bits per axis: the 2^d-ary subdivision B levels deep) with one radix
+// sort of (cell, Morton) keys; the tree over that order is implicit and
+// binary — leaves of QT_LEAF consecutive points, a complete binary tree above
+// them (node i has children 2i+1, 2i+2) — so every node is a run of points
+// sharing a Morton prefix, i.e. a union of quadtree sub-cells. Each node keeps
+// the integer bounding box of its points and their count. A query visits a
+// node only if its box intersects the eps-ball; a node whose box lies inside
+// the ball adds its count without any distance test (exact: every point of
+// the box is within eps); leaves test their points, a warp's lanes at once.
+#include "internal.h"
+
+namespace db {
+
+constexpr uint32_t QT_MIN = 256;   // cells with at least this many points get a tree
+constexpr int QT_LEAF = 32;        // points per leaf (a warp tests a leaf at once)
+
+__device__ __forceinline__ uint32_t qt_leaves(uint32_t m) {
+  uint32_t L = (m + QT_LEAF - 1) / QT_LEAF, P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  return P2;
+}
+
+// (cell << MB) | Morton code of the point's position inside its cell (B bits
+// per axis, axis 0 most significant within a level); 0 for points of cells
+// without a tree, so that a stable sort keeps their order.
+template <int D>
+__global__ void qt_keys_kernel(const int32_t* __restrict__ Ps, const uint32_t* __restrict__ cell_of,
+                               const uint32_t* __restrict__ cell_start, const uint64_t* __restrict__ cell_key,
+                               uint32_t n, Geo g, int B, int MB, uint64_t* __restrict__ keys,
+                               uint32_t* __restrict__ vals) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t c = cell_of[j];
+  const uint32_t m = cell_start[c + 1] - cell_start[c];
+  uint64_t code = 0;
+  if (m >= QT_MIN) {
+    int32_t x[D];
+    PtLoad<D>::load(Ps, j, x);
+    const uint64_t key = cell_key[c];
+    uint32_t q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      q[k] = 0;
+      if (k < g.d) {
+        // offset inside the cell, 0 .. s-1, scaled to B bits
+        const int64_t base = (int64_t)g.lo[k] + (int64_t)cell_coord(key, g, k) * (int64_t)g.s;
+        const uint64_t r = (uint64_t)((int64_t)x[k] - base);
+        q[k] = (uint32_t)((r << B) / g.s);
+      }
+    }
+    for (int b = B - 1; b >= 0; --b)
+      for (int k = 0; k < g.d; ++k) code = (code << 1) | ((q[k] >> b) & 1u);
+  }
+  keys[j] = ((uint64_t)c << MB) | code;
+  vals[j] = j;
+}
+
+template <int D>
+__global__ void qt_gather_kernel(const uint32_t* __restrict__ perm, uint32_t n, const int32_t* __restrict__ Ps,
+                                 const uint32_t* __restrict__ idx, int32_t* __restrict__ Ps2,
+                                 uint32_t* __restrict__ idx2) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t s = perm[j];
+#pragma unroll
+  for (int k = 0; k < D; ++k) Ps2[(size_t)j * D + k] = Ps[(size_t)s * D + k];
+  idx2[j] = idx[s];
+}
+
+__global__ void qt_nodes_count_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                      uint32_t* __restrict__ nnodes) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const uint32_t m = cell_start[c + 1] - cell_start[c];
+  nnodes[c] = m >= QT_MIN ? 2 * qt_leaves(m) - 1 : 0;
+}
+
+// Warp per leaf slot of every tree cell: the leaf's box and count, then the
+// lane-0 thread climbs: the second child to arrive at a node builds it.
+template <int D>
+__global__ void __launch_bounds__(256) qt_build_kernel(const int32_t* __restrict__ Ps,
+                                                       const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                                       const uint64_t* __restrict__ node_off, int d,
+                                                       int32_t* box, uint32_t* cnt, uint32_t* flags,
+                                                       const uint32_t* __restrict__ leaf_cell,
+                                                       const uint32_t* __restrict__ leaf_idx, uint64_t nleaves) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nleaves; w += nwarps) {
+    const uint32_t c = leaf_cell[w], lf = leaf_idx[w];
+    const uint32_t s = cell_start[c], e = cell_start[c + 1];
+    const uint32_t P2 = qt_leaves(e - s);
+    const uint64_t base = node_off[c];
+    const uint32_t u = s + lf * QT_LEAF + lane;
+    const bool ok = u < e && lf * QT_LEAF < e - s;
+    int32_t x[D];
+    if (ok) PtLoad<D>::load(Ps, u, x);
+    int32_t lo[D], hi[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      int32_t l = ok ? x[k] : INT32_MAX, h = ok ? x[k] : INT32_MIN;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        l = min(l, __shfl_xor_sync(DB_FULL, l, o));
+        h = max(h, __shfl_xor_sync(DB_FULL, h, o));
+      }
+      lo[k] = l; hi[k] = h;
+    }
+    const uint32_t nl = (uint32_t)__popc(__ballot_sync(DB_FULL, ok));
+    if (lane == 0) {
+      uint64_t node = P2 - 1 + lf;
+      for (int k = 0; k < D; ++k) { box[(base + node) * 2 * D + k] = lo[k]; box[(base + node) * 2 * D + D + k] = hi[k]; }
+      cnt[base + node] = nl;
+      uint32_t cnt_acc = nl;
+      while (node > 0) {
+        __threadfence();
+        const uint64_t parent = (node - 1) >> 1;
+        if (atomicAdd(flags + base + parent, 1u) == 0) break;  // the sibling builds it
+        __threadfence();
+        const uint64_t sib = (node & 1) ? node + 1 : node - 1;
+        const volatile int32_t* sb = box + (base + sib) * 2 * D;
+        for (int k = 0; k < D; ++k) { lo[k] = min(lo[k], sb[k]); hi[k] = max(hi[k], sb[D + k]); }
+        cnt_acc += ((volatile uint32_t*)cnt)[base + sib];
+        for (int k = 0; k < D; ++k) {
+          box[(base + parent) * 2 * D + k] = lo[k];
+          box[(base + parent) * 2 * D + D + k] = hi[k];
+        }
+        cnt[base + parent] = cnt_acc;
+        node = parent;
+      }
+    }
+    __syncwarp();
+  }
+  (void)d;
+  (void)ncells;
+}
+
+__global__ void qt_leaf_list_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                    const uint64_t* __restrict__ leaf_off, uint32_t* __restrict__ leaf_cell,
+                                    uint32_t* __restrict__ leaf_idx) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const uint32_t m = cell_start[c + 1] - cell_start[c];
+  if (m < QT_MIN) return;
+  const uint32_t P2 = qt_leaves(m);
+  const uint64_t o = leaf_off[c];
+  for (uint32_t l = 0; l < P2; ++l) { leaf_cell[o + l] = c; leaf_idx[o + l] = l; }
+}
+
+__global__ void qt_leaf_count_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                     uint32_t* __restrict__ nl) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const uint32_t m = cell_start[c + 1] - cell_start[c];
+  nl[c] = m >= QT_MIN ? qt_leaves(m) : 0;
+}
+
+void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx, int64_t n, QTrees* qt) {
+  const uint32_t nc = cv.ncells;
+  // 1. order the points of tree cells by (cell, Morton code inside the cell)
+  int cbits = 1;
+  while (cbits < 32 && (1ull << cbits) < nc) ++cbits;
+  const int B = std::min(10, (60 - cbits) / g.d);
+  const int MB = B * g.d;
+  uint64_t* k0 = c.alloc<uint64_t>(n);
+  uint64_t* k1 = c.alloc<uint64_t>(n);
+  uint32_t* v0 = c.alloc<uint32_t>(n);
+  uint32_t* v1 = c.alloc<uint32_t>(n);
+  auto byD = [&](auto f) {
+    if (g.D == 2) f(std::integral_constant<int, 2>());
+    else if (g.D == 4) f(std::integral_constant<int, 4>());
+    else f(std::integral_constant<int, 8>());
+  };
+  byD([&](auto Dc) {
+    constexpr int D = decltype(Dc)::value;
+    qt_keys_kernel<D><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(Ps, cv.cell_of, cv.cell_start, cv.cell_key,
+                                                                  (uint32_t)n, g, B, MB, k0, v0);
+  });
+  c.launched();
+  uint64_t* ko;
+  uint32_t* perm;
+  radix_sort_u64(c, k0, v0, k1, v1, n, cbits + MB, &ko, &perm);
+  int32_t* Ps2 = c.alloc<int32_t>((size_t)n * g.D);
+  uint32_t* idx2 = c.alloc<uint32_t>(n);
+  byD([&](auto Dc) {
+    constexpr int D = decltype(Dc)::value;
+    qt_gather_kernel<D><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(perm, (uint32_t)n, Ps, idx, Ps2, idx2);
+  });
+  c.launched();
+  DB_CUDA(cudaMemcpyAsync(Ps, Ps2, sizeof(int32_t) * (size_t)n * g.D, cudaMemcpyDeviceToDevice, c.st));
+  DB_CUDA(cudaMemcpyAsync(idx, idx2, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, c.st));
+  // 2. node offsets and leaf lists
+  uint32_t* nn = c.alloc<uint32_t>(nc);
+  uint64_t* node_off = c.alloc<uint64_t>((size_t)nc + 1);
+  qt_nodes_count_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(cv.cell_start, nc, nn);
+  c.launched();
+  exclusive_scan_u32_u64(c, nn, node_off, nc);
+  uint32_t* nl = c.alloc<uint32_t>(nc);
+  uint64_t* leaf_off = c.alloc<uint64_t>((size_t)nc + 1);
+  qt_leaf_count_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(cv.cell_start, nc, nl);
+  c.launched();
+  exclusive_scan_u32_u64(c, nl, leaf_off, nc);
+  uint64_t tot[2];
+  DB_CUDA(cudaMemcpyAsync(&tot[0], node_off + nc, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.st));
+  DB_CUDA(cudaMemcpyAsync(&tot[1], leaf_off + nc, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.st));
+  DB_CUDA(cudaStreamSynchronize(c.st));
+  qt->node_off = node_off;
+  qt->nodes = tot[0];
+  if (tot[0] == 0) { qt->box = nullptr; qt->cnt = nullptr; return; }
+  int32_t* box = c.alloc<int32_t>(tot[0] * 2 * g.D);
+  uint32_t* cnt = c.alloc<uint32_t>(tot[0]);
+  uint32_t* flags = c.alloc<uint32_t>(tot[0]);
+  c.zero(flags, sizeof(uint32_t) * tot[0]);
+  uint32_t* leaf_cell = c.alloc<uint32_t>(tot[1]);
+  uint32_t* leaf_idx = c.alloc<uint32_t>(tot[1]);
+  qt_leaf_list_kernel<<<grid_for(nc, 256, 1 << 30), 256, 0, c.st>>>(cv.cell_start, nc, leaf_off, leaf_cell,
+                                                                    leaf_idx);
+  c.launched();
+  byD([&](auto Dc) {
+    constexpr int D = decltype(Dc)::value;
+    qt_build_kernel<D><<<grid_for((int64_t)tot[1] * 32, 256, c.sms * 16), 256, 0, c.st>>>(
+        Ps, cv.cell_start, nc, node_off, g.d, box, cnt, flags, leaf_cell, leaf_idx, tot[1]);
+  });
+  c.launched();
+  qt->box = box;
+  qt->cnt = cnt;
+}
+
+}  // namespace db

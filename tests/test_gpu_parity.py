@@ -99,7 +99,8 @@ def test_random_small_vs_o1(oracle_lib):
                                    pkg.F_FORCE_SPARSE | pkg.F_FORCE_WIDE | pkg.F_NO_WAVES,
                                    pkg.F_RADIX_GROUP, pkg.F_RADIX_GROUP | pkg.F_FORCE_SPARSE,
                                    pkg.F_LATTICE_GROUP, pkg.F_LATTICE_GROUP | pkg.F_FORCE_SPARSE,
-                                   pkg.F_LATTICE_GROUP | pkg.F_NO_SPARSE])
+                                   pkg.F_LATTICE_GROUP | pkg.F_NO_SPARSE,
+                                   pkg.F_QUADTREE, pkg.F_QUADTREE | pkg.F_RADIX_GROUP | pkg.F_FORCE_TREE])
 def test_flag_variants_vs_o1(oracle_lib, flags):
     for k, (pts, eps, mp) in enumerate(_instances(200 + flags, 120, dmax=8)):
         r = run_or_erange(pts, eps, mp, flags)
@@ -290,3 +291,22 @@ def test_host_path_caller_buffers(oracle_lib):
         got = np_result(r)
         assert len(got.border_ids) == int(got.border_off[-1])
         assert_same(got, o, f"cap={cap}")
+
+
+
+@pytest.mark.parametrize("flags", [pkg.F_QUADTREE, pkg.F_QUADTREE | pkg.F_RADIX_GROUP,
+                                   pkg.F_QUADTREE | pkg.F_FORCE_WIDE])
+@pytest.mark.parametrize("d", [2, 3, 5])
+def test_quadtree_vs_o2(oracle_lib, d, flags):
+    """Row f2 (our-exact-qt, P:L955-1003): big cells get range-count trees;
+    sparse points beside them count through the trees (minPts large, so the
+    counts run long: the paper's "spike" case)."""
+    L = 30_000 if d <= 3 else 60_000
+    pts = datagen.seed_spreader(60_000, d, L, 50 + d, 0.02, noise_frac=0.05)
+    for eps, mp in [(400, 300), (400, 1500), (250, 60)]:
+        r = run_or_erange(pts, eps, mp, flags)
+        if r is None:
+            continue
+        assert_same(r, oracle_lib.o2(pts, eps, mp), f"qt d={d} eps={eps} mp={mp} flags={flags}")
+    r = gpu(pts, 400, 1500, flags)
+    assert r.stats["qt_nodes"] > 0

@@ -11,7 +11,7 @@ Each line: JSON with the dataset, eps, minPts, device ms (CUDA events on the
 launching stream, L2 flushed before each call, median of --reps), points/s,
 per-stage ms and counters. Inputs are the BASELINE configs' generators.
 
-usage: python tools/sweep.py [--n 10000000] [--reps 3] [--only eps|minpts|varden]
+usage: python tools/sweep.py [--n 10000000] [--reps 3] [--only eps|minpts|varden|qt]
 """
 import argparse
 import json
@@ -26,14 +26,14 @@ import datagen  # noqa: E402
 import paper_1912_06255_b200 as pkg  # noqa: E402
 
 
-def timed(t, eps, mp, reps, flush):
+def timed(t, eps, mp, reps, flush, flags=0):
     ms, last = [], None
     st = torch.cuda.current_stream()
     for _ in range(reps + 1):
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        r = pkg.dbscan(t, eps, mp, timing=True)
+        r = pkg.dbscan(t, eps, mp, flags=flags, timing=True)
         e1.record(st)
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
@@ -59,13 +59,21 @@ def main():
         sets += [("ss-simden-3d", ss3, 1000, mp) for mp in (10, 100, 1000, 10_000)]
         uf = datagen.uniform(a.n, 3, 100_000, 4)
         sets += [("uniform-3d", uf, 500, mp) for mp in (10, 30, 100, 1000, 10_000)]
+    if a.only in ("", "qt"):
+        # row f2: minPts sweep where sparse points beside huge cells count long
+        # (P:L1473-1477), plain scan vs per-cell trees (F_QUADTREE)
+        ss3 = datagen.seed_spreader(a.n, 3, 1e6, 2, 1000 / a.n, noise_frac=1e-4)
+        for mp in (100, 1000, 10_000, 30_000):
+            sets.append(("ss-simden-3d", ss3, 1000, mp))
+            sets.append(("ss-simden-3d+qt", ss3, 1000, mp))
     if a.only in ("", "varden"):
         for d, L, eps in ((2, 1e6, 1000), (3, 1e6, 1000), (5, 1e5, 2000), (7, 1e5, 2000)):
             vd = datagen.seed_spreader(a.n, d, L, 20 + d, 1000 / a.n, varden=True)
             sets.append((f"ss-varden-{d}d", vd, eps, 100))
     for name, pts, eps, mp in sets:
         t = torch.from_numpy(pts).cuda()
-        ms, r = timed(t, eps, mp, a.reps, flush)
+        flags = pkg.F_QUADTREE if name.endswith("+qt") else 0
+        ms, r = timed(t, eps, mp, a.reps, flush, flags)
         print(json.dumps({"data": name, "n": len(pts), "d": pts.shape[1], "eps": eps, "min_pts": mp,
                           "ms": round(ms, 4), "pts_per_s": len(pts) / (ms / 1e3),
                           "stage_ms": {k: round(v, 4) for k, v in r.stage_ms.items()},
