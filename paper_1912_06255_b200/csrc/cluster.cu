@@ -154,6 +154,82 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
   return false;
 }
 
+// Tree variant (row f2: "for each core point p in g, issue a
+// RangeCount query to h and connect if non-zero"): h's points are all core
+// and ordered under a range-count tree (qtree.cu). For each 32-point block of
+// g's core points (lanes), one warp-uniform traversal of h's tree: a node is
+// entered if its box is within eps of some lane's point; a node whose box
+// lies within eps of some lane's point in full proves a pair within eps (the
+// node holds >= 1 point, all core) and ends the search; leaves are tested 32
+// x 32 by shuffles.
+template <int D, bool WIDE>
+__device__ bool warp_bcp_tree(uint32_t ga, uint32_t hb, const CellsView& cv, const Geo& g,
+                              const int32_t* __restrict__ Ps, const uint32_t* __restrict__ core_cnt,
+                              const QTrees& qt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t sa = cv.cell_start[ga], ea = sa + core_cnt[ga];
+  const uint32_t sb = cv.cell_start[hb], eb = cv.cell_start[hb + 1];
+  uint32_t L = (eb - sb + 31) / 32, P2 = 1;
+  while (P2 < L) P2 <<= 1;
+  const uint64_t base = qt.node_off[hb];
+  int64_t boxh[D];
+  cell_box_lo<D>(cv.cell_key[hb], g, boxh);
+  for (uint32_t a0 = sa; a0 < ea; a0 += 32) {
+    const uint32_t u = a0 + lane;
+    int32_t a[D];
+    bool keep = false;
+    if (u < ea) {
+      PtLoad<D>::load(Ps, u, a);
+      keep = near_box<D>(a, boxh, g);
+    }
+    if (!__any_sync(DB_FULL, keep)) continue;
+    uint32_t stack[64];
+    int sp = 0;
+    stack[sp++] = 0;
+    while (sp > 0) {
+      const uint32_t node = stack[--sp];
+      if (node >= P2 - 1) {
+        const uint32_t v = sb + (node - (P2 - 1)) * 32 + lane;
+        int32_t b[D];
+        const bool vb = v < eb;
+        if (vb) PtLoad<D>::load(Ps, v, b);
+        uint32_t mb = __ballot_sync(DB_FULL, vb);
+        bool mine = false;
+        while (mb) {
+          const int src = __ffs(mb) - 1;
+          mb &= mb - 1;
+          int32_t q[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
+          mine |= keep && within<D, WIDE>(a, q, g.clampc, g.eps2);
+        }
+        if (__any_sync(DB_FULL, mine)) return true;
+        continue;
+      }
+      for (uint32_t ch = 2 * node + 2; ch >= 2 * node + 1; --ch) {
+        if (qt.cnt[base + ch] == 0) continue;
+        const int32_t* bx = qt.box + (base + ch) * 2 * D;
+        uint64_t mn = 0, mx = 0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          if (k < g.d) {
+            const int64_t x = a[k], lo = bx[k], hi = bx[D + k];
+            uint64_t p = (uint64_t)(x < lo ? lo - x : (x > hi ? x - hi : 0));
+            uint64_t f = (uint64_t)max(x - lo, hi - x);
+            if (p > g.clampc) p = g.clampc;
+            if (f > g.clampc) f = g.clampc;
+            mn += p * p;
+            mx += f * f;
+          }
+        }
+        if (__any_sync(DB_FULL, keep && mx <= g.eps2)) return true;  // a pair within eps exists
+        if (__any_sync(DB_FULL, keep && mn <= g.eps2)) stack[sp++] = ch;
+      }
+    }
+  }
+  return false;
+}
+
 // Warp per pair over list[0 .. min(*count, cap)) (the sparse path's queue).
 template <int D, bool WIDE>
 __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict__ list,
@@ -161,7 +237,7 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
                                                         CellsView cv, Geo g,
                                                         const int32_t* __restrict__ Ps,
                                                         const uint32_t* __restrict__ core_cnt,
-                                                        uint32_t* parent, uint32_t cap) {
+                                                        uint32_t* parent, uint32_t cap, QTrees qt) {
   const int lane = threadIdx.x & 31;
   const uint32_t m = min(*count, cap);
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -170,7 +246,15 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
     bool done = false;
     if (lane == 0) done = uf_find(parent, p.x) == uf_find(parent, p.y);
     if (__shfl_sync(DB_FULL, done, 0)) continue;
-    const bool hit = warp_bcp<D, WIDE>(p, cv, g, Ps, core_cnt, parent);
+    // a tree on an all-core side (f2): search it; else the block BCP
+    bool hit;
+    const bool ty = qt.nodes && qt.node_off[p.y + 1] > qt.node_off[p.y] &&
+                    core_cnt[p.y] == cv.cell_start[p.y + 1] - cv.cell_start[p.y];
+    const bool tx = qt.nodes && qt.node_off[p.x + 1] > qt.node_off[p.x] &&
+                    core_cnt[p.x] == cv.cell_start[p.x + 1] - cv.cell_start[p.x];
+    if (ty) hit = warp_bcp_tree<D, WIDE>(p.x, p.y, cv, g, Ps, core_cnt, qt);
+    else if (tx) hit = warp_bcp_tree<D, WIDE>(p.y, p.x, cv, g, Ps, core_cnt, qt);
+    else hit = warp_bcp<D, WIDE>(p, cv, g, Ps, core_cnt, parent);
     if (hit && lane == 0) uf_link(parent, p.x, p.y);
     __syncwarp();
   }
@@ -239,16 +323,19 @@ void uf_init(Ctx& c, uint32_t* parent, uint32_t n) {
 }
 
 void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
-               uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide) {
+               uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide,
+               const QTrees* qt) {
+  const QTrees none;
   dispatch(g.D, wide, [&]<int D, bool W>() {
-    bcp_large_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap);
+    bcp_large_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap,
+                                                          qt ? *qt : none);
   });
   c.launched();
 }
 
 void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
                   bool wide, bool waves, uint64_t nbr_total, uint32_t* parent, unsigned long long* tested,
-                  unsigned long long* npairs_out) {
+                  unsigned long long* npairs_out, const QTrees* qt) {
   const uint32_t nc = cv.ncells;
   const int nw = waves ? NWAVES : 1;
   uf_init(c, parent, nc);
@@ -282,7 +369,7 @@ void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, 
                                                  nlarge + w, tested);
     });
     c.launched();
-    bcp_large(c, g, cv, Ps, core_cnt, parent, large, nlarge + w, (uint32_t)nbr_total, wide);
+    bcp_large(c, g, cv, Ps, core_cnt, parent, large, nlarge + w, (uint32_t)nbr_total, wide, qt);
   }
 }
 

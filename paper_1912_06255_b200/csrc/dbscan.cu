@@ -347,7 +347,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     tm.stage(DBSCAN_STAGE_CLUSTER);
     uint32_t* parent = c.alloc<uint32_t>(ncells);
     if (sparse) sparse_cluster(c, g, cv, Ps, core_cnt, wide, parent, cnt64, &so);
-    else cluster_core(c, g, cv, Ps, core_cnt, wide, waves, nbr_total, parent, cnt64, cnt64 + 2);
+    else cluster_core(c, g, cv, Ps, core_cnt, wide, waves, nbr_total, parent, cnt64, cnt64 + 2, &qtrees);
 
     // ---- a9: labels, scattered to input order
     tm.stage(DBSCAN_STAGE_LABELS);

@@ -221,13 +221,15 @@ void sparse_release(SparseOut* o);
 void uf_init(Ctx& c, uint32_t* parent, uint32_t n);
 // warp-per-pair BCP over list[0 .. min(*count, cap)) with Link on success
 void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
-               uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide);
+               uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide,
+               const struct QTrees* qt = nullptr);
 // *tested (device) counts pairs that survived the Find check of their wave;
 // *npairs (device) receives the number of candidate pairs. nbr_total = CSR
 // entries (bounds the pairs; no host synchronisation).
 void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
                   bool wide, bool waves, uint64_t nbr_total, uint32_t* parent,
-                  unsigned long long* tested /*device, zeroed*/, unsigned long long* npairs);
+                  unsigned long long* tested /*device, zeroed*/, unsigned long long* npairs,
+                  const struct QTrees* qt = nullptr);
 // Smallest core input index of a cell: its first point (stable radix sort and
 // stable partition), cellmin[] for all-core cells (hash grouping: order inside
 // a cell is arbitrary), or a scan of its core points (lattice counting sort).

@@ -9,9 +9,9 @@
 // and counts points explicitly at the leaves.
 //
 // GPU form (DESIGN.md §5 f2): the points of every cell with at least QT_MIN
-// points are ordered by the Morton code of their position inside the cell
-// (B bits per axis: the 2^d-ary subdivision B levels deep) with one radix
-// sort of (cell, Morton) keys; the tree over that order is implicit and
+// points are ordered by sub-cell of the 2^d-ary subdivision B levels deep
+// (Morton order of the sub-cells, d B <= 12) with a counting sort per cell in
+// shared memory; the tree over that order is implicit and
 // binary — leaves of QT_LEAF consecutive points, a complete binary tree above
 // them (node i has children 2i+1, 2i+2) — so every node is a run of points
 // sharing a Morton prefix, i.e. a union of quadtree sub-cells. Each node keeps
@@ -19,6 +19,8 @@
 // node only if its box intersects the eps-ball; a node whose box lies inside
 // the ball adds its count without any distance test (exact: every point of
 // the box is within eps); leaves test their points, a warp's lanes at once.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace db {
@@ -32,51 +34,82 @@ __device__ __forceinline__ uint32_t qt_leaves(uint32_t m) {
   return P2;
 }
 
-// (cell << MB) | Morton code of the point's position inside its cell (B bits
-// per axis, axis 0 most significant within a level); 0 for points of cells
-// without a tree, so that a stable sort keeps their order.
-template <int D>
-__global__ void qt_keys_kernel(const int32_t* __restrict__ Ps, const uint32_t* __restrict__ cell_of,
-                               const uint32_t* __restrict__ cell_start, const uint64_t* __restrict__ cell_key,
-                               uint32_t n, Geo g, int B, int MB, uint64_t* __restrict__ keys,
-                               uint32_t* __restrict__ vals) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const uint32_t c = cell_of[j];
-  const uint32_t m = cell_start[c + 1] - cell_start[c];
-  uint64_t code = 0;
-  if (m >= QT_MIN) {
-    int32_t x[D];
-    PtLoad<D>::load(Ps, j, x);
-    const uint64_t key = cell_key[c];
-    uint32_t q[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      q[k] = 0;
-      if (k < g.d) {
-        // offset inside the cell, 0 .. s-1, scaled to B bits
-        const int64_t base = (int64_t)g.lo[k] + (int64_t)cell_coord(key, g, k) * (int64_t)g.s;
-        const uint64_t r = (uint64_t)((int64_t)x[k] - base);
-        q[k] = (uint32_t)((r << B) / g.s);
-      }
-    }
-    for (int b = B - 1; b >= 0; --b)
-      for (int k = 0; k < g.d; ++k) code = (code << 1) | ((q[k] >> b) & 1u);
-  }
-  keys[j] = ((uint64_t)c << MB) | code;
-  vals[j] = j;
-}
+// Block per tree cell: counting sort of its points by sub-cell (the top B
+// levels of the 2^d-ary subdivision, d B <= 12: up to 4096 sub-cells), the
+// paper's per-node integer sort on sub-cell keys done once for
+// B levels; then copied back in place. Order inside a sub-cell is the atomics'.
+constexpr int QT_SUB_BITS = 12;
 
 template <int D>
-__global__ void qt_gather_kernel(const uint32_t* __restrict__ perm, uint32_t n, const int32_t* __restrict__ Ps,
-                                 const uint32_t* __restrict__ idx, int32_t* __restrict__ Ps2,
-                                 uint32_t* __restrict__ idx2) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const uint32_t s = perm[j];
+__global__ void __launch_bounds__(1024) qt_sort_cells_kernel(int32_t* __restrict__ Ps, uint32_t* __restrict__ idx,
+                                                             const uint32_t* __restrict__ cell_start,
+                                                             const uint64_t* __restrict__ cell_key, uint32_t ncells,
+                                                             Geo g, int B, int32_t* __restrict__ Ps2,
+                                                             uint32_t* __restrict__ idx2) {
+  __shared__ uint32_t hist[1 << QT_SUB_BITS];
+  __shared__ uint32_t s_scan[33];
+  const int NB = 1 << (B * g.d);
+  for (uint32_t c = blockIdx.x; c < ncells; c += gridDim.x) {
+    const uint32_t s = cell_start[c], e = cell_start[c + 1];
+    if (e - s < QT_MIN) continue;  // uniform per block
+    const uint64_t key = cell_key[c];
+    int64_t base[8];
 #pragma unroll
-  for (int k = 0; k < D; ++k) Ps2[(size_t)j * D + k] = Ps[(size_t)s * D + k];
-  idx2[j] = idx[s];
+    for (int k = 0; k < 8; ++k)
+      base[k] = k < g.d ? (int64_t)g.lo[k] + (int64_t)cell_coord(key, g, k) * (int64_t)g.s : 0;
+    auto sub_of = [&](const int32_t* x) -> uint32_t {
+      uint32_t q[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        q[k] = k < g.d ? (uint32_t)((((uint64_t)((int64_t)x[k] - base[k])) << B) / g.s) : 0u;
+      uint32_t code = 0;
+      for (int b = B - 1; b >= 0; --b)
+        for (int k = 0; k < g.d; ++k) code = (code << 1) | ((q[k] >> b) & 1u);
+      return code;
+    };
+    for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t j = s + threadIdx.x; j < e; j += blockDim.x) {
+      int32_t x[D];
+      PtLoad<D>::load(Ps, j, x);
+      atomicAdd(hist + sub_of(x), 1u);
+    }
+    __syncthreads();
+    // exclusive scan of hist (blockDim = 1024 threads x 4 bins)
+    {
+      const int per = (NB + (int)blockDim.x - 1) / (int)blockDim.x;
+      uint32_t v[4] = {0, 0, 0, 0}, sum = 0;
+      for (int t = 0; t < per && t < 4; ++t) {
+        const int i = threadIdx.x * per + t;
+        v[t] = i < NB ? hist[i] : 0u;
+        sum += v[t];
+      }
+      uint32_t tot;
+      uint32_t ex = block_exclusive_scan<uint32_t>(sum, s_scan, &tot);
+      for (int t = 0; t < per && t < 4; ++t) {
+        const int i = threadIdx.x * per + t;
+        if (i < NB) hist[i] = ex;
+        ex += v[t];
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = s + threadIdx.x; j < e; j += blockDim.x) {
+      int32_t x[D];
+      PtLoad<D>::load(Ps, j, x);
+      const uint32_t pos = s + atomicAdd(hist + sub_of(x), 1u);
+#pragma unroll
+      for (int k = 0; k < D; ++k) Ps2[(size_t)pos * D + k] = x[k];
+      idx2[pos] = idx[j];
+    }
+    __syncthreads();
+    __threadfence_block();
+    for (uint32_t j = s + threadIdx.x; j < e; j += blockDim.x) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) Ps[(size_t)j * D + k] = Ps2[(size_t)j * D + k];
+      idx[j] = idx2[j];
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void qt_nodes_count_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
@@ -169,15 +202,10 @@ __global__ void qt_leaf_count_kernel(const uint32_t* __restrict__ cell_start, ui
 
 void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx, int64_t n, QTrees* qt) {
   const uint32_t nc = cv.ncells;
-  // 1. order the points of tree cells by (cell, Morton code inside the cell)
-  int cbits = 1;
-  while (cbits < 32 && (1ull << cbits) < nc) ++cbits;
-  const int B = std::min(10, (60 - cbits) / g.d);
-  const int MB = B * g.d;
-  uint64_t* k0 = c.alloc<uint64_t>(n);
-  uint64_t* k1 = c.alloc<uint64_t>(n);
-  uint32_t* v0 = c.alloc<uint32_t>(n);
-  uint32_t* v1 = c.alloc<uint32_t>(n);
+  // 1. order the points of every tree cell by sub-cell (block per cell)
+  const int B = std::max(1, QT_SUB_BITS / g.d);
+  int32_t* Ps2 = c.alloc<int32_t>((size_t)n * g.D);
+  uint32_t* idx2 = c.alloc<uint32_t>(n);
   auto byD = [&](auto f) {
     if (g.D == 2) f(std::integral_constant<int, 2>());
     else if (g.D == 4) f(std::integral_constant<int, 4>());
@@ -185,22 +213,10 @@ void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
   };
   byD([&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
-    qt_keys_kernel<D><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(Ps, cv.cell_of, cv.cell_start, cv.cell_key,
-                                                                  (uint32_t)n, g, B, MB, k0, v0);
+    qt_sort_cells_kernel<D><<<std::min<uint32_t>(nc, (uint32_t)c.sms * 8), 1024, 0, c.st>>>(
+        Ps, idx, cv.cell_start, cv.cell_key, nc, g, B, Ps2, idx2);
   });
   c.launched();
-  uint64_t* ko;
-  uint32_t* perm;
-  radix_sort_u64(c, k0, v0, k1, v1, n, cbits + MB, &ko, &perm);
-  int32_t* Ps2 = c.alloc<int32_t>((size_t)n * g.D);
-  uint32_t* idx2 = c.alloc<uint32_t>(n);
-  byD([&](auto Dc) {
-    constexpr int D = decltype(Dc)::value;
-    qt_gather_kernel<D><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(perm, (uint32_t)n, Ps, idx, Ps2, idx2);
-  });
-  c.launched();
-  DB_CUDA(cudaMemcpyAsync(Ps, Ps2, sizeof(int32_t) * (size_t)n * g.D, cudaMemcpyDeviceToDevice, c.st));
-  DB_CUDA(cudaMemcpyAsync(idx, idx2, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, c.st));
   // 2. node offsets and leaf lists
   uint32_t* nn = c.alloc<uint32_t>(nc);
   uint64_t* node_off = c.alloc<uint64_t>((size_t)nc + 1);
