@@ -96,7 +96,9 @@ extern "C" {
                                         0 LSD radix sort + segmentation                      */
 #define DBSCAN_STAT_MARKCORE_TESTS 14 /* distance tests of the sparse MarkCore (F_COUNT_WORK)  */
 #define DBSCAN_STAT_QT_NODES     15  /* tree nodes built with F_QUADTREE                         */
-#define DBSCAN_NSTATS            16
+#define DBSCAN_STAT_APPROX_SIDE  16  /* dbscan_approx: sub-cell side t of the connectivity test
+                                        (0: the test is exact)                                */
+#define DBSCAN_NSTATS            20
 
 typedef struct dbscan_result {
   int64_t  n;
@@ -136,6 +138,23 @@ typedef struct dbscan_result {
  */
 int dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
            uint32_t flags, void *stream, dbscan_result *out);
+
+/*
+ * dbscan_approx — rho-approximate DBSCAN (Gan and Tao; §2 P:L225-235,
+ * §"Approximate DBSCAN" P:L1037-1058).
+ *   Same arguments, outputs and conventions as dbscan(), plus rho > 0. Core
+ *   flags and the border rule are those of DBSCAN; core points within eps are
+ *   always in one cluster, core points farther apart than eps (1 + rho) are
+ *   connected only through chains of closer pairs, and pairs in between may or
+ *   may not be connected. Several outputs are valid; cluster ids stay canonical
+ *   (minimum input index of a core point of the cluster).
+ *   Connectivity test: both points snapped to sub-cells of integer side t, the
+ *   largest with 2 (t-1) sqrt(d) <= eps rho, connected when the sub-cell boxes
+ *   are within eps (stats[DBSCAN_STAT_APPROX_SIDE] = t; t = 1 is exact DBSCAN).
+ * Returns DBSCAN_EINVAL for rho outside (0, 1e6].
+ */
+int dbscan_approx(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts, double rho,
+                  uint32_t flags, void *stream, dbscan_result *out);
 
 /* Release what the library allocated in *r (never caller-owned F_CALLER_OUT buffers).
  * Device outputs are released with cudaFreeAsync on the stream of the dbscan() call,

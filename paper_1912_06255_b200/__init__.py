@@ -39,11 +39,11 @@ F_DEVICE_IO, F_TIMING, F_CALLER_OUT = 1, 2, 4
 F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
 F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP, F_COUNT_WORK = 128, 256, 512, 1024, 2048
 F_QUADTREE = 4096
-NSTAGES, NSTATS = 12, 16
+NSTAGES, NSTATS = 12, 20
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
-         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes"]
+         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side"]
 
 
 class _Result(C.Structure):
@@ -85,6 +85,9 @@ def load():
         lib.dbscan.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_uint32,
                                C.c_void_p, C.POINTER(_Result)]
         lib.dbscan.restype = C.c_int
+        lib.dbscan_approx.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_double,
+                                      C.c_uint32, C.c_void_p, C.POINTER(_Result)]
+        lib.dbscan_approx.restype = C.c_int
         lib.dbscan_result_free.argtypes = [C.POINTER(_Result)]
         lib.dbscan_error_string.argtypes = [C.c_int]
         lib.dbscan_error_string.restype = C.c_char_p
@@ -133,19 +136,26 @@ def _finish(res: _Result, flags: int) -> dict:
     return info
 
 
+def _call(lib, ptr, n, d, eps, min_pts, rho, flags, stream, res):
+    if rho is None:
+        return lib.dbscan(ptr, n, d, eps, min_pts, flags, stream, res)
+    return lib.dbscan_approx(ptr, n, d, eps, min_pts, float(rho), flags, stream, res)
+
+
 def _check(lib, rc):
     if rc != 0:
         raise DBSCANError(rc, lib.dbscan_error_string(rc).decode())
 
 
 def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = False, stream=None,
-           out=None) -> Result:
+           out=None, rho: float | None = None) -> Result:
     """Exact DBSCAN of integer points.
 
     points: (n, d) int32 — a CUDA torch tensor (device path: outputs are torch
     tensors on the same device, computed on `stream` or the current stream),
     or a host array / CPU tensor (host path: the library copies in and out;
     pinned memory makes those copies fast; outputs are numpy arrays).
+    rho: when given, rho-approximate DBSCAN (dbscan_approx).
     out: optional (core, cluster, border_off[, border_ids]) caller buffers for
     the host path (e.g. pinned CPU tensors), passed with DBSCAN_F_CALLER_OUT;
     border_ids is used when the result fits it (returned as a prefix view).
@@ -166,9 +176,8 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
         off = torch.empty(n + 1, dtype=torch.int64, device=dev)
         res.core, res.cluster, res.border_off = core.data_ptr(), cluster.data_ptr(), off.data_ptr()
         with torch.cuda.device(dev):
-            rc = lib.dbscan(C.c_void_p(pts.data_ptr()), n, d, int(eps), int(min_pts),
-                            flags | F_DEVICE_IO | F_CALLER_OUT, C.c_void_p(st.cuda_stream),
-                            C.byref(res))
+            rc = _call(lib, C.c_void_p(pts.data_ptr()), n, d, int(eps), int(min_pts), rho,
+                       flags | F_DEVICE_IO | F_CALLER_OUT, C.c_void_p(st.cuda_stream), C.byref(res))
         _check(lib, rc)
         nnz = int(res.nnz)
         if nnz > 0:
@@ -203,7 +212,7 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
             res.nnz = len(ids_b)
         f |= F_CALLER_OUT
     st = 0 if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
-    rc = lib.dbscan(C.c_void_p(ptr), n, d, int(eps), int(min_pts), f, C.c_void_p(st), C.byref(res))
+    rc = _call(lib, C.c_void_p(ptr), n, d, int(eps), int(min_pts), rho, f, C.c_void_p(st), C.byref(res))
     del keep
     _check(lib, rc)
     nnz = int(res.nnz)

@@ -112,7 +112,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
     bool keep = false;
     if (u < ea) {
       PtLoad<D>::load(Ps, u, a);
-      keep = near_box<D>(a, boxh, g);
+      keep = g.at || near_box<D>(a, boxh, g);  // (filters are for the exact test only)
     }
     if (!__any_sync(DB_FULL, keep)) continue;
     // bounding box of the kept block
@@ -133,7 +133,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
       bool kb = false;
       if (v < eb) {
         PtLoad<D>::load(Ps, v, b);
-        kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2);
+        kb = g.at || near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2);
       }
       uint32_t mb = __ballot_sync(DB_FULL, kb);
       bool mine = false;
@@ -143,7 +143,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
         int32_t q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
-        mine |= keep && within<D, WIDE>(a, q, g.clampc, g.eps2);
+        mine |= keep && connect_test<D, WIDE>(a, q, g);
       }
       if (__any_sync(DB_FULL, mine)) return true;
     }
@@ -248,9 +248,9 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
     if (__shfl_sync(DB_FULL, done, 0)) continue;
     // a tree on an all-core side (f2): search it; else the block BCP
     bool hit;
-    const bool ty = qt.nodes && qt.node_off[p.y + 1] > qt.node_off[p.y] &&
+    const bool ty = !g.at && qt.nodes && qt.node_off[p.y + 1] > qt.node_off[p.y] &&
                     core_cnt[p.y] == cv.cell_start[p.y + 1] - cv.cell_start[p.y];
-    const bool tx = qt.nodes && qt.node_off[p.x + 1] > qt.node_off[p.x] &&
+    const bool tx = !g.at && qt.nodes && qt.node_off[p.x + 1] > qt.node_off[p.x] &&
                     core_cnt[p.x] == cv.cell_start[p.x + 1] - cv.cell_start[p.x];
     if (ty) hit = warp_bcp_tree<D, WIDE>(p.x, p.y, cv, g, Ps, core_cnt, qt);
     else if (tx) hit = warp_bcp_tree<D, WIDE>(p.y, p.x, cv, g, Ps, core_cnt, qt);
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) wave_kernel(const uint2* __restrict__ pai
         PtLoad<D>::load(Ps, u, a);
         for (uint32_t v = sb; v < eb; ++v) {
           PtLoad<D>::load(Ps, v, q);
-          if (within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
+          if (connect_test<D, WIDE>(a, q, g)) { hit = true; break; }
         }
       }
       if (hit) uf_link(parent, p.x, p.y);

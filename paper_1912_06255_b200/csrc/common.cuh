@@ -34,6 +34,7 @@ struct Geo {
   uint32_t clampc;      // eps + 1: Lemma 3 clamp (reading 4)
   uint32_t R;           // max |delta| of lattice coordinates between neighbour cells
   uint64_t eps;         // eps
+  uint32_t at;          // rho-approximate DBSCAN (row f4): sub-cell side t >= 2; 0 = exact
 };
 
 __device__ __forceinline__ uint32_t cell_coord(uint64_t key, const Geo& g, int k) {
@@ -122,6 +123,34 @@ __device__ __forceinline__ bool within(const int32_t* a, const int32_t* b, uint3
     }
     return acc <= eps2;
   }
+}
+
+// Connectivity test of two core points in ClusterCore (Alg 3, the BCP).
+// Exact DBSCAN: ||a-b|| <= eps. rho-approximate DBSCAN (row f4, Gan and Tao,
+// PAPER.md P:L225-235): the points are snapped to sub-cells of integer side
+// t (a grid aligned with the cells' origin lo) and connected when the two
+// sub-cell boxes are within eps: sum_k gap_k^2 <= eps^2 with gap_k =
+// (|dq_k|-1) t + 1 for sub-cell index difference dq_k != 0 (the exact box
+// gap, as for cells, reading 7). A pair within eps always passes
+// (the box gap is at most the point distance); a passing pair is within
+// eps + 2 (t-1) sqrt(d) <= eps (1 + rho) because the host picks the largest
+// t with 2 (t-1) sqrt(d) <= eps rho.
+template <int D, bool WIDE>
+__device__ __forceinline__ bool connect_test(const int32_t* a, const int32_t* b, const Geo& g) {
+  if (g.at == 0) return within<D, WIDE>(a, b, g.clampc, g.eps2);
+  uint64_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < g.d) {
+      const uint32_t qa = ((uint32_t)a[k] - (uint32_t)g.lo[k]) / g.at;
+      const uint32_t qb = ((uint32_t)b[k] - (uint32_t)g.lo[k]) / g.at;
+      const uint32_t dq = qa > qb ? qa - qb : qb - qa;
+      uint64_t gap = dq ? (uint64_t)(dq - 1) * g.at + 1 : 0;
+      if (gap > g.clampc) gap = g.clampc;
+      acc += gap * gap;
+    }
+  }
+  return acc <= g.eps2;
 }
 
 // Squared distance from point p to the integer box of cell `key`, clamped as

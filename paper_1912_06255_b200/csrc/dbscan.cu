@@ -5,6 +5,7 @@
 // Every step runs in this library's kernels on the caller's stream.
 #include <mutex>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 
 #include "../../include/dbscan.h"
@@ -116,7 +117,8 @@ static cudaStream_t side_stream(int dev) {
 }
 
 static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
-               uint32_t flags, cudaStream_t st, dbscan_result* out, int32_t* uids, int64_t ucap) {
+               uint32_t flags, cudaStream_t st, dbscan_result* out, int32_t* uids, int64_t ucap,
+               double rho) {
   const bool dev_io = flags & DBSCAN_F_DEVICE_IO;
   const bool caller_out = flags & DBSCAN_F_CALLER_OUT;
   Priv* priv = new Priv();
@@ -195,6 +197,17 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   g.eps = (uint64_t)eps;
   g.clampc = (uint32_t)(eps + 1);
   g.R = (uint32_t)((uint64_t)(eps - 1) / s + 1);
+  // rho-approximate connectivity (row f4): largest integer m = t - 1 with
+  // 2 m sqrt(d) <= eps rho, i.e. 4 d m^2 <= (eps rho)^2; t = 1 is exact
+  g.at = 0;
+  if (rho > 0) {
+    const long double er = (long double)eps * (long double)rho;
+    long double mm = floorl(er / (2.0L * sqrtl((long double)d)));
+    if (mm > 2e9L) mm = 2e9L;
+    uint64_t m = (uint64_t)mm;
+    while (m > 0 && 4.0L * d * (long double)m * (long double)m > er * er) --m;
+    if (m >= 1) g.at = (uint32_t)(m + 1);
+  }
 
   tm.stage(DBSCAN_STAGE_BBOX);
   const int32_t* dpts = pts;
@@ -427,6 +440,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group ? 1 : (lat_group ? 2 : 0);
   out->stats[DBSCAN_STAT_MARKCORE_TESTS] = (int64_t)hw[0];
   out->stats[DBSCAN_STAT_QT_NODES] = (int64_t)qtrees.nodes;
+  out->stats[DBSCAN_STAT_APPROX_SIDE] = g.at;
   return DBSCAN_OK;
 }
 
@@ -453,8 +467,8 @@ static void free_priv(dbscan_result* r) {
 
 extern "C" {
 
-int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts, uint32_t flags,
-           void* stream, dbscan_result* out) {
+static int dbscan_impl(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts, uint32_t flags,
+                       void* stream, dbscan_result* out, double rho) {
   g_last_error.clear();
   if (!out) { g_last_error = "out is NULL"; return DBSCAN_EINVAL; }
   const bool caller_out = flags & DBSCAN_F_CALLER_OUT;
@@ -480,7 +494,7 @@ int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pt
   if (bad) { g_last_error = bad; return DBSCAN_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   try {
-    return run(pts, n, d, eps, min_pts, flags, st, out, uids, ucap);
+    return run(pts, n, d, eps, min_pts, flags, st, out, uids, ucap, rho);
   } catch (const Error& e) {
     g_last_error = e.what();
     cudaDeviceSynchronize();  // the call's stream and its side stream
@@ -495,6 +509,21 @@ int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pt
     free_priv(out);
     return DBSCAN_ECUDA;
   }
+}
+
+int dbscan(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts, uint32_t flags,
+           void* stream, dbscan_result* out) {
+  return dbscan_impl(pts, n, d, eps, min_pts, flags, stream, out, 0.0);
+}
+
+int dbscan_approx(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts, double rho,
+                  uint32_t flags, void* stream, dbscan_result* out) {
+  if (!(rho > 0) || rho > 1e6) {
+    g_last_error = "rho must be in (0, 1e6]";
+    if (out) std::memset(out, 0, sizeof(*out));
+    return DBSCAN_EINVAL;
+  }
+  return dbscan_impl(pts, n, d, eps, min_pts, flags, stream, out, rho);
 }
 
 void dbscan_result_free(dbscan_result* r) {

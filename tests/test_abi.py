@@ -27,7 +27,7 @@ def declared_functions():
 
 
 def test_header_declares_entry_points():
-    assert declared_functions() == ["dbscan", "dbscan_error_string", "dbscan_result_free",
+    assert declared_functions() == ["dbscan", "dbscan_approx", "dbscan_error_string", "dbscan_result_free",
                                     "dbscan_stage_name", "dbscan_version"]
 
 
@@ -46,7 +46,7 @@ def test_struct_layout_matches_header(lib):
     body = re.search(r"typedef struct dbscan_result \{(.*?)\} dbscan_result;", src, flags=re.S).group(1)
     hdr = re.findall(r"\*?\s*(\w+)(?:\[\w+\])?\s*[,;]", body)
     assert names == [h for h in hdr if h not in ("int64_t", "uint8_t", "int32_t", "float", "uint32_t", "void")]
-    assert C.sizeof(pkg._Result) == 8 * 10 + 4 * 12 + 8 * 16 + 8 + 8
+    assert C.sizeof(pkg._Result) == 8 * 10 + 4 * 12 + 8 * 20 + 8 + 8
 
 
 @pytest.mark.parametrize("args", [

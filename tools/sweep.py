@@ -11,7 +11,7 @@ Each line: JSON with the dataset, eps, minPts, device ms (CUDA events on the
 launching stream, L2 flushed before each call, median of --reps), points/s,
 per-stage ms and counters. Inputs are the BASELINE configs' generators.
 
-usage: python tools/sweep.py [--n 10000000] [--reps 3] [--only eps|minpts|varden|qt]
+usage: python tools/sweep.py [--n 10000000] [--reps 3] [--only eps|minpts|varden|qt|approx]
 """
 import argparse
 import json
@@ -26,14 +26,14 @@ import datagen  # noqa: E402
 import paper_1912_06255_b200 as pkg  # noqa: E402
 
 
-def timed(t, eps, mp, reps, flush, flags=0):
+def timed(t, eps, mp, reps, flush, flags=0, rho=None):
     ms, last = [], None
     st = torch.cuda.current_stream()
     for _ in range(reps + 1):
         flush.fill_(1)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        r = pkg.dbscan(t, eps, mp, flags=flags, timing=True)
+        r = pkg.dbscan(t, eps, mp, flags=flags, timing=True, rho=rho)
         e1.record(st)
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
@@ -66,6 +66,13 @@ def main():
         for mp in (100, 1000, 10_000, 30_000):
             sets.append(("ss-simden-3d", ss3, 1000, mp))
             sets.append(("ss-simden-3d+qt", ss3, 1000, mp))
+    if a.only in ("", "approx"):
+        # row f4: rho-approximate DBSCAN on the same configs (rho = 0: exact)
+        for cfgname in ("c3", "c4_7d"):
+            cfg = datagen.CONFIGS[cfgname]
+            pts = cfg.points()
+            for rho in (0.0, 0.01, 0.1, 0.5, 1.0):
+                sets.append((f"{cfgname}~rho={rho}", pts, cfg.eps, cfg.min_pts))
     if a.only in ("", "varden"):
         for d, L, eps in ((2, 1e6, 1000), (3, 1e6, 1000), (5, 1e5, 2000), (7, 1e5, 2000)):
             vd = datagen.seed_spreader(a.n, d, L, 20 + d, 1000 / a.n, varden=True)
@@ -73,7 +80,8 @@ def main():
     for name, pts, eps, mp in sets:
         t = torch.from_numpy(pts).cuda()
         flags = pkg.F_QUADTREE if name.endswith("+qt") else 0
-        ms, r = timed(t, eps, mp, a.reps, flush, flags)
+        rho = float(name.split("rho=")[1]) if "~rho=" in name else 0.0
+        ms, r = timed(t, eps, mp, a.reps, flush, flags, rho or None)
         print(json.dumps({"data": name, "n": len(pts), "d": pts.shape[1], "eps": eps, "min_pts": mp,
                           "ms": round(ms, 4), "pts_per_s": len(pts) / (ms / 1e3),
                           "stage_ms": {k: round(v, 4) for k, v in r.stage_ms.items()},
