@@ -41,6 +41,7 @@ import datagen  # noqa: E402
 METRIC = "points/sec end-to-end exact grid DBSCAN (10M pts, d=2–7); per-stage HBM GB/s"
 SUITE = ["c2", "c3", "c4_5d", "c4_7d", "c5_10", "c5_10k"]
 REF_FRACTION = 0.05
+E2E_THREADS = 2
 
 
 # int32 issue peak: 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz = 37.2 T
@@ -317,21 +318,45 @@ def main():
                     torch.empty(cfg.n + 1, dtype=torch.int64).pin_memory(),
                     torch.empty(cfg.n, dtype=torch.int32).pin_memory())
             host.append((cfg, hp, outs))
+        # Two host threads, each with its own CUDA stream, take the runs in
+        # turn through the blocking host-buffer C-ABI call (the library keeps
+        # no global state): one call's H2D overlaps another's kernels and D2H.
+        streams = [torch.cuda.Stream(dev) for _ in range(E2E_THREADS)]
+
         def e2e_step():
             nonlocal h2d, d2h
+            b_in = [0] * E2E_THREADS
+            b_out = [0] * E2E_THREADS
+            errs = []
+
+            def worker(w):
+                try:
+                    torch.cuda.set_device(dev)
+                    for k in range(w, len(host), E2E_THREADS):
+                        cfg, hp, outs = host[k]
+                        r = pkg.dbscan(hp, cfg.eps, cfg.min_pts, out=outs, stream=streams[w])
+                        b_in[w] += hp.numel() * 4
+                        b_out[w] += cfg.n * (1 + 4 + 8) + 8 + 4 * len(r.border_ids)
+                except Exception as e:  # pragma: no cover
+                    errs.append(e)
             t0 = time.perf_counter()
-            b_in = b_out = 0
-            for cfg, hp, outs in host:
-                r = pkg.dbscan(hp, cfg.eps, cfg.min_pts, out=outs, stream=stream)
-                b_in += hp.numel() * 4
-                b_out += cfg.n * (1 + 4 + 8) + 8 + 4 * len(r.border_ids)
-            h2d, d2h = b_in, b_out
-            return time.perf_counter() - t0
+            ths = [threading.Thread(target=worker, args=(w,)) for w in range(E2E_THREADS)]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            dt = time.perf_counter() - t0
+            if errs:
+                raise errs[0]
+            h2d, d2h = sum(b_in), sum(b_out)
+            return dt
         for _ in range(1):
             e2e_step()
         ts = [e2e_step() for _ in range(max(1, min(args.steps, 3)))]
         e2e = {"value": npts_step * len(ts) / sum(ts), "unit": "points/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "timer": "host wall clock around blocking C-ABI calls"}
+               "d2h_bytes_per_step": d2h,
+               "timer": f"host wall clock around the step: {E2E_THREADS} host threads with one CUDA stream each "
+                        "call the blocking host-buffer C ABI on the runs in turn (pinned inputs and outputs)"}
 
     # ---- CPU baseline: the oracle as it stands, bounded sample (rank 0, N=1)
     cpu = None

@@ -76,13 +76,14 @@ __global__ void __launch_bounds__(256) pair_kernel(int fill, int nwaves, CellsVi
 // distance from p to the integer box [lo, hi] within eps?
 template <int D>
 __device__ __forceinline__ bool near_range(const int32_t* p, const int32_t* lo, const int32_t* hi,
-                                           int d, uint32_t clampc, uint64_t eps2) {
+                                           int d, uint32_t clampc, uint64_t eps2, uint32_t slack = 0) {
   uint64_t acc = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (k < d) {
       int64_t x = p[k];
       int64_t t = x < lo[k] ? (int64_t)lo[k] - x : (x > hi[k] ? x - (int64_t)hi[k] : 0);
+      t = t > (int64_t)slack ? t - (int64_t)slack : 0;
       uint64_t u = (uint64_t)t;
       if (u > clampc) u = clampc;
       acc += u * u;
@@ -112,9 +113,11 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
     bool keep = false;
     if (u < ea) {
       PtLoad<D>::load(Ps, u, a);
-      keep = g.at || near_box<D>(a, boxh, g);  // (filters are for the exact test only)
+      keep = near_box<D>(a, boxh, g, g.at ? 2 * (g.at - 1) : 0);  // (both sub-cell boxes)
     }
     if (!__any_sync(DB_FULL, keep)) continue;
+    int32_t qa[D];
+    connect_prep<D>(a, g, qa);
     // bounding box of the kept block
     int32_t lo[D], hi[D];
 #pragma unroll
@@ -133,7 +136,9 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
       bool kb = false;
       if (v < eb) {
         PtLoad<D>::load(Ps, v, b);
-        kb = g.at || near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2);
+        // (approximate: both sub-cell boxes reach up to t-1 past their points)
+        kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2, g.at ? 2 * (g.at - 1) : 0);
+        connect_prep<D>(b, g, b);
       }
       uint32_t mb = __ballot_sync(DB_FULL, kb);
       bool mine = false;
@@ -143,7 +148,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
         int32_t q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
-        mine |= keep && connect_test<D, WIDE>(a, q, g);
+        mine |= keep && connect_q<D, WIDE>(qa, q, g);
       }
       if (__any_sync(DB_FULL, mine)) return true;
     }
@@ -301,9 +306,11 @@ __global__ void __launch_bounds__(256) wave_kernel(const uint2* __restrict__ pai
       int32_t a[D], q[D];
       for (uint32_t u = sa; u < ea && !hit; ++u) {
         PtLoad<D>::load(Ps, u, a);
+        connect_prep<D>(a, g, a);
         for (uint32_t v = sb; v < eb; ++v) {
           PtLoad<D>::load(Ps, v, q);
-          if (connect_test<D, WIDE>(a, q, g)) { hit = true; break; }
+          connect_prep<D>(q, g, q);
+          if (connect_q<D, WIDE>(a, q, g)) { hit = true; break; }
         }
       }
       if (hit) uf_link(parent, p.x, p.y);

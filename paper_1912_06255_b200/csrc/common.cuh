@@ -135,16 +135,24 @@ __device__ __forceinline__ bool within(const int32_t* a, const int32_t* b, uint3
 // (the box gap is at most the point distance); a passing pair is within
 // eps + 2 (t-1) sqrt(d) <= eps (1 + rho) because the host picks the largest
 // t with 2 (t-1) sqrt(d) <= eps rho.
+// The sub-cell snap is done once per point (connect_prep: identity for the
+// exact test, sub-cell indices for the approximate one) and the test runs on
+// the prepared values (connect_q); connect_test = both.
+template <int D>
+__device__ __forceinline__ void connect_prep(const int32_t* x, const Geo& g, int32_t* q) {
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    q[k] = (g.at && k < g.d) ? (int32_t)(((uint32_t)x[k] - (uint32_t)g.lo[k]) / g.at) : x[k];
+}
+
 template <int D, bool WIDE>
-__device__ __forceinline__ bool connect_test(const int32_t* a, const int32_t* b, const Geo& g) {
-  if (g.at == 0) return within<D, WIDE>(a, b, g.clampc, g.eps2);
+__device__ __forceinline__ bool connect_q(const int32_t* qa, const int32_t* qb, const Geo& g) {
+  if (g.at == 0) return within<D, WIDE>(qa, qb, g.clampc, g.eps2);
   uint64_t acc = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (k < g.d) {
-      const uint32_t qa = ((uint32_t)a[k] - (uint32_t)g.lo[k]) / g.at;
-      const uint32_t qb = ((uint32_t)b[k] - (uint32_t)g.lo[k]) / g.at;
-      const uint32_t dq = qa > qb ? qa - qb : qb - qa;
+      const uint32_t dq = __sad(qa[k], qb[k], 0u);
       uint64_t gap = dq ? (uint64_t)(dq - 1) * g.at + 1 : 0;
       if (gap > g.clampc) gap = g.clampc;
       acc += gap * gap;
@@ -153,17 +161,29 @@ __device__ __forceinline__ bool connect_test(const int32_t* a, const int32_t* b,
   return acc <= g.eps2;
 }
 
+template <int D, bool WIDE>
+__device__ __forceinline__ bool connect_test(const int32_t* a, const int32_t* b, const Geo& g) {
+  int32_t qa[D], qb[D];
+  connect_prep<D>(a, g, qa);
+  connect_prep<D>(b, g, qb);
+  return connect_q<D, WIDE>(qa, qb, g);
+}
+
 // Squared distance from point p to the integer box of cell `key`, clamped as
 // above: [lo_k + c_k s, lo_k + c_k s + s - 1] per axis. Used by the BCP filter
 // ("filter out points further than eps from the other cell").
+// slack (rho-approximate DBSCAN): each per-axis gap is first reduced by
+// slack = 2(t-1), the most the two sub-cell boxes of connect_test reach past
+// their points; the filter then keeps every point that can pass the test.
 template <int D>
-__device__ __forceinline__ bool near_box(const int32_t* p, const int64_t* blo, const Geo& g) {
+__device__ __forceinline__ bool near_box(const int32_t* p, const int64_t* blo, const Geo& g, uint32_t slack = 0) {
   uint64_t acc = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (k < g.d) {
       int64_t x = p[k], lo = blo[k], hi = blo[k] + (int64_t)g.s - 1;
       int64_t t = x < lo ? lo - x : (x > hi ? x - hi : 0);
+      t = t > (int64_t)slack ? t - (int64_t)slack : 0;
       uint64_t u = (uint64_t)t;
       if (u > g.clampc) u = g.clampc;
       acc += u * u;

@@ -324,7 +324,10 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
           for (uint32_t v = sh; v < sh + kh; ++v) {
             int32_t q[D];
             load_pt<D>(a.Ps, v, q);
-            if (connect_test<D, WIDE>(p, q, a.g)) { hit = true; break; }
+            if (a.g.at ? connect_test<D, WIDE>(p, q, a.g) : within_dim<DIM, D, WIDE>(p, q, a.g)) {
+              hit = true;
+              break;
+            }
           }
         }
         if (hit) uf_link(a.parent, g, h);

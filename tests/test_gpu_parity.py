@@ -310,3 +310,34 @@ def test_quadtree_vs_o2(oracle_lib, d, flags):
         assert_same(r, oracle_lib.o2(pts, eps, mp), f"qt d={d} eps={eps} mp={mp} flags={flags}")
     r = gpu(pts, 400, 1500, flags)
     assert r.stats["qt_nodes"] > 0
+
+
+def test_concurrent_host_calls(oracle_lib):
+    """Two host threads, one stream each, calling the blocking host-buffer
+    path at once (bench.py's e2e mode): no shared state, same results."""
+    import threading
+    cases = [(datagen.seed_spreader(40_000, 3, 20_000, 81, 0.02, noise_frac=0.03), 200, 15),
+             (datagen.uniform(80_000, 3, 6_000, 82), 300, 10),
+             (datagen.seed_spreader(30_000, 5, 30_000, 83, 0.02), 600, 20),
+             (datagen.uniform(50_000, 2, 20_000, 84), 150, 6)]
+    want = [oracle_lib.o2(p, e, m) for p, e, m in cases]
+    got = [None] * len(cases)
+    errs = []
+
+    def worker(w):
+        try:
+            st = torch.cuda.Stream()
+            for k in range(w, len(cases), 2):
+                for _ in range(3):
+                    p, e, m = cases[k]
+                    got[k] = np_result(pkg.dbscan(torch.from_numpy(p).pin_memory(), e, m, stream=st))
+        except Exception as ex:  # pragma: no cover
+            errs.append(ex)
+    ths = [threading.Thread(target=worker, args=(w,)) for w in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for k in range(len(cases)):
+        assert_same(got[k], want[k], f"case {k}")
