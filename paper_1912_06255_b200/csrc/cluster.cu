@@ -99,7 +99,7 @@ __device__ __forceinline__ bool near_range(const int32_t* p, const int32_t* lo, 
 // broadcast by shuffle and tested against every lane's point; the first pair
 // within eps ends the search. Between g blocks, a Find check
 // stops early when another warp has connected the pair meanwhile.
-template <int D, bool WIDE>
+template <int D, bool WIDE, bool APX>
 __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32_t* __restrict__ Ps,
                          const uint32_t* __restrict__ core_cnt, uint32_t* parent) {
   const int lane = threadIdx.x & 31;
@@ -113,11 +113,11 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
     bool keep = false;
     if (u < ea) {
       PtLoad<D>::load(Ps, u, a);
-      keep = near_box<D>(a, boxh, g, g.at ? 2 * (g.at - 1) : 0);  // (both sub-cell boxes)
+      keep = near_box<D>(a, boxh, g, APX ? 2 * (g.at - 1) : 0);  // (approximate: both sub-cell boxes)
     }
     if (!__any_sync(DB_FULL, keep)) continue;
     int32_t qa[D];
-    connect_prep<D>(a, g, qa);
+    if (APX) connect_prep<D>(a, g, qa);
     // bounding box of the kept block
     int32_t lo[D], hi[D];
 #pragma unroll
@@ -137,8 +137,8 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
       if (v < eb) {
         PtLoad<D>::load(Ps, v, b);
         // (approximate: both sub-cell boxes reach up to t-1 past their points)
-        kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2, g.at ? 2 * (g.at - 1) : 0);
-        connect_prep<D>(b, g, b);
+        kb = near_range<D>(b, lo, hi, g.d, g.clampc, g.eps2, APX ? 2 * (g.at - 1) : 0);
+        if (APX) connect_prep<D>(b, g, b);
       }
       uint32_t mb = __ballot_sync(DB_FULL, kb);
       bool mine = false;
@@ -148,7 +148,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
         int32_t q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
-        mine |= keep && connect_q<D, WIDE>(qa, q, g);
+        mine |= keep && (APX ? connect_q<D, WIDE>(qa, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2));
       }
       if (__any_sync(DB_FULL, mine)) return true;
     }
@@ -236,7 +236,9 @@ __device__ bool warp_bcp_tree(uint32_t ga, uint32_t hb, const CellsView& cv, con
 }
 
 // Warp per pair over list[0 .. min(*count, cap)) (the sparse path's queue).
-template <int D, bool WIDE>
+// MODE 0: exact; 1: exact with range-count trees (row f2); 2: approximate
+// connectivity (row f4). Separate instantiations keep the exact kernel lean.
+template <int D, bool WIDE, int MODE>
 __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict__ list,
                                                         const uint32_t* __restrict__ count,
                                                         CellsView cv, Geo g,
@@ -253,13 +255,16 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
     if (__shfl_sync(DB_FULL, done, 0)) continue;
     // a tree on an all-core side (f2): search it; else the block BCP
     bool hit;
-    const bool ty = !g.at && qt.nodes && qt.node_off[p.y + 1] > qt.node_off[p.y] &&
-                    core_cnt[p.y] == cv.cell_start[p.y + 1] - cv.cell_start[p.y];
-    const bool tx = !g.at && qt.nodes && qt.node_off[p.x + 1] > qt.node_off[p.x] &&
-                    core_cnt[p.x] == cv.cell_start[p.x + 1] - cv.cell_start[p.x];
-    if (ty) hit = warp_bcp_tree<D, WIDE>(p.x, p.y, cv, g, Ps, core_cnt, qt);
-    else if (tx) hit = warp_bcp_tree<D, WIDE>(p.y, p.x, cv, g, Ps, core_cnt, qt);
-    else hit = warp_bcp<D, WIDE>(p, cv, g, Ps, core_cnt, parent);
+    bool ty = false, tx = false;
+    if (MODE == 1) {
+      ty = qt.node_off[p.y + 1] > qt.node_off[p.y] &&
+           core_cnt[p.y] == cv.cell_start[p.y + 1] - cv.cell_start[p.y];
+      tx = qt.node_off[p.x + 1] > qt.node_off[p.x] &&
+           core_cnt[p.x] == cv.cell_start[p.x + 1] - cv.cell_start[p.x];
+    }
+    if (MODE == 1 && ty) hit = warp_bcp_tree<D, WIDE>(p.x, p.y, cv, g, Ps, core_cnt, qt);
+    else if (MODE == 1 && tx) hit = warp_bcp_tree<D, WIDE>(p.y, p.x, cv, g, Ps, core_cnt, qt);
+    else hit = warp_bcp<D, WIDE, MODE == 2>(p, cv, g, Ps, core_cnt, parent);
     if (hit && lane == 0) uf_link(parent, p.x, p.y);
     __syncwarp();
   }
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
 // the small ones (|A| |B| <= SMALL_PAIR core points) each in its lane (Link on
 // success) and queue the large ones for bcp_large_kernel (a warp per pair),
 // with one atomic per warp.
-template <int D, bool WIDE>
+template <int D, bool WIDE, bool APX>
 __global__ void __launch_bounds__(256) wave_kernel(const uint2* __restrict__ pairs,
                                                    const uint64_t* __restrict__ bounds, CellsView cv, Geo g,
                                                    const int32_t* __restrict__ Ps,
@@ -306,11 +311,11 @@ __global__ void __launch_bounds__(256) wave_kernel(const uint2* __restrict__ pai
       int32_t a[D], q[D];
       for (uint32_t u = sa; u < ea && !hit; ++u) {
         PtLoad<D>::load(Ps, u, a);
-        connect_prep<D>(a, g, a);
+        if (APX) connect_prep<D>(a, g, a);
         for (uint32_t v = sb; v < eb; ++v) {
           PtLoad<D>::load(Ps, v, q);
-          connect_prep<D>(q, g, q);
-          if (connect_q<D, WIDE>(a, q, g)) { hit = true; break; }
+          if (APX) connect_prep<D>(q, g, q);
+          if (APX ? connect_q<D, WIDE>(a, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
         }
       }
       if (hit) uf_link(parent, p.x, p.y);
@@ -333,9 +338,14 @@ void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, con
                uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide,
                const QTrees* qt) {
   const QTrees none;
+  const QTrees& q = qt ? *qt : none;
   dispatch(g.D, wide, [&]<int D, bool W>() {
-    bcp_large_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap,
-                                                          qt ? *qt : none);
+    if (g.at)
+      bcp_large_kernel<D, W, 2><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap, q);
+    else if (q.nodes)
+      bcp_large_kernel<D, W, 1><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap, q);
+    else
+      bcp_large_kernel<D, W, 0><<<c.sms * 8, 256, 0, c.st>>>(list, count, cv, g, Ps, core_cnt, parent, cap, q);
   });
   c.launched();
 }
@@ -372,8 +382,12 @@ void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, 
   const unsigned wgrid = grid_for((int64_t)(nbr_total / 2 + 32), 256, c.sms * 8);
   for (int w = 0; w < nw; ++w) {
     dispatch(g.D, wide, [&]<int D, bool W>() {
-      wave_kernel<D, W><<<wgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, cv, g, Ps, core_cnt, parent, large,
-                                                 nlarge + w, tested);
+      if (g.at)
+        wave_kernel<D, W, true><<<wgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, cv, g, Ps, core_cnt, parent, large,
+                                                         nlarge + w, tested);
+      else
+        wave_kernel<D, W, false><<<wgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, cv, g, Ps, core_cnt, parent,
+                                                          large, nlarge + w, tested);
     });
     c.launched();
     bcp_large(c, g, cv, Ps, core_cnt, parent, large, nlarge + w, (uint32_t)nbr_total, wide, qt);

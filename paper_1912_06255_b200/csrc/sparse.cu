@@ -77,8 +77,9 @@ struct SpArgs {
   uint2* large;
   uint32_t large_cap;
   uint32_t* bcnt;            // [n] input order
-  uint32_t* tmp_lab;         // [n*SP_MAXL] sorted order
-  uint8_t* tmp_n;            // [n] sorted order; 0xff = overflow
+  uint32_t* tmp_lab;         // [n*SP_MAXL] input order
+  uint8_t* tmp_n;            // [n] input order; 0xff = overflow
+  uint32_t* ovf_pos;         // [n] input order: sorted position of an overflowed point
   unsigned long long* nborder;
   int64_t n;
 };
@@ -275,7 +276,9 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 //    P:L642-644) and Links on success;
 //  * larger pairs are skipped if Find(g) == Find(h) and queued
 //    for the warp BCP kernel (cluster.cu), which re-checks Find first.
-template <int DIM, int D, bool WIDE, bool BY_CELLS>
+// APX: the rho-approximate connectivity test (row f4), a separate
+// instantiation so that the exact kernel keeps its register budget.
+template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
 __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
           for (uint32_t v = sh; v < sh + kh; ++v) {
             int32_t q[D];
             load_pt<D>(a.Ps, v, q);
-            if (a.g.at ? connect_test<D, WIDE>(p, q, a.g) : within_dim<DIM, D, WIDE>(p, q, a.g)) {
+            if (APX ? connect_test<D, WIDE>(p, q, a.g) : within_dim<DIM, D, WIDE>(p, q, a.g)) {
               hit = true;
               break;
             }
@@ -411,45 +414,44 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
         hit = within_dim<DIM, D, WIDE>(p, q, a.g);
       }
       if (!hit) continue;
-      uint32_t* L = a.tmp_lab + (size_t)u * SP_MAXL;
+      const uint32_t i = a.idx[u];  // label sets live in input order (the CSR's)
+      uint32_t* L = a.tmp_lab + (size_t)i * SP_MAXL;
       bool placed = false;
 #pragma unroll
       for (int k = 0; k < SP_MAXL; ++k) {
         const uint32_t old = atomicCAS(L + k, MISS, lab);
         if (old == MISS || old == lab) { placed = true; break; }
       }
-      if (!placed) a.tmp_n[u] = 0xff;  // overflow: enumerate later
+      if (!placed) {  // overflow: enumerate later from the sorted position
+        a.ovf_pos[i] = u;
+        a.tmp_n[i] = 0xff;
+      }
     }
   }
 }
 
-// Thread per sorted non-core point: sort its label set (4-input network),
-// count it into bcnt (input order), or count an overflowed set by the
-// storage-free ascending enumeration.
+// Thread per point in INPUT order (coalesced): the number of labels in its
+// set (core points: none), or, for an overflowed set, the count of the
+// storage-free ascending enumeration from its sorted position.
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
   __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool bord = false;
-  if (j < a.n && !a.core_s[j]) {
-    uint32_t cnt;
-    if (a.tmp_n[j] != 0xff) {
-      uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
-      auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
-      cs(v.x, v.y); cs(v.z, v.w); cs(v.x, v.z); cs(v.y, v.w); cs(v.y, v.z);
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t cnt = 0;
+  if (i < a.n) {
+    if (a.tmp_n[i] != 0xff) {
+      const uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)i * SP_MAXL);
       cnt = (v.x != MISS) + (v.y != MISS) + (v.z != MISS) + (v.w != MISS);
-      if (cnt > 1) *reinterpret_cast<uint4*>(a.tmp_lab + (size_t)j * SP_MAXL) = v;
-      a.tmp_n[j] = (uint8_t)cnt;
     } else {
+      const uint32_t j = a.ovf_pos[i];
       const uint32_t g = a.cell_of[j];
       const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
       int32_t p[D];
       load_pt<D>(a.Ps, j, p);
       int64_t after = -1;
-      cnt = 0;
       while (true) {
         const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
         if (nx == MISS) break;
@@ -457,30 +459,34 @@ __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
         after = nx;
       }
     }
-    if (cnt) a.bcnt[a.idx[j]] = cnt;  // bcnt was cleared: only border points scatter
-    bord = cnt > 0;
+    a.bcnt[i] = cnt;
   }
-  const uint32_t nb = __syncthreads_count(bord);
+  const uint32_t nb = __syncthreads_count(cnt > 0);
   if (threadIdx.x == 0 && nb) atomicAdd(a.nborder, (unsigned long long)nb);
 }
 
-// Copy the staged label sets into the CSR (thread per sorted point).
+// Thread per point in input order: its row of the CSR, the set sorted by a
+// 4-input network (unused slots are ~0 and sort last), or the enumeration.
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_fill_kernel(SpArgs a, const int64_t* __restrict__ border_off,
                                                              int32_t* __restrict__ border_ids) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
   __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n || a.core_s[j]) return;
-  const uint8_t nl = a.tmp_n[j];
-  if (nl == 0) return;
-  const int64_t o = border_off[a.idx[j]];
-  if (nl != 0xff) {
-    for (int q = 0; q < nl; ++q) border_ids[o + q] = (int32_t)a.tmp_lab[(size_t)j * SP_MAXL + q];
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const int64_t o = border_off[i], e = border_off[i + 1];
+  if (o == e) return;
+  if (a.tmp_n[i] != 0xff) {
+    uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)i * SP_MAXL);
+    auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
+    cs(v.x, v.y); cs(v.z, v.w); cs(v.x, v.z); cs(v.y, v.w); cs(v.y, v.z);
+    const uint32_t L[4] = {v.x, v.y, v.z, v.w};
+    for (int64_t q = 0; q < e - o; ++q) border_ids[o + q] = (int32_t)L[q];
     return;
   }
+  const uint32_t j = a.ovf_pos[i];
   const uint32_t g = a.cell_of[j];
   const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
   int32_t p[D];
@@ -689,7 +695,8 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
-      sp_pairs_kernel<DIM, D, W, true><<<grid, 256, 0, c.st>>>(a, tested);
+      if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested);
+      else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested);
     });
     c.launched();
     bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
@@ -703,10 +710,10 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   a.bcnt = c.alloc<uint32_t>(n);
   a.tmp_lab = c.alloc<uint32_t>((size_t)n * SP_MAXL);
   a.tmp_n = c.alloc<uint8_t>(n);
+  a.ovf_pos = c.alloc<uint32_t>(n);  // written only for flagged points
   a.nborder = nborder;
-  // core-centric: label sets of SP_MAXL slots per sorted point, empty = ~0
+  // core-centric: label sets of SP_MAXL slots per point (input order), empty = ~0
   DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
-  c.zero(a.bcnt, sizeof(uint32_t) * (size_t)n);
   c.zero(a.tmp_n, (size_t)n);
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
