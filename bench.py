@@ -41,7 +41,7 @@ import datagen  # noqa: E402
 METRIC = "points/sec end-to-end exact grid DBSCAN (10M pts, d=2–7); per-stage HBM GB/s"
 SUITE = ["c2", "c3", "c4_5d", "c4_7d", "c5_10", "c5_10k"]
 REF_FRACTION = 0.05
-E2E_THREADS = 2
+E2E_THREADS = 3
 
 
 # int32 issue peak: 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz = 37.2 T
@@ -120,6 +120,20 @@ class ClockSampler:
         sm = [r[0] for r in self.rows]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_sm,
                 "reasons": reasons, "samples": len(self.rows), "source": "NVML, 10 ms"}
+
+
+def job_value(npts_per_rank_step: int, steps: int, local_ms: float, dist=None, device="cpu"):
+    """Whole-job throughput of N replicas ("replicas only"):
+    points of all ranks / the slowest rank's device time (max over ranks).
+    Returns (value, max_ms). dist: torch.distributed (initialised) or None."""
+    world = 1
+    if dist is not None:
+        import torch
+        world = dist.get_world_size()
+        t = torch.tensor([local_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        local_ms = float(t.item())
+    return npts_per_rank_step * steps * world / (local_ms / 1000.0), local_ms
 
 
 # ------------------------------------------------------------- reference
@@ -248,13 +262,8 @@ def main():
         dist.barrier()
     clocks = clk.stop()
     step_ms = [sum(per_run_ms[i][s] for i in range(len(runs))) for s in range(args.steps)]
-    total_ms = sum(step_ms)
-    if dist:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
     npts_step = sum(c.n for _, c, _, _ in data)
-    value = npts_step * args.steps * world / (total_ms / 1000.0)
+    value, total_ms = job_value(npts_step, args.steps, sum(step_ms), dist, dev)
 
     # ---- rooflines. Stage times come from CUDA events the
     # library records on the launching stream (F_TIMING); algorithmic work per
