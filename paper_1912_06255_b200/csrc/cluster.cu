@@ -35,44 +35,6 @@ __device__ __forceinline__ int wave_of(uint64_t kg, uint64_t kh, const Geo& g) {
   return l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);
 }
 
-// pass 0: count candidate pairs per (wave, cell); pass 1: fill, wave-major.
-// Warp per cell, lanes over its CSR row (rows hold up to ~10^3 cells in 7D),
-// ballots place each wave's pairs.
-__global__ void __launch_bounds__(256) pair_kernel(int fill, int nwaves, CellsView cv, Geo g,
-                                                   const uint32_t* __restrict__ core_cnt,
-                                                   uint32_t* __restrict__ cnt,
-                                                   const uint64_t* __restrict__ off,
-                                                   uint2* __restrict__ pairs) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t gc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gc < cv.ncells; gc += nwarps) {
-    uint32_t local[NWAVES] = {0, 0, 0};
-    if (core_cnt[gc] > 0) {
-      const uint64_t kg = cv.cell_key[gc];
-      const uint64_t r0 = cv.nbr_off[gc], r1 = cv.nbr_off[gc + 1];
-      for (uint64_t t0 = r0; t0 < r1; t0 += 32) {
-        const uint64_t t = t0 + lane;
-        int w = -1;
-        uint32_t h = 0;
-        if (t < r1) {
-          h = cv.nbr[t];
-          if (h < gc && core_cnt[h] > 0) w = nwaves == 1 ? 0 : wave_of(kg, cv.cell_key[h], g);
-        }
-#pragma unroll
-        for (int ww = 0; ww < NWAVES; ++ww) {
-          if (ww >= nwaves) break;
-          const uint32_t b = __ballot_sync(DB_FULL, w == ww);
-          if (fill && w == ww) pairs[off[(size_t)ww * cv.ncells + gc] + local[ww] + __popc(b & lt)] = make_uint2(gc, h);
-          local[ww] += __popc(b);
-        }
-      }
-    }
-    if (!fill && lane == 0)
-      for (int w = 0; w < nwaves; ++w) cnt[(size_t)w * cv.ncells + gc] = local[w];
-  }
-}
-
 // distance from p to the integer box [lo, hi] within eps?
 template <int D>
 __device__ __forceinline__ bool near_range(const int32_t* p, const int32_t* lo, const int32_t* hi,
@@ -270,58 +232,71 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
   }
 }
 
-// One wave of ClusterCore (Alg 3), first half: the lanes of a warp take 32
-// pairs of the wave, drop those already connected (Find), test
-// the small ones (|A| |B| <= SMALL_PAIR core points) each in its lane (Link on
-// success) and queue the large ones for bcp_large_kernel (a warp per pair),
-// with one atomic per warp.
+// One wave of ClusterCore straight from the neighbour CSR (no pair list):
+// a warp per core cell g, lanes over its row; an entry h is a candidate of
+// wave w if h < g ("g > h"), h holds core points and the pair's
+// lattice L1 distance falls in the wave. Find filter, small BCPs in the lane
+// and the queue of large ones as in wave_kernel. Counts candidate pairs in
+// *npairs (every wave once).
 template <int D, bool WIDE, bool APX>
-__global__ void __launch_bounds__(256) wave_kernel(const uint2* __restrict__ pairs,
-                                                   const uint64_t* __restrict__ bounds, CellsView cv, Geo g,
-                                                   const int32_t* __restrict__ Ps,
-                                                   const uint32_t* __restrict__ core_cnt, uint32_t* parent,
-                                                   uint2* __restrict__ large, uint32_t* __restrict__ nlarge,
-                                                   unsigned long long* tested) {
+__global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, CellsView cv, Geo g,
+                                                       const int32_t* __restrict__ Ps,
+                                                       const uint32_t* __restrict__ core_cnt, uint32_t* parent,
+                                                       uint2* __restrict__ large, uint32_t* __restrict__ nlarge,
+                                                       unsigned long long* tested, unsigned long long* npairs) {
   const int lane = threadIdx.x & 31;
-  const uint64_t b0 = bounds[0], b1 = bounds[1];
-  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-  uint32_t mine = 0;
-  for (uint64_t c0 = b0 + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; c0 < b1;
-       c0 += nwarps * 32) {
-    const uint64_t i = c0 + lane;
-    uint2 p = make_uint2(0, 0);
-    bool need = false, small = false;
-    if (i < b1) {
-      p = pairs[i];
-      need = uf_find(parent, p.x) != uf_find(parent, p.y);
-      small = need && (uint64_t)core_cnt[p.x] * core_cnt[p.y] <= SMALL_PAIR;
-    }
-    mine += need;
-    const uint32_t lm = __ballot_sync(DB_FULL, need && !small);
-    if (lm) {
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(nlarge, (uint32_t)__popc(lm));
-      base = __shfl_sync(DB_FULL, base, 0);
-      if (need && !small) large[base + __popc(lm & lanemask_lt())] = p;
-    }
-    if (small) {
-      const uint32_t sa = cv.cell_start[p.x], ea = sa + core_cnt[p.x];
-      const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
-      bool hit = false;
-      int32_t a[D], q[D];
-      for (uint32_t u = sa; u < ea && !hit; ++u) {
-        PtLoad<D>::load(Ps, u, a);
-        if (APX) connect_prep<D>(a, g, a);
-        for (uint32_t v = sb; v < eb; ++v) {
-          PtLoad<D>::load(Ps, v, q);
-          if (APX) connect_prep<D>(q, g, q);
-          if (APX ? connect_q<D, WIDE>(a, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t mine = 0, cand = 0;
+  for (uint32_t gc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gc < cv.ncells; gc += nwarps) {
+    const uint32_t kg = core_cnt[gc];
+    if (kg == 0) continue;
+    const uint64_t key_g = cv.cell_key[gc];
+    const uint64_t r0 = cv.nbr_off[gc], r1 = cv.nbr_off[gc + 1];
+    for (uint64_t t0 = r0; t0 < r1; t0 += 32) {
+      const uint64_t t = t0 + lane;
+      uint2 p = make_uint2(gc, 0);
+      bool is = false, need = false, small = false;
+      if (t < r1) {
+        const uint32_t h = cv.nbr[t];
+        p.y = h;
+        if (h < gc) {
+          const uint32_t kh = core_cnt[h];
+          is = kh > 0 && (nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
+          if (is) {
+            need = uf_find(parent, gc) != uf_find(parent, h);
+            small = need && (uint64_t)kg * kh <= SMALL_PAIR;
+          }
         }
       }
-      if (hit) uf_link(parent, p.x, p.y);
+      cand += is;
+      mine += need;
+      const uint32_t lm = __ballot_sync(DB_FULL, need && !small);
+      if (lm) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(nlarge, (uint32_t)__popc(lm));
+        base = __shfl_sync(DB_FULL, base, 0);
+        if (need && !small) large[base + __popc(lm & lanemask_lt())] = p;
+      }
+      if (small) {
+        const uint32_t sa = cv.cell_start[p.x], ea = sa + kg;
+        const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
+        bool hit = false;
+        int32_t a[D], q[D];
+        for (uint32_t u = sa; u < ea && !hit; ++u) {
+          PtLoad<D>::load(Ps, u, a);
+          if (APX) connect_prep<D>(a, g, a);
+          for (uint32_t v = sb; v < eb; ++v) {
+            PtLoad<D>::load(Ps, v, q);
+            if (APX) connect_prep<D>(q, g, q);
+            if (APX ? connect_q<D, WIDE>(a, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
+          }
+        }
+        if (hit) uf_link(parent, p.x, p.y);
+      }
     }
   }
   block_add_u64(mine, tested);
+  block_add_u64(cand, npairs);
 }
 
 __global__ void uf_init_kernel(uint32_t* parent, uint32_t n) {
@@ -357,37 +332,19 @@ void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, 
   const int nw = waves ? NWAVES : 1;
   uf_init(c, parent, nc);
   if (nbr_total == 0) return;
-  uint32_t* cnt = c.alloc<uint32_t>((size_t)nw * nc);
-  uint64_t* off = c.alloc<uint64_t>((size_t)nw * nc + 1);
-  const unsigned pgrid = grid_for((int64_t)nc * 32, 256, c.sms * 16);
-  pair_kernel<<<pgrid, 256, 0, c.st>>>(0, nw, cv, g, core_cnt, cnt, nullptr, nullptr);
-  c.launched();
-  exclusive_scan_u32_u64(c, cnt, off, (int64_t)nw * nc);
-  // at most one pair per CSR entry: no host read of the pair count is needed
-  uint2* pairs = c.alloc<uint2>(nbr_total);
-  pair_kernel<<<pgrid, 256, 0, c.st>>>(1, nw, cv, g, core_cnt, nullptr, off, pairs);
-  c.launched();
-  // wave w: pairs[off[w*nc] .. off[(w+1)*nc]), bounds kept on the device
-  uint64_t* bounds = c.alloc<uint64_t>(2 * NWAVES);
-  for (int w = 0; w < nw; ++w) {
-    DB_CUDA(cudaMemcpyAsync(bounds + 2 * w, off + (size_t)w * nc, sizeof(uint64_t),
-                            cudaMemcpyDeviceToDevice, c.st));
-    DB_CUDA(cudaMemcpyAsync(bounds + 2 * w + 1, off + (size_t)(w + 1) * nc, sizeof(uint64_t),
-                            cudaMemcpyDeviceToDevice, c.st));
-  }
-  DB_CUDA(cudaMemcpyAsync(npairs_out, off + (size_t)nw * nc, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c.st));
+  // large pairs of a wave: at most one per CSR entry
   uint2* large = c.alloc<uint2>(nbr_total);
   uint32_t* nlarge = c.alloc<uint32_t>(NWAVES);
   c.zero(nlarge, sizeof(uint32_t) * NWAVES);
-  const unsigned wgrid = grid_for((int64_t)(nbr_total / 2 + 32), 256, c.sms * 8);
+  const unsigned wgrid = grid_for((int64_t)nc * 32, 256, c.sms * 16);
   for (int w = 0; w < nw; ++w) {
     dispatch(g.D, wide, [&]<int D, bool W>() {
       if (g.at)
-        wave_kernel<D, W, true><<<wgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, cv, g, Ps, core_cnt, parent, large,
-                                                         nlarge + w, tested);
+        wave_csr_kernel<D, W, true><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large, nlarge + w,
+                                                             tested, npairs_out);
       else
-        wave_kernel<D, W, false><<<wgrid, 256, 0, c.st>>>(pairs, bounds + 2 * w, cv, g, Ps, core_cnt, parent,
-                                                          large, nlarge + w, tested);
+        wave_csr_kernel<D, W, false><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+                                                              nlarge + w, tested, npairs_out);
     });
     c.launched();
     bcp_large(c, g, cv, Ps, core_cnt, parent, large, nlarge + w, (uint32_t)nbr_total, wide, qt);

@@ -311,6 +311,7 @@ __device__ __forceinline__ void block_add_u64(unsigned long long v, unsigned lon
   __shared__ unsigned long long s_part[32];
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(DB_FULL, v, o);
+  __syncthreads();  // s_part is free (a previous call may still be reading it)
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -461,8 +461,8 @@ __global__ void __launch_bounds__(LAT_THREADS) lat_cells_kernel(const uint32_t* 
 //      writes them out coalesced. cell_of is filled cell by cell from
 //      cell_start (the bucket's cells are one contiguous id range).
 constexpr int BK_T = 8192;           // positions per bucket (3b: 8192 x 24 B in shared memory)
-constexpr int BK_THREADS = 1024;
-constexpr int BK_ITEMS = 8;          // 3a: 8192 points per block (runs of ~7 records per bucket)
+constexpr int BK_THREADS = 512;
+constexpr int BK_ITEMS = 8;          // 3a: 4096 points per block
 constexpr int BK_MAXB = 4096;        // buckets held by a 3a block's shared histogram
 
 template <int DD>
