@@ -338,7 +338,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     // ---- a7: core-first compaction
     tm.stage(DBSCAN_STAGE_COMPACT);
     compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
-    core_cells = c.read(cnt32);
+    // no host read here: with no core cell the later stages produce the
+    // all-noise result by themselves (the count is read with the final stats)
+    core_cells = UINT32_MAX;
   }
 
   cudaStream_t side = c.side;
@@ -428,7 +430,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_KEY_BITS] = bits;
   out->stats[DBSCAN_STAT_SORT_PASSES] = passes;
   out->stats[DBSCAN_STAT_NBR_ENTRIES] = (int64_t)nbr_total;
-  out->stats[DBSCAN_STAT_CORE_CELLS] = core_cells;
+  out->stats[DBSCAN_STAT_CORE_CELLS] = core_cells == UINT32_MAX ? h32[0] : core_cells;
   out->stats[DBSCAN_STAT_PAIRS] = (int64_t)h64[2];
   out->stats[DBSCAN_STAT_PAIRS_TESTED] = (int64_t)h64[0];
   out->stats[DBSCAN_STAT_LAUNCHES] = c.launches;

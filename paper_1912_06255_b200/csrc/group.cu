@@ -61,49 +61,70 @@ __global__ void group_init_kernel(GSlot* T, uint64_t cap) {
   if (h < cap) reinterpret_cast<uint4*>(T)[h] = make_uint4(0xffffffffu, 0xffffffffu, 0u, 0u);
 }
 
-// A: count points per key. Every thread runs the same number of iterations so
-// the warp-wide match is always full.
+// find-or-insert a key; returns the slot, or ~0 when the probe runs too long
+// (too many cells for the table: *overflow is set)
+__device__ __forceinline__ uint64_t gslot_insert(GSlot* T, uint64_t mask, uint64_t key, uint32_t* overflow) {
+  uint64_t h = gslot(key, mask);
+  for (int probe = 0; probe < MAX_PROBE; ++probe) {
+    const unsigned long long prev = atomicCAS(&T[h].key, (unsigned long long)EMPTY_KEY, (unsigned long long)key);
+    if (prev == EMPTY_KEY || prev == key) return h;
+    h = (h + 1) & mask;
+  }
+  atomicExch(overflow, 1u);
+  return ~0ull;
+}
+
+// A: count points per key. A warp walks a contiguous chunk of the input, 32
+// points per step (coalesced). Clustered data keeps one key for long runs:
+// while the whole warp holds the key of the current run, lane 0 only adds to
+// a register; the count is flushed with one atomic when the key changes.
+// Steps with several keys go through __match_any_sync, one atomic per key.
+constexpr uint32_t GR_CHUNK = 256;  // points per warp chunk (several chunks per warp: balance)
+
 template <int DD>
 __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* __restrict__ pts, uint32_t n,
                                                                  Geo g, uint64_t magic, GSlot* T,
                                                                  uint64_t mask, uint32_t* overflow) {
   const int lane = threadIdx.x & 31;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  const uint32_t iters = (n + stride - 1) / stride;
-  for (uint32_t it = 0; it < iters; ++it) {
-    if ((it & 7) == 0) {
-      uint32_t ov = 0;
-      if (lane == 0) ov = *(volatile uint32_t*)overflow;
-      if (__shfl_sync(DB_FULL, ov, 0)) return;  // warp-uniform
-    }
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
-    const bool valid = i < n;
-    int32_t x[DD];
-    const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
-    // clustered data: usually one key for the whole warp (no match needed)
-    const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
-    const uint32_t vmask = __ballot_sync(DB_FULL, valid);
-    uint32_t peers;
-    if (__all_sync(DB_FULL, !valid || key == k0)) {
-      if (lane != 0 || !valid) continue;
-      peers = vmask;
-    } else {
-      peers = __match_any_sync(DB_FULL, key);
-      if (!valid || (peers & lanemask_lt()) != 0) continue;  // one leader per distinct key
-    }
-    uint64_t h = gslot(key, mask);
-    int probe = 0;
-    while (true) {
-      const unsigned long long prev = atomicCAS(&T[h].key, (unsigned long long)EMPTY_KEY,
-                                                (unsigned long long)key);
-      if (prev == EMPTY_KEY || prev == key) {
-        atomicAdd(&T[h].cnt, (uint32_t)__popc(peers));
-        break;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nchunks = (n + GR_CHUNK - 1) / GR_CHUNK;
+  uint64_t run_key = ~0ull, run_slot = ~0ull;  // lane 0's current run
+  uint32_t run_cnt = 0;
+  auto flush = [&]() {
+    if (run_cnt && run_slot != ~0ull) atomicAdd(&T[run_slot].cnt, run_cnt);
+    run_cnt = 0;
+  };
+  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nwarps) {
+    uint32_t ov = 0;
+    if (lane == 0) ov = *(volatile uint32_t*)overflow;
+    if (__shfl_sync(DB_FULL, ov, 0)) return;  // warp-uniform
+    const uint32_t c0 = ch * GR_CHUNK, c1 = min(n, c0 + GR_CHUNK);
+    for (uint32_t i0 = c0; i0 < c1; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const bool valid = i < c1;
+      int32_t x[DD];
+      const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
+      const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
+      const uint32_t vmask = __ballot_sync(DB_FULL, valid);
+      if (__all_sync(DB_FULL, !valid || key == k0)) {
+        if (lane == 0) {
+          if (k0 != run_key) {
+            flush();
+            run_key = k0;
+            run_slot = gslot_insert(T, mask, k0, overflow);
+          }
+          run_cnt += __popc(vmask);
+        }
+        continue;
       }
-      if (++probe == MAX_PROBE) { atomicExch(overflow, 1u); break; }
-      h = (h + 1) & mask;
+      const uint32_t peers = __match_any_sync(DB_FULL, key);
+      if (valid && (peers & lanemask_lt()) == 0) {
+        const uint64_t h = gslot_insert(T, mask, key, overflow);
+        if (h != ~0ull) atomicAdd(&T[h].cnt, (uint32_t)__popc(peers));
+      }
     }
   }
+  if (lane == 0) flush();
 }
 
 // B1: compact the non-empty slots (slot index list; one atomic per block).
@@ -160,53 +181,74 @@ __global__ void group_cells_kernel(GSlot* T, const uint32_t* __restrict__ rank_s
   cellmin[r] = 0xffffffffu;
 }
 
-// C: scatter points to their cells (padded rows), see the file comment.
+// C: scatter points to their cells (padded rows), see the file comment. A
+// warp walks a contiguous chunk of the input (as in the count pass): while
+// the whole warp stays in the cell of the previous step, its id is reused
+// without a table probe and its run minimum is already recorded.
 template <int DD, int D>
 __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
     const int32_t* __restrict__ pts, uint32_t n, Geo g, uint64_t magic, const GSlot* __restrict__ T,
     uint64_t mask, uint32_t* __restrict__ cursor, uint32_t* __restrict__ cellmin, int32_t* __restrict__ Ps,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ cell_of) {
   const int lane = threadIdx.x & 31;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  const uint32_t iters = (n + stride - 1) / stride;
-  for (uint32_t it = 0; it < iters; ++it) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
-    const bool valid = i < n;
-    int32_t x[DD];
-    uint32_t id = 0xffffffffu;
-    if (valid) {
-      const uint64_t key = point_key<DD>(pts, i, g, magic, x);
-      uint64_t h = gslot(key, mask);
-      while (true) {
-        const uint4 s = __ldg(reinterpret_cast<const uint4*>(T + h));
-        if ((((uint64_t)s.y << 32) | s.x) == key) { id = s.w; break; }
-        h = (h + 1) & mask;  // present: inserted by the count pass
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nchunks = (n + GR_CHUNK - 1) / GR_CHUNK;
+  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nwarps) {
+    const uint32_t c0 = ch * GR_CHUNK, c1 = min(n, c0 + GR_CHUNK);
+    uint64_t run_key = ~0ull;
+    uint32_t run_id = 0xffffffffu;
+    for (uint32_t i0 = c0; i0 < c1; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const bool valid = i < c1;
+      int32_t x[DD];
+      const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
+      const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
+      const bool uniform = __all_sync(DB_FULL, !valid || key == k0);
+      uint32_t id = 0xffffffffu;
+      bool new_run = true;
+      if (uniform && k0 == run_key) {
+        id = run_id;  // same cell as the previous step
+        new_run = false;
+      } else if (valid) {
+        uint64_t h = gslot(key, mask);
+        while (true) {
+          const uint4 s = __ldg(reinterpret_cast<const uint4*>(T + h));
+          if ((((uint64_t)s.y << 32) | s.x) == key) { id = s.w; break; }
+          h = (h + 1) & mask;  // present: inserted by the count pass
+        }
       }
-    }
-    const uint32_t id0 = __shfl_sync(DB_FULL, id, 0);
-    const uint32_t peers = __all_sync(DB_FULL, id == id0) ? DB_FULL : __match_any_sync(DB_FULL, id);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (valid && lane == leader) {
-      base = atomicAdd(cursor + id, (uint32_t)__popc(peers));
-      atomicMin(cellmin + id, i);  // lanes hold increasing i: the leader's is the run's minimum
-    }
-    base = __shfl_sync(DB_FULL, base, leader);
-    if (!valid) continue;
-    const uint32_t pos = base + __popc(peers & lanemask_lt());
-    int32_t y[D];
+      if (uniform) {
+        run_key = k0;
+        run_id = __shfl_sync(DB_FULL, id, 0);
+        id = run_id;
+      } else {
+        run_key = ~0ull;
+      }
+      const uint32_t peers = uniform ? __ballot_sync(DB_FULL, valid) : __match_any_sync(DB_FULL, id);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (valid && lane == leader) {
+        base = atomicAdd(cursor + id, (uint32_t)__popc(peers));
+        // lanes hold increasing i: the leader's is the minimum of its run
+        if (new_run) atomicMin(cellmin + id, i);
+      }
+      base = __shfl_sync(DB_FULL, base, leader);
+      if (!valid) continue;
+      const uint32_t pos = base + __popc(peers & lanemask_lt());
+      int32_t y[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) y[k] = k < DD ? x[k] : 0;
-    if constexpr (D == 2) {
-      reinterpret_cast<int2*>(Ps)[pos] = make_int2(y[0], y[1]);
-    } else if constexpr (D == 4) {
-      reinterpret_cast<int4*>(Ps)[pos] = make_int4(y[0], y[1], y[2], y[3]);
-    } else {
-      reinterpret_cast<int4*>(Ps)[2 * pos] = make_int4(y[0], y[1], y[2], y[3]);
-      reinterpret_cast<int4*>(Ps)[2 * pos + 1] = make_int4(y[4], y[5], y[6], y[7]);
+      for (int k = 0; k < D; ++k) y[k] = k < DD ? x[k] : 0;
+      if constexpr (D == 2) {
+        reinterpret_cast<int2*>(Ps)[pos] = make_int2(y[0], y[1]);
+      } else if constexpr (D == 4) {
+        reinterpret_cast<int4*>(Ps)[pos] = make_int4(y[0], y[1], y[2], y[3]);
+      } else {
+        reinterpret_cast<int4*>(Ps)[2 * pos] = make_int4(y[0], y[1], y[2], y[3]);
+        reinterpret_cast<int4*>(Ps)[2 * pos + 1] = make_int4(y[4], y[5], y[6], y[7]);
+      }
+      idx[pos] = i;
+      cell_of[pos] = id;
     }
-    idx[pos] = i;
-    cell_of[pos] = id;
   }
 }
 
