@@ -59,3 +59,37 @@ def test_full_config(oracle_lib, name):
     # whole output vs the independent grid oracle
     o = oracle_lib.o2(pts, cfg.eps, cfg.min_pts)
     assert_same(g, o, name)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "spreader"])
+def test_large_inputs_sampled(oracle_lib, kind):
+    """Beyond the BASELINE sizes (40M points): the lattice counting sort's
+    limit is passed (uniform data takes the radix sort), the hash table holds
+    the seed spreader's cells. Checked by sampled O1 evaluations (core flags,
+    border rows, label consistency) and global invariants of canonical ids."""
+    n = 40_000_000
+    if kind == "uniform":
+        pts = datagen.uniform(n, 3, 200_000, 17)
+        eps, mp = 500, 10
+    else:
+        pts = datagen.seed_spreader(n, 3, 1e6, 18, 1000 / n, noise_frac=1e-4)
+        eps, mp = 1000, 100
+    g = run_gpu(pts, eps, mp)
+    core = g.core.astype(bool)
+    # canonical ids: a core point's id is a core point of the same cluster, the smallest
+    assert (g.cluster[~core] == -1).all()
+    cl = g.cluster[core]
+    assert core[cl].all() and (g.cluster[cl] == cl).all()
+    assert (cl <= np.flatnonzero(core)).all()
+    rng = np.random.default_rng(5)
+    sample = rng.choice(n, SAMPLES, replace=False)
+    cnt = oracle_lib.counts_for(pts, eps, sample)
+    assert np.array_equal(core[sample], cnt >= mp), "sampled core flags"
+    nc = sample[~core[sample]]
+    if len(nc):
+        off, ids = oracle_lib.labels_near_for(pts, eps, g.core, g.cluster, nc)
+        for k, i in enumerate(nc):
+            assert list(g.border_ids[g.border_off[i]:g.border_off[i + 1]]) == list(ids[off[k]:off[k + 1]])
+    cs = sample[core[sample]][:64]
+    if len(cs):
+        assert (oracle_lib.core_label_violations(pts, eps, g.core, g.cluster, cs) == 0).all()
