@@ -62,6 +62,8 @@ extern "C" {
 #define DBSCAN_F_QUADTREE    4096u /* our-exact-qt: MarkCore's
                                       RangeCount on cells with >= 256 points traverses a
                                       per-cell tree instead of scanning (CSR path)           */
+#define DBSCAN_F_NO_BRICK    8192u /* sparse path, d = 3: MarkCore with a thread per point
+                                      instead of the shared-memory brick kernel (testing)    */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
@@ -98,6 +100,8 @@ extern "C" {
 #define DBSCAN_STAT_QT_NODES     15  /* tree nodes built with F_QUADTREE                         */
 #define DBSCAN_STAT_APPROX_SIDE  16  /* dbscan_approx: sub-cell side t of the connectivity test
                                         (0: the test is exact)                                */
+#define DBSCAN_STAT_BRICK        17  /* sparse MarkCore: 1 brick kernel, 2 brick kernel with
+                                        overflowed bricks taken by the thread kernel, 0 none  */
 #define DBSCAN_NSTATS            20
 
 typedef struct dbscan_result {

@@ -312,7 +312,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     tm.stage(DBSCAN_STAGE_MARKCORE);
     so.counters = c.alloc<uint32_t>(4);
     c.zero(so.counters, 16);
-    core_cells = sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, lat_dir, &so);
+    core_cells = sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, lat_dir,
+                                 !(flags & DBSCAN_F_NO_BRICK), &so);
   } else {
     // ---- a4-a5: cell lookup + neighbour CSR (+ MarkCore bound ub)
     uint64_t* nbr_off;
@@ -443,6 +444,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_MARKCORE_TESTS] = (int64_t)hw[0];
   out->stats[DBSCAN_STAT_QT_NODES] = (int64_t)qtrees.nodes;
   out->stats[DBSCAN_STAT_APPROX_SIDE] = g.at;
+  out->stats[DBSCAN_STAT_BRICK] = so.brick;
   return DBSCAN_OK;
 }
 

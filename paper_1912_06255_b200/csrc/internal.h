@@ -199,15 +199,17 @@ struct SparseOut {
   void* stash = nullptr;         // kernel arguments kept between the stages
   const uint32_t* core_list = nullptr;  // cells holding core points, linear order
   uint32_t ncore = 0;
+  int brick = 0;                 // MarkCore: 1 brick kernel, 2 with overflowed bricks
 };
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);
 // a4 + a6 + a7 on the rank directories: core flags, core-first compaction,
 // core_cnt, the core-cell directory; returns the number of core cells (0 =
 // no core point, the caller takes the all-noise exit; synchronises).
 // dir: the rank directory from the lattice counting sort, or NULL (built here).
+// brick_ok: the brick MarkCore may run (DBSCAN_F_NO_BRICK unset).
 uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
                          uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
-                         const uint4* dir, SparseOut* o);
+                         const uint4* dir, bool brick_ok, SparseOut* o);
 void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                     const uint32_t* core_cnt, bool wide, uint32_t* parent,
                     unsigned long long* tested, SparseOut* o);

@@ -36,6 +36,7 @@
 //    sorted position; larger sets are enumerated without storage in
 //    ascending order.
 #include <algorithm>
+#include <array>
 #include <map>
 
 #include "internal.h"
@@ -69,7 +70,7 @@ struct SpArgs {
   uint8_t* core_s;
   uint32_t* core_cnt;
   int64_t min_pts;
-  uint32_t* counters;        // [0] core cells, [1] unused, [2] large pairs, [3] mixed cells
+  uint32_t* counters;        // [0] core cells, [1] brick overflow, [2] large pairs, [3] mixed cells
   uint32_t* mixed_list;
   uint32_t* core_tmp;        // cells with core points, unordered (count in counters[0])
   const uint32_t* cell_label;
@@ -195,15 +196,18 @@ __global__ void __launch_bounds__(256) cell_max_kernel(const uint32_t* __restric
 // symmetric counting with atomics were all slower.
 // COUNT (F_COUNT_WORK, measurement runs only): distance tests, summed into
 // work[0] with one atomic per block.
+// fb != NULL (after the brick kernel): runs only if *fb is set, and only on
+// the points of bricks that overflowed (core_s still 0xff).
 template <int DIM, int D, bool WIDE, int U, bool COUNT>
-__global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, unsigned long long* work) {
+__global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, unsigned long long* work, const uint32_t* fb) {
+  if (fb && *fb == 0) return;
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
   __syncthreads();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t tests = 0;
-  if (j < a.n) {
+  if (j < a.n && (!fb || a.core_s[j] == 0xff)) {
     const uint32_t g = a.cell_of[j];
     const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
     if ((int64_t)m >= a.min_pts) {
@@ -232,6 +236,174 @@ __global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, unsigned long lo
       }
       a.core_s[j] = count >= need;
     }
+  }
+  if (COUNT) block_add_u64(tests, work);
+}
+
+// Brick variant of MarkCore (d = 3, R <= 2; the default for 3D sparse
+// lattices). A CTA takes a brick of BRK^3 lattice cells: it stages the points
+// of the brick and of its R-cell halo in shared memory — every halo column (a
+// run of BRK_H cells along z) is one contiguous range of Ps, read with one
+// directory probe and copied coalesced — together with, per halo column, the
+// prefix of its cells' sizes. Then a thread per own point counts over the 25
+// stencil columns from shared memory only (no directory probes, no global
+// point loads), nearest column first, stopping at minPts (Alg 2, P:L571-598;
+// a dense cell is all core). A brick whose halo holds more than
+// BRK_CAP points sets *overflow and leaves its points to the thread kernel
+// (core_s stays 0xff for them).
+constexpr int BRK = 16;                  // brick side in cells
+constexpr int BRK_R = 2;                 // halo (R = 2; the usual case for d = 3)
+constexpr int BRK_H = BRK + 2 * BRK_R;   // 20
+constexpr int BRK_COLS = BRK_H * BRK_H;  // halo columns
+constexpr int BRK_CAP = 3072;            // halo points held in shared memory
+constexpr int BRK_THREADS = 512;
+constexpr int BRK_PER = (BRK_COLS + BRK_THREADS - 1) / BRK_THREADS;
+
+struct BrickSmem {
+  int4 pts[BRK_CAP];
+  uint16_t abs[BRK_COLS][BRK_H + 1];     // per column: index in pts of its cell z (z = BRK_H: end)
+  int32_t gdelta[BRK_COLS];              // sorted position - index in pts, per column
+  uint32_t obase[BRK_COLS];              // prefix of the own points per column
+  int2 rng[SP_MAX_COLS + 1];             // stencil columns (nearest first): offsets into abs; sentinel
+  uint32_t scan[33];
+  uint32_t total, own;
+};
+
+template <bool WIDE, bool COUNT>
+__global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a, const int8_t* __restrict__ geo,
+                                                                    uint32_t nby, uint32_t nbz,
+                                                                    uint32_t* overflow,
+                                                                    unsigned long long* work) {
+  extern __shared__ __align__(16) uint8_t brick_raw[];
+  BrickSmem& S = *reinterpret_cast<BrickSmem*>(brick_raw);
+  const uint32_t bid = blockIdx.x;
+  const uint32_t bz = bid % nbz, by = (bid / nbz) % nby, bx = bid / (nbz * nby);
+  const uint64_t Dx = a.g.maxc[0] + 1 + 2 * BRK_R, Dy = a.g.maxc[1] + 1 + 2 * BRK_R,
+                 Dz = a.g.maxc[2] + 1 + 2 * BRK_R;
+  // padded lattice coordinates of the halo origin: own cells start at +R
+  const uint64_t X0 = (uint64_t)bx * BRK, Y0 = (uint64_t)by * BRK, Z0 = (uint64_t)bz * BRK;
+  // stencil column k of a cell at abs index i spans abs[i + rng.x] .. abs[i + rng.y]
+  for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) {
+    const int dc = ((int)geo[3 * k] * BRK_H + geo[3 * k + 1]) * (BRK_H + 1), mz = geo[3 * k + 2];
+    S.rng[k] = make_int2(dc - mz, dc + mz + 1);
+  }
+  if (threadIdx.x == 0) S.rng[a.ncols] = make_int2(0, 0);
+  // ---- phase 1: a thread per halo column — one directory word pair covers its
+  // BRK_H cells (b0 + 20 <= 51 bits); cell ends are independent loads
+  uint32_t len[BRK_PER], own[BRK_PER], g0s[BRK_PER];
+#pragma unroll
+  for (int q = 0; q < BRK_PER; ++q) {
+    const int cc = threadIdx.x * BRK_PER + q;
+    len[q] = own[q] = g0s[q] = 0;
+    if (cc >= BRK_COLS) continue;
+    const uint32_t hx = cc / BRK_H, hy = cc % BRK_H;
+    const uint64_t X = X0 + hx, Y = Y0 + hy;
+    uint32_t bits = 0, r = 0;
+    if (X < Dx && Y < Dy) {
+      const uint32_t hz = (uint32_t)min((uint64_t)BRK_H, Dz - Z0);
+      const uint64_t lin0 = (X * Dy + Y) * Dz + Z0;
+      const uint4 e = __ldg(a.dir + (lin0 >> 5));
+      const uint32_t b0 = (uint32_t)lin0 & 31u;
+      bits = __funnelshift_r(e.x, e.y, b0) & ((1u << hz) - 1u);
+      r = e.z + __popc(e.x & ((1u << b0) - 1u));
+    }
+    const uint32_t g0 = __ldg(a.cell_start + r);
+    uint32_t run = 0, o0 = 0, o1 = 0;
+#pragma unroll
+    for (int z = 0; z < BRK_H; ++z) {
+      if (z == BRK_R) o0 = run;
+      if (z == BRK_R + BRK) o1 = run;
+      S.abs[cc][z] = (uint16_t)min(run, 65535u);  // (made absolute below)
+      if ((bits >> z) & 1u) run = __ldg(a.cell_start + r + __popc(bits & ((2u << z) - 1u))) - g0;
+    }
+    S.abs[cc][BRK_H] = (uint16_t)min(run, 65535u);
+    len[q] = run;
+    g0s[q] = g0;
+    own[q] = (hx >= BRK_R && hx < BRK_R + BRK && hy >= BRK_R && hy < BRK_R + BRK) ? o1 - o0 : 0u;
+  }
+  // column bases (all halo points) and own-point prefixes
+  uint32_t el;
+  {
+    uint32_t sl = 0, so = 0;
+#pragma unroll
+    for (int q = 0; q < BRK_PER; ++q) { sl += len[q]; so += own[q]; }
+    uint32_t tl, to;
+    el = block_exclusive_scan<uint32_t>(sl, S.scan, &tl);
+    __syncthreads();
+    uint32_t eo = block_exclusive_scan<uint32_t>(so, S.scan, &to);
+#pragma unroll
+    for (int q = 0; q < BRK_PER; ++q) {
+      const int cc = threadIdx.x * BRK_PER + q;
+      if (cc < BRK_COLS) S.obase[cc] = eo;
+      eo += own[q];
+    }
+    if (threadIdx.x == 0) { S.total = tl; S.own = to; }
+  }
+  __syncthreads();
+  const uint32_t total = S.total, nown = S.own;
+  if (nown == 0) return;
+  if (total > BRK_CAP) {  // (a column over 65535 points is caught here too)
+    if (threadIdx.x == 0) atomicExch(overflow, 1u);
+    return;  // the thread kernel takes this brick's points (core_s left at 0xff)
+  }
+  // ---- phase 1b: each thread copies its columns' points and makes abs absolute
+#pragma unroll
+  for (int q = 0; q < BRK_PER; ++q) {
+    const int cc = threadIdx.x * BRK_PER + q;
+    if (cc >= BRK_COLS) continue;
+    for (uint32_t t = 0; t < len[q]; ++t) S.pts[el + t] = __ldg(reinterpret_cast<const int4*>(a.Ps) + g0s[q] + t);
+#pragma unroll
+    for (int z = 0; z <= BRK_H; ++z) S.abs[cc][z] += (uint16_t)el;
+    S.gdelta[cc] = (int32_t)(g0s[q] - el);
+    el += len[q];
+  }
+  __syncthreads();
+  // ---- phase 2: a thread per own point; one flat loop over (stencil column,
+  // candidate) steps so that lanes stay converged whatever the column sizes
+  const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
+  const int ncols = a.ncols;
+  uint32_t tests = 0;
+  for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
+    // its column: the last one whose own prefix is <= t (never an empty one)
+    int cc = 0;
+#pragma unroll
+    for (int step = 256; step; step >>= 1)
+      if (cc + step < BRK_COLS && S.obase[cc + step] <= t) cc += step;
+    const uint16_t* col = S.abs[cc];
+    const uint32_t i = t - S.obase[cc] + col[BRK_R];  // index in pts
+    // its cell: the last own z whose start is <= i
+    int hz = BRK_R;
+#pragma unroll
+    for (int step = 8; step; step >>= 1)
+      if (col[hz + step] <= i) hz += step;
+    const uint32_t j = (uint32_t)((int32_t)i + S.gdelta[cc]);  // sorted position
+    if ((int64_t)(col[hz + 1] - col[hz]) >= a.min_pts) { a.core_s[j] = 1; continue; }  // dense cell
+    const int4 pv = S.pts[i];
+    const int32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
+    const uint16_t* base = &S.abs[0][0] + cc * (BRK_H + 1) + hz;
+    // Branch-free steps: each one advances to the next stencil column when
+    // the current range is spent, then tests one candidate if there is one
+    // (the read past a spent range stays inside the shared block).
+    uint32_t count = 0, u = 0, u1 = 0;
+    int k = 0;
+    int2 rg = S.rng[0];
+    for (;;) {
+      const bool adv = u >= u1;
+      if (adv && k == ncols) break;
+      const uint32_t nu = base[rg.x], nu1 = base[rg.y];
+      u = adv ? nu : u;
+      u1 = adv ? nu1 : u1;
+      k += adv;
+      rg = S.rng[k];
+      const int4 qv = S.pts[u];
+      const int32_t q[4] = {qv.x, qv.y, qv.z, qv.w};
+      const bool live = u < u1;
+      count += (live && within_dim<3, 4, WIDE>(p, q, a.g)) ? 1u : 0u;
+      if (COUNT) tests += live;
+      u += live;
+      if (count >= need) break;
+    }
+    a.core_s[j] = count >= need;
   }
   if (COUNT) block_add_u64(tests, work);
 }
@@ -523,7 +695,8 @@ static unsigned __int128 padded_volume(const Geo& g) {
 // Returns {squared gap of the prefix, {start offset, mask}} nearest first;
 // *back gets the columns of cells before the centre in linear order.
 typedef std::vector<std::pair<unsigned __int128, std::pair<long long, uint32_t>>> Cols;
-static Cols stencil_columns(const Geo& g, const uint64_t* stride, Cols* back) {
+static Cols stencil_columns(const Geo& g, const uint64_t* stride, Cols* back,
+                            std::vector<int8_t>* geom = nullptr /* dx, dy, mz per column (d = 3) */) {
   const std::vector<int8_t> offs = stencil_offsets(g);
   const int noffs = (int)(offs.size() / g.d);
   std::map<std::vector<int>, int> colm;
@@ -535,6 +708,7 @@ static Cols stencil_columns(const Geo& g, const uint64_t* stride, Cols* back) {
     mm = std::max(mm, v < 0 ? -v : v);
   }
   Cols cols;
+  std::vector<std::pair<unsigned __int128, std::array<int8_t, 3>>> gg3;
   back->clear();
   for (auto& [pfx, mm] : colm) {
     int first = 0;  // sign of the first non-zero prefix component
@@ -549,12 +723,18 @@ static Cols stencil_columns(const Geo& g, const uint64_t* stride, Cols* back) {
     }
     const uint32_t full = (uint32_t)((1ull << (2 * mm + 1)) - 1);
     cols.push_back({gap, {off, full}});
+    if (g.d == 3) gg3.push_back({gap, {(int8_t)pfx[0], (int8_t)pfx[1], (int8_t)mm}});
     if (first < 0) back->push_back({gap, {off, full}});
     else if (first == 0 && mm > 0) back->push_back({gap, {off, (uint32_t)((1ull << mm) - 1)}});
   }
   auto by_gap = [](const auto& x, const auto& y) { return x.first < y.first; };
   std::stable_sort(cols.begin(), cols.end(), by_gap);
   std::stable_sort(back->begin(), back->end(), by_gap);
+  if (geom) {
+    std::stable_sort(gg3.begin(), gg3.end(), by_gap);
+    geom->clear();
+    for (auto& e : gg3) geom->insert(geom->end(), e.second.begin(), e.second.end());
+  }
   return cols;
 }
 
@@ -596,7 +776,7 @@ static uint4* build_dir(Ctx& c, const SpArgs& a, uint64_t words, const uint32_t*
 
 uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,
                          uint8_t* core_s, uint32_t* core_cnt, int64_t n, int64_t min_pts, bool wide,
-                         const uint4* dir, SparseOut* o) {
+                         const uint4* dir, bool brick_ok, SparseOut* o) {
   SpArgs a{};
   a.g = g;
   unsigned __int128 vol = 1;
@@ -650,17 +830,51 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   // a4: directory of all cells
   const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
   a.dir = dir ? dir : build_dir(c, a, words, nullptr, nullptr);
-  // a6: MarkCore, thread per point over the stencil columns (U = 2)
+  // a6: MarkCore — bricks staged in shared memory (d = 3, R = 2), else a
+  // thread per point over the stencil columns (U = 2)
   c.stage(DBSCAN_STAGE_MARKCORE);
-  by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
-    constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
-    constexpr bool W = decltype(Wd)::value;
-    if (c.work)
-      sp_core_kernel<DIM, D, W, 2, true><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, c.work);
-    else
-      sp_core_kernel<DIM, D, W, 2, false><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr);
-  });
-  c.launched();
+  // bricks hold BRK_CAP / BRK_H^3 = 0.38 points per halo cell: taken when the
+  // mean over the lattice is below 0.3 (denser data would overflow them)
+  o->brick = brick_ok && g.d == 3 && g.R == BRK_R && !g.at && (unsigned __int128)n * 10 <= vol * 3;
+  if (o->brick) {
+    std::vector<int8_t> geom;
+    stencil_columns(g, a.stride, &back, &geom);
+    int8_t* dgeo = c.alloc<int8_t>(geom.size());
+    DB_CUDA(cudaMemcpyAsync(dgeo, geom.data(), geom.size(), cudaMemcpyHostToDevice, c.st));
+    const uint32_t nb[3] = {(g.maxc[0] + BRK) / BRK, (g.maxc[1] + BRK) / BRK, (g.maxc[2] + BRK) / BRK};
+    const uint64_t nbricks = (uint64_t)nb[0] * nb[1] * nb[2];
+    if (nbricks >= (1ull << 31)) throw Error(-4, "sparse path: brick grid too large");
+    DB_CUDA(cudaMemsetAsync(core_s, 0xff, (size_t)n, c.st));
+    const size_t smem = sizeof(BrickSmem);
+    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
+      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
+      constexpr bool W = decltype(Wd)::value;
+      if constexpr (DIM == 3) {
+        auto launch = [&](auto kern, unsigned long long* work) {
+          DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, dgeo, nb[1], nb[2], a.counters + 1, work);
+          c.launched();
+        };
+        if (c.work) launch(sp_core_brick_kernel<W, true>, c.work);
+        else launch(sp_core_brick_kernel<W, false>, nullptr);
+        if (c.work)
+          sp_core_kernel<DIM, D, W, 2, true><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, c.work, a.counters + 1);
+        else
+          sp_core_kernel<DIM, D, W, 2, false><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr, a.counters + 1);
+        c.launched();
+      }
+    });
+  } else {
+    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
+      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
+      constexpr bool W = decltype(Wd)::value;
+      if (c.work)
+        sp_core_kernel<DIM, D, W, 2, true><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, c.work, nullptr);
+      else
+        sp_core_kernel<DIM, D, W, 2, false><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr, nullptr);
+    });
+    c.launched();
+  }
   // a7: core counts, core-first partition of mixed cells
   c.stage(DBSCAN_STAGE_COMPACT);
   a.mixed_list = c.alloc<uint32_t>(cv.ncells);
@@ -674,7 +888,9 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.core_list = core_list;
   core_list_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a, core_list);
   c.launched();
-  a.ncore = c.read(a.counters);
+  const uint64_t cnt01 = c.read(reinterpret_cast<const uint64_t*>(a.counters));  // [0] and [1]
+  a.ncore = (uint32_t)cnt01;
+  if (o->brick && (uint32_t)(cnt01 >> 32)) o->brick = 2;
   o->stash = new SpArgs(a);
   o->core_list = core_list;
   o->ncore = a.ncore;

@@ -232,6 +232,36 @@ def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"d={d} flags={flags}")
 
 
+@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP])
+def test_brick_markcore_vs_o2(oracle_lib, grouping):
+    """The 3D brick MarkCore (16^3 cells staged with their halo in shared
+    memory) against O2 and against the thread-per-point kernel: lattices with
+    ragged brick edges, a dense blob whose brick overflows the shared-memory
+    capacity (its points go to the thread kernel), and one cell holding more
+    than 65535 points."""
+    cases = []
+    cases.append((datagen.uniform(150_000, 3, 40_000, 31), 500, 3, 1))
+    cases.append((datagen.uniform(100_000, 3, 25_000, 32), 600, 4, 1))
+    blob = datagen.uniform(200_000, 3, 40_000, 33)
+    blob[:6000] = blob[0] + datagen.uniform(6000, 3, 600, 34)   # ~6000 points in a few cells
+    cases.append((blob, 500, 10, 2))
+    big = datagen.uniform(260_000, 3, 50_000, 35)
+    big[:66_000] = big[0]                                        # one cell, > 65535 points
+    cases.append((big, 500, 10, 2))
+    # denser than 0.3 points per lattice cell: the thread kernel alone
+    cases.append((datagen.uniform(150_000, 3, 12_000, 36), 500, 8, 0))
+    for pts, eps, mp, want in cases:
+        r = gpu(pts, eps, mp, grouping)
+        assert r.stats["sparse"] == 1 and r.stats["brick"] == want, (r.stats, eps)
+        if want == 0:
+            assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"dense eps={eps}")
+            continue
+        t = gpu(pts, eps, mp, grouping | pkg.F_NO_BRICK)
+        assert t.stats["brick"] == 0
+        assert_same(np_result(r), np_result(t), f"brick vs thread eps={eps}")
+        assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"brick eps={eps}")
+
+
 def test_grouping_choice():
     """Few cells: the hash counting sort groups the points; many distinct
     cells (uniform 3D, 2M points, ~2M cells) on a lattice too large to count
