@@ -491,113 +491,116 @@ __global__ void __launch_bounds__(LAT_THREADS) lat_cells_kernel(const uint32_t* 
   }
 }
 
-// pass 3: the permutation, in two steps so that no write is random.
-// Every point's final position pos = cell_start[rank] + slot is known; the
-// positions are split into buckets of BK_T consecutive positions.
-//  3a: a block takes BK_ITEMS consecutive points, ranks them by bucket in
-//      shared memory, reserves room in each bucket's staging range with one
-//      atomic per (block, bucket) and writes the records {pos, x, y, z} and
-//      the input index there (runs per bucket);
-//  3b: a block per bucket loads its BK_T records, places the points, input
-//      indices and cell ids in shared memory by pos - bucket start, and
-//      writes them out coalesced. cell_of is filled cell by cell from
-//      cell_start (the bucket's cells are one contiguous id range).
-constexpr int BK_T = 8192;           // positions per bucket (3b: 8192 x 24 B in shared memory)
+// pass 3: the permutation, in two steps so that no write lands far from the
+// others of its time. The lattice words are cut into buckets of 2^ws
+// consecutive words; a bucket's points take the contiguous positions
+// ppre[b 2^ws] .. ppre[(b+1) 2^ws) (key order = linear order), about
+// BK_TARGET of them.
+//  3a: a block takes BK_ITEMS consecutive points per thread, ranks them by
+//      bucket in shared memory, reserves room in each bucket's range with one
+//      atomic per (block, bucket) and writes the records {lin - bucket start
+//      | slot << 24, x, y, z} and the input index there (runs of ~BK_ITEMS x
+//      BK_THREADS / buckets records). No gather: the bucket is lin >> (5+ws).
+//  3b: a thread per staged record (read coalesced) finds its cell rank on
+//      the directory and its position cell_start[rank] + slot, and writes the
+//      point, its input index and the cell id there. A block's records belong
+//      to one or two buckets, so its directory words, cell starts and output
+//      positions lie in one small window (L1 / L2 merge the writes).
 constexpr int BK_THREADS = 512;
-constexpr int BK_ITEMS = 8;          // 3a: 4096 points per block
-constexpr int BK_MAXB = 4096;        // buckets held by a 3a block's shared histogram
+constexpr int BK_ITEMS = 8;            // 3a: 4096 points per block
+constexpr int BK_MAXB = 4096;          // buckets held by a 3a block's shared histogram
+constexpr uint32_t BK_TARGET = 16384;  // points per bucket aimed at
+constexpr int BK_MAXWS = 19;           // lin - bucket start < 2^24
+constexpr int64_t LAT_MAX_N = 1 << 25;  // (the documented limit of the lattice sort)
 
 template <int DD>
-__global__ void __launch_bounds__(BK_THREADS) lat_stage_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                               LatArgs L, const uint4* __restrict__ dir,
-                                                               const uint8_t* __restrict__ slot,
-                                                               const uint32_t* __restrict__ cell_start,
-                                                               uint32_t nbk, uint32_t* __restrict__ bcur,
-                                                               uint4* __restrict__ rec, uint32_t* __restrict__ reci) {
+__global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t* __restrict__ pts, uint32_t n,
+                                                                  LatArgs L, const uint8_t* __restrict__ slot,
+                                                                  const uint32_t* __restrict__ ppre, int ws,
+                                                                  uint32_t nbk, uint32_t* __restrict__ bcur,
+                                                                  uint4* __restrict__ rec,
+                                                                  uint32_t* __restrict__ reci) {
   __shared__ uint32_t hist[BK_MAXB];
   for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS) hist[b] = 0;
   __syncthreads();
   const uint32_t i0 = blockIdx.x * (BK_THREADS * BK_ITEMS);
-  uint32_t pos[BK_ITEMS], lr[BK_ITEMS];
+  uint32_t lr[BK_ITEMS], key[BK_ITEMS], bk[BK_ITEMS];
   int32_t x[BK_ITEMS][3];
 #pragma unroll
   for (int t = 0; t < BK_ITEMS; ++t) {
     const uint32_t i = i0 + t * BK_THREADS + threadIdx.x;
-    pos[t] = 0xffffffffu;
+    bk[t] = 0xffffffffu;
     if (i < n) {
       int32_t xx[DD];
       const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, xx);
 #pragma unroll
       for (int k = 0; k < 3; ++k) x[t][k] = k < DD ? xx[k] : 0;
-      const uint4 e = __ldg(dir + (lin >> 5));
-      const uint32_t rank = e.z + __popc(e.x & ((1u << ((uint32_t)lin & 31u)) - 1u));
-      pos[t] = cell_start[rank] + slot[i];
-      lr[t] = atomicAdd(hist + pos[t] / BK_T, 1u);
+      bk[t] = (uint32_t)(lin >> (5 + ws));
+      key[t] = (uint32_t)(lin - ((uint64_t)bk[t] << (5 + ws))) | ((uint32_t)__ldg(slot + i) << 24);
     }
   }
+#pragma unroll
+  for (int t = 0; t < BK_ITEMS; ++t)
+    if (bk[t] != 0xffffffffu) lr[t] = atomicAdd(hist + bk[t], 1u);
   __syncthreads();
-  // reserve each touched bucket's room (hist[b] becomes the global base)
+  // reserve each touched bucket's room: hist[b] becomes the staging position
   for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS)
-    if (hist[b]) hist[b] = atomicAdd(bcur + b, hist[b]);
+    if (hist[b]) hist[b] = __ldg(ppre + ((uint64_t)b << ws)) + atomicAdd(bcur + b, hist[b]);
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < BK_ITEMS; ++t) {
-    if (pos[t] == 0xffffffffu) continue;
-    const uint32_t b = pos[t] / BK_T;
-    const uint64_t o = (uint64_t)b * BK_T + hist[b] + lr[t];
-    rec[o] = make_uint4(pos[t], (uint32_t)x[t][0], (uint32_t)x[t][1], (uint32_t)x[t][2]);
+    if (bk[t] == 0xffffffffu) continue;
+    const uint32_t o = hist[bk[t]] + lr[t];
+    rec[o] = make_uint4(key[t], (uint32_t)x[t][0], (uint32_t)x[t][1], (uint32_t)x[t][2]);
     reci[o] = i0 + t * BK_THREADS + threadIdx.x;
   }
 }
 
+constexpr int PL_THREADS = 512;
+
+// 3b's block -> bucket table: chunk c (records c PL_THREADS ..) starts in the
+// bucket b with base(b) <= c PL_THREADS < base(b + 1); a thread per bucket.
+__global__ void lat_chunks_kernel(const uint32_t* __restrict__ ppre, int ws, uint64_t words, uint32_t nbk,
+                                  uint32_t nchunks, uint32_t* __restrict__ chunk_bucket) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbk) return;
+  const uint32_t lo = ppre[min((uint64_t)b << ws, words)];
+  const uint32_t hi = b + 1 < nbk ? ppre[min((uint64_t)(b + 1) << ws, words)] : 0xffffffffu;
+  for (uint32_t c = (lo + PL_THREADS - 1) / PL_THREADS; c < nchunks && (uint64_t)c * PL_THREADS < hi; ++c)
+    chunk_bucket[c] = b;
+}
+
 template <int D>
-__global__ void __launch_bounds__(1024) lat_place_kernel(uint32_t n, const uint4* __restrict__ rec,
-                                                         const uint32_t* __restrict__ reci,
-                                                         const uint32_t* __restrict__ cell_start, uint32_t ncells,
-                                                         int32_t* __restrict__ Ps, uint32_t* __restrict__ idx,
-                                                         uint32_t* __restrict__ cell_of) {
-  extern __shared__ __align__(16) uint8_t sm_raw[];
-  int4* sp = reinterpret_cast<int4*>(sm_raw);                        // [BK_T] points (x, y, z, 0)
-  uint32_t* si = reinterpret_cast<uint32_t*>(sp + BK_T);             // [BK_T] input index
-  uint32_t* sc = si + BK_T;                                          // [BK_T] cell id
-  const uint32_t base = blockIdx.x * BK_T;
-  const uint32_t cnt = min((uint32_t)BK_T, n - base);
-  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
-    const uint4 r = rec[(uint64_t)base + t];
-    const uint32_t q = r.x - base;
-    sp[q] = make_int4((int32_t)r.y, (int32_t)r.z, (int32_t)r.w, 0);
-    si[q] = reci[(uint64_t)base + t];
-  }
-  // cells overlapping [base, base + cnt): ids first .. last, found by binary
-  // search (the last cell with start <= p); then a thread per cell fills
-  // its positions' cell ids
-  __shared__ uint32_t s_fl[2];
-  if (threadIdx.x < 2) {
-    const uint32_t p = threadIdx.x == 0 ? base : base + cnt - 1;
-    uint32_t lo = 0, hi = ncells - 1;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (cell_start[mid] <= p) lo = mid; else hi = mid - 1;
-    }
-    s_fl[threadIdx.x] = lo;
-  }
-  __syncthreads();
-  for (uint32_t r = s_fl[0] + threadIdx.x; r <= s_fl[1]; r += blockDim.x) {
-    const uint32_t lo = max(cell_start[r], base), hi = min(cell_start[r + 1], base + cnt);
-    for (uint32_t p = lo; p < hi; ++p) sc[p - base] = r;
-  }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
-    const int4 v = sp[t];
-    if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[base + t] = make_int2(v.x, v.y);
-    else reinterpret_cast<int4*>(Ps)[base + t] = v;
-    idx[base + t] = si[t];
-    cell_of[base + t] = sc[t];
-  }
+__global__ void __launch_bounds__(PL_THREADS) lat_place_kernel(uint32_t n, const uint4* __restrict__ rec,
+                                                               const uint32_t* __restrict__ reci,
+                                                               const uint4* __restrict__ dir,
+                                                               const uint32_t* __restrict__ cell_start,
+                                                               const uint32_t* __restrict__ ppre, int ws,
+                                                               uint64_t words, uint32_t nbk,
+                                                               const uint32_t* __restrict__ chunk_bucket,
+                                                               int32_t* __restrict__ Ps, uint32_t* __restrict__ idx,
+                                                               uint32_t* __restrict__ cell_of) {
+  const uint32_t t0 = blockIdx.x * PL_THREADS;
+  auto base_of = [&](uint32_t b) { return __ldg(ppre + min((uint64_t)b << ws, words)); };
+  const uint32_t s_b0 = __ldg(chunk_bucket + blockIdx.x);  // bucket of t0
+  const uint32_t t = t0 + threadIdx.x;
+  if (t >= n) return;
+  const uint4 r = __ldg(rec + t);
+  const uint32_t i = __ldg(reci + t);
+  uint32_t b = s_b0;
+  while (b + 1 < nbk && base_of(b + 1) <= t) ++b;
+  const uint64_t lin = ((uint64_t)b << (5 + ws)) + (r.x & 0xffffffu);
+  const uint4 e = __ldg(dir + (lin >> 5));
+  const uint32_t rank = e.z + __popc(e.x & ((1u << ((uint32_t)lin & 31u)) - 1u));
+  const uint32_t pos = __ldg(cell_start + rank) + (r.x >> 24);
+  if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[pos] = make_int2((int32_t)r.y, (int32_t)r.z);
+  else reinterpret_cast<int4*>(Ps)[pos] = make_int4((int32_t)r.y, (int32_t)r.z, (int32_t)r.w, 0);
+  idx[pos] = i;
+  cell_of[pos] = rank;
 }
 
 bool lattice_applicable(const Geo& g, int64_t n) {
-  if (g.d > 3 || n == 0 || n > (int64_t)BK_MAXB * BK_T) return false;
+  if (g.d > 3 || n == 0 || n > LAT_MAX_N) return false;
   unsigned __int128 vol = 1;
   for (int k = 0; k < g.d; ++k) vol *= (unsigned __int128)g.maxc[k] + 1 + 2 * (unsigned __int128)g.R;
   return vol <= (unsigned __int128)LAT_PER_POINT * (unsigned __int128)n + (1u << 20);
@@ -658,22 +661,29 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
   c.launched();
   const uint32_t ncells = c.read(cpre + L.words);
   DB_CUDA(cudaMemcpyAsync(cell_start + ncells, ppre + L.words, sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.st));
-  // pass 3: stage by bucket of positions, then place bucket by bucket
-  const uint32_t nbk = (uint32_t)((n + BK_T - 1) / BK_T);
+  // pass 3: stage by bucket of lattice words, then place
+  int ws = 0;
+  const double ppw = (double)n / (double)L.words;  // points per word
+  while (ws < BK_MAXWS && (((L.words + (1ull << ws) - 1) >> ws) > (uint64_t)BK_MAXB ||
+                           ppw * (double)(1ull << ws) < (double)BK_TARGET / 2))
+    ++ws;
+  const uint32_t nbk = (uint32_t)((L.words + (1ull << ws) - 1) >> ws);
   if (nbk > (uint32_t)BK_MAXB) throw Error(-4, "lattice sort: too many buckets");
   uint32_t* bcur = c.alloc<uint32_t>(nbk);
-  uint4* rec = c.alloc<uint4>((size_t)nbk * BK_T);
-  uint32_t* reci = c.alloc<uint32_t>((size_t)nbk * BK_T);
+  uint4* rec = c.alloc<uint4>((size_t)n);
+  uint32_t* reci = c.alloc<uint32_t>((size_t)n);
   c.zero(bcur, sizeof(uint32_t) * nbk);
+  const unsigned nchunks = (unsigned)((n + PL_THREADS - 1) / PL_THREADS);
+  uint32_t* chunk_bucket = c.alloc<uint32_t>(nchunks);
   const unsigned sgrid = (unsigned)((n + BK_THREADS * BK_ITEMS - 1) / (BK_THREADS * BK_ITEMS));
   by_d([&](auto Dd, auto Dp) {
     constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
-    lat_stage_kernel<DD><<<sgrid, BK_THREADS, 0, c.st>>>(pts, (uint32_t)n, L, dir, slot, cell_start, nbk, bcur,
-                                                         rec, reci);
+    lat_stage_kernel<DD><<<sgrid, BK_THREADS, 0, c.st>>>(pts, (uint32_t)n, L, slot, ppre, ws, nbk, bcur, rec, reci);
     c.launched();
-    const int smem = BK_T * (16 + 4 + 4);
-    DB_CUDA(cudaFuncSetAttribute(lat_place_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    lat_place_kernel<D><<<nbk, 1024, smem, c.st>>>((uint32_t)n, rec, reci, cell_start, ncells, Ps, idx, cell_of);
+    lat_chunks_kernel<<<(nbk + 255) / 256, 256, 0, c.st>>>(ppre, ws, L.words, nbk, nchunks, chunk_bucket);
+    c.launched();
+    lat_place_kernel<D><<<nchunks, PL_THREADS, 0, c.st>>>((uint32_t)n, rec, reci, dir, cell_start, ppre, ws,
+                                                          L.words, nbk, chunk_bucket, Ps, idx, cell_of);
     c.launched();
   });
   *dir_out = dir;
