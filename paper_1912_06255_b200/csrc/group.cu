@@ -414,9 +414,14 @@ __global__ void __launch_bounds__(LAT_THREADS) lat_words_kernel(const uint32_t* 
     wcells[w] = __popc(bits);
     wpts[w] = sum;
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(DB_FULL, m, o));
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(mx, m);
+  // largest cell: one atomic per block (same-address atomics serialise)
+  __shared__ uint32_t s_m;
+  if (threadIdx.x == 0) s_m = 0;
+  __syncthreads();
+  m = __reduce_max_sync(DB_FULL, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&s_m, m);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_m) atomicMax(mx, s_m);
 }
 
 // pass 2b: cells in linear order: cell_start, cell_key, and the directory

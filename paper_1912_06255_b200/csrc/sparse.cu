@@ -548,35 +548,59 @@ __device__ uint32_t sp_next_label(const SpArgs& a, const long long* s_off, const
 // Core-centric ClusterBorder. Alg 4 asks, for every non-core point p, which
 // clusters have a core point within eps of p. On a sparse
 // lattice most stencil cells of p hold no core point (c5: 8% of points are
-// core), so the search runs from the other side: a thread per (core cell h,
-// stencil column) item probes the column on the directory of all cells and
-// tests every non-core point p found against h's core points; on a hit it
-// adds label(h) to p's label set, a lock-free set of SP_MAXL slots
-// (atomicCAS into the first slot that is empty or already holds the label;
-// slots fill in order, so a label appears once). A point whose set overflows
-// is flagged and enumerated later without storage (sp_next_label). "Core
-// point within eps" is symmetric, so both sides find the same pairs; p's own
-// cell is h's centre column (same cell => within eps, the test passes).
+// core), so the search runs from the other side: a warp per core cell h.
+// Lane k probes stencil column k on the directory of all cells; a warp scan
+// of the column sizes lays the candidate points out flat, and the lanes take
+// them 32 at a time (lane -> column by a shuffle search), so the lanes stay
+// busy whatever the column sizes. Every non-core candidate p is tested
+// against h's core points; on a hit label(h) joins p's label set, a
+// lock-free set of SP_MAXL slots (atomicCAS into the first slot that is
+// empty or already holds the label; slots fill in order, so a label appears
+// once). A point whose set overflows is flagged and enumerated later without
+// storage (sp_next_label). "Core point within eps" is symmetric, so both
+// sides find the same pairs; p's own cell is h's centre column (same cell =>
+// within eps, the test passes).
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
   __syncthreads();
-  const uint64_t items = (uint64_t)a.ncore * (uint64_t)a.ncols;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < items;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = (uint32_t)(t / (uint32_t)a.ncols), c = (uint32_t)(t - (uint64_t)r * a.ncols);
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.ncore; r += nwarps) {
     const uint32_t h = a.core_list[r];
     const uint64_t base = cell_lin<DIM>(a.cell_key[h], a);
-    uint32_t id0;
-    const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[c], s_mask[c], &id0);
-    if (!nc) continue;
     const uint32_t sh = a.cell_start[h], kh = a.core_cnt[h];
     const uint32_t lab = a.cell_label[h];
-    const uint32_t ue = a.cell_start[id0 + nc];
-    for (uint32_t u = a.cell_start[id0]; u < ue; ++u) {
-      if (a.core_s[u]) continue;
+    uint32_t lo = 0, len = 0;
+    if (lane < a.ncols) {
+      uint32_t id0;
+      const uint32_t nc = dir_probe(a.dir, base + (uint64_t)s_off[lane], s_mask[lane], &id0);
+      if (nc) {
+        lo = a.cell_start[id0];
+        len = a.cell_start[id0 + nc] - lo;
+      }
+    }
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(DB_FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
+    const uint32_t excl = incl - len;
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      // column of candidate t: the last lane whose exclusive start is <= t
+      int k = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t e = __shfl_sync(DB_FULL, excl, k + step);
+        if (e <= t) k += step;
+      }
+      const uint32_t u = __shfl_sync(DB_FULL, lo, k) + t - __shfl_sync(DB_FULL, excl, k);
+      if (t >= total || a.core_s[u]) continue;
       int32_t p[D];
       load_pt<D>(a.Ps, u, p);
       bool hit = false;
@@ -590,8 +614,8 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
       uint32_t* L = a.tmp_lab + (size_t)i * SP_MAXL;
       bool placed = false;
 #pragma unroll
-      for (int k = 0; k < SP_MAXL; ++k) {
-        const uint32_t old = atomicCAS(L + k, MISS, lab);
+      for (int s = 0; s < SP_MAXL; ++s) {
+        const uint32_t old = atomicCAS(L + s, MISS, lab);
         if (old == MISS || old == lab) { placed = true; break; }
       }
       if (!placed) {  // overflow: enumerate later from the sorted position
@@ -602,9 +626,6 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
   }
 }
 
-// Thread per point in INPUT order (coalesced): the number of labels in its
-// set (core points: none), or, for an overflowed set, the count of the
-// storage-free ascending enumeration from its sorted position.
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
@@ -934,7 +955,7 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
-    sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * a.ncols, 256, c.sms * 32), 256, 0, c.st>>>(a);
+    sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * 32, 256, c.sms * 16), 256, 0, c.st>>>(a);
     c.launched();
     sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
     c.launched();
