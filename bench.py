@@ -308,16 +308,17 @@ def main():
                 continue
             ach = work_tests[name] / (ms / 1e3) / 1e12
             tp = INT_TESTS_PEAK / 1e12
-            rooflines.append({"stage": f"a6 MarkCore ({name})", "bound": "alu", "kernel": "sp_core_kernel",
+            kname = "sp_core_brick_kernel" if stats[i].get("brick") else "sp_core_kernel"
+            rooflines.append({"stage": f"a6 MarkCore ({name})", "bound": "alu", "kernel": kname,
                               "achieved": ach, "peak": tp, "unit": "T distance tests/s", "frac": ach / tp,
-                              "traffic": traffic.get("sp_core_kernel"),
+                              "traffic": traffic.get(kname),
                               "traffic_note": "DRAM bytes per launch, ncu --set full (cold L2)",
                               "peak_kind": "derived (DESIGN.md §8): int32 issue rate / 10 SASS per 3D test",
                               "launch_ms": ms,
                               "ms_share": ms * args.steps / max(1e-9, sum(stage_tot.values())),
                               "tests_per_launch": work_tests[name]})
     # the headline is the dominant single KERNEL (the sparse MarkCore's
-    # sp_core_kernel, one launch per c5 run, the longest kernel of the step);
+    # brick kernel, one launch per c5 run, the longest kernel of the step);
     # the grouping stage (several kernels per run) is reported beside it
     kern = [r for r in rooflines if r["bound"] == "alu"]
     roofline = max(kern or rooflines, key=lambda r: r["ms_share"]) if rooflines else None
