@@ -213,7 +213,14 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   const int32_t* dpts = pts;
   if (!dev_io) {
     int32_t* p = c.alloc<int32_t>((size_t)n * d);
+    // Concurrent host-path calls copy their inputs one at a time: the copy
+    // engine would interleave them, so every call's input would arrive late
+    // and all the calls would compute at the end together. In turn, each
+    // call computes while the next one's input is in flight.
+    static std::mutex h2d_mu;
+    std::lock_guard<std::mutex> lk(h2d_mu);
     DB_CUDA(cudaMemcpyAsync(p, pts, sizeof(int32_t) * (size_t)n * d, cudaMemcpyHostToDevice, st));
+    DB_CUDA(cudaStreamSynchronize(st));
     dpts = p;
   }
   int32_t* lohi_d = c.alloc<int32_t>(17);
