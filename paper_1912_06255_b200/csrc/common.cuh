@@ -327,6 +327,35 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// One-dimensional TMA bulk copy global -> shared (cp.async.bulk, SASS
+// UBLKCP) completing on an mbarrier: one elected thread moves a whole
+// contiguous chunk, so a block's input arrives with no per-thread load
+// latency chains. dst, src and bytes must be multiples of 16.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
 // Hash of a packed cell key into an open-addressing table of 16-byte slots.
 // Keys that differ only in the low 3 bits (consecutive cells along the last
 // axis) land in the same 8-slot (128-byte) group, so stencil probes of

@@ -518,6 +518,12 @@ constexpr uint32_t BK_TARGET = 16384;  // points per bucket aimed at
 constexpr int BK_MAXWS = 19;           // lin - bucket start < 2^24
 constexpr int64_t LAT_MAX_N = 1 << 25;  // (the documented limit of the lattice sort)
 
+constexpr int BK_N = BK_THREADS * BK_ITEMS;  // points per 3a block
+
+// 3a. Shared memory (dynamic): the block's points (bulk copy) and, reusing the
+// space once they are in registers, its records ordered by bucket — so the
+// write-out is coalesced: consecutive threads write consecutive positions of
+// one bucket's run, whole sectors at a time — then hist / gbase [nbk].
 template <int DD>
 __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t* __restrict__ pts, uint32_t n,
                                                                   LatArgs L, const uint8_t* __restrict__ slot,
@@ -525,10 +531,26 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
                                                                   uint32_t nbk, uint32_t* __restrict__ bcur,
                                                                   uint4* __restrict__ rec,
                                                                   uint32_t* __restrict__ reci) {
-  __shared__ uint32_t hist[BK_MAXB];
+  extern __shared__ __align__(16) uint8_t st_raw[];
+  int32_t* s_pts = reinterpret_cast<int32_t*>(st_raw);             // [BK_N * DD], then:
+  uint4* srec = reinterpret_cast<uint4*>(st_raw);                  // [BK_N] records by bucket
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(st_raw + BK_N * 16); // [BK_N] input index
+  uint32_t* spos = sidx + BK_N;                                    // [BK_N] staging position
+  uint32_t* hist = spos + BK_N;                                    // [nbk] count, then local base
+  uint32_t* gbase = hist + nbk;                                    // [nbk] staging base
+  __shared__ uint64_t bar;
+  __shared__ uint32_t s_scan[33];
+  const uint32_t i0 = blockIdx.x * BK_N;
+  // a full chunk at a 16-byte aligned address comes in with one bulk copy
+  const bool bulk = i0 + BK_N <= n && (((uintptr_t)(pts + (uint64_t)i0 * DD)) & 15) == 0;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    bulk_load(s_pts, pts + (uint64_t)i0 * DD, BK_N * DD * 4, &bar);
+  }
   for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS) hist[b] = 0;
   __syncthreads();
-  const uint32_t i0 = blockIdx.x * (BK_THREADS * BK_ITEMS);
+  if (bulk) mbar_wait(&bar, 0);
   uint32_t lr[BK_ITEMS], key[BK_ITEMS], bk[BK_ITEMS];
   int32_t x[BK_ITEMS][3];
 #pragma unroll
@@ -537,7 +559,15 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
     bk[t] = 0xffffffffu;
     if (i < n) {
       int32_t xx[DD];
-      const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, xx);
+      const int32_t* src = bulk ? s_pts + (uint64_t)(t * BK_THREADS + threadIdx.x) * DD : pts + (uint64_t)i * DD;
+      uint64_t lin = 0;
+#pragma unroll
+      for (int k = 0; k < DD; ++k) {
+        xx[k] = src[k];
+        const uint32_t off = (uint32_t)xx[k] - (uint32_t)L.g.lo[k];
+        const uint32_t ck = L.magic ? (uint32_t)__umul64hi((uint64_t)off, L.magic) : off;
+        lin += (uint64_t)(ck + L.g.R) * L.stride[k];
+      }
 #pragma unroll
       for (int k = 0; k < 3; ++k) x[t][k] = k < DD ? xx[k] : 0;
       bk[t] = (uint32_t)(lin >> (5 + ws));
@@ -547,17 +577,37 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
 #pragma unroll
   for (int t = 0; t < BK_ITEMS; ++t)
     if (bk[t] != 0xffffffffu) lr[t] = atomicAdd(hist + bk[t], 1u);
-  __syncthreads();
-  // reserve each touched bucket's room: hist[b] becomes the staging position
+  __syncthreads();  // (the points are in registers from here on)
+  // reserve each touched bucket's run (one atomic per block and bucket)
   for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS)
-    if (hist[b]) hist[b] = __ldg(ppre + ((uint64_t)b << ws)) + atomicAdd(bcur + b, hist[b]);
+    if (hist[b]) gbase[b] = __ldg(ppre + ((uint64_t)b << ws)) + atomicAdd(bcur + b, hist[b]);
+  // local bases: exclusive scan of the counts, a run of buckets per thread
+  const uint32_t per = (nbk + BK_THREADS - 1) / BK_THREADS, b0 = threadIdx.x * per;
+  uint32_t sum = 0;
+  for (uint32_t q = 0; q < per; ++q)
+    if (b0 + q < nbk) sum += hist[b0 + q];
+  uint32_t tot;
+  uint32_t ex = block_exclusive_scan<uint32_t>(sum, s_scan, &tot);  // (synchronises: all reads done)
+  for (uint32_t q = 0; q < per; ++q)
+    if (b0 + q < nbk) {
+      const uint32_t v = hist[b0 + q];
+      hist[b0 + q] = ex;
+      ex += v;
+    }
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < BK_ITEMS; ++t) {
     if (bk[t] == 0xffffffffu) continue;
-    const uint32_t o = hist[bk[t]] + lr[t];
-    rec[o] = make_uint4(key[t], (uint32_t)x[t][0], (uint32_t)x[t][1], (uint32_t)x[t][2]);
-    reci[o] = i0 + t * BK_THREADS + threadIdx.x;
+    const uint32_t j = hist[bk[t]] + lr[t];
+    srec[j] = make_uint4(key[t], (uint32_t)x[t][0], (uint32_t)x[t][1], (uint32_t)x[t][2]);
+    sidx[j] = i0 + t * BK_THREADS + threadIdx.x;
+    spos[j] = gbase[bk[t]] + lr[t];
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < tot; j += BK_THREADS) {
+    const uint32_t o = spos[j];
+    rec[o] = srec[j];
+    reci[o] = sidx[j];
   }
 }
 
@@ -683,7 +733,9 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
   const unsigned sgrid = (unsigned)((n + BK_THREADS * BK_ITEMS - 1) / (BK_THREADS * BK_ITEMS));
   by_d([&](auto Dd, auto Dp) {
     constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
-    lat_stage_kernel<DD><<<sgrid, BK_THREADS, 0, c.st>>>(pts, (uint32_t)n, L, slot, ppre, ws, nbk, bcur, rec, reci);
+    const int ssm = BK_N * 24 + 2 * 4 * (int)nbk;
+    DB_CUDA(cudaFuncSetAttribute(lat_stage_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    lat_stage_kernel<DD><<<sgrid, BK_THREADS, ssm, c.st>>>(pts, (uint32_t)n, L, slot, ppre, ws, nbk, bcur, rec, reci);
     c.launched();
     lat_chunks_kernel<<<(nbk + 255) / 256, 256, 0, c.st>>>(ppre, ws, L.words, nbk, nchunks, chunk_bucket);
     c.launched();
