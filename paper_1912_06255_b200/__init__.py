@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = ["dbscan", "Result", "lib_path", "load", "F_DEVICE_IO", "F_TIMING", "F_CALLER_OUT",
            "F_FORCE_STENCIL", "F_FORCE_TREE", "F_FORCE_WIDE", "F_NO_WAVES", "F_NO_SPARSE",
-           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "F_COUNT_WORK", "F_QUADTREE", "F_NO_BRICK", "STAGES",
+           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "F_COUNT_WORK", "F_QUADTREE", "F_NO_BRICK", "STAGES", "release_workspace",
            "STATS",
            "DBSCANError"]
 
@@ -94,6 +94,8 @@ def load():
         lib.dbscan_stage_name.argtypes = [C.c_int]
         lib.dbscan_stage_name.restype = C.c_char_p
         lib.dbscan_version.restype = C.c_int
+        lib.dbscan_release_workspace.argtypes = []
+        lib.dbscan_release_workspace.restype = None
         _lib = lib
     return _lib
 
@@ -125,6 +127,11 @@ class _DeviceBuffer:
         if _lib is not None and self._res is not None:
             _lib.dbscan_result_free(C.byref(self._res))
             self._res = None
+
+
+def release_workspace() -> None:
+    """Free the calling thread's device workspace (dbscan_release_workspace)."""
+    load().dbscan_release_workspace()
 
 
 def _finish(res: _Result, flags: int) -> dict:

@@ -5,6 +5,7 @@
 // Every step runs in this library's kernels on the caller's stream.
 #include <mutex>
 #include <cstdlib>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
@@ -76,17 +77,10 @@ static void init_device_once(int dev, int* sms) {
 struct Timer {
   bool on;
   cudaStream_t st;
-  cudaEvent_t ev[DBSCAN_NSTAGES + 1] = {};
+  cudaEvent_t* ev = nullptr;  // DBSCAN_NSTAGES + 1 events of the thread's cache
   int mark[DBSCAN_NSTAGES + 1];
   int n = 0;
-  Timer(bool on_, cudaStream_t s) : on(on_), st(s) {
-    if (on)
-      for (auto& e : ev) DB_CUDA(cudaEventCreate(&e));
-  }
-  ~Timer() {
-    if (on)
-      for (auto& e : ev) cudaEventDestroy(e);
-  }
+  Timer(bool on_, cudaStream_t s, cudaEvent_t* evs) : on(on_), st(s), ev(evs) {}
   void stage(int s) {  // begin stage s (ends the previous one)
     if (!on) return;
     DB_CUDA(cudaEventRecord(ev[n], st));
@@ -116,6 +110,94 @@ static cudaStream_t side_stream(int dev) {
   return s[dev];
 }
 
+// Per-thread workspaces, one per device (Ctx::alloc). Calls are blocking, so
+// a thread's next call starts only after its previous one finished with it.
+struct ArenaSet {
+  Arena a[64];
+  ~ArenaSet() {
+    for (auto& x : a)
+      if (x.base) (void)cudaFree(x.base);  // (may fail after CUDA teardown at exit)
+  }
+};
+static thread_local ArenaSet g_arenas;
+
+Arena* thread_arena(int dev) { return dev >= 0 && dev < 64 ? &g_arenas.a[dev] : nullptr; }
+
+static thread_local struct PinnedHolder {
+  Arena a;
+  ~PinnedHolder() {
+    if (a.base) (void)cudaFreeHost(a.base);
+  }
+} g_pinned;
+
+Arena* thread_pinned() {
+  if (!g_pinned.a.base) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, (size_t)1 << 20) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    g_pinned.a.base = static_cast<char*>(p);
+    g_pinned.a.cap = (size_t)1 << 20;
+  }
+  return &g_pinned.a;
+}
+
+void arena_grow(Arena& a, size_t need, cudaStream_t st) {
+  if (a.base) DB_CUDA(cudaFreeAsync(a.base, st));
+  a.base = nullptr;
+  a.cap = 0;
+  const size_t cap = (need + need / 8 + ((size_t)1 << 20)) & ~(size_t)255;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, cap, st) != cudaSuccess) {  // keep going without a workspace
+    (void)cudaGetLastError();
+    return;
+  }
+  DB_CUDA(cudaStreamSynchronize(st));
+  a.base = static_cast<char*>(p);
+  a.cap = cap;
+}
+
+static void arena_release_all() {
+  for (auto& x : g_arenas.a)
+    if (x.base) {
+      (void)cudaFree(x.base);
+      x.base = nullptr;
+      x.cap = 0;
+    }
+}
+
+// Events of a call (4, and the stage timer's), created once per thread.
+struct EventCache {
+  int dev = -1;
+  cudaEvent_t plain[4] = {};
+  cudaEvent_t timed[DBSCAN_NSTAGES + 1] = {};
+  bool timed_made = false;
+};
+static thread_local struct EventCacheHolder {
+  EventCache c;
+  ~EventCacheHolder() {
+    for (auto& x : c.plain) if (x) (void)cudaEventDestroy(x);
+    for (auto& x : c.timed) if (x) (void)cudaEventDestroy(x);
+  }
+} g_events_holder;
+
+static EventCache& thread_events(int dev, bool timed) {
+  EventCache& e = g_events_holder.c;
+  if (e.dev != dev) {  // (first call, or the thread moved to another device)
+    for (auto& x : e.plain) if (x) (void)cudaEventDestroy(x);
+    for (auto& x : e.timed) if (x) (void)cudaEventDestroy(x);
+    e = EventCache();
+    for (auto& x : e.plain) DB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    e.dev = dev;
+  }
+  if (timed && !e.timed_made) {
+    for (auto& x : e.timed) DB_CUDA(cudaEventCreate(&x));
+    e.timed_made = true;
+  }
+  return e;
+}
+
 static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
                uint32_t flags, cudaStream_t st, dbscan_result* out, int32_t* uids, int64_t ucap,
                double rho) {
@@ -130,12 +212,16 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   int dev = 0;
   DB_CUDA(cudaGetDevice(&dev));
   init_device_once(dev, &c.sms);
-  Timer tm(flags & DBSCAN_F_TIMING, st);
-  struct Evs {
-    cudaEvent_t e[4] = {};
-    ~Evs() { for (auto x : e) if (x) cudaEventDestroy(x); }
-  } evs;
-  for (auto& x : evs.e) DB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  c.ar = thread_arena(dev);
+  c.pin = thread_pinned();
+  static const bool tracing = getenv("DB_TRACE") != nullptr;
+  c.tracing = tracing;
+  if (tracing) c.mark("start");
+  EventCache& evc = thread_events(dev, flags & DBSCAN_F_TIMING);
+  Timer tm(flags & DBSCAN_F_TIMING, st, evc.timed);
+  struct {
+    cudaEvent_t* e;
+  } evs{evc.plain};
   c.side = side_stream(dev);
   c.fork_ev = evs.e[0];
   c.join_ev = evs.e[1];
@@ -226,8 +312,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   int32_t* lohi_d = c.alloc<int32_t>(17);
   bbox(c, dpts, n, d, g.s, lohi_d);
   int32_t lohi[17];
-  DB_CUDA(cudaMemcpyAsync(lohi, lohi_d, sizeof(lohi), cudaMemcpyDeviceToHost, st));
-  DB_CUDA(cudaStreamSynchronize(st));
+  const int32_t* lohi_h = c.fetch(lohi_d, 17);
+  c.sync();
+  std::memcpy(lohi, lohi_h, sizeof(lohi));
   uint32_t bits = 0;
   for (int k = d - 1; k >= 0; --k) {  // axis 0 most significant
     const uint64_t span = (uint64_t)((int64_t)lohi[8 + k] - (int64_t)lohi[k]);
@@ -397,7 +484,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     if (!dev_io)
       DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost,
                               side));
+    if (c.tracing) c.mark("border nnz known");
     out->border_ids = ids_alloc(nnz);
+    if (c.tracing) c.mark("ids alloc");
     int32_t* ids_d = dev_io ? out->border_ids : c.alloc<int32_t>(nnz);
     if (nnz > 0) {
       if (sparse) sparse_border_fill(c, g, wide, off_d, ids_d, &so);
@@ -422,12 +511,24 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   uint32_t h32[4];
   unsigned long long h64[3];
   unsigned long long hw[4] = {0, 0, 0, 0};
-  if (c.work) DB_CUDA(cudaMemcpyAsync(hw, c.work, sizeof(hw), cudaMemcpyDeviceToHost, st));
-  DB_CUDA(cudaMemcpyAsync(h32, cnt32, sizeof(h32), cudaMemcpyDeviceToHost, st));
-  DB_CUDA(cudaMemcpyAsync(h64, cnt64, sizeof(h64), cudaMemcpyDeviceToHost, st));
+  const unsigned long long* hw_h = c.work ? c.fetch(c.work, 4) : nullptr;
+  const uint32_t* h32_h = c.fetch(cnt32, 4);
+  const unsigned long long* h64_h = c.fetch(cnt64, 3);
+  if (c.tracing) c.mark("timer finish");
   tm.finish(out->stage_ms);
+  if (c.tracing) c.mark("timer done");
   c.free_all();
+  if (c.tracing) c.mark("final sync");
   DB_CUDA(cudaStreamSynchronize(st));
+  c.finish();
+  std::memcpy(h32, h32_h, sizeof(h32));
+  std::memcpy(h64, h64_h, sizeof(h64));
+  if (hw_h) std::memcpy(hw, hw_h, sizeof(hw));
+  if (c.tracing) {
+    c.mark("end");
+    const double t0 = c.trace.front().second;
+    for (auto& e : c.trace) fprintf(stderr, "  %9.1f us  %s %d\n", e.second - t0, e.first.first, e.first.second);
+  }
 
   out->nnz = nnz;
   out->n_core = h32[3];
@@ -541,6 +642,8 @@ void dbscan_result_free(dbscan_result* r) {
   if (!r) return;
   free_priv(r);
 }
+
+void dbscan_release_workspace(void) { arena_release_all(); }
 
 const char* dbscan_error_string(int code) {
   static thread_local std::string s;

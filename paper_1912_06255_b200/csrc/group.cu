@@ -289,8 +289,10 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
                                                                                                ctr + 1);
   c.launched();
   uint32_t h2[2];
-  DB_CUDA(cudaMemcpyAsync(h2, ctr, sizeof(h2), cudaMemcpyDeviceToHost, c.st));
-  DB_CUDA(cudaStreamSynchronize(c.st));
+  const uint32_t* h2_h = c.fetch(ctr, 2);
+  c.sync();
+  h2[0] = h2_h[0];
+  h2[1] = h2_h[1];
   if (h2[0]) return false;  // too many cells for the table: radix path
   const uint32_t m = h2[1];
   // Cell ids in key order are needed by the sparse path's rank directory
@@ -701,8 +703,10 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
   lat_words_kernel<<<wgrid, LAT_THREADS, 0, c.st>>>(cnt8, L, bm, wcells, wpts, flags + 1);
   c.launched();
   uint32_t h[2];
-  DB_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, c.st));
-  DB_CUDA(cudaStreamSynchronize(c.st));
+  const uint32_t* h_h = c.fetch(flags, 2);
+  c.sync();
+  h[0] = h_h[0];
+  h[1] = h_h[1];
   if (h[0]) return LAT_FALLBACK;
   // Alg 2's count is at most (stencil cells) x (largest cell): below minPts,
   // no point is core and nothing needs to be grouped (reading 13)

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -20,6 +22,15 @@ struct Error : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 #define DB_CUDA(call) ::db::cuda_check((call), #call)
+
+// Per-thread device workspace (see Ctx::alloc).
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+};
+Arena* thread_arena(int dev);                         // the calling thread's workspace on dev
+Arena* thread_pinned();                               // the calling thread's pinned host staging
+void arena_grow(Arena& a, size_t need, cudaStream_t st);  // (after the stream is idle)
 
 // Per-call context: stream, stream-ordered temporaries, launch counter.
 struct Ctx {
@@ -43,18 +54,71 @@ struct Ctx {
   }
   void stage(int s) {
     if (stage_fn) stage_fn(stage_obj, s);
+    if (tracing) mark("stage", s);
+  }
+  // host-side trace (DB_TRACE=1 in the environment): what the host thread
+  // does when, to find where the GPU waits for it
+  bool tracing = false;
+  std::vector<std::pair<std::pair<const char*, int>, double>> trace;
+  void mark(const char* what, int v = -1) {
+    trace.push_back({{what, v}, std::chrono::duration<double, std::micro>(
+                                    std::chrono::steady_clock::now().time_since_epoch()).count()});
   }
   std::vector<void*> temps;
   int64_t launches = 0;
   int sms = 148;
   uint32_t* dense_dir = nullptr;  // dense cell directory, when built
   uint64_t dense_lat[3] = {0, 0, 0};
+  // Temporaries come out of the calling thread's workspace (one device
+  // allocation kept across its calls: no allocator call per temporary); past
+  // its end they fall back to stream-ordered allocations and the workspace
+  // is regrown once the call has finished (finish()).
+  Arena* ar = nullptr;
+  size_t used = 0;
+  bool finished = false;
+  // Small host<->device transfers go through pinned host staging (per thread):
+  // from pageable memory each one is a synchronous staged copy of ~10-20 us.
+  Arena* pin = nullptr;
+  size_t pin_used = 0;
+  void* pin_take(size_t bytes) {
+    bytes = (bytes + 15) & ~(size_t)15;
+    if (!pin || pin_used + bytes > pin->cap) return nullptr;
+    void* p = pin->base + pin_used;
+    pin_used += bytes;
+    return p;
+  }
+  template <typename T>
+  void upload(T* dst, const T* src, size_t count) {
+    const size_t bytes = sizeof(T) * count;
+    void* h = pin_take(bytes);
+    if (h) std::memcpy(h, src, bytes);
+    DB_CUDA(cudaMemcpyAsync(dst, h ? h : (const void*)src, bytes, cudaMemcpyHostToDevice, st));
+  }
+  // device -> host, complete after the next sync(): returns the host copy
+  template <typename T>
+  const T* fetch(const T* dsrc, size_t count) {
+    T* h = static_cast<T*>(pin_take(sizeof(T) * count));
+    if (!h) {
+      fetch_spill.emplace_back(sizeof(T) * count);
+      h = reinterpret_cast<T*>(fetch_spill.back().data());
+    }
+    DB_CUDA(cudaMemcpyAsync(h, dsrc, sizeof(T) * count, cudaMemcpyDeviceToHost, st));
+    return h;
+  }
+  std::vector<std::vector<char>> fetch_spill;
 
   template <typename T>
   T* alloc(size_t count) {
-    void* p = nullptr;
     size_t bytes = count * sizeof(T);
-    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (bytes == 0) bytes = 256;
+    if (ar && used + bytes <= ar->cap) {
+      void* p = ar->base + used;
+      used += bytes;
+      return static_cast<T*>(p);
+    }
+    used += bytes;  // (the size the workspace should have had)
+    void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, bytes, st);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
@@ -66,6 +130,7 @@ struct Ctx {
   void zero(void* p, size_t bytes) { DB_CUDA(cudaMemsetAsync(p, 0, bytes, st)); }
   void launched() {
     ++launches;
+    if (tracing) mark("launch", (int)launches);
 #ifdef DB_DEBUG_SYNC
     DB_CUDA(cudaStreamSynchronize(st));
 #endif
@@ -75,14 +140,29 @@ struct Ctx {
     for (void* p : temps) cudaFreeAsync(p, st);
     temps.clear();
   }
-  ~Ctx() { free_all(); }  // error paths (the success path frees explicitly)
+  // after the call's final synchronisation: regrow an undersized workspace
+  void finish() {
+    finished = true;
+    if (ar && used > ar->cap) arena_grow(*ar, used, st);
+  }
+  ~Ctx() {  // error paths: the stream may still use the workspace; wait for it
+    if (!finished && st) (void)cudaStreamSynchronize(st);
+    (void)cudaGetLastError();
+    free_all();
+  }
   // Read a small device value (synchronises the stream).
+  void sync() {
+    if (tracing) mark("sync");
+    DB_CUDA(cudaStreamSynchronize(st));
+    if (tracing) mark("sync done");
+  }
   template <typename T>
   T read(const T* dptr) {
-    T v;
-    DB_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, st));
+    if (tracing) mark("read");
+    const T* h = fetch(dptr, 1);
     DB_CUDA(cudaStreamSynchronize(st));
-    return v;
+    if (tracing) mark("read done");
+    return *h;
   }
 };
 

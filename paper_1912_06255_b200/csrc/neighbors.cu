@@ -227,7 +227,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
     o.delta = dl;
   }
   StencilOff* doffs = c.alloc<StencilOff>(so.size());
-  DB_CUDA(cudaMemcpyAsync(doffs, so.data(), sizeof(StencilOff) * so.size(), cudaMemcpyHostToDevice, c.st));
+  c.upload(doffs, so.data(), so.size());
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
   uint32_t* ub = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
@@ -409,7 +409,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   }
   gt[gmax] = g.eps2 + 1;
   unsigned long long* dgt = c.alloc<unsigned long long>(gt.size());
-  DB_CUDA(cudaMemcpyAsync(dgt, gt.data(), sizeof(unsigned long long) * gt.size(), cudaMemcpyHostToDevice, c.st));
+  c.upload(dgt, gt.data(), gt.size());
   uint32_t* cc = c.alloc<uint32_t>((size_t)ncells * 8);
   decode_cells_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, cc);
   c.launched();
@@ -429,7 +429,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   } else {
     // one bucket: every cell (cc[0] is then clamped by maxb = 0 -> buckets 0..0)
     const uint32_t h2[2] = {0u, ncells};
-    DB_CUDA(cudaMemcpyAsync(bstart, h2, sizeof(h2), cudaMemcpyHostToDevice, c.st));
+    c.upload(bstart, h2, 2);
     iota_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(order, ncells);
     c.launched();
   }

@@ -229,9 +229,11 @@ void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
   c.launched();
   exclusive_scan_u32_u64(c, nl, leaf_off, nc);
   uint64_t tot[2];
-  DB_CUDA(cudaMemcpyAsync(&tot[0], node_off + nc, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.st));
-  DB_CUDA(cudaMemcpyAsync(&tot[1], leaf_off + nc, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.st));
-  DB_CUDA(cudaStreamSynchronize(c.st));
+  const uint64_t* t0 = c.fetch(node_off + nc, 1);
+  const uint64_t* t1 = c.fetch(leaf_off + nc, 1);
+  c.sync();
+  tot[0] = *t0;
+  tot[1] = *t1;
   qt->node_off = node_off;
   qt->nodes = tot[0];
   if (tot[0] == 0) { qt->box = nullptr; qt->cnt = nullptr; return; }

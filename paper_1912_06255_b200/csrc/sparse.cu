@@ -839,8 +839,8 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
     cm.push_back(0);
     long long* dco = c.alloc<long long>(co.size());
     uint32_t* dcm = c.alloc<uint32_t>(cm.size());
-    DB_CUDA(cudaMemcpyAsync(dco, co.data(), sizeof(long long) * co.size(), cudaMemcpyHostToDevice, c.st));
-    DB_CUDA(cudaMemcpyAsync(dcm, cm.data(), sizeof(uint32_t) * cm.size(), cudaMemcpyHostToDevice, c.st));
+    c.upload(dco, co.data(), co.size());
+    c.upload(dcm, cm.data(), cm.size());
     *off = dco;
     *mask = dcm;
   };
@@ -861,7 +861,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
     std::vector<int8_t> geom;
     stencil_columns(g, a.stride, &back, &geom);
     int8_t* dgeo = c.alloc<int8_t>(geom.size());
-    DB_CUDA(cudaMemcpyAsync(dgeo, geom.data(), geom.size(), cudaMemcpyHostToDevice, c.st));
+    c.upload(dgeo, geom.data(), geom.size());
     const uint32_t nb[3] = {(g.maxc[0] + BRK) / BRK, (g.maxc[1] + BRK) / BRK, (g.maxc[2] + BRK) / BRK};
     const uint64_t nbricks = (uint64_t)nb[0] * nb[1] * nb[2];
     if (nbricks >= (1ull << 31)) throw Error(-4, "sparse path: brick grid too large");

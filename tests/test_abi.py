@@ -27,8 +27,8 @@ def declared_functions():
 
 
 def test_header_declares_entry_points():
-    assert declared_functions() == ["dbscan", "dbscan_approx", "dbscan_error_string", "dbscan_result_free",
-                                    "dbscan_stage_name", "dbscan_version"]
+    assert declared_functions() == ["dbscan", "dbscan_approx", "dbscan_error_string", "dbscan_release_workspace",
+                                    "dbscan_result_free", "dbscan_stage_name", "dbscan_version"]
 
 
 def test_exports(lib):
