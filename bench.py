@@ -383,9 +383,13 @@ def main():
                 raise errs[0]
             h2d, d2h = sum(b_in), sum(b_out)
             return dt
-        for _ in range(1):
-            e2e_step()
+        for _ in range(max(1, args.warmup)):
+            w = e2e_step()
+            if os.environ.get("DB_E2E_DEBUG"):
+                print("e2e warm-up step ms:", round(w * 1e3, 2), file=sys.stderr)
         ts = [e2e_step() for _ in range(max(1, min(args.steps, 3)))]
+        if os.environ.get("DB_E2E_DEBUG"):
+            print("e2e step seconds:", [round(t * 1e3, 2) for t in ts], file=sys.stderr)
         e2e = {"value": npts_step * len(ts) / sum(ts), "unit": "points/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
                "timer": f"host wall clock around the step: {E2E_THREADS} host threads with one CUDA stream each take the runs from a shared queue and "

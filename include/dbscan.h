@@ -166,11 +166,12 @@ int dbscan_approx(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t
  * them. Safe on a zeroed result. */
 void dbscan_result_free(dbscan_result *r);
 
-/* Device temporaries of a call come from a workspace owned by the calling thread
- * (one allocation per device, kept across the thread's calls so a call makes no
- * allocator call per temporary; grown after a call that needed more; released at
- * thread exit). This frees the calling thread's workspaces now; the next call
- * allocates again. Call it only with no dbscan() call of this thread in flight. */
+/* A call's temporaries (device memory, 1 MB of pinned host memory, events, a
+ * second stream) come from a workspace taken from a process-wide pool and
+ * returned when the call ends, so calls make no allocator call per temporary and
+ * concurrent calls (any threads) use different workspaces. A workspace's device
+ * memory grows after a call that needed more and is kept. This frees the idle
+ * workspaces (those of calls in flight are kept); later calls allocate again. */
 void dbscan_release_workspace(void);
 
 /* Static description of a code, with the detail of this thread's last error. */

@@ -3,6 +3,7 @@
 //   Cells (a1-a4) -> NeighborCells (a5) -> MarkCore (a6, a7)
 //   -> ClusterCore (a8) -> labels (a9) -> ClusterBorder (a10).
 // Every step runs in this library's kernels on the caller's stream.
+#include <algorithm>
 #include <mutex>
 #include <cstdlib>
 #include <cstdio>
@@ -101,53 +102,118 @@ struct Timer {
   }
 };
 
-// Host-path copies of finished outputs run on a side stream (one per thread
-// and device), overlapping the remaining stages on the call's stream.
-static cudaStream_t side_stream(int dev) {
-  static thread_local cudaStream_t s[64] = {};
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!s[dev]) DB_CUDA(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking));
-  return s[dev];
+// Workspaces: what a call needs beyond its inputs and outputs, kept across
+// calls in a process-wide pool (per device) so that a call makes no allocator
+// call per temporary and creates no events or streams — whichever thread
+// makes it (threads may come and go). A call takes an idle workspace (or a new
+// one) and returns it when it has finished with it (its stream is idle).
+//  * dev: device memory for the temporaries (Ctx::alloc), regrown after a
+//    call that needed more;
+//  * pin: 1 MB of pinned host memory for small transfers (Ctx::upload, fetch);
+//  * events: the call's 4 events and the stage timer's;
+//  * side: a second stream (host-path copies of finished outputs overlap the
+//    remaining stages on the call's stream).
+struct Workspace {
+  int dev = -1;
+  Arena mem, pin;
+  cudaEvent_t plain[4] = {};
+  cudaEvent_t timed[DBSCAN_NSTAGES + 1] = {};
+  bool timed_made = false;
+  cudaStream_t side = nullptr;
+};
+
+static std::mutex g_ws_mu;
+static std::vector<Workspace*>* g_ws_idle = new std::vector<Workspace*>();  // (never destroyed: exit order)
+
+static size_t g_ws_hwm[64] = {};  // largest workspace memory so far, per device (under g_ws_mu)
+
+static Workspace* ws_acquire(int dev, bool timed, cudaStream_t st) {
+  Workspace* w = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (size_t i = 0; i < g_ws_idle->size(); ++i)
+      if ((*g_ws_idle)[i]->dev == dev) {
+        w = (*g_ws_idle)[i];
+        (*g_ws_idle)[i] = g_ws_idle->back();
+        g_ws_idle->pop_back();
+        break;
+      }
+  }
+  if (!w) {
+    static const bool trace = getenv("DB_TRACE_WS") != nullptr;
+    if (trace) fprintf(stderr, "workspace: new\n");
+    w = new Workspace();
+    w->dev = dev;
+    // a new workspace (a call concurrent with others) starts at the size the
+    // others have grown to (stream-ordered: usable by this call's kernels)
+    size_t hwm = 0;
+    {
+      std::lock_guard<std::mutex> lk(g_ws_mu);
+      hwm = dev >= 0 && dev < 64 ? g_ws_hwm[dev] : 0;
+    }
+    void* m = nullptr;
+    if (hwm && cudaMallocAsync(&m, hwm, st) == cudaSuccess) {
+      w->mem.base = static_cast<char*>(m);
+      w->mem.cap = hwm;
+    } else {
+      (void)cudaGetLastError();
+    }
+    for (auto& x : w->plain) DB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    DB_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
+    void* p = nullptr;
+    if (cudaMallocHost(&p, (size_t)1 << 20) == cudaSuccess) {
+      w->pin.base = static_cast<char*>(p);
+      w->pin.cap = (size_t)1 << 20;
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
+  else {  // an idle workspace smaller than another one has grown to: catch up (stream-ordered)
+    size_t hwm = 0;
+    {
+      std::lock_guard<std::mutex> lk(g_ws_mu);
+      hwm = dev >= 0 && dev < 64 ? g_ws_hwm[dev] : 0;
+    }
+    void* m = nullptr;
+    if (w->mem.cap < hwm && cudaMallocAsync(&m, hwm, st) == cudaSuccess) {
+      if (w->mem.base) (void)cudaFreeAsync(w->mem.base, st);
+      w->mem.base = static_cast<char*>(m);
+      w->mem.cap = hwm;
+    }
+    (void)cudaGetLastError();
+  }
+  if (timed && !w->timed_made) {
+    for (auto& x : w->timed) DB_CUDA(cudaEventCreate(&x));
+    w->timed_made = true;
+  }
+  return w;
 }
 
-// Per-thread workspaces, one per device (Ctx::alloc). Calls are blocking, so
-// a thread's next call starts only after its previous one finished with it.
-struct ArenaSet {
-  Arena a[64];
-  ~ArenaSet() {
-    for (auto& x : a)
-      if (x.base) (void)cudaFree(x.base);  // (may fail after CUDA teardown at exit)
+static void ws_release(Workspace* w) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  g_ws_idle->push_back(w);
+}
+
+// returns w to the pool when the call ends (Ctx has already waited for its stream)
+struct WsGuard {
+  Workspace* w;
+  ~WsGuard() {
+    if (w) ws_release(w);
   }
 };
-static thread_local ArenaSet g_arenas;
-
-Arena* thread_arena(int dev) { return dev >= 0 && dev < 64 ? &g_arenas.a[dev] : nullptr; }
-
-static thread_local struct PinnedHolder {
-  Arena a;
-  ~PinnedHolder() {
-    if (a.base) (void)cudaFreeHost(a.base);
-  }
-} g_pinned;
-
-Arena* thread_pinned() {
-  if (!g_pinned.a.base) {
-    void* p = nullptr;
-    if (cudaMallocHost(&p, (size_t)1 << 20) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return nullptr;
-    }
-    g_pinned.a.base = static_cast<char*>(p);
-    g_pinned.a.cap = (size_t)1 << 20;
-  }
-  return &g_pinned.a;
-}
 
 void arena_grow(Arena& a, size_t need, cudaStream_t st) {
+  static const bool trace = getenv("DB_TRACE_WS") != nullptr;
+  if (trace) fprintf(stderr, "workspace %p: grow %zu -> need %zu\n", (void*)&a, a.cap, need);
   if (a.base) DB_CUDA(cudaFreeAsync(a.base, st));
   a.base = nullptr;
   a.cap = 0;
-  const size_t cap = (need + need / 8 + ((size_t)1 << 20)) & ~(size_t)255;
+  size_t cap = (need + need / 8 + ((size_t)1 << 20)) & ~(size_t)255;
+  int dv = 0;
+  if (cudaGetDevice(&dv) == cudaSuccess && dv >= 0 && dv < 64) {  // at least what the others have
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    cap = std::max(cap, g_ws_hwm[dv]);
+  }
   void* p = nullptr;
   if (cudaMallocAsync(&p, cap, st) != cudaSuccess) {  // keep going without a workspace
     (void)cudaGetLastError();
@@ -156,46 +222,28 @@ void arena_grow(Arena& a, size_t need, cudaStream_t st) {
   DB_CUDA(cudaStreamSynchronize(st));
   a.base = static_cast<char*>(p);
   a.cap = cap;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    g_ws_hwm[dev] = std::max(g_ws_hwm[dev], cap);
+  }
 }
 
-static void arena_release_all() {
-  for (auto& x : g_arenas.a)
-    if (x.base) {
-      (void)cudaFree(x.base);
-      x.base = nullptr;
-      x.cap = 0;
-    }
-}
-
-// Events of a call (4, and the stage timer's), created once per thread.
-struct EventCache {
-  int dev = -1;
-  cudaEvent_t plain[4] = {};
-  cudaEvent_t timed[DBSCAN_NSTAGES + 1] = {};
-  bool timed_made = false;
-};
-static thread_local struct EventCacheHolder {
-  EventCache c;
-  ~EventCacheHolder() {
-    for (auto& x : c.plain) if (x) (void)cudaEventDestroy(x);
-    for (auto& x : c.timed) if (x) (void)cudaEventDestroy(x);
+// frees the idle workspaces (dbscan_release_workspace)
+static void ws_release_idle() {
+  std::vector<Workspace*> v;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    v.swap(*g_ws_idle);
   }
-} g_events_holder;
-
-static EventCache& thread_events(int dev, bool timed) {
-  EventCache& e = g_events_holder.c;
-  if (e.dev != dev) {  // (first call, or the thread moved to another device)
-    for (auto& x : e.plain) if (x) (void)cudaEventDestroy(x);
-    for (auto& x : e.timed) if (x) (void)cudaEventDestroy(x);
-    e = EventCache();
-    for (auto& x : e.plain) DB_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
-    e.dev = dev;
+  for (Workspace* w : v) {
+    if (w->mem.base) (void)cudaFree(w->mem.base);
+    if (w->pin.base) (void)cudaFreeHost(w->pin.base);
+    for (auto& x : w->plain) if (x) (void)cudaEventDestroy(x);
+    for (auto& x : w->timed) if (x) (void)cudaEventDestroy(x);
+    if (w->side) (void)cudaStreamDestroy(w->side);
+    delete w;
   }
-  if (timed && !e.timed_made) {
-    for (auto& x : e.timed) DB_CUDA(cudaEventCreate(&x));
-    e.timed_made = true;
-  }
-  return e;
 }
 
 static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
@@ -207,22 +255,23 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   priv->dev = dev_io;
   priv->st = st;
   out->priv = priv;
-  Ctx c;
-  c.st = st;
   int dev = 0;
   DB_CUDA(cudaGetDevice(&dev));
+  WsGuard wsg{ws_acquire(dev, flags & DBSCAN_F_TIMING, st)};  // (declared first: released last)
+  Workspace& ws = *wsg.w;
+  Ctx c;
+  c.st = st;
   init_device_once(dev, &c.sms);
-  c.ar = thread_arena(dev);
-  c.pin = thread_pinned();
+  c.ar = &ws.mem;
+  c.pin = ws.pin.base ? &ws.pin : nullptr;
   static const bool tracing = getenv("DB_TRACE") != nullptr;
   c.tracing = tracing;
   if (tracing) c.mark("start");
-  EventCache& evc = thread_events(dev, flags & DBSCAN_F_TIMING);
-  Timer tm(flags & DBSCAN_F_TIMING, st, evc.timed);
+  Timer tm(flags & DBSCAN_F_TIMING, st, ws.timed);
   struct {
     cudaEvent_t* e;
-  } evs{evc.plain};
-  c.side = side_stream(dev);
+  } evs{ws.plain};
+  c.side = ws.side;
   c.fork_ev = evs.e[0];
   c.join_ev = evs.e[1];
   c.stage_fn = [](void* t, int s) { static_cast<Timer*>(t)->stage(s); };
@@ -643,7 +692,7 @@ void dbscan_result_free(dbscan_result* r) {
   free_priv(r);
 }
 
-void dbscan_release_workspace(void) { arena_release_all(); }
+void dbscan_release_workspace(void) { ws_release_idle(); }
 
 const char* dbscan_error_string(int code) {
   static thread_local std::string s;

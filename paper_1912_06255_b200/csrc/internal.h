@@ -23,13 +23,11 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what);
 #define DB_CUDA(call) ::db::cuda_check((call), #call)
 
-// Per-thread device workspace (see Ctx::alloc).
+// A block of device or pinned host memory of a workspace (see Ctx::alloc, dbscan.cu).
 struct Arena {
   char* base = nullptr;
   size_t cap = 0;
 };
-Arena* thread_arena(int dev);                         // the calling thread's workspace on dev
-Arena* thread_pinned();                               // the calling thread's pinned host staging
 void arena_grow(Arena& a, size_t need, cudaStream_t st);  // (after the stream is idle)
 
 // Per-call context: stream, stream-ordered temporaries, launch counter.
@@ -69,14 +67,14 @@ struct Ctx {
   int sms = 148;
   uint32_t* dense_dir = nullptr;  // dense cell directory, when built
   uint64_t dense_lat[3] = {0, 0, 0};
-  // Temporaries come out of the calling thread's workspace (one device
-  // allocation kept across its calls: no allocator call per temporary); past
-  // its end they fall back to stream-ordered allocations and the workspace
-  // is regrown once the call has finished (finish()).
+  // Temporaries come out of the call's workspace (one device allocation kept
+  // across calls: no allocator call per temporary); past its end they fall
+  // back to stream-ordered allocations and the workspace is regrown once the
+  // call has finished (finish()).
   Arena* ar = nullptr;
   size_t used = 0;
   bool finished = false;
-  // Small host<->device transfers go through pinned host staging (per thread):
+  // Small host<->device transfers go through pinned host staging (workspace):
   // from pageable memory each one is a synchronous staged copy of ~10-20 us.
   Arena* pin = nullptr;
   size_t pin_used = 0;
