@@ -371,3 +371,49 @@ def test_concurrent_host_calls(oracle_lib):
     assert not errs, errs
     for k in range(len(cases)):
         assert_same(got[k], want[k], f"case {k}")
+
+
+def test_workspace_pool(oracle_lib):
+    """Pooled workspaces (include/dbscan.h dbscan_release_workspace): calls of
+    growing size (the workspace regrows), short-lived threads calling at once
+    on both paths (each takes its own workspace from the pool, the idle ones
+    catch up in size), an invalid call in between, and a release of the idle
+    workspaces: every result equals the oracle's."""
+    import threading
+    cases = [(datagen.uniform(2_000, 3, 3_000, 91), 300, 4),
+             (datagen.seed_spreader(30_000, 3, 20_000, 92, 0.02, noise_frac=0.03), 200, 15),
+             (datagen.uniform(120_000, 3, 9_000, 93), 300, 10),
+             (datagen.seed_spreader(25_000, 7, 30_000, 94, 0.02), 900, 20)]
+    want = [oracle_lib.o2(p, e, m) for p, e, m in cases]
+    pkg.release_workspace()
+    for (p, e, m), w in zip(cases, want):  # sequential, growing
+        assert_same(np_result(gpu(p, e, m)), w, "sequential")
+    with pytest.raises(pkg.DBSCANError):
+        gpu(cases[0][0], 0, 4)  # eps = 0: rejected before any kernel
+    for rnd in range(3):
+        got, errs = {}, []
+
+        def worker(k, host):
+            try:
+                p, e, m = cases[k]
+                st = torch.cuda.Stream()
+                if host:
+                    r = pkg.dbscan(torch.from_numpy(p).pin_memory(), e, m, stream=st)
+                else:
+                    t = torch.from_numpy(np.ascontiguousarray(p)).cuda()
+                    with torch.cuda.stream(st):
+                        r = pkg.dbscan(t, e, m, stream=st)
+                    st.synchronize()
+                got[(k, host)] = np_result(r)
+            except Exception as ex:  # pragma: no cover
+                errs.append(ex)
+        ths = [threading.Thread(target=worker, args=(k, h)) for k in range(len(cases)) for h in (False, True)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        assert not errs, errs
+        for (k, h), r in got.items():
+            assert_same(r, want[k], f"round {rnd} case {k} host {h}")
+        if rnd == 1:
+            pkg.release_workspace()
