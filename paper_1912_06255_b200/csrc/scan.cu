@@ -89,10 +89,9 @@ static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n, const in
     return;
   }
   const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
-  uint64_t* status = c.alloc<uint64_t>(tiles);
-  uint32_t* ctr = c.alloc<uint32_t>(1);
-  c.zero(status, sizeof(uint64_t) * tiles);
-  c.zero(ctr, sizeof(uint32_t));
+  uint64_t* status = c.alloc<uint64_t>(tiles + 1);  // [tiles]: the tile counter
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(status + tiles);
+  c.zero(status, sizeof(uint64_t) * (tiles + 1));
   scan_kernel<TOut><<<(unsigned)tiles, SC_THREADS, 0, c.st>>>(in, mask, out, n, status, ctr);
   c.launched();
 }
