@@ -5,6 +5,7 @@
 // Every step runs in this library's kernels on the caller's stream.
 #include <algorithm>
 #include <mutex>
+#include <thread>
 #include <cstdlib>
 #include <cstdio>
 #include <cmath>
@@ -244,6 +245,27 @@ static void ws_release_idle() {
     if (w->side) (void)cudaStreamDestroy(w->side);
     delete w;
   }
+}
+
+// Host-path outputs that are constant (no border point: border_off = 0; no
+// core point: every output) are written on the host instead of crossing the
+// host link, by several threads (one thread writes pinned memory at ~10 GB/s,
+// slower than the link; the link is what concurrent calls share).
+static void host_fill(void* dst, int byte, size_t bytes) {
+  const size_t chunk = (size_t)8 << 20;
+  const int nt = (int)std::min<size_t>(8, (bytes + chunk - 1) / chunk);
+  if (nt <= 1) {
+    std::memset(dst, byte, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + nt - 1) / nt;
+  for (int t = 1; t < nt; ++t) {
+    const size_t o = per * t;
+    if (o < bytes) th.emplace_back([=] { std::memset((char*)dst + o, byte, std::min(per, bytes - o)); });
+  }
+  std::memset(dst, byte, std::min(per, bytes));
+  for (auto& x : th) x.join();
 }
 
 static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
@@ -530,7 +552,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     if (sparse) nnz = sparse_border(c, g, cell_label, cluster_d, n, wide, off_d, cnt64 + 1, &so);
     else nnz = border_count(c, g, cv, Ps, sidx, core_cnt, cell_label, cluster_d, n, wide, off_d, cnt64 + 1);
     // (border_count synchronised the stream: border_off is final)
-    if (!dev_io)
+    if (!dev_io && nnz == 0) host_fill(out->border_off, 0, sizeof(int64_t) * (size_t)(n + 1));
+    else if (!dev_io)
       DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost,
                               side));
     if (c.tracing) c.mark("border nnz known");
@@ -546,12 +569,10 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
                               cudaMemcpyDeviceToHost, st));
   }
 
-  if (!dev_io && !side_used) {
-    DB_CUDA(cudaMemcpyAsync(out->core, core_d, (size_t)n, cudaMemcpyDeviceToHost, st));
-    DB_CUDA(cudaMemcpyAsync(out->cluster, cluster_d, sizeof(int32_t) * (size_t)n,
-                            cudaMemcpyDeviceToHost, st));
-    DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1),
-                            cudaMemcpyDeviceToHost, st));
+  if (!dev_io && !side_used) {  // no core point: core 0, cluster -1, border_off 0
+    host_fill(out->core, 0, (size_t)n);
+    host_fill(out->cluster, 0xff, sizeof(int32_t) * (size_t)n);
+    host_fill(out->border_off, 0, sizeof(int64_t) * (size_t)(n + 1));
   }
   if (side_used) {  // the temporaries stay alive until the side copies are done
     DB_CUDA(cudaEventRecord(ev_side, side));
