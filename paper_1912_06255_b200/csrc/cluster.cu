@@ -251,7 +251,14 @@ __global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, Cel
     const uint32_t kg = core_cnt[gc];
     if (kg == 0) continue;
     const uint64_t key_g = cv.cell_key[gc];
-    const uint64_t r0 = cv.nbr_off[gc], r1 = cv.nbr_off[gc + 1];
+    uint64_t r0 = cv.nbr_off[gc], r1 = cv.nbr_off[gc + 1];
+    const bool by_class = cv.ccls && nwaves == NWAVES;  // class-sorted rows: the wave's segment only
+    if (by_class) {
+      const uint32_t c1 = cv.ccls[gc], c2 = cv.ccls[cv.ncells + gc];
+      if (wave == 0) r1 = r0 + c1;
+      else if (wave == 1) { r0 += c1; r1 = r0 + c2; }
+      else r0 += c1 + c2;
+    }
     for (uint64_t t0 = r0; t0 < r1; t0 += 32) {
       const uint64_t t = t0 + lane;
       uint2 p = make_uint2(gc, 0);
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, Cel
         p.y = h;
         if (h < gc) {
           const uint32_t kh = core_cnt[h];
-          is = kh > 0 && (nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
+          is = kh > 0 && (by_class || nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
           if (is) {
             need = uf_find(parent, gc) != uf_find(parent, h);
             small = need && (uint64_t)kg * kh <= SMALL_PAIR;

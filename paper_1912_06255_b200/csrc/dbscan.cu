@@ -489,7 +489,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
       neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir);
     else
       neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total,
-                     !(flags & DBSCAN_F_FORCE_TREE));
+                     !(flags & DBSCAN_F_FORCE_TREE), &cv.ccls);
     cv.nbr_off = nbr_off;
     cv.nbr = nbr;
     cv.ub = ub;

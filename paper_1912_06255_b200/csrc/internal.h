@@ -232,7 +232,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
 // (allow_brute = false forces the tree).
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                     uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub,
-                    uint64_t* total, bool allow_brute);
+                    uint64_t* total, bool allow_brute, const uint32_t** ccls /* NULL unless class-sorted */);
 // host: exact stencil offsets (Delta != 0 with sum gap^2 <= eps^2), flat [count*d] int8
 std::vector<int8_t> stencil_offsets(const Geo& g);
 
@@ -245,6 +245,9 @@ struct CellsView {
   const uint64_t* nbr_off;
   const uint32_t* nbr;
   const uint32_t* ub;  // sum of neighbour-cell sizes (saturating)
+  // rows sorted by class (lattice L1 distance 1, 2, >= 3; the all-pairs
+  // neighbour path): per cell the class-1 and class-2 counts, [2][ncells]; or NULL
+  const uint32_t* ccls = nullptr;
 };
 // Per-cell range-count trees (qtree.cu, row f2): cells with >= QT_MIN points;
 // node_off[c] = first node of cell c's implicit binary tree (heap order),

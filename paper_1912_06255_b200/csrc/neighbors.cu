@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
 
 static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                             uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub_out,
-                            uint64_t* total) {
+                            uint64_t* total, const uint32_t** ccls) {
   // squared gap per |delta| (u = |delta| clamped to R+1; entry R+1 > eps^2)
   const int gmax = (int)g.R + 1;
   if (gmax > GT_MAX || g.d < 4) return false;
@@ -455,6 +455,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   *nbr_off = off;
   *nbr = list;
   *ub_out = ub;
+  *ccls = ccount;  // rows are class-sorted: waves read only their class's segment
   return true;
 }
 
@@ -659,9 +660,10 @@ __global__ void __launch_bounds__(256) sort_rows_kernel(const uint64_t* __restri
 
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                     uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub_out,
-                    uint64_t* total, bool allow_brute) {
+                    uint64_t* total, bool allow_brute, const uint32_t** ccls) {
+  *ccls = nullptr;
   if (allow_brute && ncells <= BRUTE_MAX_CELLS &&
-      neighbors_brute(c, g, cell_key, cell_start, ncells, nbr_off, nbr, ub_out, total))
+      neighbors_brute(c, g, cell_key, cell_start, ncells, nbr_off, nbr, ub_out, total, ccls))
     return;
   uint64_t* code0 = c.alloc<uint64_t>(ncells);
   uint64_t* code1 = c.alloc<uint64_t>(ncells);
