@@ -232,7 +232,7 @@ def test_sparse_and_csr_paths_vs_o2(oracle_lib, flags):
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"d={d} flags={flags}")
 
 
-@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP])
+@pytest.mark.parametrize("grouping", [0, pkg.F_RADIX_GROUP, pkg.F_FORCE_WIDE], ids=["lattice", "radix", "wide"])
 def test_brick_markcore_vs_o2(oracle_lib, grouping):
     """The 3D brick MarkCore (16^3 cells staged with their halo in shared
     memory) against O2 and against the thread-per-point kernel: lattices with
