@@ -653,7 +653,17 @@ __global__ void __launch_bounds__(PL_THREADS) lat_place_kernel(uint32_t n, const
   if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[pos] = make_int2((int32_t)r.y, (int32_t)r.z);
   else reinterpret_cast<int4*>(Ps)[pos] = make_int4((int32_t)r.y, (int32_t)r.z, (int32_t)r.w, 0);
   idx[pos] = i;
-  cell_of[pos] = rank;
+}
+
+// cell_of from the cell ranges: a thread per cell writes its positions, so
+// consecutive threads write consecutive words (in 3b they would be a fourth
+// scattered partial-sector stream)
+__global__ void lat_cell_of_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                   uint32_t* __restrict__ cell_of) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < ncells; r += gridDim.x * blockDim.x) {
+    const uint32_t e = cell_start[r + 1];
+    for (uint32_t p = cell_start[r]; p < e; ++p) cell_of[p] = r;
+  }
 }
 
 bool lattice_applicable(const Geo& g, int64_t n) {
@@ -745,6 +755,8 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
     c.launched();
     lat_place_kernel<D><<<nchunks, PL_THREADS, 0, c.st>>>((uint32_t)n, rec, reci, dir, cell_start, ppre, ws,
                                                           L.words, nbk, chunk_bucket, Ps, idx, cell_of);
+    c.launched();
+    lat_cell_of_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_start, ncells, cell_of);
     c.launched();
   });
   *dir_out = dir;
