@@ -316,6 +316,18 @@ void uf_init(Ctx& c, uint32_t* parent, uint32_t n) {
   c.launched();
 }
 
+// only the listed cells (the sparse path's union-find touches core cells only)
+__global__ void uf_init_list_kernel(uint32_t* parent, const uint32_t* __restrict__ list, uint32_t m) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) parent[list[t]] = list[t];
+}
+
+void uf_init_list(Ctx& c, uint32_t* parent, const uint32_t* list, uint32_t m) {
+  if (m == 0) return;
+  uf_init_list_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(parent, list, m);
+  c.launched();
+}
+
 void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
                uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide,
                const QTrees* qt) {

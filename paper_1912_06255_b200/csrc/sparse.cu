@@ -925,7 +925,7 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   a.parent = parent;
   a.large_cap = a.ncore + 4096;
   a.large = c.alloc<uint2>(a.large_cap);
-  uf_init(c, parent, cv.ncells);
+  uf_init_list(c, parent, a.core_list, a.ncore);  // (Find and Link touch core cells only)
   if (a.nbcols > 0 && a.ncore > 0) {
     const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
     c.zero(a.counters + 2, sizeof(uint32_t));
