@@ -303,6 +303,38 @@ __device__ __forceinline__ uint64_t lb_exclusive(uint64_t* status, int64_t tile,
   return excl;
 }
 
+// The same look-back by a whole warp (call from every lane of ONE warp; the
+// result is valid in every lane): the lanes read 32 predecessors at once,
+// wait until all of them have published, and stop at the nearest inclusive
+// prefix — a chain of aggregate-only tiles costs one round trip per 32 tiles.
+__device__ __forceinline__ uint64_t lb_exclusive_warp(uint64_t* status, int64_t tile, int64_t stride,
+                                                      uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) lb_publish(status, LB_INC | agg);
+    return 0;
+  }
+  if (lane == 0) lb_publish(status + tile * stride, LB_AGG | agg);
+  uint64_t excl = 0;
+  int64_t t = tile - 1;
+  while (true) {
+    const int64_t tt = t - lane;
+    uint64_t s = tt >= 0 ? lb_read(status + tt * stride) : (LB_INC | 0ull);
+    while (!__all_sync(0xffffffffu, (s & ~LB_VAL) != 0))
+      if ((s & ~LB_VAL) == 0) s = lb_read(status + tt * stride);
+    const uint32_t inc = __ballot_sync(0xffffffffu, (s & LB_INC) != 0);
+    const int k = inc ? __ffs(inc) - 1 : 31;  // lanes 0..k count
+    uint64_t v = lane <= k ? (s & LB_VAL) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (inc) break;
+    t -= 32;
+  }
+  if (lane == 0) lb_publish(status + tile * stride, LB_INC | (excl + agg));
+  return excl;
+}
+
 // Add v over the whole block to *dst with ONE atomic (thread 0). Every thread
 // of the block must call it. Same-address atomics serialise in L2 (about one
 // per clock), so per-thread or per-warp counters over millions of items cost

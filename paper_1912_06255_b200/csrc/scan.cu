@@ -54,7 +54,10 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
   for (int i = 0; i < SC_ITEMS; ++i) sum += v[i];
   uint64_t tot;
   const uint64_t ex = block_exclusive_scan<uint64_t>(sum, s_scan, &tot);
-  if (threadIdx.x == 0) s_pref = lb_exclusive(status, tile, 1, tot);
+  if (threadIdx.x < 32) {
+    const uint64_t pref = lb_exclusive_warp(status, tile, 1, tot);
+    if (threadIdx.x == 0) s_pref = pref;
+  }
   __syncthreads();
   uint64_t run = s_pref + ex;
   TOut o[SC_ITEMS];
