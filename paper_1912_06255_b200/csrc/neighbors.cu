@@ -273,13 +273,14 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
 // with a per-warp stack). Warp per query cell, lanes over all cells, lattice
 // coordinates pre-decoded (cc[8] per cell), the squared gap per axis from a
 // shared table indexed by min(|delta|, R+1) (entry R+1 exceeds eps^2 on its
-// own). Cells are bucketed by their axis-0 coordinate first (counting sort),
-// so a query scans only the buckets c0 - R .. c0 + R (seed-spreader cells sit
-// in ~10 walk clusters: ~1/15 of the cells). Rows come out in three classes
+// own). Cells are bucketed by their axis-0 and axis-1 coordinates first
+// (counting sort; axis 0 only when the 2D buckets would outnumber the cells
+// four times), so a query scans 2R+1 runs of `order`: the axis-1 window
+// c1 - R .. c1 + R of each axis-0 bucket c0 - R .. c0 + R. Rows come out in three classes
 // of lattice L1 distance (1, 2, >= 3), nearest class first; the count pass
 // records the class sizes so that the fill pass places every entry in one
 // sweep.
-constexpr uint32_t BRUTE_MAX_CELLS = 16384;
+constexpr uint32_t BRUTE_MAX_CELLS = 131072;
 constexpr int GT_MAX = 64;
 
 __global__ void decode_cells_kernel(const uint64_t* __restrict__ cell_key, uint32_t ncells, Geo g,
@@ -302,17 +303,23 @@ __global__ void iota_kernel(uint32_t* __restrict__ v, uint32_t n) {
   if (i < n) v[i] = i;
 }
 
-__global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t* __restrict__ bcnt) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < ncells) atomicAdd(bcnt + cc[8 * (size_t)i], 1u);
+// bucket of a cell: (axis-0, axis-1) coordinates, c0 * B1 + c1 (B1 = 1: axis 0 only)
+__device__ __forceinline__ uint32_t cell_bucket(const uint32_t* __restrict__ cc, uint32_t i, uint32_t B1) {
+  return B1 > 1 ? cc[8 * (size_t)i] * B1 + cc[8 * (size_t)i + 1] : cc[8 * (size_t)i];
 }
 
-__global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells,
+__global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1,
+                                    uint32_t* __restrict__ bcnt) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ncells) atomicAdd(bcnt + cell_bucket(cc, i, B1), 1u);
+}
+
+__global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1,
                                    const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcur,
                                    uint32_t* __restrict__ order) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ncells) return;
-  const uint32_t b = cc[8 * (size_t)i];
+  const uint32_t b = cell_bucket(cc, i, B1);
   order[bstart[b] + atomicAdd(bcur + b, 1u)] = i;
 }
 
@@ -320,7 +327,7 @@ template <int DD>
 __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t* __restrict__ cc,
                                                         const uint32_t* __restrict__ order,
                                                         const uint32_t* __restrict__ bstart, uint32_t maxb,
-                                                        uint32_t ncells, Geo g,
+                                                        uint32_t B1, uint32_t ncells, Geo g,
                                                         const uint64_t* __restrict__ gtab_g, int gmax,
                                                         const uint32_t* __restrict__ cell_start,
                                                         uint32_t* __restrict__ ccount /*[3][ncells]*/,
@@ -350,8 +357,13 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     uint64_t sum = 0;
     const uint32_t c0 = maxb ? cq[0] : 0u;  // maxb = 0: a single bucket
     const uint32_t blo = c0 > g.R ? c0 - g.R : 0u, bhi = min(maxb, c0 + g.R);
-    const uint32_t t1 = bstart[bhi + 1];
-    for (uint32_t t0 = bstart[blo]; t0 < t1; t0 += 32) {
+    // B1 > 1: buckets by (axis 0, axis 1); for each axis-0 bucket the axis-1
+    // window c1 - R .. c1 + R is one contiguous run of `order`
+    const uint32_t y0 = B1 > 1 ? (cq[1] > g.R ? cq[1] - g.R : 0u) : 0u;
+    const uint32_t y1 = B1 > 1 ? min(B1 - 1, cq[1] + g.R) : 0u;
+    for (uint32_t b0 = blo; b0 <= bhi; ++b0) {
+    const uint32_t t1 = bstart[b0 * B1 + y1 + 1];
+    for (uint32_t t0 = bstart[b0 * B1 + y0]; t0 < t1; t0 += 32) {
       const uint32_t t = t0 + lane;
       const uint32_t h = t < t1 ? order[t] : 0u;
       int cls = -1;
@@ -381,6 +393,7 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
         n3[c] += __popc(b);
       }
       if (!fill && cls >= 0) sum += cell_start[h + 1] - cell_start[h];
+    }
     }
     if (!fill) {
 #pragma unroll
@@ -414,17 +427,23 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   decode_cells_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_key, ncells, g, cc);
   c.launched();
   // axis-0 buckets (one bucket if the axis is too long to bucket cheaply)
-  const uint32_t maxb = (uint64_t)g.maxc[0] < 4ull * ncells + 1024 ? g.maxc[0] : 0u;
-  uint32_t* bcnt = c.alloc<uint32_t>((size_t)maxb + 2);
-  uint32_t* bstart = c.alloc<uint32_t>((size_t)maxb + 2);
+  uint32_t maxb = (uint64_t)g.maxc[0] < 4ull * ncells + 1024 ? g.maxc[0] : 0u;
+  // two bucketed axes when their buckets fit the same budget
+  const uint32_t B1 = maxb && g.d >= 2 &&
+                              ((uint64_t)g.maxc[0] + 1) * ((uint64_t)g.maxc[1] + 1) < 4ull * ncells + 1024
+                          ? g.maxc[1] + 1
+                          : 1u;
+  const uint64_t nbk = ((uint64_t)maxb + 1) * B1;  // buckets 0 .. nbk - 1
+  uint32_t* bcnt = c.alloc<uint32_t>((size_t)nbk + 1);
+  uint32_t* bstart = c.alloc<uint32_t>((size_t)nbk + 1);
   uint32_t* order = c.alloc<uint32_t>(ncells);
-  c.zero(bcnt, sizeof(uint32_t) * ((size_t)maxb + 2));
+  c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
   if (maxb) {
-    bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, bcnt);
+    bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, bcnt);
     c.launched();
-    exclusive_scan_u32_u32(c, bcnt, bstart, (int64_t)maxb + 1);
-    c.zero(bcnt, sizeof(uint32_t) * ((size_t)maxb + 2));
-    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, bstart, bcnt, order);
+    exclusive_scan_u32_u32(c, bcnt, bstart, (int64_t)nbk);
+    c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
+    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, bstart, bcnt, order);
     c.launched();
   } else {
     // one bucket: every cell (cc[0] is then clamped by maxb = 0 -> buckets 0..0)
@@ -440,10 +459,10 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
   auto launch = [&](int fill, uint32_t* list) {
     if (g.d <= 4)
-      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, ncells, g, (const uint64_t*)dgt,
+      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, ncells, g, (const uint64_t*)dgt,
                                                   gmax, cell_start, ccount, cnt, ub, off, list);
     else
-      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, ncells, g, (const uint64_t*)dgt,
+      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, ncells, g, (const uint64_t*)dgt,
                                                   gmax, cell_start, ccount, cnt, ub, off, list);
     c.launched();
   };
