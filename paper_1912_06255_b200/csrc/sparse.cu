@@ -61,6 +61,7 @@ struct SpArgs {
   const long long* bcoff;    // back columns (cells before g in linear order)
   const uint32_t* bcmask;
   int nbcols;
+  int nbnear;                // back columns at gap 0 (first in the list): ClusterCore's first pass
   uint32_t ncells;
   const uint32_t* cell_start;
   const uint64_t* cell_key;
@@ -450,12 +451,20 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 //    for the warp BCP kernel (cluster.cu), which re-checks Find first.
 // APX: the rho-approximate connectivity test (row f4), a separate
 // instantiation so that the exact kernel keeps its register budget.
+// Two launches: back columns [0, nbnear) (gap 0: the pairs most likely to
+// connect, tested directly), then the rest with Find first — on data where
+// most cells join one component the second pass is pruned almost entirely
+// instead of testing and linking every pair against one contended root.
 template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
-__global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested) {
+__global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
+                                                       int col_hi, bool find_first) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
-  const int nb = a.nbcols;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) { s_off[i] = a.bcoff[i]; s_mask[i] = a.bcmask[i]; }
+  const int nb = col_hi - col_lo;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    s_off[i] = a.bcoff[col_lo + i];
+    s_mask[i] = a.bcmask[col_lo + i];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -484,6 +493,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
       for (uint32_t r = id0; r < id0 + nc; ++r) {
         const uint32_t h = a.core_list[r];
         const uint32_t kh = a.core_cnt[h];
+        if (find_first && uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
         if ((uint64_t)kg * kh > SP_SMALL) {
           if (uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
           const uint32_t slot = atomicAdd(a.counters + 2, 1u);
@@ -848,6 +858,8 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.ncols = (int)cols.size();
   upload(back, &a.bcoff, &a.bcmask);
   a.nbcols = (int)back.size();
+  a.nbnear = 0;
+  while (a.nbnear < a.nbcols && back[a.nbnear].first == 0) ++a.nbnear;
   // a4: directory of all cells
   const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
   a.dir = dir ? dir : build_dir(c, a, words, nullptr, nullptr);
@@ -932,10 +944,18 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
-      if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested);
-      else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested);
+      // (two passes only when most cells hold core points: on sparse core
+      // cells (c5: 8%) the second probe pass costs more than it prunes)
+      const bool two = 2ull * a.ncore >= cv.ncells;
+      for (int pass = 0; pass < 2; ++pass) {
+        const int lo = two ? (pass ? a.nbnear : 0) : (pass ? a.nbcols : 0);
+        const int hi = two ? (pass ? a.nbcols : a.nbnear) : a.nbcols;
+        if (lo == hi) continue;
+        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass == 1);
+        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass == 1);
+        c.launched();
+      }
     });
-    c.launched();
     bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
   }
 }
