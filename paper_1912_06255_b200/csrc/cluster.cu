@@ -386,7 +386,9 @@ __global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ lis
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t g = t < nc ? cell_at(list, t) : 0;
   bool root = false;
-  if (t < nc && core_cnt[g] > 0) {
+  const bool has = t < nc && core_cnt[g] > 0;
+  const uint32_t hm = __ballot_sync(DB_FULL, has);
+  if (has) {
     const uint32_t r = uf_find(parent, g);
     const uint32_t s = cell_start[g], k = core_cnt[g];
     uint32_t mn;
@@ -402,7 +404,11 @@ __global__ void label_roots_kernel(uint32_t nc, const uint32_t* __restrict__ lis
       mn = 0xffffffffu;
       for (uint32_t u = s; u < s + k; ++u) mn = min(mn, idx[u]);
     }
-    atomicMin(comp_min + r, mn);
+    // lanes of one component share one atomic (a component over millions of
+    // cells would otherwise serialise millions of same-address atomics)
+    const uint32_t peers = __match_any_sync(hm, r);
+    mn = __reduce_min_sync(peers, mn);
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicMin(comp_min + r, mn);
     root = r == g;
   }
   const uint32_t b = __syncthreads_count(root);  // one atomic per block, not per warp
