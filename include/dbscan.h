@@ -102,6 +102,8 @@ extern "C" {
                                         (0: the test is exact)                                */
 #define DBSCAN_STAT_BRICK        17  /* sparse MarkCore: 1 brick kernel, 2 brick kernel with
                                         overflowed bricks taken by the thread kernel, 0 none  */
+#define DBSCAN_STAT_POINT_BORDER 18  /* sparse ClusterBorder from the non-core points (1) or from
+                                        the core cells (0)                                    */
 #define DBSCAN_NSTATS            20
 
 typedef struct dbscan_result {

@@ -43,7 +43,7 @@ NSTAGES, NSTATS = 12, 20
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
-         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick"]
+         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick", "point_border"]
 
 
 class _Result(C.Structure):

@@ -475,8 +475,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   } else if (sparse) {
     // ---- a4 + a6 + a7 on the rank directory
     tm.stage(DBSCAN_STAGE_MARKCORE);
-    so.counters = c.alloc<uint32_t>(4);
-    c.zero(so.counters, 16);
+    so.counters = c.alloc<uint32_t>(6);
+    c.zero(so.counters, 24);
     core_cells = sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, lat_dir,
                                  !(flags & DBSCAN_F_NO_BRICK), &so);
   } else {
@@ -623,6 +623,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_QT_NODES] = (int64_t)qtrees.nodes;
   out->stats[DBSCAN_STAT_APPROX_SIDE] = g.at;
   out->stats[DBSCAN_STAT_BRICK] = so.brick;
+  out->stats[DBSCAN_STAT_POINT_BORDER] = so.point_border;
   return DBSCAN_OK;
 }
 

@@ -276,11 +276,12 @@ void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* 
 // ---- sparse.cu (cell-centric path for sparse lattices, d <= 3) ----
 constexpr uint64_t SPARSE_MEAN_PER_CELL = 4;  // n / ncells at or below: sparse path
 struct SparseOut {
-  uint32_t* counters = nullptr;  // device [4]: core cells, non-core cells, large pairs, mixed
+  uint32_t* counters = nullptr;  // device [6]: core cells, brick overflow, large pairs, mixed, core points (u64)
   void* stash = nullptr;         // kernel arguments kept between the stages
   const uint32_t* core_list = nullptr;  // cells holding core points, linear order
   uint32_t ncore = 0;
   int brick = 0;                 // MarkCore: 1 brick kernel, 2 with overflowed bricks
+  bool point_border = false;     // ClusterBorder from the non-core points (few of them)
 };
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);
 // a4 + a6 + a7 on the rank directories: core flags, core-first compaction,

@@ -71,7 +71,8 @@ struct SpArgs {
   uint8_t* core_s;
   uint32_t* core_cnt;
   int64_t min_pts;
-  uint32_t* counters;        // [0] core cells, [1] brick overflow, [2] large pairs, [3] mixed cells
+  uint32_t* counters;        // [0] core cells, [1] brick overflow, [2] large pairs, [3] mixed cells,
+                             // [4..5] core points (u64)
   uint32_t* mixed_list;
   uint32_t* core_tmp;        // cells with core points, unordered (count in counters[0])
   const uint32_t* cell_label;
@@ -423,6 +424,12 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
     core_cell = k > 0;
     mixed = k > 0 && k < m;
   }
+  // core points (counters[4], one atomic per block): ClusterBorder's choice
+  {
+    unsigned long long kp = 0;
+    if (g < a.ncells) kp = a.core_cnt[g];
+    block_add_u64(kp, reinterpret_cast<unsigned long long*>(a.counters + 4));
+  }
   // core cells (unordered, for the core directory) and mixed cells (for the
   // partition) are appended with one atomic per block each
   __shared__ uint32_t s_scan[33];
@@ -553,6 +560,59 @@ __device__ uint32_t sp_next_label(const SpArgs& a, const long long* s_off, const
     }
   }
   return best;
+}
+
+// Point-centric ClusterBorder, for lattices where almost every point is core
+// (few non-core points, millions of core cells): a thread per non-core point
+// walks the stencil columns on the core directory, tests the core points of
+// each core cell found whose label it does not hold yet, and writes its label
+// set (ascending order is the fill's job) with no atomics — one thread owns
+// the row. More than SP_MAXL labels: flagged, enumerated later.
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(256) sp_border_point_kernel(SpArgs a) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
+  __syncthreads();
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n || a.core_s[j]) return;
+  const uint32_t g = a.cell_of[j];
+  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
+  int32_t p[D];
+  load_pt<D>(a.Ps, j, p);
+  uint32_t L[SP_MAXL];
+#pragma unroll
+  for (int k = 0; k < SP_MAXL; ++k) L[k] = MISS;
+  int nl = 0;
+  bool ovf = false;
+  for (int c = 0; c < a.ncols && !ovf; ++c) {
+    uint32_t id0;
+    const uint32_t nc = dir_probe(a.cdir, base + (uint64_t)s_off[c], s_mask[c], &id0);
+    for (uint32_t r = id0; r < id0 + nc && !ovf; ++r) {
+      const uint32_t h = a.core_list[r];
+      const uint32_t lab = a.cell_label[h];
+      bool have = false;
+#pragma unroll
+      for (int k = 0; k < SP_MAXL; ++k) have |= L[k] == lab;
+      if (have || !sp_core_within<DIM, D, WIDE>(a, p, h)) continue;
+      if (nl == SP_MAXL) { ovf = true; break; }
+#pragma unroll
+      for (int k = 0; k < SP_MAXL; ++k)
+        if (k == nl) L[k] = lab;
+      ++nl;
+    }
+  }
+  const uint32_t i = a.idx[j];
+  if (ovf) {
+    a.ovf_pos[i] = j;
+    a.tmp_n[i] = 0xff;
+    return;
+  }
+  if (nl) {
+    uint32_t* row = a.tmp_lab + (size_t)i * SP_MAXL;
+#pragma unroll
+    for (int k = 0; k < SP_MAXL; ++k) row[k] = L[k];
+  }
 }
 
 // Core-centric ClusterBorder. Alg 4 asks, for every non-core point p, which
@@ -921,9 +981,14 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.core_list = core_list;
   core_list_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a, core_list);
   c.launched();
-  const uint64_t cnt01 = c.read(reinterpret_cast<const uint64_t*>(a.counters));  // [0] and [1]
-  a.ncore = (uint32_t)cnt01;
-  if (o->brick && (uint32_t)(cnt01 >> 32)) o->brick = 2;
+  const uint32_t* hc = c.fetch(a.counters, 6);  // [0] core cells, [1] brick overflow, [4..5] core points
+  c.sync();
+  a.ncore = hc[0];
+  if (o->brick && hc[1]) o->brick = 2;
+  const uint64_t core_pts = (uint64_t)hc[4] | ((uint64_t)hc[5] << 32);
+  // ClusterBorder from the side with less work: the non-core points when they
+  // are fewer than the core cells (almost every point core), else the cells
+  o->point_border = (uint64_t)n - core_pts < (uint64_t)a.ncore;
   o->stash = new SpArgs(a);
   o->core_list = core_list;
   o->ncore = a.ncore;
@@ -975,7 +1040,10 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
-    sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * 32, 256, c.sms * 16), 256, 0, c.st>>>(a);
+    if (o->point_border)
+      sp_border_point_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+    else
+      sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * 32, 256, c.sms * 16), 256, 0, c.st>>>(a);
     c.launched();
     sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
     c.launched();

@@ -262,6 +262,21 @@ def test_brick_markcore_vs_o2(oracle_lib, grouping):
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"brick eps={eps}")
 
 
+def test_point_centric_border_vs_o2(oracle_lib):
+    """Sparse lattice where almost every point is core: ClusterBorder runs from
+    the few non-core points (domain-boundary points here) instead of from the
+    core cells; same result as O2, border points included."""
+    for pts, eps, mp in [(datagen.uniform(200_000, 3, 20_000, 97), 600, 5),
+                         (datagen.uniform(100_000, 2, 60_000, 98), 250, 4)]:
+        r = gpu(pts, eps, mp)
+        assert r.stats["sparse"] == 1 and r.stats["point_border"] == 1, r.stats
+        want = oracle_lib.o2(pts, eps, mp)
+        assert len(want.border_ids) > 0
+        assert_same(np_result(r), want, f"point-centric border eps={eps}")
+        t = gpu(pts, eps, mp, pkg.F_NO_SPARSE)
+        assert_same(np_result(t), want, "csr")
+
+
 def test_grouping_choice():
     """Few cells: the hash counting sort groups the points; many distinct
     cells (uniform 3D, 2M points, ~2M cells) on a lattice too large to count
