@@ -928,7 +928,11 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   c.stage(DBSCAN_STAGE_MARKCORE);
   // bricks hold BRK_CAP / BRK_H^3 = 0.38 points per halo cell: taken when the
   // mean over the lattice is below 0.3 (denser data would overflow them)
-  o->brick = brick_ok && g.d == 3 && g.R == BRK_R && !g.at && (unsigned __int128)n * 10 <= vol * 3;
+  // ... and at least 0.15: below it most halo columns are empty and the
+  // per-brick staging costs more than it saves (measured: 0.08 points per
+  // cell 1.32 ms against 0.93 ms for the thread kernel; 0.23 (c5) 1.04 / 1.07)
+  o->brick = brick_ok && g.d == 3 && g.R == BRK_R && !g.at && (unsigned __int128)n * 10 <= vol * 3 &&
+             (unsigned __int128)n * 20 >= vol * 3;
   if (o->brick) {
     std::vector<int8_t> geom;
     stencil_columns(g, a.stride, &back, &geom);

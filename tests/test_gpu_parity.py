@@ -240,16 +240,17 @@ def test_brick_markcore_vs_o2(oracle_lib, grouping):
     capacity (its points go to the thread kernel), and one cell holding more
     than 65535 points."""
     cases = []
-    cases.append((datagen.uniform(150_000, 3, 40_000, 31), 500, 3, 1))
+    cases.append((datagen.uniform(150_000, 3, 25_000, 31), 500, 3, 1))
     cases.append((datagen.uniform(100_000, 3, 25_000, 32), 600, 4, 1))
-    blob = datagen.uniform(200_000, 3, 40_000, 33)
+    blob = datagen.uniform(200_000, 3, 28_000, 33)
     blob[:6000] = blob[0] + datagen.uniform(6000, 3, 600, 34)   # ~6000 points in a few cells
     cases.append((blob, 500, 10, 2))
-    big = datagen.uniform(260_000, 3, 50_000, 35)
+    big = datagen.uniform(260_000, 3, 31_000, 35)
     big[:66_000] = big[0]                                        # one cell, > 65535 points
     cases.append((big, 500, 10, 2))
-    # denser than 0.3 points per lattice cell: the thread kernel alone
+    # denser than 0.3 points per lattice cell, or sparser than 0.15: the thread kernel alone
     cases.append((datagen.uniform(150_000, 3, 12_000, 36), 500, 8, 0))
+    cases.append((datagen.uniform(150_000, 3, 40_000, 37), 500, 3, 0))
     for pts, eps, mp, want in cases:
         r = gpu(pts, eps, mp, grouping)
         assert r.stats["sparse"] == 1 and r.stats["brick"] == want, (r.stats, eps)
