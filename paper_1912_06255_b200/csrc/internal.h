@@ -276,7 +276,7 @@ void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* 
 // ---- sparse.cu (cell-centric path for sparse lattices, d <= 3) ----
 constexpr uint64_t SPARSE_MEAN_PER_CELL = 4;  // n / ncells at or below: sparse path
 struct SparseOut {
-  uint32_t* counters = nullptr;  // device [6]: core cells, brick overflow, large pairs, mixed, core points (u64)
+  uint32_t* counters = nullptr;  // device [6]: -, brick overflow, large pairs, mixed, core cells, core points
   void* stash = nullptr;         // kernel arguments kept between the stages
   const uint32_t* core_list = nullptr;  // cells holding core points, linear order
   uint32_t ncore = 0;

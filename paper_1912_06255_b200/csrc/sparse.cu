@@ -71,10 +71,10 @@ struct SpArgs {
   uint8_t* core_s;
   uint32_t* core_cnt;
   int64_t min_pts;
-  uint32_t* counters;        // [0] core cells, [1] brick overflow, [2] large pairs, [3] mixed cells,
-                             // [4..5] core points (u64)
+  uint32_t* counters;        // [1] brick overflow, [2] large pairs, [3] mixed cells,
+                             // [4] core cells, [5] core points (one u64 atomic)
   uint32_t* mixed_list;
-  uint32_t* core_tmp;        // cells with core points, unordered (count in counters[0])
+  uint32_t* core_tmp;        // cells with core points, unordered (count in counters[4])
   const uint32_t* cell_label;
   uint32_t* parent;
   uint2* large;
@@ -155,9 +155,9 @@ __global__ void dir_pack_kernel(const uint32_t* __restrict__ bm, const uint32_t*
 }
 
 // core_list[rank in cdir] = cell id, for every cell holding core points
-// (from the unordered list core_tmp[0 .. counters[0]))
+// (from the unordered list core_tmp[0 .. counters[4]))
 __global__ void core_list_kernel(SpArgs a, uint32_t* __restrict__ core_list) {
-  const uint32_t m = a.counters[0];
+  const uint32_t m = a.counters[4];
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
     const uint32_t g = a.core_tmp[t];
     uint64_t lin = 0;
@@ -414,35 +414,37 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
 __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   bool core_cell = false, mixed = false;
+  uint32_t k = 0;
   if (g < a.ncells) {
     const uint32_t s = a.cell_start[g], e = a.cell_start[g + 1], m = e - s;
-    uint32_t k = 0;
     if ((int64_t)m >= a.min_pts) k = m;
     else
       for (uint32_t u = s; u < e; ++u) k += a.core_s[u];
-  a.core_cnt[g] = k;
+    a.core_cnt[g] = k;
     core_cell = k > 0;
     mixed = k > 0 && k < m;
   }
-  // core points (counters[4], one atomic per block): ClusterBorder's choice
-  {
-    unsigned long long kp = 0;
-    if (g < a.ncells) kp = a.core_cnt[g];
-    block_add_u64(kp, reinterpret_cast<unsigned long long*>(a.counters + 4));
-  }
-  // core cells (unordered, for the core directory) and mixed cells (for the
-  // partition) are appended with one atomic per block each
-  __shared__ uint32_t s_scan[33];
+  // one 64-bit block scan for three block totals: core cells (bits 0-15),
+  // mixed cells (16-31) and core points (32-63); core cells (unordered, for
+  // the core directory) and mixed cells (for the partition) are appended
+  // with one atomic per block each, core points summed into counters[4..5]
+  __shared__ uint64_t s_scan[33];
   __shared__ uint32_t s_base, s_cbase;
-  uint32_t nc;
-  const uint32_t cx = block_exclusive_scan<uint32_t>(core_cell ? 1u : 0u, s_scan, &nc);
-  if (threadIdx.x == 0 && nc) s_cbase = atomicAdd(a.counters + 0, nc);
-  uint32_t nm;
-  const uint32_t ex = block_exclusive_scan<uint32_t>(mixed ? 1u : 0u, s_scan, &nm);
-  if (threadIdx.x == 0 && nm) s_base = atomicAdd(a.counters + 3, nm);
+  uint64_t tot;
+  const uint64_t ex = block_exclusive_scan<uint64_t>(
+      (uint64_t)core_cell | ((uint64_t)mixed << 16) | ((uint64_t)k << 32), s_scan, &tot);
+  if (threadIdx.x == 0) {
+    // core cells (low word, the base of this block's list entries) and core
+    // points (high word) in ONE 64-bit atomic: same-address atomics from 35K
+    // blocks serialise, a third one per block cost ~25 us on c5
+    const uint64_t nc = tot & 0xffffu, nm = (tot >> 16) & 0xffffu;
+    if (nc) s_cbase = (uint32_t)atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 4),
+                                          (unsigned long long)(nc | ((tot >> 32) << 32)));
+    if (nm) s_base = atomicAdd(a.counters + 3, (uint32_t)nm);
+  }
   __syncthreads();
-  if (core_cell) a.core_tmp[s_cbase + cx] = g;
-  if (mixed) a.mixed_list[s_base + ex] = g;
+  if (core_cell) a.core_tmp[s_cbase + (uint32_t)(ex & 0xffffu)] = g;
+  if (mixed) a.mixed_list[s_base + (uint32_t)((ex >> 16) & 0xffffu)] = g;
 }
 
 // ---------------------------------------------------------- ClusterCore (a8)
@@ -980,16 +982,16 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   c.launched();
   partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, Ps, idx, core_s, n);
   // directory of the cells holding core points, and their list in linear order
-  a.cdir = build_dir(c, a, words, a.core_tmp, a.counters);
+  a.cdir = build_dir(c, a, words, a.core_tmp, a.counters + 4);
   uint32_t* core_list = c.alloc<uint32_t>(cv.ncells);
   a.core_list = core_list;
   core_list_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a, core_list);
   c.launched();
-  const uint32_t* hc = c.fetch(a.counters, 6);  // [0] core cells, [1] brick overflow, [4..5] core points
+  const uint32_t* hc = c.fetch(a.counters, 6);  // [1] brick overflow, [4] core cells, [5] core points
   c.sync();
-  a.ncore = hc[0];
+  a.ncore = hc[4];
   if (o->brick && hc[1]) o->brick = 2;
-  const uint64_t core_pts = (uint64_t)hc[4] | ((uint64_t)hc[5] << 32);
+  const uint64_t core_pts = hc[5];
   // ClusterBorder from the side with less work: the non-core points when they
   // are fewer than the core cells (almost every point core), else the cells
   o->point_border = (uint64_t)n - core_pts < (uint64_t)a.ncore;
