@@ -439,15 +439,22 @@ __global__ void __launch_bounds__(256) write_positions_kernel(uint32_t n, const 
                                                               const uint32_t* __restrict__ cell_label,
                                                               int32_t* __restrict__ cluster_out,
                                                               uint32_t* counters) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool is_core = false;
-  if (j < n) {
+  // grid-stride over a bounded grid: one atomic per block (same-address
+  // atomics from n/256 blocks serialise: ~25 us at n = 10M)
+  unsigned long long nc = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint32_t g = cell_of[j];
-    is_core = j - cell_start[g] < core_cnt[g];
+    const bool is_core = j - cell_start[g] < core_cnt[g];
     cluster_out[idx[j]] = is_core ? (int32_t)cell_label[g] : -1;
+    nc += is_core;
   }
-  const uint32_t b = __syncthreads_count(is_core);  // one atomic per block
-  if (threadIdx.x == 0 && b) atomicAdd(counters + 1, b);
+  __shared__ unsigned long long s_c;
+  if (threadIdx.x == 0) s_c = 0;
+  __syncthreads();
+  nc = __reduce_add_sync(DB_FULL, (uint32_t)nc);
+  if ((threadIdx.x & 31) == 0 && nc) atomicAdd(&s_c, nc);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_c) atomicAdd(counters + 1, (uint32_t)s_c);
 }
 
 __global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const uint32_t* __restrict__ list,
@@ -509,7 +516,7 @@ void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* cor
                                                                   cell_label);
   c.launched();
   if (!core_list && (int64_t)nc * 32 <= n) {
-    write_positions_kernel<<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(
+    write_positions_kernel<<<grid_for(n, 256, c.sms * 16), 256, 0, c.st>>>(
         (uint32_t)n, idx, cv.cell_of, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
   } else {
     DB_CUDA(cudaMemsetAsync(cluster_out, 0xff, sizeof(int32_t) * (size_t)n, c.st));

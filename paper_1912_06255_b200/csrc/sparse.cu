@@ -704,9 +704,9 @@ __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
   __syncthreads();
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t cnt = 0;
-  if (i < a.n) {
+  uint32_t nb = 0;  // border points of this thread (grid-stride: one atomic per block)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+    uint32_t cnt = 0;
     if (a.tmp_n[i] != 0xff) {
       const uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)i * SP_MAXL);
       cnt = (v.x != MISS) + (v.y != MISS) + (v.z != MISS) + (v.w != MISS);
@@ -725,9 +725,9 @@ __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
       }
     }
     a.bcnt[i] = cnt;
+    nb += cnt > 0;
   }
-  const uint32_t nb = __syncthreads_count(cnt > 0);
-  if (threadIdx.x == 0 && nb) atomicAdd(a.nborder, (unsigned long long)nb);
+  block_add_u64(nb, a.nborder);
 }
 
 // Thread per point in input order: its row of the CSR, the set sorted by a
@@ -1051,7 +1051,7 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
     else
       sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * 32, 256, c.sms * 16), 256, 0, c.st>>>(a);
     c.launched();
-    sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a);
+    sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, c.sms * 16), 256, 0, c.st>>>(a);
     c.launched();
   });
   if (c.read(nborder) == 0) {
