@@ -411,40 +411,52 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
 }
 
 // Thread per cell: core count (a7); mixed cells are listed for the partition.
+constexpr int SC_CELLS = 8;  // consecutive cells per thread in sp_cells (fewer blocks, fewer atomics)
+
 __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  bool core_cell = false, mixed = false;
-  uint32_t k = 0;
-  if (g < a.ncells) {
-    const uint32_t s = a.cell_start[g], e = a.cell_start[g + 1], m = e - s;
-    if ((int64_t)m >= a.min_pts) k = m;
-    else
-      for (uint32_t u = s; u < e; ++u) k += a.core_s[u];
-    a.core_cnt[g] = k;
-    core_cell = k > 0;
-    mixed = k > 0 && k < m;
+  const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) * SC_CELLS;
+  uint32_t ncc = 0, nmx = 0, kpts = 0;
+  uint8_t flags[SC_CELLS];  // bit 0 core cell, bit 1 mixed
+#pragma unroll
+  for (int q = 0; q < SC_CELLS; ++q) {
+    const uint32_t g = g0 + q;
+    flags[q] = 0;
+    if (g < a.ncells) {
+      const uint32_t s = a.cell_start[g], e = a.cell_start[g + 1], m = e - s;
+      uint32_t k = 0;
+      if ((int64_t)m >= a.min_pts) k = m;
+      else
+        for (uint32_t u = s; u < e; ++u) k += a.core_s[u];
+      a.core_cnt[g] = k;
+      flags[q] = (k > 0 ? 1 : 0) | (k > 0 && k < m ? 2 : 0);
+      ncc += k > 0;
+      nmx += k > 0 && k < m;
+      kpts += k;
+    }
   }
   // one 64-bit block scan for three block totals: core cells (bits 0-15),
   // mixed cells (16-31) and core points (32-63); core cells (unordered, for
   // the core directory) and mixed cells (for the partition) are appended
-  // with one atomic per block each, core points summed into counters[4..5]
+  // with one 64-bit atomic per block for core cells + core points (same-
+  // address atomics from many blocks serialise) and one for mixed cells
   __shared__ uint64_t s_scan[33];
   __shared__ uint32_t s_base, s_cbase;
   uint64_t tot;
   const uint64_t ex = block_exclusive_scan<uint64_t>(
-      (uint64_t)core_cell | ((uint64_t)mixed << 16) | ((uint64_t)k << 32), s_scan, &tot);
+      (uint64_t)ncc | ((uint64_t)nmx << 16) | ((uint64_t)kpts << 32), s_scan, &tot);
   if (threadIdx.x == 0) {
-    // core cells (low word, the base of this block's list entries) and core
-    // points (high word) in ONE 64-bit atomic: same-address atomics from 35K
-    // blocks serialise, a third one per block cost ~25 us on c5
     const uint64_t nc = tot & 0xffffu, nm = (tot >> 16) & 0xffffu;
     if (nc) s_cbase = (uint32_t)atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 4),
                                           (unsigned long long)(nc | ((tot >> 32) << 32)));
     if (nm) s_base = atomicAdd(a.counters + 3, (uint32_t)nm);
   }
   __syncthreads();
-  if (core_cell) a.core_tmp[s_cbase + (uint32_t)(ex & 0xffffu)] = g;
-  if (mixed) a.mixed_list[s_base + (uint32_t)((ex >> 16) & 0xffffu)] = g;
+  uint32_t pc = s_cbase + (uint32_t)(ex & 0xffffu), pm = s_base + (uint32_t)((ex >> 16) & 0xffffu);
+#pragma unroll
+  for (int q = 0; q < SC_CELLS; ++q) {
+    if (flags[q] & 1) a.core_tmp[pc++] = g0 + q;
+    if (flags[q] & 2) a.mixed_list[pm++] = g0 + q;
+  }
 }
 
 // ---------------------------------------------------------- ClusterCore (a8)
@@ -978,7 +990,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   c.stage(DBSCAN_STAGE_COMPACT);
   a.mixed_list = c.alloc<uint32_t>(cv.ncells);
   a.core_tmp = c.alloc<uint32_t>(cv.ncells);
-  sp_cells_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(a);
+  sp_cells_kernel<<<grid_for(((int64_t)cv.ncells + SC_CELLS - 1) / SC_CELLS, 256, 1 << 30), 256, 0, c.st>>>(a);
   c.launched();
   partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, Ps, idx, core_s, n);
   // directory of the cells holding core points, and their list in linear order
