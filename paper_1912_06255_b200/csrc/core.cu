@@ -301,6 +301,35 @@ __global__ void partition_kernel(CellsView cv, const uint32_t* __restrict__ mixe
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
     const uint32_t g = mixed[t];
     const uint32_t s = cv.cell_start[g], e = cv.cell_start[g + 1];
+    if constexpr (D <= 4) {
+      if (e - s <= 8) {  // small cell (sparse lattices): in registers, no scratch round trip
+        constexpr int SM = 8;
+        int32_t P[SM][D];
+        uint32_t I[SM];
+        uint8_t C[SM];
+        const uint32_t nn = e - s;
+#pragma unroll
+        for (int q = 0; q < SM; ++q)
+          if ((uint32_t)q < nn) {
+            PtLoad<D>::load(Ps, s + q, P[q]);
+            I[q] = idx[s + q];
+            C[q] = core_s[s + q];
+          }
+        uint32_t w = s;
+#pragma unroll
+        for (int pass = 1; pass >= 0; --pass)
+#pragma unroll
+          for (int q = 0; q < SM; ++q)
+            if ((uint32_t)q < nn && C[q] == pass) {
+              if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[w] = make_int2(P[q][0], P[q][1]);
+              else reinterpret_cast<int4*>(Ps)[w] = make_int4(P[q][0], P[q][1], P[q][2], P[q][3]);
+              idx[w] = I[q];
+              core_s[w] = (uint8_t)pass;
+              ++w;
+            }
+        continue;
+      }
+    }
     for (uint32_t u = s; u < e; ++u) {
       for (int k = 0; k < D; ++k) scratchP[(size_t)u * D + k] = Ps[(size_t)u * D + k];
       scratchI[u] = idx[u] | ((uint32_t)core_s[u] << 31);
@@ -334,7 +363,7 @@ void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* 
   uint32_t* sI = c.alloc<uint32_t>(n);
   auto go = [&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
-    partition_kernel<D><<<c.sms * 4, 128, 0, c.st>>>(cv, mixed, nmixed, Ps, idx, core_s, sP, sI);
+    partition_kernel<D><<<c.sms * 16, 256, 0, c.st>>>(cv, mixed, nmixed, Ps, idx, core_s, sP, sI);
   };
   if (g.D == 2) go(std::integral_constant<int, 2>());
   else if (g.D == 4) go(std::integral_constant<int, 4>());
