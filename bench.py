@@ -387,7 +387,7 @@ def main():
             w = e2e_step()
             if os.environ.get("DB_E2E_DEBUG"):
                 print("e2e warm-up step ms:", round(w * 1e3, 2), file=sys.stderr)
-        ts = [e2e_step() for _ in range(max(1, min(args.steps, 3)))]
+        ts = [e2e_step() for _ in range(max(1, min(args.steps, 5)))]
         if os.environ.get("DB_E2E_DEBUG"):
             print("e2e step seconds:", [round(t * 1e3, 2) for t in ts], file=sys.stderr)
         e2e = {"value": npts_step * len(ts) / sum(ts), "unit": "points/s", "h2d_bytes_per_step": h2d,
