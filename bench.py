@@ -391,7 +391,9 @@ def main():
                 raise errs[0]
             h2d, d2h = sum(b_in), sum(b_out)
             return dt
-        for _ in range(max(1, args.warmup)):
+        # (at least 5: the first steps create and grow the threads' workspaces,
+        # device memory mapped in the pool and pinned staging, ~0.2 s each)
+        for _ in range(max(5, args.warmup)):
             w = e2e_step()
             if os.environ.get("DB_E2E_DEBUG"):
                 print("e2e warm-up step ms:", round(w * 1e3, 2), file=sys.stderr)
