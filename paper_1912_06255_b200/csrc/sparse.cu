@@ -15,26 +15,29 @@
 //    along the last axis (25 in 3D, 5 in 2D); a column's cells have
 //    consecutive ids and their points are one contiguous range of Ps.
 //    Out-of-range neighbours land in the padding (no range checks).
-//  * MarkCore (a6, Alg 2): a warp per cell; lane c probes column
-//    c, a warp prefix sum flattens the columns' point ranges into one
-//    candidate list (nearest columns first), and for each point of the cell
-//    the lanes test 32 candidates at a time and count with a ballot, stopping
-//    at minPts. A cell with |g| >= minPts is all core.
-//  * a7: a thread per cell counts core points; mixed cells are partitioned
-//    core-first (core.cu); a second directory covers only the cells holding
-//    core points, with the list of those cells in linear order.
+//  * MarkCore (a6, Alg 2): 3D lattices with 0.15-0.3 points per
+//    cell and R = 2 (c5): bricks of 16^3 cells staged with their halo in
+//    shared memory, a thread per own point walking the 25 column ranges in
+//    one branch-free loop (sp_core_brick_kernel); otherwise a thread per
+//    point over the columns on the directory (sp_core_kernel). Counting stops
+//    at minPts; a cell with |g| >= minPts is all core.
+//  * a7: a thread per 8 cells counts core points; mixed cells are
+//    partitioned core-first (core.cu); a second directory covers only the
+//    cells holding core points, with the list of those cells in linear order.
 //  * ClusterCore (a8, Alg 3): over the core cells, the lanes of a
 //    warp take (core cell g, back column) items — back columns hold the
 //    cells before g in linear order, so each pair is seen once, from its
 //    higher id ("g > h") — probe the core directory and test the
 //    core cells found: small BCPs directly (cheaper than the Finds that could
 //    prune them), larger ones after a Find check through the warp BCP kernel
-//    (cluster.cu).
-//  * ClusterBorder (a10, Alg 4): a thread per non-core point
-//    walks the stencil columns on the core directory (only cells with core
-//    points are visited), label sets of up to SP_MAXL in registers staged per
-//    sorted position; larger sets are enumerated without storage in
-//    ascending order.
+//    (cluster.cu). When most cells hold core points, the gap-0 columns run
+//    first and the rest with Find first.
+//  * ClusterBorder (a10, Alg 4): from the core cells (a warp per
+//    core cell: candidates of its 25 columns laid out flat over the lanes,
+//    labels added to lock-free 4-slot sets in input order), or, when the
+//    non-core points are fewer than the core cells, from the points (a
+//    thread per non-core point on the core directory). Larger sets are
+//    enumerated without storage in ascending order.
 #include <algorithm>
 #include <array>
 #include <map>
