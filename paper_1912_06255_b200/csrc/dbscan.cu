@@ -88,10 +88,11 @@ struct Timer {
     DB_CUDA(cudaEventRecord(ev[n], st));
     mark[n++] = s;
   }
-  void finish(float* out) {
+  void close() {  // end the last stage
+    if (on && n > 0) DB_CUDA(cudaEventRecord(ev[n], st));
+  }
+  void finish(float* out) {  // after close() and a synchronisation of the stream
     if (!on || n == 0) return;
-    DB_CUDA(cudaEventRecord(ev[n], st));
-    DB_CUDA(cudaEventSynchronize(ev[n]));
     for (int i = 0; i < n; ++i) {
       float ms = 0;
       DB_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
@@ -584,12 +585,11 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   const unsigned long long* hw_h = c.work ? c.fetch(c.work, 4) : nullptr;
   const uint32_t* h32_h = c.fetch(cnt32, 4);
   const unsigned long long* h64_h = c.fetch(cnt64, 3);
-  if (c.tracing) c.mark("timer finish");
-  tm.finish(out->stage_ms);
-  if (c.tracing) c.mark("timer done");
+  tm.close();  // (the last event; read after the stream is idle)
   c.free_all();
   if (c.tracing) c.mark("final sync");
   DB_CUDA(cudaStreamSynchronize(st));
+  tm.finish(out->stage_ms);
   c.finish();
   std::memcpy(h32, h32_h, sizeof(h32));
   std::memcpy(h64, h64_h, sizeof(h64));
