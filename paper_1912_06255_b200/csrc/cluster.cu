@@ -457,18 +457,24 @@ __global__ void __launch_bounds__(256) write_positions_kernel(uint32_t n, const 
   if (threadIdx.x == 0 && s_c) atomicAdd(counters + 1, (uint32_t)s_c);
 }
 
+// (also sets cell_label: the cell's component minimum, ~0 without core points)
 __global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const uint32_t* __restrict__ list,
                                                            const uint32_t* __restrict__ idx,
                                                            const uint32_t* __restrict__ cell_start,
                                                            const uint32_t* __restrict__ core_cnt,
-                                                           const uint32_t* __restrict__ cell_label,
+                                                           uint32_t* parent, const uint32_t* __restrict__ comp_min,
+                                                           uint32_t* __restrict__ cell_label,
                                                            int32_t* __restrict__ cluster_out, uint32_t* counters) {
   unsigned long long ncore = 0;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += gridDim.x * blockDim.x) {
     const uint32_t g = cell_at(list, t);
     const uint32_t k = core_cnt[g];
-    if (!k) continue;
-    const int32_t lab = (int32_t)cell_label[g];
+    if (!k) {
+      cell_label[g] = 0xffffffffu;
+      continue;
+    }
+    const int32_t lab = (int32_t)comp_min[uf_find(parent, g)];
+    cell_label[g] = (uint32_t)lab;
     const uint32_t s = cell_start[g];
     for (uint32_t u = s; u < s + k; ++u) cluster_out[idx[u]] = lab;
     ncore += k;
@@ -512,16 +518,16 @@ void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* cor
                                                                     min_mode, cellmin, parent, comp_min,
                                                                     counters);
   c.launched();
-  cell_label_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(m, core_list, core_cnt, parent, comp_min,
-                                                                  cell_label);
-  c.launched();
   if (!core_list && (int64_t)nc * 32 <= n) {
+    cell_label_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(m, core_list, core_cnt, parent, comp_min,
+                                                                    cell_label);
+    c.launched();
     write_positions_kernel<<<grid_for(n, 256, c.sms * 16), 256, 0, c.st>>>(
         (uint32_t)n, idx, cv.cell_of, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
   } else {
     DB_CUDA(cudaMemsetAsync(cluster_out, 0xff, sizeof(int32_t) * (size_t)n, c.st));
     write_points_kernel<<<grid_for(m, 256, c.sms * 16), 256, 0, c.st>>>(
-        m, core_list, idx, cv.cell_start, core_cnt, cell_label, cluster_out, counters);
+        m, core_list, idx, cv.cell_start, core_cnt, parent, comp_min, cell_label, cluster_out, counters);
   }
   c.launched();
   core_from_cluster_kernel<<<grid_for((n + 3) / 4, 256, 1 << 30), 256, 0, c.st>>>((uint32_t)n, cluster_out,
