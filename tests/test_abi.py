@@ -36,6 +36,9 @@ def test_exports(lib):
         assert hasattr(lib, name), name
     assert lib.dbscan_version() >= 100
     assert lib.dbscan_stage_name(11) == b"total"
+    # no workspace was created (no GPU call): releasing the idle ones is a no-op
+    import paper_1912_06255_b200 as pkg
+    pkg.release_workspace()
 
 
 def test_struct_layout_matches_header(lib):
