@@ -6,7 +6,7 @@
 
 namespace db {
 
-constexpr int SC_THREADS = 512;
+constexpr int SC_THREADS = 256;
 constexpr int SC_ITEMS = 16;  // consecutive items per thread: 4 x 16-byte loads
 constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 
