@@ -433,3 +433,19 @@ def test_workspace_pool(oracle_lib):
             assert_same(r, want[k], f"round {rnd} case {k} host {h}")
         if rnd == 1:
             pkg.release_workspace()
+
+
+def test_host_path_constant_outputs(oracle_lib):
+    """Host path: outputs that are constant are written on the host (all noise:
+    core 0, cluster -1, border_off 0; no border point: border_off 0); pinned
+    caller buffers pre-filled with garbage must come back exactly right."""
+    pts = datagen.uniform(300_000, 3, 3_000, 71)        # dense: every point core, no border point
+    noise = datagen.uniform(300_000, 3, 1_000_000, 72)  # sparse: minPts unreachable
+    for p, eps, mp in [(pts, 100, 4), (noise, 50, 50), (pts[:5000], 40, 10_000)]:
+        want = oracle_lib.o2(p, eps, mp)
+        n = len(p)
+        outs = (torch.full((n,), 7, dtype=torch.uint8).pin_memory(), torch.full((n,), 7, dtype=torch.int32).pin_memory(),
+                torch.full((n + 1,), 7, dtype=torch.int64).pin_memory(), torch.full((n,), 7, dtype=torch.int32).pin_memory())
+        r = pkg.dbscan(torch.from_numpy(np.ascontiguousarray(p)).pin_memory(), eps, mp, out=outs)
+        assert_same(np_result(r), want, f"eps={eps} minPts={mp}")
+        assert len(want.border_ids) == 0
