@@ -487,7 +487,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     uint32_t* ub;
     tm.stage(DBSCAN_STAGE_NEIGHBORS);
     if (!tree)
-      neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir);
+      neighbors_stencil(c, g, cell_key, cell_start, ncells, n, &nbr_off, &nbr, &ub, &nbr_total, &dense_dir,
+                        &cv.ccls);
     else
       neighbors_tree(c, g, cell_key, cell_start, ncells, &nbr_off, &nbr, &ub, &nbr_total,
                      !(flags & DBSCAN_F_FORCE_TREE), &cv.ccls);

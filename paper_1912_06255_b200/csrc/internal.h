@@ -227,7 +227,7 @@ uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** ta
 // d <= 3 (or forced): builds a dense cell directory or a hash table itself.
 void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                        uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,
-                       uint32_t** ub, uint64_t* total, bool* dense);
+                       uint32_t** ub, uint64_t* total, bool* dense, const uint32_t** ccls);
 // d >= 4: all-pairs over cells when there are few (<= 16384), else the cell tree
 // (allow_brute = false forces the tree).
 void neighbors_tree(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,

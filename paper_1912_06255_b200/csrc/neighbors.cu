@@ -21,6 +21,8 @@
 //           cells of a leaf at once.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace db {
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(256) nbr_stencil_kernel(
     const StencilOff* __restrict__ offs, int noffs, const Slot* __restrict__ T, uint64_t mask,
     const uint32_t* __restrict__ dir, Lattice lat, const uint32_t* __restrict__ cell_start,
     uint32_t* __restrict__ cnt, uint32_t* __restrict__ ub, const uint64_t* __restrict__ off,
-    uint32_t* __restrict__ nbr) {
+    uint32_t* __restrict__ nbr, int n0, int n01, uint32_t* __restrict__ ccount) {
   __shared__ StencilOff s_offs[MAX_SMEM_OFFS];
   const bool in_smem = noffs <= MAX_SMEM_OFFS;
   if (in_smem)
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(256) nbr_stencil_kernel(
       for (int k = 0; k < DIM; ++k) base += (uint64_t)(cc[k] + g.R) * lat.stride[k];
     }
     uint64_t wpos = fill ? off[cell] : 0;
-    uint32_t total = 0;
+    uint32_t total = 0, c0 = 0, c1 = 0;  // (offsets are class-sorted: [0, n0) class 0, [n0, n01) class 1)
     uint64_t sum = 0;
     if constexpr (WARP) {
       const uint32_t lt = lanemask_lt();
@@ -148,6 +150,8 @@ __global__ void __launch_bounds__(256) nbr_stencil_kernel(
         } else if (found) {
           sum += cell_start[id + 1] - cell_start[id];
         }
+        c0 += __popc(__ballot_sync(DB_FULL, found && t < n0));
+        c1 += __popc(__ballot_sync(DB_FULL, found && t >= n0 && t < n01));
         wpos += __popc(b);
         total += __popc(b);
       }
@@ -157,6 +161,7 @@ __global__ void __launch_bounds__(256) nbr_stencil_kernel(
         if (lane == 0) {
           cnt[cell] = total;
           ub[cell] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+          if (ccount) { ccount[cell] = c0; ccount[ncells + cell] = c1; }
         }
       }
     } else {
@@ -166,10 +171,13 @@ __global__ void __launch_bounds__(256) nbr_stencil_kernel(
         if (fill) nbr[wpos++] = id;
         else sum += cell_start[id + 1] - cell_start[id];
         ++total;
+        c0 += t < n0;
+        c1 += t >= n0 && t < n01;
       }
       if (!fill) {
         cnt[cell] = total;
         ub[cell] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+        if (ccount) { ccount[cell] = c0; ccount[ncells + cell] = c1; }
       }
     }
   }
@@ -187,9 +195,24 @@ __global__ void dense_fill_kernel(const uint64_t* __restrict__ cell_key, uint32_
 
 void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                        uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,
-                       uint32_t** ub_out, uint64_t* total, bool* dense_out) {
-  std::vector<int8_t> offs = stencil_offsets(g);
-  const int noffs = (int)(offs.size() / g.d);
+                       uint32_t** ub_out, uint64_t* total, bool* dense_out, const uint32_t** ccls) {
+  std::vector<int8_t> offs0 = stencil_offsets(g);
+  const int noffs = (int)(offs0.size() / g.d);
+  // rows by class of lattice L1 distance (1, 2, >= 3; gap order inside a
+  // class) so that ClusterCore's waves read only their segment
+  std::vector<int8_t> offs;
+  offs.reserve(offs0.size());
+  int ncls[3] = {0, 0, 0};
+  for (int cl = 0; cl < 3; ++cl)
+    for (int t = 0; t < noffs; ++t) {
+      int l1 = 0;
+      for (int k = 0; k < g.d; ++k) l1 += std::abs((int)offs0[(size_t)t * g.d + k]);
+      const int c = l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);
+      if (c != cl) continue;
+      offs.insert(offs.end(), offs0.begin() + (size_t)t * g.d, offs0.begin() + (size_t)(t + 1) * g.d);
+      ++ncls[cl];
+    }
+  const int n0 = ncls[0], n01 = ncls[0] + ncls[1];
   // dense directory when the padded lattice is small relative to n (d <= 3 only)
   Lattice lat{{0, 0, 0}};
   bool dense = false;
@@ -231,6 +254,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
   uint32_t* ub = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
+  uint32_t* ccount = c.alloc<uint32_t>(2 * (size_t)ncells);
   const bool warp = ncells < WARP_PER_CELL_BELOW;
   const unsigned grid = warp ? grid_for((int64_t)ncells * 32, 256, 1 << 30) : grid_for(ncells, 256, 1 << 30);
   auto launch = [&](int fill, uint32_t* list) {
@@ -239,7 +263,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
       constexpr bool DN = decltype(Dn)::value, WP = decltype(Wp)::value;
       nbr_stencil_kernel<DIM, DN, WP><<<grid, 256, 0, c.st>>>(fill, cell_key, ncells, g, doffs, noffs, T,
                                                               mask, c.dense_dir, lat, cell_start, cnt, ub,
-                                                              off, list);
+                                                              off, list, n0, n01, ccount);
     };
     using F = std::false_type;
     using Tt = std::true_type;
@@ -264,6 +288,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
   *nbr_off = off;
   *nbr = list;
   *ub_out = ub;
+  *ccls = ccount;
 }
 
 // ------------------------------------------------------------ all-pairs cells
