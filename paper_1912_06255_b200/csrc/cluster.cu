@@ -233,72 +233,96 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
 }
 
 // One wave of ClusterCore straight from the neighbour CSR (no pair list):
-// a warp per core cell g, lanes over its row; an entry h is a candidate of
-// wave w if h < g ("g > h"), h holds core points and the pair's
-// lattice L1 distance falls in the wave. Find filter, small BCPs in the lane
-// and the queue of large ones as in wave_kernel. Counts candidate pairs in
-// *npairs (every wave once).
-template <int D, bool WIDE, bool APX>
+// a group of G lanes per core cell g, lanes over its row; an entry h is a
+// candidate of wave w if h < g ("g > h"), h holds core points and
+// the pair's lattice L1 distance falls in the wave. Find filter, small BCPs in
+// the lane and the queue of large ones as in wave_kernel. Counts candidate
+// pairs in *npairs (every wave once). G < 32 serves short rows (the face
+// segment of class-sorted rows holds at most 2d cells): each group walks its
+// own cells and the warp runs until all of its groups are done.
+template <int D, bool WIDE, bool APX, int G>
 __global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, CellsView cv, Geo g,
                                                        const int32_t* __restrict__ Ps,
                                                        const uint32_t* __restrict__ core_cnt, uint32_t* parent,
                                                        uint2* __restrict__ large, uint32_t* __restrict__ nlarge,
                                                        unsigned long long* tested, unsigned long long* npairs) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  static_assert(G == 8 || G == 16 || G == 32, "group size");
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1);
+  constexpr uint32_t NG = 32 / G;
+  const uint32_t gstride = ((gridDim.x * blockDim.x) >> 5) * NG;
+  const bool by_class = cv.ccls && nwaves == NWAVES;  // class-sorted rows: the wave's segment only
   uint32_t mine = 0, cand = 0;
-  for (uint32_t gc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gc < cv.ncells; gc += nwarps) {
-    const uint32_t kg = core_cnt[gc];
-    if (kg == 0) continue;
-    const uint64_t key_g = cv.cell_key[gc];
-    uint64_t r0 = cv.nbr_off[gc], r1 = cv.nbr_off[gc + 1];
-    const bool by_class = cv.ccls && nwaves == NWAVES;  // class-sorted rows: the wave's segment only
-    if (by_class) {
-      const uint32_t c1 = cv.ccls[gc], c2 = cv.ccls[cv.ncells + gc];
-      if (wave == 0) r1 = r0 + c1;
-      else if (wave == 1) { r0 += c1; r1 = r0 + c2; }
-      else r0 += c1 + c2;
+  uint32_t gc = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NG + lane / G;
+  uint32_t kg = 0;
+  uint64_t key_g = 0, t0 = 0, r1 = 0;
+  // move the group to its next core cell with a non-empty segment
+  auto seek = [&]() {
+    for (; gc < cv.ncells; gc += gstride) {
+      kg = core_cnt[gc];
+      if (kg == 0) continue;
+      uint64_t r0 = cv.nbr_off[gc];
+      r1 = cv.nbr_off[gc + 1];
+      if (by_class) {
+        const uint32_t c1 = cv.ccls[gc], c2 = cv.ccls[cv.ncells + gc];
+        if (wave == 0) r1 = r0 + c1;
+        else if (wave == 1) { r0 += c1; r1 = r0 + c2; }
+        else r0 += c1 + c2;
+      }
+      if (r0 < r1) {
+        t0 = r0;
+        if (!by_class && nwaves > 1) key_g = cv.cell_key[gc];
+        return;
+      }
     }
-    for (uint64_t t0 = r0; t0 < r1; t0 += 32) {
-      const uint64_t t = t0 + lane;
-      uint2 p = make_uint2(gc, 0);
-      bool is = false, need = false, small = false;
-      if (t < r1) {
-        const uint32_t h = cv.nbr[t];
-        p.y = h;
-        if (h < gc) {
-          const uint32_t kh = core_cnt[h];
-          is = kh > 0 && (by_class || nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
-          if (is) {
-            need = uf_find(parent, gc) != uf_find(parent, h);
-            small = need && (uint64_t)kg * kh <= SMALL_PAIR;
-          }
+  };
+  seek();
+  while (__any_sync(DB_FULL, gc < cv.ncells)) {
+    const bool act = gc < cv.ncells;
+    const uint64_t t = t0 + gl;
+    uint2 p = make_uint2(gc, 0);
+    bool is = false, need = false, small = false;
+    if (act && t < r1) {
+      const uint32_t h = cv.nbr[t];
+      p.y = h;
+      if (h < gc) {
+        const uint32_t kh = core_cnt[h];
+        is = kh > 0 && (by_class || nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
+        if (is) {
+          need = uf_find(parent, gc) != uf_find(parent, h);
+          small = need && (uint64_t)kg * kh <= SMALL_PAIR;
         }
       }
-      cand += is;
-      mine += need;
-      const uint32_t lm = __ballot_sync(DB_FULL, need && !small);
-      if (lm) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(nlarge, (uint32_t)__popc(lm));
-        base = __shfl_sync(DB_FULL, base, 0);
-        if (need && !small) large[base + __popc(lm & lanemask_lt())] = p;
-      }
-      if (small) {
-        const uint32_t sa = cv.cell_start[p.x], ea = sa + kg;
-        const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
-        bool hit = false;
-        int32_t a[D], q[D];
-        for (uint32_t u = sa; u < ea && !hit; ++u) {
-          PtLoad<D>::load(Ps, u, a);
-          if (APX) connect_prep<D>(a, g, a);
-          for (uint32_t v = sb; v < eb; ++v) {
-            PtLoad<D>::load(Ps, v, q);
-            if (APX) connect_prep<D>(q, g, q);
-            if (APX ? connect_q<D, WIDE>(a, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
-          }
+    }
+    cand += is;
+    mine += need;
+    const uint32_t lm = __ballot_sync(DB_FULL, need && !small);
+    if (lm) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(nlarge, (uint32_t)__popc(lm));
+      base = __shfl_sync(DB_FULL, base, 0);
+      if (need && !small) large[base + __popc(lm & lanemask_lt())] = p;
+    }
+    if (small) {
+      const uint32_t sa = cv.cell_start[p.x], ea = sa + kg;
+      const uint32_t sb = cv.cell_start[p.y], eb = sb + core_cnt[p.y];
+      bool hit = false;
+      int32_t a[D], q[D];
+      for (uint32_t u = sa; u < ea && !hit; ++u) {
+        PtLoad<D>::load(Ps, u, a);
+        if (APX) connect_prep<D>(a, g, a);
+        for (uint32_t v = sb; v < eb; ++v) {
+          PtLoad<D>::load(Ps, v, q);
+          if (APX) connect_prep<D>(q, g, q);
+          if (APX ? connect_q<D, WIDE>(a, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
         }
-        if (hit) uf_link(parent, p.x, p.y);
+      }
+      if (hit) uf_link(parent, p.x, p.y);
+    }
+    if (act) {
+      t0 += G;
+      if (t0 >= r1) {
+        gc += gstride;
+        seek();
       }
     }
   }
@@ -355,15 +379,26 @@ void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, 
   uint2* large = c.alloc<uint2>(nbr_total);
   uint32_t* nlarge = c.alloc<uint32_t>(NWAVES);
   c.zero(nlarge, sizeof(uint32_t) * NWAVES);
-  const unsigned wgrid = grid_for((int64_t)nc * 32, 256, c.sms * 16);
   for (int w = 0; w < nw; ++w) {
+    // the face segment of class-sorted rows is short (<= 2d cells): groups of 8
+    const bool narrow = cv.ccls && nw == NWAVES && w == 0;
+    const unsigned wgrid = grid_for((int64_t)nc * (narrow ? 8 : 32), 256, c.sms * 16);
     dispatch(g.D, wide, [&]<int D, bool W>() {
-      if (g.at)
-        wave_csr_kernel<D, W, true><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large, nlarge + w,
-                                                             tested, npairs_out);
-      else
-        wave_csr_kernel<D, W, false><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
-                                                              nlarge + w, tested, npairs_out);
+      if (g.at) {
+        if (narrow)
+          wave_csr_kernel<D, W, true, 8><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+                                                                  nlarge + w, tested, npairs_out);
+        else
+          wave_csr_kernel<D, W, true, 32><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+                                                                   nlarge + w, tested, npairs_out);
+      } else {
+        if (narrow)
+          wave_csr_kernel<D, W, false, 8><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+                                                                   nlarge + w, tested, npairs_out);
+        else
+          wave_csr_kernel<D, W, false, 32><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+                                                                    nlarge + w, tested, npairs_out);
+      }
     });
     c.launched();
     bcp_large(c, g, cv, Ps, core_cnt, parent, large, nlarge + w, (uint32_t)nbr_total, wide, qt);
