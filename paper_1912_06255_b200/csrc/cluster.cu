@@ -115,7 +115,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
       if (__any_sync(DB_FULL, mine)) return true;
     }
     bool dn = false;
-    if (lane == 0) dn = uf_find(parent, p.x) == uf_find(parent, p.y);
+    if (lane == 0) dn = uf_same(parent, p.x, p.y);
     if (__shfl_sync(DB_FULL, dn, 0)) return false;
   }
   return false;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += nwarps) {
     const uint2 p = list[i];
     bool done = false;
-    if (lane == 0) done = uf_find(parent, p.x) == uf_find(parent, p.y);
+    if (lane == 0) done = uf_same(parent, p.x, p.y);
     if (__shfl_sync(DB_FULL, done, 0)) continue;
     // a tree on an all-core side (f2): search it; else the block BCP
     bool hit;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, Cel
         const uint32_t kh = core_cnt[h];
         is = kh > 0 && (by_class || nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
         if (is) {
-          need = uf_find(parent, gc) != uf_find(parent, h);
+          need = !uf_same(parent, gc, h);
           small = need && (uint64_t)kg * kh <= SMALL_PAIR;
         }
       }

@@ -217,6 +217,26 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
   }
 }
 
+// Root through L1-cached loads, no writes. A cached parent value may be stale
+// but is always an ancestor taken at some earlier time (values only move up
+// the tree, ids strictly decrease along every chain, so the walk ends), and
+// components only merge: equal stale roots prove a and b connected, unequal
+// ones prove nothing. Keeps the Find filter off the one L2 line of a large
+// component's root, which every volatile Find reads (same-address hot spot).
+__device__ __forceinline__ uint32_t uf_root_cached(const uint32_t* parent, uint32_t x) {
+  while (true) {
+    const uint32_t px = __ldca(parent + x);
+    if (px == x) return x;
+    x = px;
+  }
+}
+
+// Find(a) == Find(b): the cached walk first, the coherent one if it differs.
+__device__ __forceinline__ bool uf_same(uint32_t* parent, uint32_t a, uint32_t b) {
+  if (uf_root_cached(parent, a) == uf_root_cached(parent, b)) return true;
+  return uf_find(parent, a) == uf_find(parent, b);
+}
+
 __device__ __forceinline__ void uf_link(uint32_t* parent, uint32_t a, uint32_t b) {
   while (true) {
     a = uf_find(parent, a);
