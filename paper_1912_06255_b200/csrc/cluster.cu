@@ -352,6 +352,24 @@ void uf_init_list(Ctx& c, uint32_t* parent, const uint32_t* list, uint32_t m) {
   c.launched();
 }
 
+// parent[x] = Find(x) for the listed cells (all when list is null), between
+// passes, so that the next pass's parent comparison (uf_same_hop) settles
+// most pairs in one hop (a concurrent Link only moves a root below another
+// root, so the stored value stays an ancestor).
+__global__ void uf_flatten_kernel(uint32_t* parent, const uint32_t* __restrict__ list, uint32_t m) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+    const uint32_t x = list ? list[t] : t;
+    const uint32_t r = uf_find(parent, x);
+    if (r != x) parent[x] = r;
+  }
+}
+
+void uf_flatten(Ctx& c, uint32_t* parent, const uint32_t* list, uint32_t m) {
+  if (m == 0) return;
+  uf_flatten_kernel<<<grid_for(m, 256, c.sms * 8), 256, 0, c.st>>>(parent, list, m);
+  c.launched();
+}
+
 void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,
                uint32_t* parent, const uint2* list, const uint32_t* count, uint32_t cap, bool wide,
                const QTrees* qt) {

@@ -237,6 +237,16 @@ __device__ __forceinline__ bool uf_same(uint32_t* parent, uint32_t a, uint32_t b
   return uf_find(parent, a) == uf_find(parent, b);
 }
 
+// Find(a) == Find(b) with the parents compared first: equal parents (both
+// ancestors) prove the pair connected with two loads spread over the array,
+// none of them on the root's line. Pays off after a flatten pass
+// (parent[x] = root), when most pairs share one root.
+__device__ __forceinline__ bool uf_same_hop(uint32_t* parent, uint32_t a, uint32_t b) {
+  volatile uint32_t* p = parent;
+  if (p[a] == p[b]) return true;
+  return uf_find(parent, a) == uf_find(parent, b);
+}
+
 __device__ __forceinline__ void uf_link(uint32_t* parent, uint32_t a, uint32_t b) {
   while (true) {
     a = uf_find(parent, a);

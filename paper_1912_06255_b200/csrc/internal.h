@@ -303,6 +303,7 @@ void sparse_release(SparseOut* o);
 
 // ---- cluster.cu (a8, a9) ----
 void uf_init_list(Ctx& c, uint32_t* parent, const uint32_t* list, uint32_t m);  // list[0..m) only
+void uf_flatten(Ctx& c, uint32_t* parent, const uint32_t* list, uint32_t m);  // parent[x] = Find(x)
 void uf_init(Ctx& c, uint32_t* parent, uint32_t n);
 // warp-per-pair BCP over list[0 .. min(*count, cap)) with Link on success
 void bcp_large(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, const uint32_t* core_cnt,

@@ -506,7 +506,13 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
       k = min(32u, a.ncore - r0);
     }
     const uint32_t items = k * (uint32_t)nb;
-    for (uint32_t it = lane; it < items; it += 32) {
+    // warp-uniform rounds of 32 items, reconverged after each: left to
+    // independent thread scheduling the lanes drift apart over their runs and
+    // the h loop issued with ~3 of 32 lanes active (ncu, uniform-3d eps=1000)
+    for (uint32_t it0 = 0; it0 < items; it0 += 32) {
+      __syncwarp();
+      const uint32_t it = it0 + lane;
+      if (it >= items) continue;
       const uint32_t ci = it / nb, col = it - ci * nb;
       const uint32_t g = BY_CELLS ? r0 + (uint32_t)__fns(cm, 0, ci + 1) : a.core_list[r0 + ci];
       const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
@@ -517,7 +523,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
       for (uint32_t r = id0; r < id0 + nc; ++r) {
         const uint32_t h = a.core_list[r];
         const uint32_t kh = a.core_cnt[h];
-        if (find_first && uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
+        if (find_first && uf_same_hop(a.parent, g, h)) continue;
         if ((uint64_t)kg * kh > SP_SMALL) {
           if (uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
           const uint32_t slot = atomicAdd(a.counters + 2, 1u);
@@ -1040,6 +1046,7 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
         if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass == 1);
         else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass == 1);
         c.launched();
+        if (two && pass == 0) uf_flatten(c, parent, a.core_list, a.ncore);
       }
     });
     bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
