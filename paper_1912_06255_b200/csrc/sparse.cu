@@ -65,6 +65,7 @@ struct SpArgs {
   const uint32_t* bcmask;
   int nbcols;
   int nbnear;                // back columns at gap 0 (first in the list): ClusterCore's first pass
+  int nbmid;                 // back columns adjacent laterally (gap <= d - 1): the second pass
   uint32_t ncells;
   const uint32_t* cell_start;
   const uint64_t* cell_key;
@@ -943,6 +944,9 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.nbcols = (int)back.size();
   a.nbnear = 0;
   while (a.nbnear < a.nbcols && back[a.nbnear].first == 0) ++a.nbnear;
+  a.nbmid = a.nbnear;
+  // (columns whose lateral offsets are all within 1 have gap <= d - 1)
+  while (a.nbmid < a.nbcols && back[a.nbmid].first <= (unsigned)(g.d - 1)) ++a.nbmid;
   // a4: directory of all cells
   const uint64_t words = ((uint64_t)vol + 31) / 32 + 1;
   a.dir = dir ? dir : build_dir(c, a, words, nullptr, nullptr);
@@ -1038,15 +1042,16 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
       constexpr bool W = decltype(Wd)::value;
       // (two passes only when most cells hold core points: on sparse core
       // cells (c5: 8%) the second probe pass costs more than it prunes)
+      // (with two: gap 0, then gap 1, then the rest, flattening in between)
       const bool two = 2ull * a.ncore >= cv.ncells;
-      for (int pass = 0; pass < 2; ++pass) {
-        const int lo = two ? (pass ? a.nbnear : 0) : (pass ? a.nbcols : 0);
-        const int hi = two ? (pass ? a.nbcols : a.nbnear) : a.nbcols;
+      const int cut[4] = {0, two ? a.nbnear : a.nbcols, two ? a.nbmid : a.nbcols, a.nbcols};
+      for (int pass = 0; pass < 3; ++pass) {
+        const int lo = cut[pass], hi = cut[pass + 1];
         if (lo == hi) continue;
-        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass == 1);
-        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass == 1);
+        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
+        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         c.launched();
-        if (two && pass == 0) uf_flatten(c, parent, a.core_list, a.ncore);
+        if (two && hi < a.nbcols) uf_flatten(c, parent, a.core_list, a.ncore);
       }
     });
     bcp_large(c, g, cv, Ps, core_cnt, parent, a.large, a.counters + 2, a.large_cap, wide);
