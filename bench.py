@@ -136,6 +136,77 @@ def job_value(npts_per_rank_step: int, steps: int, local_ms: float, dist=None, d
     return npts_per_rank_step * steps * world / (local_ms / 1000.0), local_ms
 
 
+# --------------------------------------------------------------- e2e calls
+def e2e_calls(pkg, host, order, streams, dev, keep=False):
+    """One e2e step: len(streams) host threads, one CUDA stream each, take the
+    runs from a shared queue (in `order`) and call the blocking host-buffer C
+    ABI (pinned input, pinned caller-owned outputs). host[k] = (cfg, pinned
+    points, (core, cluster, border_off, border_ids) pinned buffers).
+    Returns (seconds, H2D bytes, D2H bytes, results by run if keep)."""
+    import torch
+    nthreads = len(streams)
+    b_in = [0] * nthreads
+    b_out = [0] * nthreads
+    errs = []
+    results = [None] * len(host)
+    nxt = [0]
+    lock = threading.Lock()
+
+    def worker(w):
+        try:
+            torch.cuda.set_device(dev)
+            while True:
+                with lock:  # runs taken in turn from a shared queue
+                    if nxt[0] >= len(order):
+                        return
+                    k = order[nxt[0]]
+                    nxt[0] += 1
+                cfg, hp, outs = host[k]
+                r = pkg.dbscan(hp, cfg.eps, cfg.min_pts, out=outs, stream=streams[w])
+                b_in[w] += hp.numel() * 4
+                # bytes that cross the link: the library writes constant
+                # outputs on the host (border_off when no point is a border
+                # point; every output when no point is core)
+                nnz = len(r.border_ids)
+                if r.n_core:
+                    b_out[w] += cfg.n * (1 + 4) + ((8 * (cfg.n + 1) + 4 * nnz) if nnz else 0)
+                if keep:
+                    results[k] = r
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker, args=(w,)) for w in range(nthreads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    dt = time.perf_counter() - t0
+    if errs:
+        raise errs[0]
+    return dt, sum(b_in), sum(b_out), results
+
+
+def e2e_order(host, dev_ms):
+    """The run with the longest device time first (its kernels overlap the
+    other runs' input copies), then by input size, largest first (measured on
+    B200: 22.1 ms per step against 24.4 ms for input size alone)."""
+    first = max(range(len(host)), key=lambda k: dev_ms[k])
+    return [first] + sorted((k for k in range(len(host)) if k != first), key=lambda k: -host[k][1].numel())
+
+
+def e2e_host_buffers(data, torch):
+    """Pinned host input and caller-owned pinned output buffers per run."""
+    host = []
+    for name, cfg, _, pts in data:
+        hp = torch.from_numpy(pts).pin_memory()
+        outs = (torch.empty(cfg.n, dtype=torch.uint8).pin_memory(),
+                torch.empty(cfg.n, dtype=torch.int32).pin_memory(),
+                torch.empty(cfg.n + 1, dtype=torch.int64).pin_memory(),
+                torch.empty(cfg.n, dtype=torch.int32).pin_memory())
+        host.append((cfg, hp, outs))
+    return host
+
+
 # ------------------------------------------------------------- reference
 def run_reference(args):
     """Time the CPU oracle O2 on a bounded sample of every run."""
@@ -334,62 +405,15 @@ def main():
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        host = []
+        host = e2e_host_buffers(data, torch)
         h2d = d2h = 0
-        for name, cfg, _, pts in data:
-            hp = torch.from_numpy(pts).pin_memory()
-            outs = (torch.empty(cfg.n, dtype=torch.uint8).pin_memory(),
-                    torch.empty(cfg.n, dtype=torch.int32).pin_memory(),
-                    torch.empty(cfg.n + 1, dtype=torch.int64).pin_memory(),
-                    torch.empty(cfg.n, dtype=torch.int32).pin_memory())
-            host.append((cfg, hp, outs))
-        # E2E_THREADS host threads, each with its own CUDA stream, take the runs
-        # from a shared queue through the blocking host-buffer C-ABI call (the
-        # library keeps no global state): one call's H2D overlaps another's
-        # kernels and D2H.
         streams = [torch.cuda.Stream(dev) for _ in range(E2E_THREADS)]
-        # the run with the longest device time first (its kernels overlap the
-        # other runs' input copies), then by input size, smallest last
-        # (measured on B200: 22.1 ms per step against 24.4 ms for input size
-        # alone and 26 ms for Johnson's two-machine rule)
         dev_ms = [statistics.median(per_run_ms[k]) for k in range(len(host))]
-        first = max(range(len(host)), key=lambda k: dev_ms[k])
-        order = [first] + sorted((k for k in range(len(host)) if k != first), key=lambda k: -host[k][1].numel())
+        order = e2e_order(host, dev_ms)
 
         def e2e_step():
             nonlocal h2d, d2h
-            b_in = [0] * E2E_THREADS
-            b_out = [0] * E2E_THREADS
-            errs = []
-
-            nxt = [0]
-            lock = threading.Lock()
-
-            def worker(w):
-                try:
-                    torch.cuda.set_device(dev)
-                    while True:
-                        with lock:  # runs taken in turn from a shared queue, largest inputs first
-                            if nxt[0] >= len(order):
-                                return
-                            k = order[nxt[0]]
-                            nxt[0] += 1
-                        cfg, hp, outs = host[k]
-                        r = pkg.dbscan(hp, cfg.eps, cfg.min_pts, out=outs, stream=streams[w])
-                        b_in[w] += hp.numel() * 4
-                        b_out[w] += cfg.n * (1 + 4 + 8) + 8 + 4 * len(r.border_ids)
-                except Exception as e:  # pragma: no cover
-                    errs.append(e)
-            t0 = time.perf_counter()
-            ths = [threading.Thread(target=worker, args=(w,)) for w in range(E2E_THREADS)]
-            for th in ths:
-                th.start()
-            for th in ths:
-                th.join()
-            dt = time.perf_counter() - t0
-            if errs:
-                raise errs[0]
-            h2d, d2h = sum(b_in), sum(b_out)
+            dt, h2d, d2h, _ = e2e_calls(pkg, host, order, streams, dev)
             return dt
         # (at least 5: the first steps create and grow the threads' workspaces,
         # device memory mapped in the pool and pinned staging, ~0.2 s each)

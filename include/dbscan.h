@@ -104,6 +104,9 @@ extern "C" {
                                         overflowed bricks taken by the thread kernel, 0 none  */
 #define DBSCAN_STAT_POINT_BORDER 18  /* sparse ClusterBorder from the non-core points (1) or from
                                         the core cells (0)                                    */
+#define DBSCAN_STAT_SPARSE_PASSES 19 /* sparse ClusterCore: pair-search launches over the back columns
+                                        (1; 3 when most cells hold core points: gap-0 columns, then
+                                        laterally adjacent ones, then the rest, flattened between) */
 #define DBSCAN_NSTATS            20
 
 typedef struct dbscan_result {
@@ -131,15 +134,18 @@ typedef struct dbscan_result {
  *   eps      radius, >= 1; the predicate is  sum_k (x_k - y_k)^2 <= eps^2  (closed).
  *   min_pts  >= 1; min_pts > n makes every point noise.
  *   flags    DBSCAN_F_* bits.
- *   stream   cudaStream_t to run on (NULL = legacy default stream). Without F_DEVICE_IO
- *            the call returns after the outputs are in host memory; with it the call
- *            returns once border_ids is allocated (one internal sync for its size) and
- *            the remaining work is ordered on `stream`.
+ *   stream   cudaStream_t to run on (NULL = legacy default stream). The call blocks
+ *            until its work on `stream` is done (with F_DEVICE_IO the outputs are then
+ *            final in device memory; without it they are in host memory). It reads a
+ *            few scalars back during the call (cell count, border count, ...).
  *   out      result; zeroed on entry unless F_CALLER_OUT (then core/cluster/border_off
  *            must be set by the caller). On error *out is left with every library-
  *            allocated pointer NULL and nothing leaks.
  * Ownership: the caller releases library-allocated outputs with dbscan_result_free.
- * Threads: no global mutable state; concurrent calls on different streams are safe.
+ * Threads: concurrent calls on different streams (any host threads) are safe. Shared
+ *   state: a mutex-protected process-wide pool of workspaces (dbscan_release_workspace),
+ *   and a mutex that serialises the host-to-device input copies of concurrent host-path
+ *   calls (each call computes while the next one's input is in flight).
  * Returns DBSCAN_OK or a negative code above.
  */
 int dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min_pts,
@@ -181,6 +187,27 @@ const char *dbscan_error_string(int code);
 
 /* Name of stage i (0 <= i < DBSCAN_NSTAGES) for reports. */
 const char *dbscan_stage_name(int i);
+
+/*
+ * dbscan_peak_dist — U1 microbenchmark (SURVEY §2.7 `peak_dist`, §8(d)): the
+ * measured throughput of the exact distance predicate ||p-q||^2 <= eps^2
+ * (P:L199-202), the unit of work of MarkCore (Alg 2; O(n minPts) tests,
+ * P:L1106-1121) and of the BCP (Alg 3). It is the denominator of
+ * the a6/a8 roofline fractions that bench.py reports. Not part of DBSCAN.
+ *   d        dimension 1..8 (candidates stored D-padded as the stage kernels do)
+ *   variant  0: the shipped uint32 `__sad` predicate; 1: the shipped 64-bit
+ *            clamped predicate; 2: an fp64 FMA predicate (north_star's fp64 pipe)
+ *   qt       queries held in registers per thread (1, 2 or 4) against a
+ *            1024-point shared-memory tile of candidates (one tile load per
+ *            candidate serves qt tests)
+ *   reps     passes over the tile (about 90 us each on a B200 at qt = 1)
+ *   stream   cudaStream_t (NULL = legacy default); the call synchronises it
+ *   out: *tests_per_s; optional *ms (CUDA-event time of the timed launch, after
+ *   one untimed launch), *tests, *hits (tests that passed: about half).
+ * Returns DBSCAN_OK, DBSCAN_EINVAL (bad argument) or DBSCAN_ECUDA.
+ */
+int dbscan_peak_dist(int32_t d, int32_t variant, int32_t qt, int64_t reps, void *stream,
+                     double *tests_per_s, double *ms, int64_t *tests, int64_t *hits);
 
 /* Library version, as 10000*major + 100*minor + patch. */
 int dbscan_version(void);

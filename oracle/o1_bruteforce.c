@@ -189,11 +189,11 @@ void o1_labels_near_for(const int32_t *pts, int64_t n, int32_t d, int64_t eps,
 }
 
 /*
- * Sampled check helper: for each sampled core point s, the number of core
- * points within eps whose label differs from label[sample[s]] (must be 0:
- * P:L206-211, eps-adjacent core points share a cluster), and the minimum
- * index among core points within eps that carry the same label (used to
- * check label <= index for the component).
+ * Sampled check helper: for each sampled point s, viol[s] = the number of
+ * core points q with dist2(p_s, q) <= eps^2 (closed ball) whose
+ * label differs from label[sample[s]]. For a core sample this must be 0
+ * (eps-adjacent core points share a cluster). Pinned negatively in
+ * tests/test_oracle.py (a split cluster and an exact-eps tie both count).
  */
 void o1_core_label_violations(const int32_t *pts, int64_t n, int32_t d, int64_t eps,
                               const uint8_t *core, const int32_t *label,

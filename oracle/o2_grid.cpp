@@ -200,12 +200,17 @@ int o2_dbscan(const int32_t *pts, int64_t n, int32_t d, int64_t eps, int64_t min
       for (int64_t c = 0; c < nc; ++c) probe(c, qq, nbr.data() + noff[c]);
     }
   } else {
+    // each row scans every other cell in ascending order (rows are
+    // independent, so they are spread over threads; the row content and
+    // order are those of a sequential scan)
     std::vector<std::vector<int64_t>> tmp((size_t)nc);
+#pragma omp parallel for schedule(dynamic, 64)
     for (int64_t a = 0; a < nc; ++a)
-      for (int64_t b = a + 1; b < nc; ++b) {
+      for (int64_t b = 0; b < nc; ++b) {
+        if (b == a) continue;
         bool ok = true;
         for (int k = 0; k < d && ok; ++k) ok = std::llabs(ck(a, k) - ck(b, k)) <= R;
-        if (ok) { tmp[a].push_back(b); tmp[b].push_back(a); }
+        if (ok) tmp[a].push_back(b);
       }
     for (int64_t c = 0; c < nc; ++c) {
       nbr.insert(nbr.end(), tmp[c].begin(), tmp[c].end());

@@ -28,7 +28,7 @@ import numpy as np
 __all__ = ["dbscan", "Result", "lib_path", "load", "F_DEVICE_IO", "F_TIMING", "F_CALLER_OUT",
            "F_FORCE_STENCIL", "F_FORCE_TREE", "F_FORCE_WIDE", "F_NO_WAVES", "F_NO_SPARSE",
            "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "F_COUNT_WORK", "F_QUADTREE", "F_NO_BRICK", "STAGES", "release_workspace",
-           "STATS",
+           "STATS", "peak_dist",
            "DBSCANError"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -43,7 +43,8 @@ NSTAGES, NSTATS = 12, 20
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
-         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick", "point_border"]
+         "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick", "point_border",
+         "sparse_passes"]
 
 
 class _Result(C.Structure):
@@ -94,6 +95,10 @@ def load():
         lib.dbscan_stage_name.argtypes = [C.c_int]
         lib.dbscan_stage_name.restype = C.c_char_p
         lib.dbscan_version.restype = C.c_int
+        lib.dbscan_peak_dist.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        lib.dbscan_peak_dist.restype = C.c_int
         lib.dbscan_release_workspace.argtypes = []
         lib.dbscan_release_workspace.restype = None
         _lib = lib
@@ -127,6 +132,23 @@ class _DeviceBuffer:
         if _lib is not None and self._res is not None:
             _lib.dbscan_result_free(C.byref(self._res))
             self._res = None
+
+
+def peak_dist(d: int, variant: int = 0, qt: int = 1, reps: int = 200, stream=None) -> dict:
+    """U1 microbenchmark (dbscan_peak_dist): measured distance tests per second
+    of the exact predicate on the current CUDA device. variant 0 = shipped
+    uint32 path, 1 = shipped 64-bit path, 2 = fp64."""
+    lib = load()
+    tps, ms = C.c_double(), C.c_double()
+    tests, hits = C.c_int64(), C.c_int64()
+    st = None
+    if stream is not None:
+        st = C.c_void_p(stream.cuda_stream)
+    rc = lib.dbscan_peak_dist(int(d), int(variant), int(qt), int(reps), st, C.byref(tps), C.byref(ms),
+                              C.byref(tests), C.byref(hits))
+    _check(lib, rc)
+    return {"d": d, "variant": ("u32", "i64", "f64")[variant], "qt": qt, "tests_per_s": tps.value,
+            "ms": ms.value, "tests": tests.value, "hits": hits.value}
 
 
 def release_workspace() -> None:
@@ -177,7 +199,10 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
         pts = points.contiguous()
         n, d = pts.shape
         dev = pts.device
-        st = torch.cuda.current_stream(dev) if stream is None else stream
+        cur = torch.cuda.current_stream(dev)
+        st = cur if stream is None else stream
+        if st != cur:  # order the call after the work that produced `points` on the current stream
+            st.wait_stream(cur)
         core = torch.empty(n, dtype=torch.uint8, device=dev)
         cluster = torch.empty(n, dtype=torch.int32, device=dev)
         off = torch.empty(n + 1, dtype=torch.int64, device=dev)
@@ -186,6 +211,9 @@ def dbscan(points, eps: int, min_pts: int, *, flags: int = 0, timing: bool = Fal
             rc = _call(lib, C.c_void_p(pts.data_ptr()), n, d, int(eps), int(min_pts), rho,
                        flags | F_DEVICE_IO | F_CALLER_OUT, C.c_void_p(st.cuda_stream), C.byref(res))
         _check(lib, rc)
+        if st != cur:  # outputs come from the current stream's allocator but are written on st
+            for t in (core, cluster, off):
+                t.record_stream(st)
         nnz = int(res.nnz)
         if nnz > 0:
             ids = torch.as_tensor(_DeviceBuffer(res, res.border_ids, nnz, "<i4"), device=dev)

@@ -625,6 +625,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_APPROX_SIDE] = g.at;
   out->stats[DBSCAN_STAT_BRICK] = so.brick;
   out->stats[DBSCAN_STAT_POINT_BORDER] = so.point_border;
+  out->stats[DBSCAN_STAT_SPARSE_PASSES] = so.passes;
   return DBSCAN_OK;
 }
 
@@ -681,7 +682,7 @@ static int dbscan_impl(const int32_t* pts, int64_t n, int32_t d, int64_t eps, in
     return run(pts, n, d, eps, min_pts, flags, st, out, uids, ucap, rho);
   } catch (const Error& e) {
     g_last_error = e.what();
-    cudaDeviceSynchronize();  // the call's stream and its side stream
+    // (the call's stream and its side stream were synchronised by ~Ctx)
     (void)cudaGetLastError();
     free_priv(out);
     if (!caller_out) { out->core = nullptr; out->cluster = nullptr; out->border_off = nullptr; }

@@ -143,8 +143,10 @@ struct Ctx {
     finished = true;
     if (ar && used > ar->cap) arena_grow(*ar, used, st);
   }
-  ~Ctx() {  // error paths: the stream may still use the workspace; wait for it
+  ~Ctx() {  // error paths: the streams may still use the workspace; wait for both
+    // before the workspace goes back to the pool (Ctx is destroyed before WsGuard)
     if (!finished && st) (void)cudaStreamSynchronize(st);
+    if (!finished && side) (void)cudaStreamSynchronize(side);
     (void)cudaGetLastError();
     free_all();
   }
@@ -282,6 +284,7 @@ struct SparseOut {
   uint32_t ncore = 0;
   int brick = 0;                 // MarkCore: 1 brick kernel, 2 with overflowed bricks
   bool point_border = false;     // ClusterBorder from the non-core points (few of them)
+  int passes = 0;                // ClusterCore pair-search launches (stats[DBSCAN_STAT_SPARSE_PASSES])
 };
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);
 // a4 + a6 + a7 on the rank directories: core flags, core-first compaction,

@@ -1051,6 +1051,7 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
         if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         c.launched();
+        ++o->passes;
         if (two && hi < a.nbcols) uf_flatten(c, parent, a.core_list, a.ncore);
       }
     });

@@ -27,8 +27,8 @@ def declared_functions():
 
 
 def test_header_declares_entry_points():
-    assert declared_functions() == ["dbscan", "dbscan_approx", "dbscan_error_string", "dbscan_release_workspace",
-                                    "dbscan_result_free", "dbscan_stage_name", "dbscan_version"]
+    assert declared_functions() == ["dbscan", "dbscan_approx", "dbscan_error_string", "dbscan_peak_dist",
+                                    "dbscan_release_workspace", "dbscan_result_free", "dbscan_stage_name", "dbscan_version"]
 
 
 def test_exports(lib):
@@ -66,6 +66,13 @@ def test_einval_before_cuda(lib, args):
     assert rc == -1
     assert lib.dbscan_error_string(rc).startswith(b"invalid argument")
     assert not res.border_ids and not res.priv
+
+
+@pytest.mark.parametrize("args", [(0, 0, 1, 1), (9, 0, 1, 1), (3, 3, 1, 1), (3, 0, 3, 1), (3, 0, 1, 0)])
+def test_peak_dist_einval(lib, args):
+    """U1 rejects bad arguments before touching CUDA."""
+    v = C.c_double()
+    assert lib.dbscan_peak_dist(*args, None, C.byref(v), None, None, None) == -1
 
 
 def test_product_does_not_import_oracle():

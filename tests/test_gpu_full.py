@@ -23,6 +23,15 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_1912_06255_b200 as pkg  # noqa: E402
 
 SAMPLES = 256
+_O2 = {}
+
+
+def o2_of(oracle_lib, name):
+    """O2 on a BASELINE run, computed once per session (several tests compare with it)."""
+    if name not in _O2:
+        cfg = datagen.CONFIGS[name]
+        _O2[name] = oracle_lib.o2(cfg.points(), cfg.eps, cfg.min_pts)
+    return _O2[name]
 
 
 def run_gpu(pts, eps, mp):
@@ -57,8 +66,37 @@ def test_full_config(oracle_lib, name):
     if len(cs):
         assert (oracle_lib.core_label_violations(pts, cfg.eps, g.core, g.cluster, cs) == 0).all()
     # whole output vs the independent grid oracle
-    o = oracle_lib.o2(pts, cfg.eps, cfg.min_pts)
-    assert_same(g, o, name)
+    assert_same(g, o2_of(oracle_lib, name), name)
+
+
+def test_e2e_host_path_full(oracle_lib):
+    """The path bench.py's `e2e` times, at full size: every BASELINE run
+    (c2, c3, c4 5D/7D, c5 at minPts 10 and 10^4) through the blocking
+    host-buffer C ABI with pinned inputs and caller-owned pinned outputs,
+    three host threads with one stream each taking the runs from a shared
+    queue (concurrent calls, serialised input copies, side-stream output
+    copies, host-written constant outputs). Two steps; every output
+    byte-compared with O2."""
+    import bench
+    names = ["c2", "c3", "c4_5d", "c4_7d", "c5_10", "c5_10k"]
+    data = [(nm, datagen.CONFIGS[nm], None, datagen.CONFIGS[nm].points()) for nm in names]
+    dev = torch.device("cuda", 0)
+    host = bench.e2e_host_buffers(data, torch)
+    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    order = bench.e2e_order(host, [float(c.n) for _, c, _, _ in data])
+    for step in range(2):
+        for _, _, outs in host:  # stale bytes must not survive a step
+            for t in outs:
+                t.fill_(0x5A if t.dtype == torch.uint8 else 0x5A5A5A5A)
+        _, h2d, _, res = bench.e2e_calls(pkg, host, order, streams, dev, keep=True)
+        assert h2d == sum(p.nbytes for _, _, _, p in data)
+        for (nm, cfg, _, _), r in zip(data, res):
+            class O:
+                pass
+            o = O()
+            o.core, o.cluster, o.border_off = (t.numpy() for t in (r.core, r.cluster, r.border_off))
+            o.border_ids = np.asarray(r.border_ids)
+            assert_same(o, o2_of(oracle_lib, nm), f"e2e {nm} step {step}")
 
 
 @pytest.mark.parametrize("kind", ["uniform", "spreader"])

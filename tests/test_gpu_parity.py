@@ -278,7 +278,7 @@ def test_point_centric_border_vs_o2(oracle_lib):
         assert_same(np_result(t), want, "csr")
 
 
-def test_grouping_choice():
+def test_grouping_choice(oracle_lib):
     """Few cells: the hash counting sort groups the points; many distinct
     cells (uniform 3D, 2M points, ~2M cells) on a lattice too large to count
     over: the radix sort runs; on a small lattice: the lattice counting sort;
@@ -291,16 +291,18 @@ def test_grouping_choice():
     assert a.stats["hash_group"] == 0 and a.stats["sort_passes"] > 0
     b = gpu(many, 3000, 3, pkg.F_RADIX_GROUP)
     assert_same(np_result(a), np_result(b), "hash fallback vs radix")
+    assert_same(np_result(a), oracle_lib.o2(many, 3000, 3), "radix vs O2")
     dense = datagen.uniform(2_000_000, 3, 40_000, 7)
     c = gpu(dense, 300, 4)
     assert c.stats["hash_group"] == 2 and c.stats["sparse"] == 1
     assert_same(np_result(c), np_result(gpu(dense, 300, 4, pkg.F_RADIX_GROUP)), "lattice vs radix")
+    assert_same(np_result(c), oracle_lib.o2(dense, 300, 4), "lattice vs O2")
     # Alg 2's global bound: no point can reach minPts, nothing is grouped
     e = gpu(dense, 300, 5000)
     assert e.n_core == 0 and e.stats["ncells"] == 0 and e.n_noise == len(dense)
 
 
-def test_lattice_overflow_falls_back():
+def test_lattice_overflow_falls_back(oracle_lib):
     """More than 255 points in one lattice cell overflows its 8-bit counter:
     the radix sort takes over with the same result."""
     pts = datagen.uniform(300_000, 2, 3000, 8)
@@ -308,6 +310,7 @@ def test_lattice_overflow_falls_back():
     r = gpu(pts, 20, 3, pkg.F_LATTICE_GROUP)
     assert r.stats["hash_group"] == 0
     assert_same(np_result(r), np_result(gpu(pts, 20, 3, pkg.F_RADIX_GROUP)), "overflow fallback")
+    assert_same(np_result(r), oracle_lib.o2(pts, 20, 3), "overflow fallback vs O2")
 
 
 @pytest.mark.parametrize("d", [2, 3, 5, 7])
@@ -449,3 +452,39 @@ def test_host_path_constant_outputs(oracle_lib):
         r = pkg.dbscan(torch.from_numpy(np.ascontiguousarray(p)).pin_memory(), eps, mp, out=outs)
         assert_same(np_result(r), want, f"eps={eps} minPts={mp}")
         assert len(want.border_ids) == 0
+
+
+@pytest.mark.parametrize("d,hi", [(5, 20_000), (7, 10_300)])
+def test_cell_tree_at_scale_vs_o2(oracle_lib, d, hi):
+    """The cell tree (Morton-ordered BVH over the cells, the GPU form of the
+    paper's k-d tree range queries) is the default neighbour
+    search for d >= 4 above 131,072 cells: uniform 5D / 7D points with ~one
+    point per cell and ~10 eps-neighbours each (core, border and noise
+    points, tens to hundreds of clusters) — a multi-block bottom-up build and
+    deep DFS queries — against O2 (all-pairs cell scan, independent code)."""
+    pts = datagen.uniform(160_000, d, hi, 41 + d)
+    r = gpu(pts, 2000, 10)
+    assert r.stats["tree"] == 1 and r.stats["ncells"] > 131_072, r.stats
+    want = oracle_lib.o2(pts, 2000, 10)
+    assert want.core.sum() > 10_000 and len(want.border_ids) > 10_000
+    assert_same(np_result(r), want, f"cell tree d={d}")
+
+
+@pytest.mark.parametrize("flags", [pkg.F_FORCE_SPARSE, 0, pkg.F_NO_SPARSE])
+def test_sparse_three_pass_cluster_vs_o2(oracle_lib, flags):
+    """Sparse ClusterCore in three launches (gap-0 back columns, laterally
+    adjacent columns, the rest; the union-find flattened between and the
+    parent comparison before Find) runs when most cells hold core points:
+    dense uniform 3D where every cell holds core points and one component
+    spans the lattice, plus a sparser corner. Checked against O2, and against
+    the CSR path (F_NO_SPARSE)."""
+    pts = datagen.uniform(400_000, 3, 20_000, 55)
+    pts[:20_000] = datagen.uniform(20_000, 3, 60_000, 56)  # sparse surroundings: border and noise
+    r = gpu(pts, 700, 6, flags)
+    if not flags & pkg.F_NO_SPARSE:
+        assert r.stats["sparse"] == 1 and r.stats["sparse_passes"] == 3, r.stats
+    else:
+        assert r.stats["sparse"] == 0
+    want = oracle_lib.o2(pts, 700, 6)
+    assert len(want.border_ids) > 0
+    assert_same(np_result(r), want, f"three-pass flags={flags}")

@@ -196,3 +196,37 @@ def test_sampled_helpers(oracle_lib):
         assert list(ids[off[i]:off[i + 1]]) == list(c.rows(i))
     v = oracle_lib.core_label_violations(pts, eps, c.core, c.cluster, np.flatnonzero(c.core))
     assert (v == 0).all()
+
+
+def test_core_label_violations_negative(oracle_lib):
+    """Negative pins for core_label_violations: a labelling that
+    splits one cluster must count violations, and the closed ball (<= eps,
+    P:L201-202) must count a pair at exactly eps, not only pairs inside it."""
+    # chain 0 - 3 - 6 - 9 on a line, eps = 3: every gap is exactly eps
+    pts = np.array([[0, 0], [3, 0], [6, 0], [9, 0]], dtype=np.int32)
+    core = np.ones(4, dtype=np.uint8)
+    good = np.zeros(4, dtype=np.int32)
+    assert (oracle_lib.core_label_violations(pts, 3, core, good, np.arange(4)) == 0).all()
+    # split at the exact-eps gap between points 1 and 2: each sees one violation
+    split = np.array([0, 0, 2, 2], dtype=np.int32)
+    v = oracle_lib.core_label_violations(pts, 3, core, split, np.arange(4))
+    assert v.tolist() == [0, 1, 1, 0]
+    # one eps less: no point is within eps of another, the split is not seen
+    assert (oracle_lib.core_label_violations(pts, 2, core, split, np.arange(4)) == 0).all()
+    # a non-core neighbour with another label is not a violation
+    core2 = np.array([1, 1, 0, 1], dtype=np.uint8)
+    lab2 = np.array([0, 0, -1, 3], dtype=np.int32)
+    assert (oracle_lib.core_label_violations(pts, 3, core2, lab2, np.array([0, 1, 3])) == 0).all()
+    # 3-4-5 triangle in 2D at eps = 5 (an exact diagonal tie): points 0 and 2
+    tri = np.array([[0, 0], [30, 0], [3, 4]], dtype=np.int32)
+    lab3 = np.array([0, 1, 2], dtype=np.int32)
+    v = oracle_lib.core_label_violations(tri, 5, np.ones(3, dtype=np.uint8), lab3, np.arange(3))
+    assert v.tolist() == [1, 0, 1]
+    # a 7D tie (6^2 + 2^2 + 3^2 = 7^2) counts, one unit further does not
+    a = np.zeros((2, 7), dtype=np.int32)
+    a[1, :3] = [6, 2, 3]
+    lab = np.array([0, 1], dtype=np.int32)
+    one = np.ones(2, dtype=np.uint8)
+    assert oracle_lib.core_label_violations(a, 7, one, lab, np.arange(2)).tolist() == [1, 1]
+    a[1, 0] = 7
+    assert oracle_lib.core_label_violations(a, 7, one, lab, np.arange(2)).tolist() == [0, 0]
