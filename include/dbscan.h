@@ -57,8 +57,9 @@ extern "C" {
                                       the hash-table or lattice counting sorts)              */
 #define DBSCAN_F_LATTICE_GROUP 1024u /* skip the hash counting sort: use the lattice counting
                                       sort whenever d <= 3 and its lattice fits               */
-#define DBSCAN_F_COUNT_WORK  2048u /* count the sparse MarkCore's distance tests into
-                                      stats[DBSCAN_STAT_MARKCORE_TESTS] (measurement runs)   */
+#define DBSCAN_F_COUNT_WORK  2048u /* reserved (accepted, no effect): distance tests are counted
+                                      by the measurement build libdbscan_b200_count.so
+                                      (`make count`), see DBSCAN_STAT_COUNTING_BUILD         */
 #define DBSCAN_F_QUADTREE    4096u /* our-exact-qt: MarkCore's
                                       RangeCount on cells with >= 256 points traverses a
                                       per-cell tree instead of scanning (CSR path)           */
@@ -96,7 +97,7 @@ extern "C" {
 #define DBSCAN_STAT_SPARSE       12  /* 1 if the cell-centric sparse-lattice path ran       */
 #define DBSCAN_STAT_HASH_GROUP   13  /* grouping: 1 hash counting sort, 2 lattice counting sort,
                                         0 LSD radix sort + segmentation                      */
-#define DBSCAN_STAT_MARKCORE_TESTS 14 /* distance tests of the sparse MarkCore (F_COUNT_WORK)  */
+#define DBSCAN_STAT_MARKCORE_TESTS 14 /* distance tests of MarkCore, a6 (measurement build only) */
 #define DBSCAN_STAT_QT_NODES     15  /* tree nodes built with F_QUADTREE                         */
 #define DBSCAN_STAT_APPROX_SIDE  16  /* dbscan_approx: sub-cell side t of the connectivity test
                                         (0: the test is exact)                                */
@@ -107,7 +108,14 @@ extern "C" {
 #define DBSCAN_STAT_SPARSE_PASSES 19 /* sparse ClusterCore: pair-search launches over the back columns
                                         (1; 3 when most cells hold core points: gap-0 columns, then
                                         laterally adjacent ones, then the rest, flattened between) */
-#define DBSCAN_NSTATS            20
+#define DBSCAN_STAT_BCP_TESTS    20  /* distance tests of the BCPs of ClusterCore, a8 (measurement
+                                        build only)                                           */
+#define DBSCAN_STAT_BORDER_TESTS 21  /* distance tests of ClusterBorder, a10 (measurement build)  */
+#define DBSCAN_STAT_COUNTING_BUILD 22 /* 1 in libdbscan_b200_count.so (built with -DDB_COUNT_WORK:
+                                        every distance test adds to a device counter; not
+                                        thread-safe across concurrent calls, measurement only),
+                                        0 in the product library                              */
+#define DBSCAN_NSTATS            24
 
 typedef struct dbscan_result {
   int64_t  n;

@@ -42,6 +42,7 @@ __device__ __forceinline__ bool cell_has_core_within(const int32_t* p, uint32_t 
   int32_t q[D];
   for (uint32_t u = s; u < e; ++u) {
     PtLoad<D>::load(Ps, u, q);
+    DB_WORK(2);
     if (within<D, WIDE>(p, q, clampc, eps2)) return true;
   }
   return false;

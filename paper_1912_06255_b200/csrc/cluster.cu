@@ -110,6 +110,7 @@ __device__ bool warp_bcp(uint2 p, const CellsView& cv, const Geo& g, const int32
         int32_t q[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
+        if (keep) DB_WORK(1);
         mine |= keep && (APX ? connect_q<D, WIDE>(qa, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2));
       }
       if (__any_sync(DB_FULL, mine)) return true;
@@ -168,6 +169,7 @@ __device__ bool warp_bcp_tree(uint32_t ga, uint32_t hb, const CellsView& cv, con
           int32_t q[D];
 #pragma unroll
           for (int k = 0; k < D; ++k) q[k] = __shfl_sync(DB_FULL, b[k], src);
+          if (keep) DB_WORK(1);
           mine |= keep && within<D, WIDE>(a, q, g.clampc, g.eps2);
         }
         if (__any_sync(DB_FULL, mine)) return true;
@@ -313,6 +315,7 @@ __global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, Cel
         for (uint32_t v = sb; v < eb; ++v) {
           PtLoad<D>::load(Ps, v, q);
           if (APX) connect_prep<D>(q, g, q);
+          DB_WORK(1);
           if (APX ? connect_q<D, WIDE>(a, q, g) : within<D, WIDE>(a, q, g.clampc, g.eps2)) { hit = true; break; }
         }
       }

@@ -14,6 +14,24 @@
 namespace db {
 
 // ---------------------------------------------------------------------------
+// Work counters of the measurement build (make count: libdbscan_b200_count.so,
+// -DDB_COUNT_WORK): every distance test of MarkCore (slot 0, a6), of the BCP
+// in ClusterCore (slot 1, a8) and of ClusterBorder (slot 2, a10) adds one to a
+// per-translation-unit device counter, summed into stats[] after the call
+// (DBSCAN_STAT_*_TESTS). bench.py runs that build in a separate, untimed pass
+// to get the algorithmic work behind the a6/a8/a10 roofline fractions; the
+// product build compiles the macros away.
+// ---------------------------------------------------------------------------
+#ifdef DB_COUNT_WORK
+static __device__ unsigned long long db_work_ctr[4];
+#define DB_WORK(slot) atomicAdd(&::db::db_work_ctr[slot], 1ull)
+#define DB_WORK_N(slot, n) atomicAdd(&::db::db_work_ctr[slot], (unsigned long long)(n))
+#else
+#define DB_WORK(slot) ((void)0)
+#define DB_WORK_N(slot, n) ((void)0)
+#endif
+
+// ---------------------------------------------------------------------------
 // Grid geometry (reading 5).
 // Integer cell side s = isqrt(floor(eps^2/d)) + 1 so that two points of one
 // cell differ by <= s-1 per axis and d (s-1)^2 <= eps^2 (same cell => within

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
           const uint32_t he = cv.cell_start[h + 1];
           for (uint32_t u = cv.cell_start[h]; u < he; ++u) {
             PtLoad<D>::load(Ps, u, q);
+            DB_WORK(0);
             count += within<D, WIDE>(p, q, clampc, eps2);
             if (count >= min_pts) break;
           }
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const
         const uint32_t oex = __shfl_sync(DB_FULL, excl, lo);
         bool hit = false;
         if (tt < total) {
+          DB_WORK(0);
           PtLoad<D>::load(Ps, ost + (tt - oex), q);
           hit = within<D, WIDE>(p, q, clampc, eps2);
         }
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(256) mark_core_qt_kernel(CellsView cv, const i
         bool hit = false;
         if (tt < total) {
           PtLoad<D>::load(Ps, ost + (tt - oex), q);
+          DB_WORK(0);
           hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
         }
         count += __popc(__ballot_sync(DB_FULL, hit));
@@ -218,7 +221,8 @@ __global__ void __launch_bounds__(256) mark_core_qt_kernel(CellsView cv, const i
             bool hit = false;
             if (u < e0) {
               PtLoad<D>::load(Ps, u, q);
-              hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
+              DB_WORK(0);
+          hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
             }
             count += __popc(__ballot_sync(DB_FULL, hit));
             continue;

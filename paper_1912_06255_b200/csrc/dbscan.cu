@@ -43,6 +43,21 @@ static int bit_width(uint64_t v) {
   return w;
 }
 
+// work counters of the measurement build (common.cuh DB_WORK), one reader per
+// translation unit (registered by static initialisers: function-local list)
+static std::vector<WorkIo>& work_fns() {
+  static std::vector<WorkIo> v;
+  return v;
+}
+void work_register(WorkIo fn) { work_fns().push_back(fn); }
+static constexpr bool counting_build() {
+#ifdef DB_COUNT_WORK
+  return true;
+#else
+  return false;
+#endif
+}
+
 struct Priv {
   bool dev = false;
   cudaStream_t st = nullptr;  // stream of the call; device outputs are freed on it
@@ -299,9 +314,10 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   c.join_ev = evs.e[1];
   c.stage_fn = [](void* t, int s) { static_cast<Timer*>(t)->stage(s); };
   c.stage_obj = &tm;
-  if (flags & DBSCAN_F_COUNT_WORK) {
-    c.work = c.alloc<unsigned long long>(4);
-    c.zero(c.work, 4 * sizeof(unsigned long long));
+  unsigned long long hw[4] = {0, 0, 0, 0};
+  if (counting_build()) {  // measurement build: start the call's counters at zero
+    for (WorkIo fn : work_fns()) fn(hw, st);
+    hw[0] = hw[1] = hw[2] = hw[3] = 0;
   }
 
   // ---- outputs
@@ -582,8 +598,6 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   }
   uint32_t h32[4];
   unsigned long long h64[3];
-  unsigned long long hw[4] = {0, 0, 0, 0};
-  const unsigned long long* hw_h = c.work ? c.fetch(c.work, 4) : nullptr;
   const uint32_t* h32_h = c.fetch(cnt32, 4);
   const unsigned long long* h64_h = c.fetch(cnt64, 3);
   tm.close();  // (the last event; read after the stream is idle)
@@ -594,7 +608,8 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   c.finish();
   std::memcpy(h32, h32_h, sizeof(h32));
   std::memcpy(h64, h64_h, sizeof(h64));
-  if (hw_h) std::memcpy(hw, hw_h, sizeof(hw));
+  if (counting_build())
+    for (WorkIo fn : work_fns()) fn(hw, st);
   if (c.tracing) {
     c.mark("end");
     const double t0 = c.trace.front().second;
@@ -621,6 +636,9 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_SPARSE] = sparse;
   out->stats[DBSCAN_STAT_HASH_GROUP] = hash_group ? 1 : (lat_group ? 2 : 0);
   out->stats[DBSCAN_STAT_MARKCORE_TESTS] = (int64_t)hw[0];
+  out->stats[DBSCAN_STAT_BCP_TESTS] = (int64_t)hw[1];
+  out->stats[DBSCAN_STAT_BORDER_TESTS] = (int64_t)hw[2];
+  out->stats[DBSCAN_STAT_COUNTING_BUILD] = counting_build();
   out->stats[DBSCAN_STAT_QT_NODES] = (int64_t)qtrees.nodes;
   out->stats[DBSCAN_STAT_APPROX_SIDE] = g.at;
   out->stats[DBSCAN_STAT_BRICK] = so.brick;

@@ -33,11 +33,9 @@ void arena_grow(Arena& a, size_t need, cudaStream_t st);  // (after the stream i
 // Per-call context: stream, stream-ordered temporaries, launch counter.
 struct Ctx {
   cudaStream_t st = nullptr;
-  // stage timer hook (begin stage s; no-op without F_TIMING) and optional
-  // work counters (F_COUNT_WORK: device [4] u64, see DBSCAN_STAT_*_TESTS)
+  // stage timer hook (begin stage s; no-op without F_TIMING)
   void (*stage_fn)(void*, int) = nullptr;
   void* stage_obj = nullptr;
-  unsigned long long* work = nullptr;
   // a second stream for independent work (set by the caller with two events
   // for the fork and the join)
   cudaStream_t side = nullptr;
@@ -165,6 +163,26 @@ struct Ctx {
     return *h;
   }
 };
+
+// Work counters of the measurement build (common.cuh DB_WORK): every
+// translation unit registers a function that reads (and zeroes) its counters.
+typedef void (*WorkIo)(unsigned long long* add_to /* [4] */, cudaStream_t st);
+void work_register(WorkIo fn);
+#ifdef DB_COUNT_WORK
+namespace {
+void db_work_io(unsigned long long* add_to, cudaStream_t st) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  DB_CUDA(cudaMemcpyFromSymbolAsync(h, db_work_ctr, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+  DB_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < 4; ++i) add_to[i] += h[i];
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  DB_CUDA(cudaMemcpyToSymbolAsync(db_work_ctr, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+}
+struct DbWorkReg {
+  DbWorkReg() { work_register(&db_work_io); }
+} db_work_reg;
+}  // namespace
+#endif
 
 // ---- scan.cu ----
 // out[0..n] = exclusive prefix sums of in[0..n-1]; out[n] = total.

@@ -200,19 +200,16 @@ __global__ void __launch_bounds__(256) cell_max_kernel(const uint32_t* __restric
 // column for the warp. Measured alternatives on c5: a warp per
 // cell (latency-bound), a flat or two-phase per-point loop, U = 4, and
 // symmetric counting with atomics were all slower.
-// COUNT (F_COUNT_WORK, measurement runs only): distance tests, summed into
-// work[0] with one atomic per block.
 // fb != NULL (after the brick kernel): runs only if *fb is set, and only on
 // the points of bricks that overflowed (core_s still 0xff).
-template <int DIM, int D, bool WIDE, int U, bool COUNT>
-__global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, unsigned long long* work, const uint32_t* fb) {
+template <int DIM, int D, bool WIDE, int U>
+__global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, const uint32_t* fb) {
   if (fb && *fb == 0) return;
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
   __syncthreads();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t tests = 0;
   if (j < a.n && (!fb || a.core_s[j] == 0xff)) {
     const uint32_t g = a.cell_of[j];
     const uint32_t m = a.cell_start[g + 1] - a.cell_start[g];
@@ -237,13 +234,12 @@ __global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, unsigned long lo
 #pragma unroll
           for (int k = 0; k < U; ++k)
             if (u + k < ue) count += within_dim<DIM, D, WIDE>(p, q[k], a.g);
-          if (COUNT) tests += min((uint32_t)U, ue - u);
+          DB_WORK_N(0, min((uint32_t)U, ue - u));
         }
       }
       a.core_s[j] = count >= need;
     }
   }
-  if (COUNT) block_add_u64(tests, work);
 }
 
 // Brick variant of MarkCore (d = 3, R <= 2; the default for 3D sparse
@@ -275,11 +271,10 @@ struct BrickSmem {
   uint32_t total, own;
 };
 
-template <bool WIDE, bool COUNT>
+template <bool WIDE>
 __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a, const int8_t* __restrict__ geo,
                                                                     uint32_t nby, uint32_t nbz,
-                                                                    uint32_t* overflow,
-                                                                    unsigned long long* work) {
+                                                                    uint32_t* overflow) {
   extern __shared__ __align__(16) uint8_t brick_raw[];
   BrickSmem& S = *reinterpret_cast<BrickSmem*>(brick_raw);
   const uint32_t bid = blockIdx.x;
@@ -368,7 +363,6 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
   // candidate) steps so that lanes stay converged whatever the column sizes
   const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
   const int ncols = a.ncols;
-  uint32_t tests = 0;
   for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
     // its column: the last one whose own prefix is <= t (never an empty one)
     int cc = 0;
@@ -405,13 +399,12 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
       const int32_t q[4] = {qv.x, qv.y, qv.z, qv.w};
       const bool live = u < u1;
       count += (live && within_dim<3, 4, WIDE>(p, q, a.g)) ? 1u : 0u;
-      if (COUNT) tests += live;
+      if (live) DB_WORK(0);
       u += live;
       if (count >= need) break;
     }
     a.core_s[j] = count >= need;
   }
-  if (COUNT) block_add_u64(tests, work);
 }
 
 // Thread per cell: core count (a7); mixed cells are listed for the partition.
@@ -540,6 +533,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
           for (uint32_t v = sh; v < sh + kh; ++v) {
             int32_t q[D];
             load_pt<D>(a.Ps, v, q);
+            DB_WORK(1);
             if (APX ? connect_test<D, WIDE>(p, q, a.g) : within_dim<DIM, D, WIDE>(p, q, a.g)) {
               hit = true;
               break;
@@ -562,6 +556,7 @@ __device__ __forceinline__ bool sp_core_within(const SpArgs& a, const int32_t* p
   for (uint32_t v = sh; v < sh + kh; ++v) {
     int32_t q[D];
     load_pt<D>(a.Ps, v, q);
+    DB_WORK(2);
     if (within_dim<DIM, D, WIDE>(p, q, a.g)) return true;
   }
   return false;
@@ -701,6 +696,7 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
       for (uint32_t v = sh; v < sh + kh && !hit; ++v) {
         int32_t q[D];
         load_pt<D>(a.Ps, v, q);
+        DB_WORK(2);
         hit = within_dim<DIM, D, WIDE>(p, q, a.g);
       }
       if (!hit) continue;
@@ -974,17 +970,11 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
       if constexpr (DIM == 3) {
-        auto launch = [&](auto kern, unsigned long long* work) {
-          DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, dgeo, nb[1], nb[2], a.counters + 1, work);
-          c.launched();
-        };
-        if (c.work) launch(sp_core_brick_kernel<W, true>, c.work);
-        else launch(sp_core_brick_kernel<W, false>, nullptr);
-        if (c.work)
-          sp_core_kernel<DIM, D, W, 2, true><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, c.work, a.counters + 1);
-        else
-          sp_core_kernel<DIM, D, W, 2, false><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr, a.counters + 1);
+        auto kern = sp_core_brick_kernel<W>;
+        DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, dgeo, nb[1], nb[2], a.counters + 1);
+        c.launched();
+        sp_core_kernel<DIM, D, W, 2><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, a.counters + 1);
         c.launched();
       }
     });
@@ -992,10 +982,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
-      if (c.work)
-        sp_core_kernel<DIM, D, W, 2, true><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, c.work, nullptr);
-      else
-        sp_core_kernel<DIM, D, W, 2, false><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr, nullptr);
+      sp_core_kernel<DIM, D, W, 2><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, nullptr);
     });
     c.launched();
   }
