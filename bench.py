@@ -44,17 +44,62 @@ REF_FRACTION = 0.05
 E2E_THREADS = int(os.environ.get("DB_E2E_THREADS", "3"))
 
 
-# int32 issue peak: 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz = 37.2 T
-# lane-instructions/s; a 3D distance test is ~10 int32 SASS instructions
-# (3 x VABSDIFF/VIMNMX/IMAD + compare): ~3.7e12 tests/s
-INT_TESTS_PEAK = 148 * 4 * 32 * 1.965e9 / 10
+# Stage rooflines. Algorithmic work per
+# stage and run: HBM stages in bytes (SURVEY §8(d) formulas), distance-test
+# stages in tests counted by the measurement build (libdbscan_b200_count.so,
+# an untimed pass in a subprocess). Denominators: MEASURED_PEAKS.json hbm_gbs
+# (driver-measured copy bandwidth) and U1 `peak_dist` (dbscan_peak_dist,
+# measured live here: the shipped predicate on shared-memory tiles, best of
+# 1/2/4 register queries per thread, at the run's d and arithmetic path).
+STAGE_DEF = [  # (stage key in stage_ms, row, bound, kernels)
+    ("bbox", "a1 bbox", "hbm", "bbox_kernel"),
+    ("keys+sort", "a2-a3 grouping", "hbm", "group_count/group_scatter (hash), lat_* (lattice), keys+radix_pass"),
+    ("segment", "a2-a3 grouping", "hbm", "segment_kernel (radix path)"),
+    ("neighbors", "a4-a5 neighbour cells", "l2", "nbr_stencil / nbr_brute / tree_query"),
+    ("markcore", "a6 MarkCore", "alu", "sp_core_brick_kernel / sp_core_kernel / mark_core_*"),
+    ("compact", "a7 compaction", "hbm", "sp_cells_kernel / core_count_kernel / partition_kernel"),
+    ("cluster", "a8 ClusterCore", "alu", "sp_pairs_kernel / wave_csr_kernel / bcp_large_kernel"),
+    ("labels", "a9 labels", "hbm", "label_roots_kernel ... core_from_cluster_kernel"),
+    ("border", "a10 ClusterBorder", "alu", "sp_border_emit_kernel / border_kernel + count/scan/fill"),
+]
+
+
+def stage_work(row, cfg, st, work):
+    """Algorithmic work of one stage of one run: (amount, unit) — bytes for
+    HBM stages, distance tests for the ALU stages."""
+    n, d, nc = cfg.n, cfg.d, st["ncells"]
+    if row == "a1 bbox":
+        return 4 * d * n, "B"
+    if row == "a2-a3 grouping":
+        # read the points, write them grouped, the permutation and the cell
+        # tables (SURVEY §8(d) minimum 2*4dn + 4n + 40 ncells); a run that
+        # ended at Alg 2's global bound after the count pass read the points once
+        return (2 * 4 * d * n + 4 * n + 40 * nc) if nc else 4 * d * n, "B"
+    if row == "a7 compaction":
+        return n + 8 * nc, "B"  # core flags read, core count + list per cell
+    if row == "a9 labels":
+        return 9 * n + 8 * nc, "B"  # SURVEY §8(d): n (1+4+4) + 8 ncells
+    key = {"a6 MarkCore": "markcore_tests", "a8 ClusterCore": "bcp_tests", "a10 ClusterBorder": "border_tests"}.get(row)
+    if key and work is not None:
+        return work.get(key, 0), "tests"
+    return None, None
+
+
+def measure_peaks(pkg, dims, wide_dims):
+    """U1 peak_dist per (d, path): max over register tiles qt = 1, 2, 4."""
+    out = {}
+    for d in sorted(dims):
+        for v in ([0] + ([1] if d in wide_dims else [])):
+            best = max(pkg.peak_dist(d, v, qt, reps=60)["tests_per_s"] for qt in (1, 2, 4))
+            out[(d, v)] = best
+    return out
 
 
 def load_traffic():
     """Per-launch DRAM bytes (read + write) from the committed ncu --set full
-    summary (profiles/r1_traffic.json), or {} when absent."""
+    summary (profiles/r2_traffic.json), or {} when absent."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             return json.load(f)
     except Exception:
         return {}
@@ -134,6 +179,37 @@ def job_value(npts_per_rank_step: int, steps: int, local_ms: float, dist=None, d
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         local_ms = float(t.item())
     return npts_per_rank_step * steps * world / (local_ms / 1000.0), local_ms
+
+
+# ------------------------------------------------------------ work pass
+def work_pass_child(args):
+    """(subprocess, DBSCAN_B200_COUNT=1) one call per run through the
+    measurement build; prints {run: {markcore_tests, bcp_tests, border_tests}}."""
+    import torch
+    import paper_1912_06255_b200 as pkg
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    out = {}
+    for name in [r for r in args.runs.split(",") if r]:
+        cfg = datagen.CONFIGS[name]
+        r = pkg.dbscan(torch.from_numpy(cfg.points()).to(dev), cfg.eps, cfg.min_pts)
+        assert r.stats["counting_build"] == 1, "work pass: not the measurement build"
+        out[name] = {k: r.stats[k] for k in ("markcore_tests", "bcp_tests", "border_tests")}
+        del r
+    print("WORK " + json.dumps(out), flush=True)
+
+
+def run_work_pass(runs, local):
+    env = dict(os.environ, DBSCAN_B200_COUNT="1", LOCAL_RANK=str(local))
+    for k in ("RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, os.path.abspath(__file__), "--work-pass", "--runs", ",".join(runs)],
+                       env=env, capture_output=True, text=True)
+    for line in p.stdout.splitlines():
+        if line.startswith("WORK "):
+            return json.loads(line[5:])
+    print("work pass failed:", p.stderr[-2000:], file=sys.stderr)
+    return {}
 
 
 # --------------------------------------------------------------- e2e calls
@@ -257,9 +333,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--detail", action="store_true", help="print per-run stage times to stderr")
+    ap.add_argument("--no-work", action="store_true", help="skip the work-counting pass (no ALU fractions)")
+    ap.add_argument("--work-pass", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.work_pass:
+        return work_pass_child(args)
 
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -302,13 +382,10 @@ def main():
             del r
         return ms, stages, launches, stats
 
-    # algorithmic work of the sparse MarkCore: one counting run per run (untimed)
-    work_tests = {}
-    for name, cfg, t, _ in data:
-        r = pkg.dbscan(t, cfg.eps, cfg.min_pts, flags=pkg.F_COUNT_WORK)
-        if r.stats.get("markcore_tests"):
-            work_tests[name] = r.stats["markcore_tests"]
-        del r
+    # algorithmic work of the distance-test stages: the measurement build in a
+    # subprocess (untimed; one call per run), and U1 peaks measured live
+    work = {} if args.no_work else run_work_pass(runs, local)
+    peaks_u1 = measure_peaks(pkg, {c.d for _, c, _, _ in data}, set())
     torch.cuda.synchronize()
     for _ in range(args.warmup):
         one_step(True)
@@ -344,10 +421,7 @@ def main():
     npts_step = sum(c.n for _, c, _, _ in data)
     value, total_ms = job_value(npts_step, args.steps, sum(step_ms), dist, dev)
 
-    # ---- rooflines. Stage times come from CUDA events the
-    # library records on the launching stream (F_TIMING); algorithmic work per
-    # run from the run's shape and, for the sparse MarkCore, from one counting
-    # run (F_COUNT_WORK) outside the timed region.
+    # ---- rooflines per run and stage
     peak, peak_kind = load_peaks()
     traffic = load_traffic()
     stage_tot = {}
@@ -355,52 +429,56 @@ def main():
         for k, v in stage_acc[i].items():
             if k != "total":
                 stage_tot[k] = stage_tot.get(k, 0.0) + v
+    step_stage_ms = sum(stage_tot.values()) / args.steps
     rooflines = []
-    # grouping (a2-a4): the largest HBM stage; algorithmic bytes = read the
-    # points twice + write the padded sorted points, index and cell id, plus
-    # the cell table (12 B per cell); the radix path adds its key passes
-    g_bytes = g_ms = 0.0
     for i, (name, cfg, t, _) in enumerate(data):
         st = stats[i]
-        D = 2 if cfg.d <= 2 else (4 if cfg.d <= 4 else 8)
-        by = (8 * cfg.d + 4 * D + 8) * cfg.n + 12 * st["ncells"]
-        if st["hash_group"] == 0 and st["sort_passes"]:
-            kb = 8 if st["key_bits"] > 32 else 4
-            by += (kb + 4) * cfg.n + st["sort_passes"] * 2 * (kb + 4) * cfg.n
-        g_bytes += by * args.steps
-        g_ms += stage_acc[i].get("keys+sort", 0.0) + stage_acc[i].get("segment", 0.0)
-    if g_ms > 0:
-        ach = g_bytes / (g_ms / 1e3) / 1e9
-        rooflines.append({"stage": "a2-a4 grouping", "bound": "hbm",
-                          "kernel": "group_count/group_scatter (hash), lat_* (lattice), radix_pass+segment",
-                          "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                          "traffic": traffic.get("grouping"),
-                          "traffic_note": "DRAM bytes per call of the grouping kernels by run, ncu --set full (cold L2)",
-                          "peak_kind": peak_kind,
-                          "ms_share": g_ms / max(1e-9, sum(stage_tot.values())),
-                          "note": "algorithmic bytes: 8d+4D+8 per point + 12 per cell (+ key passes on the radix path)"})
-    # sparse MarkCore (a6): int32 ALU issue bound; tests per second
-    for i, (name, cfg, t, _) in enumerate(data):
-        if stats[i]["sparse"] and work_tests.get(name):
-            ms = stage_acc[i].get("markcore", 0.0) / args.steps
+        merged = {}
+        for key, row, bound, kern in STAGE_DEF:
+            ms = stage_acc[i].get(key, 0.0) / args.steps
             if ms <= 0:
                 continue
-            ach = work_tests[name] / (ms / 1e3) / 1e12
-            tp = INT_TESTS_PEAK / 1e12
-            kname = "sp_core_brick_kernel" if stats[i].get("brick") else "sp_core_kernel"
-            rooflines.append({"stage": f"a6 MarkCore ({name})", "bound": "alu", "kernel": kname,
-                              "achieved": ach, "peak": tp, "unit": "T distance tests/s", "frac": ach / tp,
-                              "traffic": traffic.get(kname),
-                              "traffic_note": "DRAM bytes per launch, ncu --set full (cold L2)",
-                              "peak_kind": "derived (DESIGN.md §8): int32 issue rate / 10 SASS per 3D test",
-                              "launch_ms": ms,
-                              "ms_share": ms * args.steps / max(1e-9, sum(stage_tot.values())),
-                              "tests_per_launch": work_tests[name]})
-    # the headline is the dominant single KERNEL (the sparse MarkCore's
-    # brick kernel, one launch per c5 run, the longest kernel of the step);
-    # the grouping stage (several kernels per run) is reported beside it
-    kern = [r for r in rooflines if r["bound"] == "alu"]
-    roofline = max(kern or rooflines, key=lambda r: r["ms_share"]) if rooflines else None
+            e = merged.setdefault(row, {"run": name, "stage": row, "bound": bound, "kernel": kern, "ms": 0.0})
+            e["ms"] += ms
+            if key == "segment":
+                e["kernel"] += " + " + kern
+        for row, e in merged.items():
+            amount, unit = stage_work(row, cfg, st, work.get(name))
+            e["ms_share"] = e["ms"] / max(1e-9, step_stage_ms)
+            e["ms"] = round(e["ms"], 4)
+            if amount is None or e["bound"] == "l2":
+                e["frac"] = None
+                rooflines.append(e)
+                continue
+            if unit == "B":
+                ach = amount / (e["ms"] / 1e3) / 1e9
+                e.update({"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                          "algorithmic": amount, "peak_kind": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"})
+            else:
+                pk = peaks_u1.get((cfg.d, 1 if st["wide"] else 0))
+                if not amount or not pk:
+                    e["frac"] = None
+                    rooflines.append(e)
+                    continue
+                ach = amount / (e["ms"] / 1e3)
+                e.update({"achieved": ach / 1e12, "peak": pk / 1e12, "unit": "T distance tests/s",
+                          "frac": ach / pk, "algorithmic": amount,
+                          "peak_kind": f"U1 peak_dist measured live (d={cfg.d}, {'64-bit' if st['wide'] else 'uint32'} predicate)"})
+            e["traffic"] = traffic.get(name, {}).get(row)
+            rooflines.append(e)
+    # the headline: the stage with the largest share of the step (a single
+    # kernel dominates it: c5's MarkCore brick kernel, one launch per run)
+    cand = [r for r in rooflines if r.get("frac") is not None]
+    roofline = None
+    if cand:
+        top = max(cand, key=lambda r: r["ms_share"])
+        roofline = {k: top.get(k) for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+        roofline.update({"run": top["run"], "stage": top["stage"], "kernel": top["kernel"],
+                         "ms_per_launch": top["ms"], "ms_share": top["ms_share"],
+                         "algorithmic_per_launch": top["algorithmic"], "peak_kind": top["peak_kind"],
+                         "traffic_note": "DRAM bytes (read + write) of the stage's kernels per call, ncu --set full "
+                                         "(cold L2), profiles/r2_traffic.json"})
+    peaks_out = {f"d{d}_{'i64' if v else 'u32'}": round(p / 1e12, 4) for (d, v), p in peaks_u1.items()}
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None
@@ -459,7 +537,7 @@ def main():
                        "runs": runs, "points_per_step": npts_step, "l2": "flushed (256 MB write) before every run",
                        "stage_timing": "stage_ms and rooflines from a second pass of the same steps with the library stage events (F_TIMING), outside the timed region",
                        "parallelism": "replicas" if world > 1 else "single GPU"},
-            "roofline": roofline, "rooflines": rooflines, "stage_ms_per_step": {k: round(v / args.steps, 4) for k, v in stage_tot.items()},
+            "roofline": roofline, "rooflines": rooflines, "u1_peak_T_tests_per_s": peaks_out, "stage_ms_per_step": {k: round(v / args.steps, 4) for k, v in stage_tot.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "runs": run_info}
     if args.detail and rank == 0:
