@@ -492,6 +492,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   } else if (sparse) {
     // ---- a4 + a6 + a7 on the rank directory
     tm.stage(DBSCAN_STAGE_MARKCORE);
+    so.flags = flags;
     so.counters = c.alloc<uint32_t>(6);
     c.zero(so.counters, 24);
     core_cells = sparse_pipeline(c, g, cv, Ps, sidx, core_s, core_cnt, n, min_pts, wide, lat_dir,
@@ -644,6 +645,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_BRICK] = so.brick;
   out->stats[DBSCAN_STAT_POINT_BORDER] = so.point_border;
   out->stats[DBSCAN_STAT_SPARSE_PASSES] = so.passes;
+  out->stats[DBSCAN_STAT_BRICK_BORDER] = so.brick_border;
   return DBSCAN_OK;
 }
 

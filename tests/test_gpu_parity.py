@@ -257,8 +257,10 @@ def test_brick_markcore_vs_o2(oracle_lib, grouping):
         if want == 0:
             assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"dense eps={eps}")
             continue
+        if r.stats["point_border"] == 0:
+            assert r.stats["brick_border"] == 1, r.stats
         t = gpu(pts, eps, mp, grouping | pkg.F_NO_BRICK)
-        assert t.stats["brick"] == 0
+        assert t.stats["brick"] == 0 and t.stats["brick_border"] == 0
         assert_same(np_result(r), np_result(t), f"brick vs thread eps={eps}")
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"brick eps={eps}")
 
@@ -488,3 +490,38 @@ def test_sparse_three_pass_cluster_vs_o2(oracle_lib, flags):
     want = oracle_lib.o2(pts, 700, 6)
     assert len(want.border_ids) > 0
     assert_same(np_result(r), want, f"three-pass flags={flags}")
+
+
+def _star(centre, eps):
+    """A non-core point at `centre` with six clusters within eps around it
+    (one core point per axis direction at 0.96 eps, each joined to a blob of
+    12 duplicates 0.6 eps further out): the centre is a border point of six
+    clusters, more than the SP_MAXL label slots."""
+    pts = [centre]
+    for ax in range(3):
+        for sg in (-1, 1):
+            v = np.zeros(3, np.int64)
+            v[ax] = sg
+            pts.append(centre + v * int(0.96 * eps))
+            pts.extend([centre + v * int(1.56 * eps)] * 12)
+    return np.array(pts, np.int32)
+
+
+@pytest.mark.parametrize("flags", [0, pkg.F_NO_BRICK])
+def test_brick_border_many_labels_vs_o2(oracle_lib, flags):
+    """Brick ClusterBorder on a c5-like lattice (0.24 points per cell) with
+    planted border points in 6 clusters each (label-set overflow: enumerated
+    by the overflow kernels), against O2 and the core-centric path."""
+    pts = datagen.uniform(300_000, 3, 30_000, 61)
+    eps, mp = 500, 10
+    centres = [np.array([5000, 5000, 5000]), np.array([20000, 9000, 15000]), np.array([12000, 25000, 4000])]
+    keep = np.ones(len(pts), bool)
+    for c in centres:
+        keep &= np.abs(pts.astype(np.int64) - c).max(1) > 2000
+    pts = np.concatenate([pts[keep]] + [_star(c, eps) for c in centres]).astype(np.int32)
+    r = gpu(pts, eps, mp, flags)
+    assert r.stats["sparse"] == 1 and r.stats["brick_border"] == (0 if flags else 1), r.stats
+    want = oracle_lib.o2(pts, eps, mp)
+    rows = np.diff(want.border_off)
+    assert rows.max() == 6 and (rows == 6).sum() == 3
+    assert_same(np_result(r), want, f"star flags={flags}")
