@@ -118,7 +118,10 @@ extern "C" {
                                         0 in the product library                              */
 #define DBSCAN_STAT_BRICK_BORDER 23 /* 1 if the sparse ClusterBorder ran as the brick kernel (label
                                         sets from bricks of staged core points)               */
-#define DBSCAN_NSTATS            24
+#define DBSCAN_STAT_BRICK_CLUSTER 24 /* 1 if the sparse ClusterCore ran as the brick kernel (BCPs of
+                                        staged core points; the pair kernels only for bricks
+                                        that overflowed)                                      */
+#define DBSCAN_NSTATS            32
 
 typedef struct dbscan_result {
   int64_t  n;

@@ -42,12 +42,13 @@ F_DEVICE_IO, F_TIMING, F_CALLER_OUT = 1, 2, 4
 F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
 F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP, F_COUNT_WORK = 128, 256, 512, 1024, 2048
 F_QUADTREE, F_NO_BRICK = 4096, 8192
-NSTAGES, NSTATS = 12, 24
+NSTAGES, NSTATS = 12, 32
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
          "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick", "point_border",
-         "sparse_passes", "bcp_tests", "border_tests", "counting_build", "brick_border"]
+         "sparse_passes", "bcp_tests", "border_tests", "counting_build", "brick_border",
+         "brick_cluster"]
 
 
 class _Result(C.Structure):

@@ -533,7 +533,8 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 // instead of testing and linking every pair against one contended root.
 template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
 __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
-                                                       int col_hi, bool find_first) {
+                                                       int col_hi, bool find_first, const uint32_t* run_if) {
+  if (run_if && *run_if == 0) return;  // (after the ClusterCore brick kernel: only if a brick overflowed)
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   const int nb = col_hi - col_lo;
@@ -870,7 +871,16 @@ struct BorderBrickSmem {
   uint32_t ctotal, own;
 };
 
-template <bool WIDE>
+// MODE 0: ClusterBorder (above). MODE 1: ClusterCore (Alg 3) on
+// the same staging, the padding lane holding the core point's cell id: a
+// thread per own CORE point p (cell g) walks the windows and, for every core
+// point q of a cell h < g ("higher id checks lower": each pair
+// of cells from one side) within eps, links g and h (lock-free union-find,
+// P:L837-846) — the BCP of every pair of neighbouring core cells, tested
+// point pair by point pair from shared memory. Overflowed bricks: *overflow
+// is set and the column-probing pair kernels run instead (they test every
+// pair again; links are idempotent).
+template <bool WIDE, int MODE>
 __global__ void __launch_bounds__(BRK_THREADS, 2) sp_border_brick_kernel(SpArgs a, const BrickCols cols,
                                                                      uint32_t nby, uint32_t nbz,
                                                                      uint32_t* overflow, uint8_t* cnt_s,
@@ -905,8 +915,8 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_border_brick_kernel(SpArgs 
     uint32_t run = 0, crun = 0, o0 = 0, o1 = 0;
 #pragma unroll
     for (int z = 0; z < BRK_H; ++z) {
-      if (z == BRK_R) o0 = run;
-      if (z == BRK_R + BRK) o1 = run;
+      if (z == BRK_R) o0 = MODE ? crun : run;
+      if (z == BRK_R + BRK) o1 = MODE ? crun : run;
       S.rel[cc][z] = (uint16_t)min(run, 65535u);
       S.cabs[cc][z] = (uint16_t)min(crun, 65535u);  // (made absolute below)
       if ((bits >> z) & 1u) {
@@ -964,7 +974,7 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_border_brick_kernel(SpArgs 
         const uint32_t c0 = S.cabs[cc][z], c1 = S.cabs[cc][z + 1];
         if (c0 == c1) continue;
         const uint32_t k = rr[q] + __popc(bb[q] & ((1u << z) - 1u));
-        const uint32_t lab = __ldg(a.cell_label + k);
+        const uint32_t lab = MODE ? k : __ldg(a.cell_label + k);
         const uint32_t src = g0 + S.rel[cc][z];
         for (uint32_t t = 0; t < c1 - c0; ++t) {
           int4 v = __ldg(reinterpret_cast<const int4*>(a.Ps) + src + t);
@@ -978,9 +988,46 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_border_brick_kernel(SpArgs 
     el += clen[q];
   }
   __syncthreads();
+  const uint16_t* cabs_flat = &S.cabs[0][0];
+  if constexpr (MODE == 1) {
+    // ---- ClusterCore: a thread per own core point
+    for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
+      int cc = 0;
+#pragma unroll
+      for (int step = 256; step; step >>= 1)
+        if (cc + step < BRK_COLS && S.obase[cc + step] <= t) cc += step;
+      const uint16_t* ca = S.cabs[cc];
+      const uint32_t u0 = t - S.obase[cc] + ca[BRK_R];  // index in cpts
+      int hz = BRK_R;
+#pragma unroll
+      for (int step = 8; step; step >>= 1)
+        if (ca[hz + step] <= u0) hz += step;
+      const int4 pv = S.cpts[u0];
+      const int32_t p[4] = {pv.x, pv.y, pv.z, 0};
+      const uint32_t gcell = (uint32_t)pv.w;
+      const uint32_t base = smem_addr(cabs_flat + cc * (BRK_H + 1) + hz);
+      uint32_t last = MISS;  // the cell linked last (its other points need no test)
+#pragma unroll
+      for (int k = 0; k < BRK_MAXC; ++k) {
+        if (k < cols.ncols) {
+          const uint32_t lo = lds_u16(base + cols.A[k]), hi = lds_u16(base + cols.B[k]);
+          for (uint32_t u = lo; u < hi; ++u) {
+            const int4 qv = S.cpts[u];
+            const uint32_t h = (uint32_t)qv.w;
+            if (h >= gcell || h == last) continue;
+            const int32_t q[4] = {qv.x, qv.y, qv.z, 0};
+            DB_WORK(1);
+            if (!within<3, WIDE>(p, q, a.g.clampc, a.g.eps2)) continue;
+            uf_link(a.parent, gcell, h);
+            last = h;
+          }
+        }
+      }
+    }
+    return;
+  }
   // ---- phase 2: a thread per own non-core point
   uint32_t nb = 0;
-  const uint16_t* cabs_flat = &S.cabs[0][0];
   for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
     int cc = 0;
 #pragma unroll
@@ -1355,6 +1402,27 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   if (a.nbcols > 0 && a.ncore > 0) {
     const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
     c.zero(a.counters + 2, sizeof(uint32_t));
+    // 3D bricks (the MarkCore brick ran; few core cells): every BCP from
+    // staged core points; the pair kernels below then run only if a brick
+    // overflowed (device flag, no host synchronisation)
+    const uint32_t* run_if = nullptr;
+    o->brick_cluster = o->brick != 0 && !g.at && g.d == 3 && !(o->flags & DBSCAN_F_NO_BRICK) &&
+                       2ull * a.ncore < cv.ncells;
+    if (o->brick_cluster) {
+      uint32_t* fl = c.alloc<uint32_t>(1);
+      c.zero(fl, sizeof(uint32_t));
+      const uint64_t nbricks = (uint64_t)a.nbrick[0] * a.nbrick[1] * a.nbrick[2];
+      const size_t smem = sizeof(BorderBrickSmem);
+      auto launch = [&](auto kern) {
+        DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, a.bc, a.nbrick[1], a.nbrick[2], fl, nullptr,
+                                                            nullptr, nullptr);
+        c.launched();
+      };
+      if (wide) launch(sp_border_brick_kernel<true, 1>);
+      else launch(sp_border_brick_kernel<false, 1>);
+      run_if = fl;
+    }
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
@@ -1366,8 +1434,8 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
       for (int pass = 0; pass < 3; ++pass) {
         const int lo = cut[pass], hi = cut[pass + 1];
         if (lo == hi) continue;
-        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
-        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
+        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0, run_if);
+        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0, run_if);
         c.launched();
         ++o->passes;
         if (two && hi < a.nbcols) uf_flatten(c, parent, a.core_list, a.ncore);
@@ -1400,7 +1468,7 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
       if constexpr (DIM == 3) {
-        auto kern = sp_border_brick_kernel<W>;
+        auto kern = sp_border_brick_kernel<W, 0>;
         DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, a.bc, a.nbrick[1], a.nbrick[2], fl, a.tmp_n,
                                                             a.ovf_pos, fl + 1);

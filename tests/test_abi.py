@@ -49,7 +49,7 @@ def test_struct_layout_matches_header(lib):
     body = re.search(r"typedef struct dbscan_result \{(.*?)\} dbscan_result;", src, flags=re.S).group(1)
     hdr = re.findall(r"\*?\s*(\w+)(?:\[\w+\])?\s*[,;]", body)
     assert names == [h for h in hdr if h not in ("int64_t", "uint8_t", "int32_t", "float", "uint32_t", "void")]
-    assert C.sizeof(pkg._Result) == 8 * 10 + 4 * 12 + 8 * 24 + 8 + 8
+    assert C.sizeof(pkg._Result) == 8 * 10 + 4 * 12 + 8 * 32 + 8 + 8
 
 
 @pytest.mark.parametrize("args", [
