@@ -521,6 +521,7 @@ def test_brick_border_many_labels_vs_o2(oracle_lib, flags):
     pts = np.concatenate([pts[keep]] + [_star(c, eps) for c in centres]).astype(np.int32)
     r = gpu(pts, eps, mp, flags)
     assert r.stats["sparse"] == 1 and r.stats["brick_border"] == (0 if flags else 1), r.stats
+    assert r.stats["brick_cluster"] == (0 if flags else 1), r.stats
     want = oracle_lib.o2(pts, eps, mp)
     rows = np.diff(want.border_off)
     assert rows.max() == 6 and (rows == 6).sum() == 3
