@@ -63,9 +63,8 @@ extern "C" {
 #define DBSCAN_F_QUADTREE    4096u /* our-exact-qt: MarkCore's
                                       RangeCount on cells with >= 256 points traverses a
                                       per-cell tree instead of scanning (CSR path)           */
-#define DBSCAN_F_NO_BRICK    8192u /* sparse path, d = 3: MarkCore with a thread per point and
-                                      ClusterBorder core-centric, instead of the shared-memory
-                                      brick kernels (testing)                                 */
+#define DBSCAN_F_NO_BRICK    8192u /* sparse path, d = 3: MarkCore with a thread per point
+                                      instead of the shared-memory brick kernel (testing)    */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */
@@ -116,12 +115,7 @@ extern "C" {
                                         every distance test adds to a device counter; not
                                         thread-safe across concurrent calls, measurement only),
                                         0 in the product library                              */
-#define DBSCAN_STAT_BRICK_BORDER 23 /* 1 if the sparse ClusterBorder ran as the brick kernel (label
-                                        sets from bricks of staged core points)               */
-#define DBSCAN_STAT_BRICK_CLUSTER 24 /* 1 if the sparse ClusterCore ran as the brick kernel (BCPs of
-                                        staged core points; the pair kernels only for bricks
-                                        that overflowed)                                      */
-#define DBSCAN_NSTATS            32
+#define DBSCAN_NSTATS            32  /* (23-31 reserved) */
 
 typedef struct dbscan_result {
   int64_t  n;

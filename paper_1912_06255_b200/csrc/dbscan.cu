@@ -645,8 +645,6 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_BRICK] = so.brick;
   out->stats[DBSCAN_STAT_POINT_BORDER] = so.point_border;
   out->stats[DBSCAN_STAT_SPARSE_PASSES] = so.passes;
-  out->stats[DBSCAN_STAT_BRICK_BORDER] = so.brick_border;
-  out->stats[DBSCAN_STAT_BRICK_CLUSTER] = so.brick_cluster;
   return DBSCAN_OK;
 }
 

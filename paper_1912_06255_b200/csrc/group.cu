@@ -339,31 +339,16 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
 
 // ===========================================================================
 // Lattice counting sort (d <= 3, sparse lattices such as BASELINE configs[4]):
-// when the padded lattice has at most LAT_PER_POINT cells per point, the
-// points are counted per lattice cell, in BUCKETS of LB_CELLS consecutive
-// lattice cells (linear order = key order), so that every count lives in
-// shared memory:
-//  1. hist:  per point its bucket (lin >> LB_WB); per-block shared histogram,
-//            one global atomic per (block, bucket);
-//  2. scan of the bucket counts: bucket b's points take the contiguous
-//            positions bbase[b] .. bbase[b+1] of the output;
-//  3. stage: a block takes BK_N points (one TMA bulk copy), ranks them by
-//            bucket in shared memory, reserves a run in each bucket's range
-//            with one atomic per (block, bucket) and writes the records
-//            {lin - bucket start, x, y, z} and input indices there coalesced;
-//  4. sort:  a CTA per bucket counts its records per cell with 8-bit packed
-//            shared-memory counters (the atomic's old value is the point's
-//            slot in its cell), derives, per 32-cell directory word, the
-//            occupancy bits and the point and cell prefixes (one block scan),
-//            takes the bucket's first cell id from a decoupled look-back over
-//            the buckets, writes the directory words (the sparse path's rank
-//            directory), cell_start and cell_key of its cells, then places
-//            every record at bbase[b] + (points of the cells before) + slot,
-//            with its input index and cell id (cell_of) — writes confined to
-//            the bucket's contiguous output range.
-// The largest cell size falls out of the counts (Alg 2's global bound,
-// reading 13). A cell with more than 255 points overflows its counter: the
-// pass reports it and the caller falls back to the radix sort.
+// when the padded lattice has at most LAT_PER_POINT cells per point, count
+// the points of every lattice cell directly (packed 8-bit counters, L2
+// resident: 43 MB for c5), derive the rank directory, cell_start and cell_key
+// from the counts in linear order (= key order), and scatter each point to
+// cell_start[rank] + its slot. Two reads of the points and one scattered
+// write replace the key array, four radix passes and the gather. The largest
+// cell size falls out of the counts, so Alg 2's global bound (reading 13)
+// can declare every point non-core before any point is moved.
+// A cell with more than 255 points overflows its counter: the pass reports it
+// and the caller falls back to the radix sort.
 // ===========================================================================
 constexpr int LAT_THREADS = 256;
 
@@ -391,53 +376,163 @@ struct LatArgs {
   int small;           // padded lattice volume < 2^32: 32-bit coordinates by multiply-high
 };
 
-constexpr int LB_WB = 16;                    // lattice cells per sort bucket: 2^16
-constexpr uint32_t LB_CELLS = 1u << LB_WB;
-constexpr int LB_GROUPS = LB_CELLS / 32;     // directory words per bucket
-constexpr int LB_THREADS = 512;
-constexpr int LB_GPT = LB_GROUPS / LB_THREADS;
-constexpr int BK_THREADS = 512;
-constexpr int BK_ITEMS = 8;                  // stage: 4096 points per block
-constexpr int BK_N = BK_THREADS * BK_ITEMS;
-constexpr int BK_MAXB = 8448;                // buckets (lattice <= 8 n + 2^20 cells, n <= 2^25)
-constexpr int64_t LAT_MAX_N = 1 << 25;       // (the documented limit of the lattice sort)
-
-// 1. bucket histogram: HIST_ITEMS points per thread, shared counts, one global
-// atomic per (block, touched bucket)
-constexpr int HIST_ITEMS = 16;
-
+// pass 1: slot of every point in its lattice cell (8-bit packed counters)
 template <int DD>
-__global__ void __launch_bounds__(LAT_THREADS) lat_hist_kernel(const int32_t* __restrict__ pts, uint32_t n, LatArgs L,
-                                                               uint32_t nbk, uint32_t* __restrict__ bcnt) {
-  extern __shared__ uint32_t hist[];
-  for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) hist[b] = 0;
-  __syncthreads();
-  const uint32_t i0 = blockIdx.x * (LAT_THREADS * HIST_ITEMS);
-#pragma unroll 4
-  for (int t = 0; t < HIST_ITEMS; ++t) {
-    const uint32_t i = i0 + t * LAT_THREADS + threadIdx.x;
-    if (i < n) {
-      int32_t x[DD];
-      const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, x);
-      atomicAdd(hist + (uint32_t)(lin >> LB_WB), 1u);
-    }
-  }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x)
-    if (hist[b]) atomicAdd(bcnt + b, hist[b]);
+__global__ void __launch_bounds__(LAT_THREADS) lat_count_kernel(const int32_t* __restrict__ pts, uint32_t n,
+                                                                LatArgs L, uint32_t* __restrict__ cnt8,
+                                                                uint8_t* __restrict__ slot, uint32_t* overflow) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t x[DD];
+  const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, x);
+  const uint32_t sh = ((uint32_t)lin & 3u) * 8u;
+  const uint32_t old = (atomicAdd(cnt8 + (lin >> 2), 1u << sh) >> sh) & 255u;
+  if (old == 255u) *overflow = 1u;  // the add carried into the next counter
+  slot[i] = (uint8_t)old;
 }
 
-// 3. stage by bucket. Shared memory (dynamic): the block's points (bulk copy)
-// and, reusing the space once they are in registers, its records ordered by
-// bucket — so the write-out is coalesced: consecutive threads write
-// consecutive positions of one bucket's run, whole sectors at a time — then
-// hist / gbase [nbk].
+// pass 2a: per 32-cell word, occupancy bits and point count
+__global__ void __launch_bounds__(LAT_THREADS) lat_words_kernel(const uint32_t* __restrict__ cnt8, LatArgs L,
+                                                                uint32_t* __restrict__ bm,
+                                                                uint32_t* __restrict__ wcells,
+                                                                uint32_t* __restrict__ wpts, uint32_t* mx) {
+  const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint32_t m = 0;
+  if (w < L.words) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w + 1);
+    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t bits = 0, sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c = (v[q] >> (8 * k)) & 255u;
+        bits |= (uint32_t)(c != 0) << (4 * q + k);
+        sum += c;
+        m = max(m, c);
+      }
+    bm[w] = bits;
+    wcells[w] = __popc(bits);
+    wpts[w] = sum;
+  }
+  // largest cell: one atomic per block (same-address atomics serialise)
+  __shared__ uint32_t s_m;
+  if (threadIdx.x == 0) s_m = 0;
+  __syncthreads();
+  m = __reduce_max_sync(DB_FULL, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&s_m, m);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_m) atomicMax(mx, s_m);
+}
+
+// pass 2b: cells in linear order: cell_start, cell_key, and the directory
+// entry {bits w, bits w+1, cells before w, 0} of the sparse path. The 32
+// counters of a word stay in registers; byte prefix sums by shifts; lattice
+// coordinates by multiply-high (exact for lin < 2^32, else 64-bit division).
+__global__ void __launch_bounds__(LAT_THREADS) lat_cells_kernel(const uint32_t* __restrict__ cnt8, LatArgs L,
+                                                                const uint32_t* __restrict__ bm,
+                                                                const uint32_t* __restrict__ cpre,
+                                                                const uint32_t* __restrict__ ppre,
+                                                                uint32_t* __restrict__ cell_start,
+                                                                uint64_t* __restrict__ cell_key,
+                                                                uint4* __restrict__ dir) {
+  const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (w >= L.words) return;
+  const uint32_t bits = bm[w];
+  dir[w] = make_uint4(bits, w + 1 < L.words ? bm[w + 1] : 0u, cpre[w], 0u);
+  if (!bits) return;
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w);
+  const uint4 b = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w + 1);
+  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  // excl[q]: points in counters 0 .. 4q-1 of the word; inside a u32 the byte
+  // prefix sums come from x * 0x01010101 (<= 4 * 255 would overflow a byte, so
+  // sum in 16-bit halves instead)
+  uint32_t excl[8];
+  uint32_t run = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    excl[q] = run;
+    run += (v[q] & 255u) + ((v[q] >> 8) & 255u) + ((v[q] >> 16) & 255u) + (v[q] >> 24);
+  }
+  uint32_t r = cpre[w];
+  const uint32_t p = ppre[w];
+  for (uint32_t bb = bits; bb; bb &= bb - 1) {
+    const int k = __ffs(bb) - 1;
+    const int q = k >> 2, sub = k & 3;
+    uint32_t before = excl[0];
+#pragma unroll
+    for (int qq = 1; qq < 8; ++qq)
+      if (qq == q) before = excl[qq];
+    uint32_t vq = v[0];
+#pragma unroll
+    for (int qq = 1; qq < 8; ++qq)
+      if (qq == q) vq = v[qq];
+    for (int s = 0; s < sub; ++s) before += (vq >> (8 * s)) & 255u;
+    const uint64_t lin = 32 * w + (uint64_t)k;
+    uint64_t key = 0;
+    if (L.small) {
+      uint32_t rem = (uint32_t)lin;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (ax < L.g.d) {
+          const uint32_t ca = L.smagic[ax] ? (uint32_t)__umul64hi((uint64_t)rem, L.smagic[ax]) : rem;
+          rem -= ca * (uint32_t)L.stride[ax];
+          key |= (uint64_t)(ca - L.g.R) << L.g.shift[ax];
+        }
+      }
+    } else {
+      uint64_t rem = lin;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (ax < L.g.d) {
+          const uint64_t ca = rem / L.stride[ax];
+          rem -= ca * L.stride[ax];
+          key |= (ca - L.g.R) << L.g.shift[ax];
+        }
+      }
+    }
+    cell_start[r] = p + before;
+    cell_key[r] = key;
+    ++r;
+  }
+}
+
+// pass 3: the permutation, in two steps so that no write lands far from the
+// others of its time. The lattice words are cut into buckets of 2^ws
+// consecutive words; a bucket's points take the contiguous positions
+// ppre[b 2^ws] .. ppre[(b+1) 2^ws) (key order = linear order), about
+// BK_TARGET of them.
+//  3a: a block takes BK_ITEMS consecutive points per thread, ranks them by
+//      bucket in shared memory, reserves room in each bucket's range with one
+//      atomic per (block, bucket) and writes the records {lin - bucket start
+//      | slot << 24, x, y, z} and the input index there (runs of ~BK_ITEMS x
+//      BK_THREADS / buckets records). No gather: the bucket is lin >> (5+ws).
+//  3b: a thread per staged record (read coalesced) finds its cell rank on
+//      the directory and its position cell_start[rank] + slot, and writes the
+//      point, its input index and the cell id there. A block's records belong
+//      to one or two buckets, so its directory words, cell starts and output
+//      positions lie in one small window (L1 / L2 merge the writes).
+constexpr int BK_THREADS = 512;
+constexpr int BK_ITEMS = 8;            // 3a: 4096 points per block
+constexpr int BK_MAXB = 4096;          // buckets held by a 3a block's shared histogram
+constexpr uint32_t BK_TARGET = 16384;  // points per bucket aimed at
+constexpr int BK_MAXWS = 19;           // lin - bucket start < 2^24
+constexpr int64_t LAT_MAX_N = 1 << 25;  // (the documented limit of the lattice sort)
+
+constexpr int BK_N = BK_THREADS * BK_ITEMS;  // points per 3a block
+
+// 3a. Shared memory (dynamic): the block's points (bulk copy) and, reusing the
+// space once they are in registers, its records ordered by bucket — so the
+// write-out is coalesced: consecutive threads write consecutive positions of
+// one bucket's run, whole sectors at a time — then hist / gbase [nbk].
 template <int DD>
 __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                               LatArgs L, const uint32_t* __restrict__ bbase,
-                                                               uint32_t nbk, uint32_t* __restrict__ bcur,
-                                                               uint4* __restrict__ rec,
-                                                               uint32_t* __restrict__ reci) {
+                                                                  LatArgs L, const uint8_t* __restrict__ slot,
+                                                                  const uint32_t* __restrict__ ppre, int ws,
+                                                                  uint32_t nbk, uint32_t* __restrict__ bcur,
+                                                                  uint4* __restrict__ rec,
+                                                                  uint32_t* __restrict__ reci) {
   extern __shared__ __align__(16) uint8_t st_raw[];
   int32_t* s_pts = reinterpret_cast<int32_t*>(st_raw);             // [BK_N * DD], then:
   uint4* srec = reinterpret_cast<uint4*>(st_raw);                  // [BK_N] records by bucket
@@ -477,8 +572,8 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) x[t][k] = k < DD ? xx[k] : 0;
-      bk[t] = (uint32_t)(lin >> LB_WB);
-      key[t] = (uint32_t)lin & (LB_CELLS - 1u);
+      bk[t] = (uint32_t)(lin >> (5 + ws));
+      key[t] = (uint32_t)(lin - ((uint64_t)bk[t] << (5 + ws))) | ((uint32_t)__ldg(slot + i) << 24);
     }
   }
 #pragma unroll
@@ -487,7 +582,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
   __syncthreads();  // (the points are in registers from here on)
   // reserve each touched bucket's run (one atomic per block and bucket)
   for (uint32_t b = threadIdx.x; b < nbk; b += BK_THREADS)
-    if (hist[b]) gbase[b] = __ldg(bbase + b) + atomicAdd(bcur + b, hist[b]);
+    if (hist[b]) gbase[b] = __ldg(ppre + ((uint64_t)b << ws)) + atomicAdd(bcur + b, hist[b]);
   // local bases: exclusive scan of the counts, a run of buckets per thread
   const uint32_t per = (nbk + BK_THREADS - 1) / BK_THREADS, b0 = threadIdx.x * per;
   uint32_t sum = 0;
@@ -518,163 +613,56 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
   }
 }
 
-// packed key of lattice cell `lin` (padded linear index)
-__device__ __forceinline__ uint64_t lat_key(uint64_t lin, const LatArgs& L) {
-  uint64_t key = 0;
-  if (L.small) {
-    uint32_t rem = (uint32_t)lin;
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      if (ax < L.g.d) {
-        const uint32_t ca = L.smagic[ax] ? (uint32_t)__umul64hi((uint64_t)rem, L.smagic[ax]) : rem;
-        rem -= ca * (uint32_t)L.stride[ax];
-        key |= (uint64_t)(ca - L.g.R) << L.g.shift[ax];
-      }
-    }
-  } else {
-    uint64_t rem = lin;
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      if (ax < L.g.d) {
-        const uint64_t ca = rem / L.stride[ax];
-        rem -= ca * L.stride[ax];
-        key |= (ca - L.g.R) << L.g.shift[ax];
-      }
-    }
-  }
-  return key;
+constexpr int PL_THREADS = 512;
+
+// 3b's block -> bucket table: chunk c (records c PL_THREADS ..) starts in the
+// bucket b with base(b) <= c PL_THREADS < base(b + 1); a thread per bucket.
+__global__ void lat_chunks_kernel(const uint32_t* __restrict__ ppre, int ws, uint64_t words, uint32_t nbk,
+                                  uint32_t nchunks, uint32_t* __restrict__ chunk_bucket) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbk) return;
+  const uint32_t lo = ppre[min((uint64_t)b << ws, words)];
+  const uint32_t hi = b + 1 < nbk ? ppre[min((uint64_t)(b + 1) << ws, words)] : 0xffffffffu;
+  for (uint32_t c = (lo + PL_THREADS - 1) / PL_THREADS; c < nchunks && (uint64_t)c * PL_THREADS < hi; ++c)
+    chunk_bucket[c] = b;
 }
 
-// byte-sum of the counters of cells [w*4, w*4 + k) of a packed counter word
-__device__ __forceinline__ uint32_t bytes_below(uint32_t v, uint32_t k) {
-  return __dp4a(k >= 4 ? v : (v & ((1u << (8 * k)) - 1u)), 0x01010101u, 0u);
-}
-
-// 4. a CTA per bucket (see the section comment). flags: [0] counter overflow,
-// [1] largest cell, [2] number of cells (written by the last bucket).
 template <int D>
-__global__ void __launch_bounds__(LB_THREADS, 2) lat_sort_kernel(
-    const uint4* __restrict__ rec, const uint32_t* __restrict__ reci, uint8_t* __restrict__ slot,
-    const uint32_t* __restrict__ bbase, uint32_t nbk, LatArgs L, uint64_t* __restrict__ lbst,
-    int32_t* __restrict__ Ps, uint32_t* __restrict__ idx, uint32_t* __restrict__ cell_of,
-    uint32_t* __restrict__ cell_start, uint64_t* __restrict__ cell_key, uint4* __restrict__ dir,
-    uint32_t* __restrict__ flags) {
-  extern __shared__ __align__(16) uint32_t lb_sm[];
-  uint32_t* cnt = lb_sm;                  // [LB_CELLS / 4] 8-bit counters, packed
-  uint32_t* gpts = cnt + LB_CELLS / 4;    // [LB_GROUPS] points of the bucket before the word
-  uint32_t* gcel = gpts + LB_GROUPS;      // [LB_GROUPS] cells of the bucket before the word
-  uint32_t* gbit = gcel + LB_GROUPS;      // [LB_GROUPS] occupancy bits of the word
-  __shared__ unsigned long long s_scan[33];
-  __shared__ unsigned long long s_cbase;
-  const uint32_t b = blockIdx.x;
-  const uint32_t r0 = __ldg(bbase + b), r1 = __ldg(bbase + b + 1);
-  for (uint32_t i = threadIdx.x; i < LB_CELLS / 4; i += LB_THREADS) cnt[i] = 0;
-  __syncthreads();
-  // counts; the old counter value is the record's slot in its cell
-  bool ovf = false;
-  for (uint32_t t = r0 + threadIdx.x; t < r1; t += LB_THREADS) {
-    const uint32_t rl = __ldg(&rec[t].x);
-    const uint32_t sh = (rl & 3u) * 8u;
-    const uint32_t s = (atomicAdd(cnt + (rl >> 2), 1u << sh) >> sh) & 255u;
-    ovf |= s == 255u;
-    slot[t] = (uint8_t)s;
-  }
-  // a counter passed 255 and carried into its neighbour: the caller falls
-  // back to the radix sort; this bucket publishes no cell and writes nothing
-  const bool bad = __syncthreads_or(ovf);
-  if (bad && threadIdx.x == 0) atomicExch(flags, 1u);
-  // per directory word (32 cells = 8 counter words): bits, points, largest cell
-  uint32_t gb[LB_GPT], gp[LB_GPT];
-  uint32_t sp = 0, sc = 0, mx = 0;
-#pragma unroll
-  for (int q = 0; q < LB_GPT; ++q) {
-    const uint32_t g = threadIdx.x * LB_GPT + q;
-    uint32_t bits = 0, pts = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const uint32_t v = cnt[g * 8 + w];
-      pts += __dp4a(v, 0x01010101u, 0u);
-      const uint32_t nz = __vcmpne4(v, 0u);  // 0xff per non-empty cell
-      bits |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * w);
-      const uint32_t m2 = __vmaxu4(v, v >> 16);
-      mx = max(mx, max(m2 & 255u, (m2 >> 8) & 255u));
-    }
-    gb[q] = bits;
-    gp[q] = pts;
-    sp += pts;
-    sc += __popc(bits);
-  }
-  unsigned long long tot;
-  unsigned long long ex = block_exclusive_scan<unsigned long long>(
-      (unsigned long long)sp | ((unsigned long long)sc << 32), s_scan, &tot);
-  if (bad) tot = 0;
-#pragma unroll
-  for (int q = 0; q < LB_GPT; ++q) {
-    const uint32_t g = threadIdx.x * LB_GPT + q;
-    gpts[g] = (uint32_t)ex;
-    gcel[g] = (uint32_t)(ex >> 32);
-    gbit[g] = gb[q];
-    ex += (unsigned long long)gp[q] | ((unsigned long long)__popc(gb[q]) << 32);
-  }
-  // the bucket's first cell id: look-back over the buckets (warp 0)
-  if (threadIdx.x < 32) {
-    const uint64_t cb = lb_exclusive_warp(lbst, b, 1, tot >> 32);
-    if (threadIdx.x == 0) {
-      s_cbase = cb;
-      if (b + 1 == nbk) {
-        flags[2] = (uint32_t)(cb + (tot >> 32));
-        cell_start[cb + (tot >> 32)] = r1;  // = n
-      }
-    }
-  }
-  mx = __reduce_max_sync(DB_FULL, mx);
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(flags + 1, mx);
-  __syncthreads();
-  if (bad) return;
-  const uint32_t cbase = (uint32_t)s_cbase;
-  // directory words, cell_start, cell_key: a thread per word
-#pragma unroll
-  for (int q = 0; q < LB_GPT; ++q) {
-    const uint32_t g = threadIdx.x * LB_GPT + q;
-    const uint64_t w = (uint64_t)b * LB_GROUPS + g;
-    if (w >= L.words) continue;
-    const uint32_t bits = gbit[g];
-    // {bits of word w, bits of word w + 1, cells before w, 0}; the next word
-    // of the bucket's last word belongs to the next bucket, which writes that
-    // field (disjoint bytes: no ordering needed between the two buckets)
-    if (g + 1 < (uint32_t)LB_GROUPS) {
-      dir[w] = make_uint4(bits, gbit[g + 1], cbase + gcel[g], 0u);
-    } else {
-      uint32_t* e = reinterpret_cast<uint32_t*>(dir + w);
-      e[0] = bits;
-      if (b + 1 == nbk) e[1] = 0u;
-      e[2] = cbase + gcel[g];
-      e[3] = 0u;
-    }
-    if (g == 0 && w > 0) reinterpret_cast<uint32_t*>(dir + w - 1)[1] = bits;
-    uint32_t r = cbase + gcel[g], p = r0 + gpts[g];
-    for (uint32_t bb = bits; bb; bb &= bb - 1) {
-      const int k = __ffs(bb) - 1;
-      cell_start[r] = p;
-      cell_key[r] = lat_key(w * 32 + (uint64_t)k, L);
-      p += (cnt[g * 8 + (k >> 2)] >> (8 * (k & 3))) & 255u;
-      ++r;
-    }
-  }
-  // place: bbase[b] + points of the cells before + slot
-  for (uint32_t t = r0 + threadIdx.x; t < r1; t += LB_THREADS) {
-    const uint4 v = __ldg(rec + t);
-    const uint32_t rl = v.x, g = rl >> 5, k = rl & 31u;
-    uint32_t pre = gpts[g];
-    const uint32_t cw = rl >> 2;
-    for (uint32_t w = g * 8; w < cw; ++w) pre += __dp4a(cnt[w], 0x01010101u, 0u);
-    pre += bytes_below(cnt[cw], rl & 3u);
-    const uint32_t pos = r0 + pre + __ldg(slot + t);
-    const uint32_t rank = cbase + gcel[g] + __popc(gbit[g] & ((1u << k) - 1u));
-    if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[pos] = make_int2((int32_t)v.y, (int32_t)v.z);
-    else reinterpret_cast<int4*>(Ps)[pos] = make_int4((int32_t)v.y, (int32_t)v.z, (int32_t)v.w, 0);
-    idx[pos] = __ldg(reci + t);
-    cell_of[pos] = rank;
+__global__ void __launch_bounds__(PL_THREADS) lat_place_kernel(uint32_t n, const uint4* __restrict__ rec,
+                                                               const uint32_t* __restrict__ reci,
+                                                               const uint4* __restrict__ dir,
+                                                               const uint32_t* __restrict__ cell_start,
+                                                               const uint32_t* __restrict__ ppre, int ws,
+                                                               uint64_t words, uint32_t nbk,
+                                                               const uint32_t* __restrict__ chunk_bucket,
+                                                               int32_t* __restrict__ Ps, uint32_t* __restrict__ idx,
+                                                               uint32_t* __restrict__ cell_of) {
+  const uint32_t t0 = blockIdx.x * PL_THREADS;
+  auto base_of = [&](uint32_t b) { return __ldg(ppre + min((uint64_t)b << ws, words)); };
+  const uint32_t s_b0 = __ldg(chunk_bucket + blockIdx.x);  // bucket of t0
+  const uint32_t t = t0 + threadIdx.x;
+  if (t >= n) return;
+  const uint4 r = __ldg(rec + t);
+  const uint32_t i = __ldg(reci + t);
+  uint32_t b = s_b0;
+  while (b + 1 < nbk && base_of(b + 1) <= t) ++b;
+  const uint64_t lin = ((uint64_t)b << (5 + ws)) + (r.x & 0xffffffu);
+  const uint4 e = __ldg(dir + (lin >> 5));
+  const uint32_t rank = e.z + __popc(e.x & ((1u << ((uint32_t)lin & 31u)) - 1u));
+  const uint32_t pos = __ldg(cell_start + rank) + (r.x >> 24);
+  if constexpr (D == 2) reinterpret_cast<int2*>(Ps)[pos] = make_int2((int32_t)r.y, (int32_t)r.z);
+  else reinterpret_cast<int4*>(Ps)[pos] = make_int4((int32_t)r.y, (int32_t)r.z, (int32_t)r.w, 0);
+  idx[pos] = i;
+}
+
+// cell_of from the cell ranges: a thread per cell writes its positions, so
+// consecutive threads write consecutive words (in 3b they would be a fourth
+// scattered partial-sector stream)
+__global__ void lat_cell_of_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                   uint32_t* __restrict__ cell_of) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < ncells; r += gridDim.x * blockDim.x) {
+    const uint32_t e = cell_start[r + 1];
+    for (uint32_t p = cell_start[r]; p < e; ++p) cell_of[p] = r;
   }
 }
 
@@ -702,54 +690,77 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
   for (int k = 0; k < g.d; ++k)
     L.smagic[k] = L.stride[k] > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + L.stride[k] - 1) / L.stride[k])
                                   : 0;
-  // buckets of LB_CELLS lattice cells cover the directory's words
-  const uint32_t nbk = (uint32_t)((L.words * 32 + LB_CELLS - 1) / LB_CELLS);
-  if (nbk > (uint32_t)BK_MAXB) throw Error(-4, "lattice sort: too many buckets");
+  uint32_t* cnt8 = c.alloc<uint32_t>(8 * L.words);
+  uint8_t* slot = c.alloc<uint8_t>(n);
+  uint32_t* flags = c.alloc<uint32_t>(2);  // [0] overflow, [1] largest cell
+  c.zero(cnt8, sizeof(uint32_t) * 8 * L.words);
+  c.zero(flags, 2 * sizeof(uint32_t));
+  const unsigned pgrid = grid_for(n, LAT_THREADS, 1 << 30);
   auto by_d = [&](auto f) {
     if (g.d == 1) f(std::integral_constant<int, 1>(), std::integral_constant<int, 2>());
     else if (g.d == 2) f(std::integral_constant<int, 2>(), std::integral_constant<int, 2>());
     else f(std::integral_constant<int, 3>(), std::integral_constant<int, 4>());
   };
-  uint32_t* bcnt = c.alloc<uint32_t>(nbk);
-  uint32_t* bbase = c.alloc<uint32_t>(nbk + 1);
-  uint32_t* bcur = c.alloc<uint32_t>(nbk);
-  uint64_t* lbst = c.alloc<uint64_t>(nbk);
-  uint32_t* flags = c.alloc<uint32_t>(4);  // [0] overflow, [1] largest cell, [2] cells
-  c.zero(bcnt, sizeof(uint32_t) * nbk);
-  c.zero(bcur, sizeof(uint32_t) * nbk);
-  c.zero(lbst, sizeof(uint64_t) * nbk);
-  c.zero(flags, 4 * sizeof(uint32_t));
-  uint4* rec = c.alloc<uint4>((size_t)n);
-  uint32_t* reci = c.alloc<uint32_t>((size_t)n);
-  uint8_t* slot = c.alloc<uint8_t>((size_t)n);
-  uint4* dir = c.alloc<uint4>(L.words);
-  by_d([&](auto Dd, auto Dp) {
-    constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
-    const unsigned hgrid = (unsigned)((n + LAT_THREADS * HIST_ITEMS - 1) / (LAT_THREADS * HIST_ITEMS));
-    const int hsm = 4 * (int)nbk;
-    DB_CUDA(cudaFuncSetAttribute(lat_hist_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
-    lat_hist_kernel<DD><<<hgrid, LAT_THREADS, hsm, c.st>>>(pts, (uint32_t)n, L, nbk, bcnt);
-    c.launched();
-    exclusive_scan_u32_u32(c, bcnt, bbase, nbk);
-    const unsigned sgrid = (unsigned)((n + BK_N - 1) / BK_N);
-    const int ssm = BK_N * 24 + 2 * 4 * (int)nbk;
-    DB_CUDA(cudaFuncSetAttribute(lat_stage_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
-    lat_stage_kernel<DD><<<sgrid, BK_THREADS, ssm, c.st>>>(pts, (uint32_t)n, L, bbase, nbk, bcur, rec, reci);
-    c.launched();
-    const int lsm = (int)(LB_CELLS + 3 * 4 * LB_GROUPS);
-    DB_CUDA(cudaFuncSetAttribute(lat_sort_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm));
-    lat_sort_kernel<D><<<nbk, LB_THREADS, lsm, c.st>>>(rec, reci, slot, bbase, nbk, L, lbst, Ps, idx, cell_of,
-                                                       cell_start, cell_key, dir, flags);
-    c.launched();
+  by_d([&](auto Dd, auto) {
+    constexpr int DD = decltype(Dd)::value;
+    lat_count_kernel<DD><<<pgrid, LAT_THREADS, 0, c.st>>>(pts, (uint32_t)n, L, cnt8, slot, flags);
   });
-  const uint32_t* h = c.fetch(flags, 4);
+  c.launched();
+  uint32_t* bm = c.alloc<uint32_t>(L.words);
+  uint32_t* wcells = c.alloc<uint32_t>(L.words);
+  uint32_t* wpts = c.alloc<uint32_t>(L.words);
+  const unsigned wgrid = grid_for((int64_t)L.words, LAT_THREADS, 1 << 30);
+  lat_words_kernel<<<wgrid, LAT_THREADS, 0, c.st>>>(cnt8, L, bm, wcells, wpts, flags + 1);
+  c.launched();
+  uint32_t h[2];
+  const uint32_t* h_h = c.fetch(flags, 2);
   c.sync();
+  h[0] = h_h[0];
+  h[1] = h_h[1];
   if (h[0]) return LAT_FALLBACK;
   // Alg 2's count is at most (stencil cells) x (largest cell): below minPts,
-  // no point is core (reading 13)
+  // no point is core and nothing needs to be grouped (reading 13)
   if ((uint64_t)h[1] * min_pts_bound_cells < (uint64_t)min_pts) return LAT_ALL_NOISE;
+  uint32_t* cpre = c.alloc<uint32_t>(L.words + 1);
+  uint32_t* ppre = c.alloc<uint32_t>(L.words + 1);
+  exclusive_scan_u32_u32(c, wcells, cpre, (int64_t)L.words);
+  exclusive_scan_u32_u32(c, wpts, ppre, (int64_t)L.words);
+  uint4* dir = c.alloc<uint4>(L.words);
+  lat_cells_kernel<<<wgrid, LAT_THREADS, 0, c.st>>>(cnt8, L, bm, cpre, ppre, cell_start, cell_key, dir);
+  c.launched();
+  const uint32_t ncells = c.read(cpre + L.words);
+  DB_CUDA(cudaMemcpyAsync(cell_start + ncells, ppre + L.words, sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.st));
+  // pass 3: stage by bucket of lattice words, then place
+  int ws = 0;
+  const double ppw = (double)n / (double)L.words;  // points per word
+  while (ws < BK_MAXWS && (((L.words + (1ull << ws) - 1) >> ws) > (uint64_t)BK_MAXB ||
+                           ppw * (double)(1ull << ws) < (double)BK_TARGET / 2))
+    ++ws;
+  const uint32_t nbk = (uint32_t)((L.words + (1ull << ws) - 1) >> ws);
+  if (nbk > (uint32_t)BK_MAXB) throw Error(-4, "lattice sort: too many buckets");
+  uint32_t* bcur = c.alloc<uint32_t>(nbk);
+  uint4* rec = c.alloc<uint4>((size_t)n);
+  uint32_t* reci = c.alloc<uint32_t>((size_t)n);
+  c.zero(bcur, sizeof(uint32_t) * nbk);
+  const unsigned nchunks = (unsigned)((n + PL_THREADS - 1) / PL_THREADS);
+  uint32_t* chunk_bucket = c.alloc<uint32_t>(nchunks);
+  const unsigned sgrid = (unsigned)((n + BK_THREADS * BK_ITEMS - 1) / (BK_THREADS * BK_ITEMS));
+  by_d([&](auto Dd, auto Dp) {
+    constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
+    const int ssm = BK_N * 24 + 2 * 4 * (int)nbk;
+    DB_CUDA(cudaFuncSetAttribute(lat_stage_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+    lat_stage_kernel<DD><<<sgrid, BK_THREADS, ssm, c.st>>>(pts, (uint32_t)n, L, slot, ppre, ws, nbk, bcur, rec, reci);
+    c.launched();
+    lat_chunks_kernel<<<(nbk + 255) / 256, 256, 0, c.st>>>(ppre, ws, L.words, nbk, nchunks, chunk_bucket);
+    c.launched();
+    lat_place_kernel<D><<<nchunks, PL_THREADS, 0, c.st>>>((uint32_t)n, rec, reci, dir, cell_start, ppre, ws,
+                                                          L.words, nbk, chunk_bucket, Ps, idx, cell_of);
+    c.launched();
+    lat_cell_of_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_start, ncells, cell_of);
+    c.launched();
+  });
   *dir_out = dir;
-  *ncells_out = h[2];
+  *ncells_out = ncells;
   return LAT_OK;
 }
 

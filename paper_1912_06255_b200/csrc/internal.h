@@ -303,8 +303,6 @@ struct SparseOut {
   int brick = 0;                 // MarkCore: 1 brick kernel, 2 with overflowed bricks
   bool point_border = false;     // ClusterBorder from the non-core points (few of them)
   int passes = 0;                // ClusterCore pair-search launches (stats[DBSCAN_STAT_SPARSE_PASSES])
-  bool brick_border = false;     // ClusterBorder by the brick kernel (3D, the MarkCore brick ran)
-  bool brick_cluster = false;    // ClusterCore by the brick kernel
   uint32_t flags = 0;            // the call's DBSCAN_F_* flags
 };
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced);

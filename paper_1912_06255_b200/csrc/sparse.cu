@@ -105,8 +105,6 @@ struct SpArgs {
   uint32_t* ovf_pos;         // [n] input order: sorted position of an overflowed point
   unsigned long long* nborder;
   int64_t n;
-  BrickCols bc;              // brick kernels: stencil windows (set when the MarkCore brick ran)
-  uint32_t nbrick[3];        // brick grid
 };
 
 // Cells of the lattice run start .. start+width-1 (mask = (1 << width) - 1,
@@ -533,8 +531,7 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 // instead of testing and linking every pair against one contended root.
 template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
 __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
-                                                       int col_hi, bool find_first, const uint32_t* run_if) {
-  if (run_if && *run_if == 0) return;  // (after the ClusterCore brick kernel: only if a brick overflowed)
+                                                       int col_hi, bool find_first) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   const int nb = col_hi - col_lo;
@@ -842,317 +839,6 @@ __global__ void __launch_bounds__(256) sp_border_fill_kernel(SpArgs a, const int
   }
 }
 
-// Brick variant of ClusterBorder (Alg 4) for the same 3D lattices
-// (d = 3, R = 2): a CTA stages the CORE points of a brick's halo columns in
-// shared memory — core points are first in their cell (a7), so a cell's core
-// points are Ps[cell_start .. + core_cnt), copied with their cell's label in
-// the padding lane (.w) — with, per halo column, the index of each cell's
-// first core point (cabs). A thread per own NON-core point then walks the
-// stencil windows on cabs (the MarkCore brick's column offsets), tests the
-// core points found and keeps the distinct labels of those within eps in
-// registers (at most SP_MAXL; more: listed for the enumeration kernel). The
-// own cell's core points lie in the central window (same cell => within eps,
-// the test passes). Outputs, all written coalesced or by point: the label
-// count per sorted position (cnt_s: 0 none, 1..SP_MAXL, 0xff overflow), the
-// sorted labels per sorted position (tmp_lab, only where cnt_s is 1..4), the
-// count per input index (bcnt, scattered, only non-zero) and the number of
-// border points. A brick whose halo holds more than BB_CAP core points (or a
-// column over 65535 points) sets *overflow: the caller then runs the
-// core-centric path for everything.
-constexpr int BB_CAP = 1536;
-
-struct BorderBrickSmem {
-  int4 cpts[BB_CAP];                      // halo core points, .w = cluster label
-  uint16_t cabs[BRK_COLS][BRK_H + 1];     // per column: index in cpts of cell z's first core point
-  uint16_t rel[BRK_COLS][BRK_H + 1];      // per column: offset in Ps of cell z's first point from g0
-  uint32_t g0[BRK_COLS];                  // Ps position of the column's first point
-  uint32_t obase[BRK_COLS];               // prefix of the own points per column
-  unsigned long long scan[33];
-  uint32_t ctotal, own;
-};
-
-// MODE 0: ClusterBorder (above). MODE 1: ClusterCore (Alg 3) on
-// the same staging, the padding lane holding the core point's cell id: a
-// thread per own CORE point p (cell g) walks the windows and, for every core
-// point q of a cell h < g ("higher id checks lower": each pair
-// of cells from one side) within eps, links g and h (lock-free union-find,
-// P:L837-846) — the BCP of every pair of neighbouring core cells, tested
-// point pair by point pair from shared memory. Overflowed bricks: *overflow
-// is set and the column-probing pair kernels run instead (they test every
-// pair again; links are idempotent).
-template <bool WIDE, int MODE>
-__global__ void __launch_bounds__(BRK_THREADS, 2) sp_border_brick_kernel(SpArgs a, const BrickCols cols,
-                                                                     uint32_t nby, uint32_t nbz,
-                                                                     uint32_t* overflow, uint8_t* cnt_s,
-                                                                     uint32_t* ovf_list, uint32_t* novf) {
-  extern __shared__ __align__(16) uint8_t bb_raw[];
-  BorderBrickSmem& S = *reinterpret_cast<BorderBrickSmem*>(bb_raw);
-  const uint32_t bid = blockIdx.x;
-  const uint32_t bz = bid % nbz, by = (bid / nbz) % nby, bx = bid / (nbz * nby);
-  const uint64_t Dx = a.g.maxc[0] + 1 + 2 * BRK_R, Dy = a.g.maxc[1] + 1 + 2 * BRK_R,
-                 Dz = a.g.maxc[2] + 1 + 2 * BRK_R;
-  const uint64_t X0 = (uint64_t)bx * BRK, Y0 = (uint64_t)by * BRK, Z0 = (uint64_t)bz * BRK;
-  // ---- phase 0: a thread per halo column: cell boundaries and core counts
-  uint32_t clen[BRK_PER], own[BRK_PER], rr[BRK_PER], bb[BRK_PER];
-  bool big = false;
-#pragma unroll
-  for (int q = 0; q < BRK_PER; ++q) {
-    const int cc = threadIdx.x * BRK_PER + q;
-    clen[q] = own[q] = rr[q] = bb[q] = 0;
-    if (cc >= BRK_COLS) continue;
-    const uint32_t hx = cc / BRK_H, hy = cc % BRK_H;
-    const uint64_t X = X0 + hx, Y = Y0 + hy;
-    uint32_t bits = 0, r = 0;
-    if (X < Dx && Y < Dy) {
-      const uint32_t hz = (uint32_t)min((uint64_t)BRK_H, Dz - Z0);
-      const uint64_t lin0 = (X * Dy + Y) * Dz + Z0;
-      const uint4 e = __ldg(a.dir + (lin0 >> 5));
-      const uint32_t b0 = (uint32_t)lin0 & 31u;
-      bits = __funnelshift_r(e.x, e.y, b0) & ((1u << hz) - 1u);
-      r = e.z + __popc(e.x & ((1u << b0) - 1u));
-    }
-    const uint32_t g0 = __ldg(a.cell_start + r);
-    uint32_t run = 0, crun = 0, o0 = 0, o1 = 0;
-#pragma unroll
-    for (int z = 0; z < BRK_H; ++z) {
-      if (z == BRK_R) o0 = MODE ? crun : run;
-      if (z == BRK_R + BRK) o1 = MODE ? crun : run;
-      S.rel[cc][z] = (uint16_t)min(run, 65535u);
-      S.cabs[cc][z] = (uint16_t)min(crun, 65535u);  // (made absolute below)
-      if ((bits >> z) & 1u) {
-        const uint32_t k = r + __popc(bits & ((1u << z) - 1u));  // the cell's id
-        run = __ldg(a.cell_start + k + 1) - g0;
-        crun += __ldg(a.core_cnt + k);
-      }
-    }
-    S.rel[cc][BRK_H] = (uint16_t)min(run, 65535u);
-    S.cabs[cc][BRK_H] = (uint16_t)min(crun, 65535u);
-    big |= run > 65535u;
-    S.g0[cc] = g0;
-    clen[q] = crun;
-    rr[q] = r;
-    bb[q] = bits;
-    own[q] = (hx >= BRK_R && hx < BRK_R + BRK && hy >= BRK_R && hy < BRK_R + BRK) ? o1 - o0 : 0u;
-  }
-  uint32_t el;
-  {
-    unsigned long long sv = 0;
-#pragma unroll
-    for (int q = 0; q < BRK_PER; ++q) sv += (unsigned long long)clen[q] | ((unsigned long long)own[q] << 32);
-    if (big) sv += (unsigned long long)BB_CAP + 1;  // a column over 65535 points: overflow
-    unsigned long long tot;
-    const unsigned long long ex = block_exclusive_scan<unsigned long long>(sv, S.scan, &tot);
-    el = (uint32_t)ex;
-    uint32_t eo = (uint32_t)(ex >> 32);
-#pragma unroll
-    for (int q = 0; q < BRK_PER; ++q) {
-      const int cc = threadIdx.x * BRK_PER + q;
-      if (cc < BRK_COLS) S.obase[cc] = eo;
-      eo += own[q];
-    }
-    if (threadIdx.x == 0) {
-      S.ctotal = (uint32_t)tot;
-      S.own = (uint32_t)(tot >> 32);
-    }
-  }
-  __syncthreads();
-  const uint32_t ctotal = S.ctotal, nown = S.own;
-  if (nown == 0) return;
-  if (ctotal > BB_CAP) {
-    if (threadIdx.x == 0) atomicExch(overflow, 1u);
-    return;
-  }
-  // ---- phase 1: copy each column's core points (with their labels); cabs absolute
-#pragma unroll
-  for (int q = 0; q < BRK_PER; ++q) {
-    const int cc = threadIdx.x * BRK_PER + q;
-    if (cc >= BRK_COLS) continue;
-    if (clen[q]) {
-      const uint32_t g0 = S.g0[cc];
-      for (uint32_t b = bb[q]; b; b &= b - 1) {
-        const int z = __ffs(b) - 1;
-        const uint32_t c0 = S.cabs[cc][z], c1 = S.cabs[cc][z + 1];
-        if (c0 == c1) continue;
-        const uint32_t k = rr[q] + __popc(bb[q] & ((1u << z) - 1u));
-        const uint32_t lab = MODE ? k : __ldg(a.cell_label + k);
-        const uint32_t src = g0 + S.rel[cc][z];
-        for (uint32_t t = 0; t < c1 - c0; ++t) {
-          int4 v = __ldg(reinterpret_cast<const int4*>(a.Ps) + src + t);
-          v.w = (int32_t)lab;
-          S.cpts[el + c0 + t] = v;
-        }
-      }
-    }
-#pragma unroll
-    for (int z = 0; z <= BRK_H; ++z) S.cabs[cc][z] += (uint16_t)el;
-    el += clen[q];
-  }
-  __syncthreads();
-  const uint16_t* cabs_flat = &S.cabs[0][0];
-  if constexpr (MODE == 1) {
-    // ---- ClusterCore: a thread per own core point
-    for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
-      int cc = 0;
-#pragma unroll
-      for (int step = 256; step; step >>= 1)
-        if (cc + step < BRK_COLS && S.obase[cc + step] <= t) cc += step;
-      const uint16_t* ca = S.cabs[cc];
-      const uint32_t u0 = t - S.obase[cc] + ca[BRK_R];  // index in cpts
-      int hz = BRK_R;
-#pragma unroll
-      for (int step = 8; step; step >>= 1)
-        if (ca[hz + step] <= u0) hz += step;
-      const int4 pv = S.cpts[u0];
-      const int32_t p[4] = {pv.x, pv.y, pv.z, 0};
-      const uint32_t gcell = (uint32_t)pv.w;
-      const uint32_t base = smem_addr(cabs_flat + cc * (BRK_H + 1) + hz);
-      uint32_t last = MISS;  // the cell linked last (its other points need no test)
-#pragma unroll
-      for (int k = 0; k < BRK_MAXC; ++k) {
-        if (k < cols.ncols) {
-          const uint32_t lo = lds_u16(base + cols.A[k]), hi = lds_u16(base + cols.B[k]);
-          for (uint32_t u = lo; u < hi; ++u) {
-            const int4 qv = S.cpts[u];
-            const uint32_t h = (uint32_t)qv.w;
-            if (h >= gcell || h == last) continue;
-            const int32_t q[4] = {qv.x, qv.y, qv.z, 0};
-            DB_WORK(1);
-            if (!within<3, WIDE>(p, q, a.g.clampc, a.g.eps2)) continue;
-            uf_link(a.parent, gcell, h);
-            last = h;
-          }
-        }
-      }
-    }
-    return;
-  }
-  // ---- phase 2: a thread per own non-core point
-  uint32_t nb = 0;
-  for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
-    int cc = 0;
-#pragma unroll
-    for (int step = 256; step; step >>= 1)
-      if (cc + step < BRK_COLS && S.obase[cc + step] <= t) cc += step;
-    const uint16_t* rl = S.rel[cc];
-    const uint32_t off = t - S.obase[cc] + rl[BRK_R];  // offset in the column
-    int hz = BRK_R;
-#pragma unroll
-    for (int step = 8; step; step >>= 1)
-      if (rl[hz + step] <= off) hz += step;
-    const uint32_t j = S.g0[cc] + off;  // sorted position
-    if (a.core_s[j]) continue;          // core point: no border row
-    const int4 pv = __ldg(reinterpret_cast<const int4*>(a.Ps) + j);
-    const int32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
-    const uint32_t base = smem_addr(cabs_flat + cc * (BRK_H + 1) + hz);
-    uint32_t L[SP_MAXL];
-#pragma unroll
-    for (int k = 0; k < SP_MAXL; ++k) L[k] = MISS;
-    int nl = 0;
-    bool ovf = false;
-#pragma unroll
-    for (int k = 0; k < BRK_MAXC; ++k) {
-      if (k < cols.ncols) {
-        const uint32_t lo = lds_u16(base + cols.A[k]), hi = lds_u16(base + cols.B[k]);
-        for (uint32_t u = lo; u < hi; ++u) {
-          const int4 qv = S.cpts[u];
-          const int32_t q[4] = {qv.x, qv.y, qv.z, 0};
-          DB_WORK(2);
-          if (!within<3, WIDE>(p, q, a.g.clampc, a.g.eps2)) continue;
-          const uint32_t lab = (uint32_t)qv.w;
-          bool have = false;
-#pragma unroll
-          for (int s = 0; s < SP_MAXL; ++s) have |= L[s] == lab;
-          if (have) continue;
-          if (nl == SP_MAXL) { ovf = true; continue; }
-#pragma unroll
-          for (int s = 0; s < SP_MAXL; ++s)
-            if (s == nl) L[s] = lab;
-          ++nl;
-        }
-      }
-    }
-    if (ovf) {
-      cnt_s[j] = 0xff;
-      ovf_list[atomicAdd(novf, 1u)] = j;  // (counted with the border points by the enumeration)
-      continue;
-    }
-    if (!nl) continue;
-    auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
-    cs(L[0], L[1]); cs(L[2], L[3]); cs(L[0], L[2]); cs(L[1], L[3]); cs(L[1], L[2]);
-    reinterpret_cast<uint4*>(a.tmp_lab)[j] = make_uint4(L[0], L[1], L[2], L[3]);
-    cnt_s[j] = (uint8_t)nl;
-    a.bcnt[a.idx[j]] = (uint32_t)nl;
-    ++nb;
-  }
-  block_add_u64(nb, a.nborder);
-}
-
-// Points with more than SP_MAXL labels (sorted positions in ovf_list): their
-// label count by storage-free enumeration in ascending order.
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_border_ovf_count_kernel(SpArgs a, const uint32_t* __restrict__ ovf_list,
-                                                                  const uint32_t* __restrict__ novf) {
-  __shared__ long long s_off[SP_MAX_COLS];
-  __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
-  __syncthreads();
-  const uint32_t m = *novf;
-  uint32_t nb = 0;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
-    const uint32_t j = ovf_list[t];
-    const uint32_t g = a.cell_of[j];
-    const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-    int32_t p[D];
-    load_pt<D>(a.Ps, j, p);
-    uint32_t cnt = 0;
-    int64_t after = -1;
-    while (true) {
-      const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
-      if (nx == MISS) break;
-      ++cnt;
-      after = nx;
-    }
-    a.bcnt[a.idx[j]] = cnt;
-    ++nb;
-  }
-  block_add_u64(nb, a.nborder);
-}
-
-// Fill from sorted positions: the labels of point j go to its input-order row.
-template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_border_fill_sorted_kernel(SpArgs a, const uint8_t* __restrict__ cnt_s,
-                                                                    const int64_t* __restrict__ border_off,
-                                                                    int32_t* __restrict__ border_ids) {
-  __shared__ long long s_off[SP_MAX_COLS];
-  __shared__ uint32_t s_mask[SP_MAX_COLS];
-  for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
-  __syncthreads();
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n) return;
-  const uint32_t c = cnt_s[j];
-  if (!c) return;
-  const int64_t o = border_off[a.idx[j]];
-  if (c != 0xffu) {
-    const uint4 v = reinterpret_cast<const uint4*>(a.tmp_lab)[j];
-    const uint32_t L[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if ((uint32_t)q < c) border_ids[o + q] = (int32_t)L[q];
-    return;
-  }
-  const uint32_t g = a.cell_of[j];
-  const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-  int32_t p[D];
-  load_pt<D>(a.Ps, j, p);
-  int64_t after = -1, w = 0;
-  while (true) {
-    const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
-    if (nx == MISS) break;
-    border_ids[o + w++] = (int32_t)nx;
-    after = nx;
-  }
-}
-
 // ----------------------------------------------------------------- host
 template <typename F>
 static void by_dim_sp(int d, bool wide, F&& f) {
@@ -1340,8 +1026,6 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
     const uint32_t nb[3] = {(g.maxc[0] + BRK) / BRK, (g.maxc[1] + BRK) / BRK, (g.maxc[2] + BRK) / BRK};
     const uint64_t nbricks = (uint64_t)nb[0] * nb[1] * nb[2];
     if (nbricks >= (1ull << 31)) throw Error(-4, "sparse path: brick grid too large");
-    a.bc = bc;
-    for (int k = 0; k < 3; ++k) a.nbrick[k] = nb[k];
     DB_CUDA(cudaMemsetAsync(core_s, 0xff, (size_t)n, c.st));
     const size_t smem = sizeof(BrickSmem);
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
@@ -1402,27 +1086,6 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   if (a.nbcols > 0 && a.ncore > 0) {
     const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
     c.zero(a.counters + 2, sizeof(uint32_t));
-    // 3D bricks (the MarkCore brick ran; few core cells): every BCP from
-    // staged core points; the pair kernels below then run only if a brick
-    // overflowed (device flag, no host synchronisation)
-    const uint32_t* run_if = nullptr;
-    o->brick_cluster = o->brick != 0 && !g.at && g.d == 3 && !(o->flags & DBSCAN_F_NO_BRICK) &&
-                       2ull * a.ncore < cv.ncells;
-    if (o->brick_cluster) {
-      uint32_t* fl = c.alloc<uint32_t>(1);
-      c.zero(fl, sizeof(uint32_t));
-      const uint64_t nbricks = (uint64_t)a.nbrick[0] * a.nbrick[1] * a.nbrick[2];
-      const size_t smem = sizeof(BorderBrickSmem);
-      auto launch = [&](auto kern) {
-        DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, a.bc, a.nbrick[1], a.nbrick[2], fl, nullptr,
-                                                            nullptr, nullptr);
-        c.launched();
-      };
-      if (wide) launch(sp_border_brick_kernel<true, 1>);
-      else launch(sp_border_brick_kernel<false, 1>);
-      run_if = fl;
-    }
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
       constexpr bool W = decltype(Wd)::value;
@@ -1434,8 +1097,8 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
       for (int pass = 0; pass < 3; ++pass) {
         const int lo = cut[pass], hi = cut[pass + 1];
         if (lo == hi) continue;
-        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0, run_if);
-        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0, run_if);
+        if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
+        else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         c.launched();
         ++o->passes;
         if (two && hi < a.nbcols) uf_flatten(c, parent, a.core_list, a.ncore);
@@ -1454,44 +1117,6 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   a.tmp_n = c.alloc<uint8_t>(n);
   a.ovf_pos = c.alloc<uint32_t>(n);  // written only for flagged points
   a.nborder = nborder;
-  // brick path (the MarkCore brick ran, few core points): label sets per
-  // point from the bricks' staged core points, no atomics on label sets
-  o->brick_border = o->brick != 0 && !o->point_border && !(o->flags & DBSCAN_F_NO_BRICK);
-  if (o->brick_border) {
-    uint32_t* fl = c.alloc<uint32_t>(2);  // [0] overflow, [1] overflowed label sets
-    c.zero(fl, 2 * sizeof(uint32_t));
-    c.zero(a.bcnt, sizeof(uint32_t) * (size_t)n);
-    c.zero(a.tmp_n, (size_t)n);  // cnt_s: label count per sorted position
-    const uint64_t nbricks = (uint64_t)a.nbrick[0] * a.nbrick[1] * a.nbrick[2];
-    const size_t smem = sizeof(BorderBrickSmem);
-    by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
-      constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
-      constexpr bool W = decltype(Wd)::value;
-      if constexpr (DIM == 3) {
-        auto kern = sp_border_brick_kernel<W, 0>;
-        DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, a.bc, a.nbrick[1], a.nbrick[2], fl, a.tmp_n,
-                                                            a.ovf_pos, fl + 1);
-        c.launched();
-        sp_border_ovf_count_kernel<DIM, D, W><<<c.sms * 2, 256, 0, c.st>>>(a, a.ovf_pos, fl + 1);
-        c.launched();
-      }
-    });
-    const uint32_t* hf = c.fetch(fl, 2);
-    const unsigned long long* hn = c.fetch(nborder, 1);
-    c.sync();
-    if (hf[0]) {  // a brick overflowed: the core-centric path for every point
-      o->brick_border = false;
-      c.zero(nborder, sizeof(unsigned long long));
-    } else {
-      if (*hn == 0) {
-        DB_CUDA(cudaMemsetAsync(border_off, 0, sizeof(int64_t) * (size_t)(n + 1), c.st));
-        return 0;
-      }
-      exclusive_scan_u32_i64(c, a.bcnt, border_off, n);
-      return c.read(border_off + n);
-    }
-  }
   // core-centric: label sets of SP_MAXL slots per point (input order), empty = ~0
   DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
   c.zero(a.tmp_n, (size_t)n);
@@ -1521,11 +1146,7 @@ void sparse_border_fill(Ctx& c, const Geo& g, bool wide, const int64_t* border_o
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
-    if (o->brick_border)
-      sp_border_fill_sorted_kernel<DIM, D, W><<<grid_for(a.n, 256, 1 << 30), 256, 0, c.st>>>(a, a.tmp_n, border_off,
-                                                                                          border_ids);
-    else
-      sp_border_fill_kernel<DIM, D, W><<<grid_for(a.n, 256, 1 << 30), 256, 0, c.st>>>(a, border_off, border_ids);
+    sp_border_fill_kernel<DIM, D, W><<<grid_for(a.n, 256, 1 << 30), 256, 0, c.st>>>(a, border_off, border_ids);
   });
   c.launched();
 }
