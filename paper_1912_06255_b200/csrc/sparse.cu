@@ -100,9 +100,8 @@ struct SpArgs {
   uint2* large;
   uint32_t large_cap;
   uint32_t* bcnt;            // [n] input order
-  uint32_t* tmp_lab;         // [n*SP_MAXL] input order
-  uint8_t* tmp_n;            // [n] input order; 0xff = overflow
-  uint32_t* ovf_pos;         // [n] input order: sorted position of an overflowed point
+  uint32_t* tmp_lab;         // [n*SP_MAXL] label sets by sorted position (MISS = empty slot)
+  uint8_t* tmp_n;            // [n] by sorted position: 0xff = the set overflowed
   unsigned long long* nborder;
   int64_t n;
 };
@@ -677,17 +676,11 @@ __global__ void __launch_bounds__(256) sp_border_point_kernel(SpArgs a) {
       ++nl;
     }
   }
-  const uint32_t i = a.idx[j];
   if (ovf) {
-    a.ovf_pos[i] = j;
-    a.tmp_n[i] = 0xff;
+    a.tmp_n[j] = 0xff;
     return;
   }
-  if (nl) {
-    uint32_t* row = a.tmp_lab + (size_t)i * SP_MAXL;
-#pragma unroll
-    for (int k = 0; k < SP_MAXL; ++k) row[k] = L[k];
-  }
+  if (nl) *reinterpret_cast<uint4*>(a.tmp_lab + (size_t)j * SP_MAXL) = make_uint4(L[0], L[1], L[2], L[3]);
 }
 
 // Core-centric ClusterBorder. Alg 4 asks, for every non-core point p, which
@@ -756,22 +749,22 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
         hit = within_dim<DIM, D, WIDE>(p, q, a.g);
       }
       if (!hit) continue;
-      const uint32_t i = a.idx[u];  // label sets live in input order (the CSR's)
-      uint32_t* L = a.tmp_lab + (size_t)i * SP_MAXL;
+      // label sets by sorted position: the candidates of one core cell lie in
+      // its neighbouring columns, so the atomics of a warp hit nearby lines
+      uint32_t* L = a.tmp_lab + (size_t)u * SP_MAXL;
       bool placed = false;
 #pragma unroll
       for (int s = 0; s < SP_MAXL; ++s) {
         const uint32_t old = atomicCAS(L + s, MISS, lab);
         if (old == MISS || old == lab) { placed = true; break; }
       }
-      if (!placed) {  // overflow: enumerate later from the sorted position
-        a.ovf_pos[i] = u;
-        a.tmp_n[i] = 0xff;
-      }
+      if (!placed) a.tmp_n[u] = 0xff;  // overflow: enumerated later
     }
   }
 }
 
+// Thread per sorted position: the size of its label set, written to the
+// point's input index (bcnt is zeroed first: only non-empty sets scatter).
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
@@ -779,13 +772,12 @@ __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
   for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
   __syncthreads();
   uint32_t nb = 0;  // border points of this thread (grid-stride: one atomic per block)
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += gridDim.x * blockDim.x) {
     uint32_t cnt = 0;
-    if (a.tmp_n[i] != 0xff) {
-      const uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)i * SP_MAXL);
+    if (a.tmp_n[j] != 0xff) {
+      const uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
       cnt = (v.x != MISS) + (v.y != MISS) + (v.z != MISS) + (v.w != MISS);
     } else {
-      const uint32_t j = a.ovf_pos[i];
       const uint32_t g = a.cell_of[j];
       const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
       int32_t p[D];
@@ -798,14 +790,17 @@ __global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
         after = nx;
       }
     }
-    a.bcnt[i] = cnt;
-    nb += cnt > 0;
+    if (cnt) {
+      a.bcnt[a.idx[j]] = cnt;
+      ++nb;
+    }
   }
   block_add_u64(nb, a.nborder);
 }
 
-// Thread per point in input order: its row of the CSR, the set sorted by a
-// 4-input network (unused slots are ~0 and sort last), or the enumeration.
+// Thread per sorted position: the point's row of the CSR (at its input
+// index), the set sorted by a 4-input network (unused slots are ~0 and sort
+// last), or the enumeration for an overflowed set.
 template <int DIM, int D, bool WIDE>
 __global__ void __launch_bounds__(256) sp_border_fill_kernel(SpArgs a, const int64_t* __restrict__ border_off,
                                                              int32_t* __restrict__ border_ids) {
@@ -813,19 +808,24 @@ __global__ void __launch_bounds__(256) sp_border_fill_kernel(SpArgs a, const int
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
   __syncthreads();
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  const int64_t o = border_off[i], e = border_off[i + 1];
-  if (o == e) return;
-  if (a.tmp_n[i] != 0xff) {
-    uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)i * SP_MAXL);
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  const bool ovf = a.tmp_n[j] == 0xff;
+  uint4 v = make_uint4(MISS, MISS, MISS, MISS);
+  if (!ovf) {
+    v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
+    if (v.x == MISS) return;  // (slots fill in order: an empty first slot is an empty set)
+  }
+  const int64_t o = border_off[a.idx[j]];
+  if (!ovf) {
     auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
     cs(v.x, v.y); cs(v.z, v.w); cs(v.x, v.z); cs(v.y, v.w); cs(v.y, v.z);
     const uint32_t L[4] = {v.x, v.y, v.z, v.w};
-    for (int64_t q = 0; q < e - o; ++q) border_ids[o + q] = (int32_t)L[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (L[q] != MISS) border_ids[o + q] = (int32_t)L[q];
     return;
   }
-  const uint32_t j = a.ovf_pos[i];
   const uint32_t g = a.cell_of[j];
   const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
   int32_t p[D];
@@ -1115,11 +1115,11 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   a.bcnt = c.alloc<uint32_t>(n);
   a.tmp_lab = c.alloc<uint32_t>((size_t)n * SP_MAXL);
   a.tmp_n = c.alloc<uint8_t>(n);
-  a.ovf_pos = c.alloc<uint32_t>(n);  // written only for flagged points
   a.nborder = nborder;
   // core-centric: label sets of SP_MAXL slots per point (input order), empty = ~0
   DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
   c.zero(a.tmp_n, (size_t)n);
+  c.zero(a.bcnt, sizeof(uint32_t) * (size_t)n);  // (the count pass writes non-zero counts only)
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
