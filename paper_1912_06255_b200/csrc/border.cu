@@ -117,7 +117,7 @@ __device__ __forceinline__ bool border_point(int fill, uint32_t j, const CellsVi
 // follow its core points (a7) and exist only in cells with |g| < minPts
 // (P:L883); cells without non-core points cost one load.
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(256) border_kernel(
+__global__ void __launch_bounds__(256, 4) border_kernel(
     int fill, CellsView cv, const int32_t* __restrict__ Ps, const uint32_t* __restrict__ idx,
     const uint32_t* __restrict__ core_cnt, const uint32_t* __restrict__ cell_label, uint32_t clampc,
     uint64_t eps2, uint32_t* __restrict__ bcnt, const int64_t* __restrict__ border_off,

@@ -203,7 +203,7 @@ __device__ bool warp_bcp_tree(uint32_t ga, uint32_t hb, const CellsView& cv, con
 // MODE 0: exact; 1: exact with range-count trees (row f2); 2: approximate
 // connectivity (row f4). Separate instantiations keep the exact kernel lean.
 template <int D, bool WIDE, int MODE>
-__global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict__ list,
+__global__ void __launch_bounds__(256, 2) bcp_large_kernel(const uint2* __restrict__ list,
                                                         const uint32_t* __restrict__ count,
                                                         CellsView cv, Geo g,
                                                         const int32_t* __restrict__ Ps,
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) bcp_large_kernel(const uint2* __restrict_
 // segment of class-sorted rows holds at most 2d cells): each group walks its
 // own cells and the warp runs until all of its groups are done.
 template <int D, bool WIDE, bool APX, int G>
-__global__ void __launch_bounds__(256) wave_csr_kernel(int wave, int nwaves, CellsView cv, Geo g,
+__global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, CellsView cv, Geo g,
                                                        const int32_t* __restrict__ Ps,
                                                        const uint32_t* __restrict__ core_cnt, uint32_t* parent,
                                                        uint2* __restrict__ large, uint32_t* __restrict__ nlarge,

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
 // consecutive points, so the loads coalesce. The count is warp-uniform, so
 // the exit at minPts is a uniform branch.
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+__global__ void __launch_bounds__(256, 4) mark_core_warp_kernel(CellsView cv, const int32_t* __restrict__ Ps,
                                                              const uint32_t* __restrict__ queue,
                                                              const uint32_t* __restrict__ qcount,
                                                              int64_t min_pts, uint32_t clampc,
@@ -154,7 +154,7 @@ __device__ __forceinline__ void box_dist2(const int32_t* p, const int32_t* __res
 }
 
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(256) mark_core_qt_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+__global__ void __launch_bounds__(256, 4) mark_core_qt_kernel(CellsView cv, const int32_t* __restrict__ Ps,
                                                            const uint32_t* __restrict__ queue,
                                                            const uint32_t* __restrict__ qcount, int64_t min_pts,
                                                            Geo g, QTrees qt, uint8_t* __restrict__ core_s) {

@@ -59,7 +59,7 @@ constexpr int SG_TILE = SG_THREADS * SG_ITEMS;
 // single-pass chained scan over tiles). Writes cell_of, cell_start, cell_key
 // and gathers Ps[j] = pts[idx[j]] padded to D int32 (padding = 0).
 template <typename K, int D>
-__global__ void __launch_bounds__(SG_THREADS) segment_kernel(
+__global__ void __launch_bounds__(SG_THREADS, 2) segment_kernel(
     const K* __restrict__ keys, const uint32_t* __restrict__ idx, const int32_t* __restrict__ pts,
     int d, uint32_t n, int32_t* __restrict__ Ps, uint32_t* __restrict__ cell_of,
     uint32_t* __restrict__ cell_start, uint64_t* __restrict__ cell_key, uint64_t* status,

@@ -99,9 +99,14 @@ struct SpArgs {
   uint32_t* parent;
   uint2* large;
   uint32_t large_cap;
+  uint2* edges;              // ClusterCore: positive pairs (g, h), linked by link_edges_kernel
+  uint32_t* nedges;
+  uint32_t edge_cap;
   uint32_t* bcnt;            // [n] input order
   uint32_t* tmp_lab;         // [n*SP_MAXL] label sets by sorted position (MISS = empty slot)
-  uint8_t* tmp_n;            // [n] by sorted position: 0xff = the set overflowed
+  uint8_t* tmp_n;            // [n] by sorted position: 0 no label, 1 labels in tmp_lab, 0xff overflowed
+  uint32_t* ovf_list;        // sorted positions of overflowed sets (count in ovf_count)
+  uint32_t* ovf_count;
   unsigned long long* nborder;
   int64_t n;
 };
@@ -528,11 +533,40 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 // connect, tested directly), then the rest with Find first — on data where
 // most cells join one component the second pass is pruned almost entirely
 // instead of testing and linking every pair against one contended root.
+// Positive pairs are not linked in place: the union-find walks of a link are
+// chains of dependent L2 round trips that ran with 2-3 of 32 lanes active
+// inside the lanes' divergent pair loops (ncu, c5). They go to a per-warp
+// shared buffer, flushed to a global edge list with one atomic per half
+// buffer, and link_edges_kernel links them afterwards with a thread per edge
+// (a buffer or list that is full links in place: correct, only slower).
+constexpr int SP_EB = 128;  // edges buffered per warp
+
+__device__ __forceinline__ void sp_flush_edges(const SpArgs& a, uint2* buf, uint32_t* cntp, int lane) {
+  __syncwarp();
+  const uint32_t cnt = min(*cntp, (uint32_t)SP_EB);
+  uint32_t base = 0;
+  if (lane == 0 && cnt) base = atomicAdd(a.nedges, cnt);
+  base = __shfl_sync(DB_FULL, base, 0);
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint2 e = buf[i];
+    if (base + i < a.edge_cap) a.edges[base + i] = e;
+    else uf_link(a.parent, e.x, e.y);
+  }
+  __syncwarp();
+  if (lane == 0) *cntp = 0;
+  __syncwarp();
+}
+
 template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
-__global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
+__global__ void __launch_bounds__(256, 4) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
                                                        int col_hi, bool find_first) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
+  __shared__ uint2 s_e[8][SP_EB];
+  __shared__ uint32_t s_en[8];
+  uint2* ebuf = s_e[threadIdx.x >> 5];
+  uint32_t* ecnt = s_en + (threadIdx.x >> 5);
+  if ((threadIdx.x & 31) == 0) *ecnt = 0;
   const int nb = col_hi - col_lo;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     s_off[i] = a.bcoff[col_lo + i];
@@ -560,6 +594,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
     // the h loop issued with ~3 of 32 lanes active (ncu, uniform-3d eps=1000)
     for (uint32_t it0 = 0; it0 < items; it0 += 32) {
       __syncwarp();
+      if (*ecnt >= SP_EB / 2) sp_flush_edges(a, ebuf, ecnt, lane);  // (warp-uniform)
       const uint32_t it = it0 + lane;
       if (it >= items) continue;
       const uint32_t ci = it / nb, col = it - ci * nb;
@@ -595,11 +630,25 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
             }
           }
         }
-        if (hit) uf_link(a.parent, g, h);
+        if (hit) {
+          const uint32_t pos = atomicAdd(ecnt, 1u);
+          if (pos < (uint32_t)SP_EB) ebuf[pos] = make_uint2(g, h);
+          else uf_link(a.parent, g, h);
+        }
       }
     }
   }
+  sp_flush_edges(a, ebuf, ecnt, lane);
   block_add_u64(mine, tested);
+}
+
+__global__ void __launch_bounds__(256) link_edges_kernel(uint32_t* parent, const uint2* __restrict__ edges,
+                                                         const uint32_t* __restrict__ nedges, uint32_t cap) {
+  const uint32_t m = min(*nedges, cap);
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+    const uint2 e = edges[t];
+    uf_link(parent, e.x, e.y);
+  }
 }
 
 // --------------------------------------------------------- ClusterBorder (a10)
@@ -636,6 +685,20 @@ __device__ uint32_t sp_next_label(const SpArgs& a, const long long* s_off, const
   return best;
 }
 
+// tmp_n[j] |= v with a 32-bit atomic on the word holding the byte; returns the
+// byte's previous value. (0xff | 1 = 0xff: an overflow flag is never undone.)
+__device__ __forceinline__ uint32_t flag_or(uint8_t* tmp_n, uint32_t j, uint32_t v) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(tmp_n + (j & ~3u));
+  const uint32_t sh = (j & 3u) * 8u;
+  return (atomicOr(w, v << sh) >> sh) & 255u;
+}
+
+// A label set passed SP_MAXL labels: flag it (first flagger lists it for the
+// enumeration kernel, which then writes its exact count).
+__device__ __forceinline__ void flag_overflow(const SpArgs& a, uint32_t j) {
+  if (flag_or(a.tmp_n, j, 0xffu) != 0xffu) a.ovf_list[atomicAdd(a.ovf_count, 1u)] = j;
+}
+
 // Point-centric ClusterBorder, for lattices where almost every point is core
 // (few non-core points, millions of core cells): a thread per non-core point
 // walks the stencil columns on the core directory, tests the core points of
@@ -643,7 +706,7 @@ __device__ uint32_t sp_next_label(const SpArgs& a, const long long* s_off, const
 // set (ascending order is the fill's job) with no atomics — one thread owns
 // the row. More than SP_MAXL labels: flagged, enumerated later.
 template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_border_point_kernel(SpArgs a) {
+__global__ void __launch_bounds__(256, 4) sp_border_point_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int i = threadIdx.x; i < a.ncols; i += blockDim.x) { s_off[i] = a.coff[i]; s_mask[i] = a.cmask[i]; }
@@ -676,11 +739,14 @@ __global__ void __launch_bounds__(256) sp_border_point_kernel(SpArgs a) {
       ++nl;
     }
   }
-  if (ovf) {
-    a.tmp_n[j] = 0xff;
-    return;
+  if (ovf) {  // (counted as a border point below; its count comes from the enumeration)
+    flag_overflow(a, j);
+  } else if (nl) {
+    *reinterpret_cast<uint4*>(a.tmp_lab + (size_t)j * SP_MAXL) = make_uint4(L[0], L[1], L[2], L[3]);
+    a.tmp_n[j] = 1;
+    a.bcnt[a.idx[j]] = (uint32_t)nl;
   }
-  if (nl) *reinterpret_cast<uint4*>(a.tmp_lab + (size_t)j * SP_MAXL) = make_uint4(L[0], L[1], L[2], L[3]);
+  if (ovf || nl) atomicAdd(a.nborder, 1ull);
 }
 
 // Core-centric ClusterBorder. Alg 4 asks, for every non-core point p, which
@@ -706,6 +772,7 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  uint32_t nb = 0;  // border points found first by this thread
   for (uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.ncore; r += nwarps) {
     const uint32_t h = a.core_list[r];
     const uint64_t base = cell_lin<DIM>(a.cell_key[h], a);
@@ -752,50 +819,53 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
       // label sets by sorted position: the candidates of one core cell lie in
       // its neighbouring columns, so the atomics of a warp hit nearby lines
       uint32_t* L = a.tmp_lab + (size_t)u * SP_MAXL;
+      // slots fill in order, so a label appears once; the thread that fills
+      // slot s adds one to the point's count (input order) and, for slot 0,
+      // marks it as a border point
       bool placed = false;
 #pragma unroll
       for (int s = 0; s < SP_MAXL; ++s) {
         const uint32_t old = atomicCAS(L + s, MISS, lab);
+        if (old == MISS) {
+          if (s == 0) {
+            flag_or(a.tmp_n, u, 1u);
+            ++nb;
+          }
+          atomicAdd(a.bcnt + a.idx[u], 1u);
+        }
         if (old == MISS || old == lab) { placed = true; break; }
       }
-      if (!placed) a.tmp_n[u] = 0xff;  // overflow: enumerated later
+      if (!placed) flag_overflow(a, u);  // more than SP_MAXL labels: enumerated later
     }
   }
+  block_add_u64(nb, a.nborder);
 }
 
-// Thread per sorted position: the size of its label set, written to the
-// point's input index (bcnt is zeroed first: only non-empty sets scatter).
+// Overflowed label sets (more than SP_MAXL labels; ovf_list): their exact
+// size by storage-free enumeration, written to the point's input index.
 template <int DIM, int D, bool WIDE>
-__global__ void __launch_bounds__(256) sp_border_count_kernel(SpArgs a) {
+__global__ void __launch_bounds__(256, 4) sp_border_ovf_kernel(SpArgs a) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
   for (int k = threadIdx.x; k < a.ncols; k += blockDim.x) { s_off[k] = a.coff[k]; s_mask[k] = a.cmask[k]; }
   __syncthreads();
-  uint32_t nb = 0;  // border points of this thread (grid-stride: one atomic per block)
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += gridDim.x * blockDim.x) {
+  const uint32_t m = *a.ovf_count;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+    const uint32_t j = a.ovf_list[t];
+    const uint32_t g = a.cell_of[j];
+    const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
+    int32_t p[D];
+    load_pt<D>(a.Ps, j, p);
     uint32_t cnt = 0;
-    if (a.tmp_n[j] != 0xff) {
-      const uint4 v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
-      cnt = (v.x != MISS) + (v.y != MISS) + (v.z != MISS) + (v.w != MISS);
-    } else {
-      const uint32_t g = a.cell_of[j];
-      const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-      int32_t p[D];
-      load_pt<D>(a.Ps, j, p);
-      int64_t after = -1;
-      while (true) {
-        const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
-        if (nx == MISS) break;
-        ++cnt;
-        after = nx;
-      }
+    int64_t after = -1;
+    while (true) {
+      const uint32_t nx = sp_next_label<DIM, D, WIDE>(a, s_off, s_mask, p, g, base, after);
+      if (nx == MISS) break;
+      ++cnt;
+      after = nx;
     }
-    if (cnt) {
-      a.bcnt[a.idx[j]] = cnt;
-      ++nb;
-    }
+    a.bcnt[a.idx[j]] = cnt;
   }
-  block_add_u64(nb, a.nborder);
 }
 
 // Thread per sorted position: the point's row of the CSR (at its input
@@ -810,12 +880,11 @@ __global__ void __launch_bounds__(256) sp_border_fill_kernel(SpArgs a, const int
   __syncthreads();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.n) return;
-  const bool ovf = a.tmp_n[j] == 0xff;
+  const uint32_t f = a.tmp_n[j];
+  if (!f) return;  // no label (core and noise points)
+  const bool ovf = f == 0xffu;
   uint4 v = make_uint4(MISS, MISS, MISS, MISS);
-  if (!ovf) {
-    v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
-    if (v.x == MISS) return;  // (slots fill in order: an empty first slot is an empty set)
-  }
+  if (!ovf) v = *reinterpret_cast<const uint4*>(a.tmp_lab + (size_t)j * SP_MAXL);
   const int64_t o = border_off[a.idx[j]];
   if (!ovf) {
     auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
@@ -1082,6 +1151,10 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   a.parent = parent;
   a.large_cap = a.ncore + 4096;
   a.large = c.alloc<uint2>(a.large_cap);
+  a.edge_cap = (uint32_t)std::min<uint64_t>(4ull * a.ncore + 65536, 1ull << 30);
+  a.edges = c.alloc<uint2>(a.edge_cap);
+  a.nedges = c.alloc<uint32_t>(1);
+  c.zero(a.nedges, sizeof(uint32_t));
   uf_init_list(c, parent, a.core_list, a.ncore);  // (Find and Link touch core cells only)
   if (a.nbcols > 0 && a.ncore > 0) {
     const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
@@ -1100,6 +1173,9 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
         if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         c.launched();
+        link_edges_kernel<<<c.sms * 8, 256, 0, c.st>>>(parent, a.edges, a.nedges, a.edge_cap);
+        c.launched();
+        c.zero(a.nedges, sizeof(uint32_t));
         ++o->passes;
         if (two && hi < a.nbcols) uf_flatten(c, parent, a.core_list, a.ncore);
       }
@@ -1114,12 +1190,15 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
   a.cell_label = cell_label;
   a.bcnt = c.alloc<uint32_t>(n);
   a.tmp_lab = c.alloc<uint32_t>((size_t)n * SP_MAXL);
-  a.tmp_n = c.alloc<uint8_t>(n);
+  a.tmp_n = c.alloc<uint8_t>((size_t)n + 4);  // (+4: flag_or's 32-bit word at the end)
+  a.ovf_count = c.alloc<uint32_t>(1);
+  a.ovf_list = c.alloc<uint32_t>(n);
+  c.zero(a.ovf_count, sizeof(uint32_t));
   a.nborder = nborder;
   // core-centric: label sets of SP_MAXL slots per point (input order), empty = ~0
   DB_CUDA(cudaMemsetAsync(a.tmp_lab, 0xff, sizeof(uint32_t) * (size_t)n * SP_MAXL, c.st));
-  c.zero(a.tmp_n, (size_t)n);
-  c.zero(a.bcnt, sizeof(uint32_t) * (size_t)n);  // (the count pass writes non-zero counts only)
+  c.zero(a.tmp_n, (size_t)n + 4);
+  c.zero(a.bcnt, sizeof(uint32_t) * (size_t)n);  // (counts are added or written for border points only)
   by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
     constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
     constexpr bool W = decltype(Wd)::value;
@@ -1128,7 +1207,7 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
     else
       sp_border_emit_kernel<DIM, D, W><<<grid_for((int64_t)a.ncore * 32, 256, c.sms * 16), 256, 0, c.st>>>(a);
     c.launched();
-    sp_border_count_kernel<DIM, D, W><<<grid_for(n, 256, c.sms * 16), 256, 0, c.st>>>(a);
+    sp_border_ovf_kernel<DIM, D, W><<<c.sms * 2, 256, 0, c.st>>>(a);
     c.launched();
   });
   if (c.read(nborder) == 0) {
