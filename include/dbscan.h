@@ -63,6 +63,8 @@ extern "C" {
 #define DBSCAN_F_QUADTREE    4096u /* our-exact-qt: MarkCore's
                                       RangeCount on cells with >= 256 points traverses a
                                       per-cell tree instead of scanning (CSR path)           */
+#define DBSCAN_F_NO_QBOUND  16384u /* never run the sub-cell lower bounds before MarkCore (row f2)  */
+#define DBSCAN_F_FORCE_QBOUND 32768u /* run them whatever minPts (testing; CSR path)              */
 #define DBSCAN_F_NO_BRICK    8192u /* sparse path, d = 3: MarkCore with a thread per point
                                       instead of the shared-memory brick kernel (testing)    */
 
@@ -115,7 +117,9 @@ extern "C" {
                                         every distance test adds to a device counter; not
                                         thread-safe across concurrent calls, measurement only),
                                         0 in the product library                              */
-#define DBSCAN_NSTATS            32  /* (23-31 reserved) */
+#define DBSCAN_STAT_QB_DECIDED   23  /* MarkCore points proved core by the sub-cell lower bounds
+                                        (row f2, minPts >= 2000 on the CSR path); -1: not run  */
+#define DBSCAN_NSTATS            32  /* (24-31 reserved) */
 
 typedef struct dbscan_result {
   int64_t  n;

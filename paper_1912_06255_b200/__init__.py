@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = ["dbscan", "Result", "lib_path", "load", "F_DEVICE_IO", "F_TIMING", "F_CALLER_OUT",
            "F_FORCE_STENCIL", "F_FORCE_TREE", "F_FORCE_WIDE", "F_NO_WAVES", "F_NO_SPARSE",
-           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "F_COUNT_WORK", "F_QUADTREE", "F_NO_BRICK", "STAGES", "release_workspace",
+           "F_FORCE_SPARSE", "F_RADIX_GROUP", "F_LATTICE_GROUP", "F_COUNT_WORK", "F_QUADTREE", "F_NO_BRICK", "F_NO_QBOUND", "F_FORCE_QBOUND", "STAGES", "release_workspace",
            "STATS", "peak_dist",
            "DBSCANError"]
 
@@ -41,13 +41,13 @@ lib_path = os.path.join(_HERE, "libdbscan_b200_count.so" if os.environ.get("DBSC
 F_DEVICE_IO, F_TIMING, F_CALLER_OUT = 1, 2, 4
 F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
 F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP, F_COUNT_WORK = 128, 256, 512, 1024, 2048
-F_QUADTREE, F_NO_BRICK = 4096, 8192
+F_QUADTREE, F_NO_BRICK, F_NO_QBOUND, F_FORCE_QBOUND = 4096, 8192, 16384, 32768
 NSTAGES, NSTATS = 12, 32
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
          "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick", "point_border",
-         "sparse_passes", "bcp_tests", "border_tests", "counting_build"]
+         "sparse_passes", "bcp_tests", "border_tests", "counting_build", "qb_decided"]
 
 
 class _Result(C.Structure):

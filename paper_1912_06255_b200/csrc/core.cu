@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
                                                         int64_t min_pts, uint32_t clampc, uint64_t eps2,
                                                         uint8_t* __restrict__ core_s,
                                                         uint32_t* __restrict__ queue,
-                                                        uint32_t* __restrict__ qcount) {
+                                                        uint32_t* __restrict__ qcount, bool pre) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < cv.ncells; g += nwarps) {
@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
     }
     for (uint32_t j0 = s; j0 < e; j0 += 32) {
       const uint32_t j = j0 + lane;
-      const bool valid = j < e;
+      // (pre: points the sub-cell bounds proved core are set already)
+      const bool valid = j < e && !(pre && core_s[j]);
       const bool enqueue = valid && ub > WARP_CANDIDATES;
       if (valid && !enqueue) {
         int32_t p[D], q[D];
@@ -244,13 +245,13 @@ __global__ void __launch_bounds__(256, 4) mark_core_qt_kernel(CellsView cv, cons
 }
 
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
-               int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt) {
+               int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt, bool pre) {
   uint32_t* queue = c.alloc<uint32_t>(n);
   uint32_t* qcount = c.alloc<uint32_t>(1);
   c.zero(qcount, sizeof(uint32_t));
   dispatch(g.D, wide, [&]<int D, bool W>() {
     mark_core_kernel<D, W><<<grid_for((int64_t)cv.ncells * 32, 256, c.sms * 16), 256, 0, c.st>>>(
-        cv, Ps, min_pts, g.clampc, g.eps2, core_s, queue, qcount);
+        cv, Ps, min_pts, g.clampc, g.eps2, core_s, queue, qcount, pre);
     c.launched();
     if (qt && qt->nodes)
       mark_core_qt_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts, g, *qt, core_s);

@@ -483,6 +483,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
 
   uint64_t nbr_total = 0;
   bool dense_dir = false;
+  unsigned long long* qb_decided = nullptr;  // points proved core by the sub-cell bounds
   CellsView cv{ncells, cell_start, cell_key, cell_of, nullptr, nullptr, nullptr};
   SparseOut so;
   struct SpGuard { SparseOut* o; ~SpGuard() { sparse_release(o); } } sp_guard{&so};
@@ -517,9 +518,18 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
       build_qtrees(c, g, cv, Ps, sidx, n, &qtrees);
       if (min_mode == LABEL_MIN_FIRST) min_mode = LABEL_MIN_SCAN;  // cells are no longer stable
     }
-    // ---- a6: MarkCore
+    // ---- a6: MarkCore (large minPts: sub-cell lower bounds first, row f2)
     tm.stage(DBSCAN_STAGE_MARKCORE);
-    mark_core(c, g, cv, Ps, n, min_pts, wide, core_s, &qtrees);
+    const bool bounds = !(flags & DBSCAN_F_QUADTREE) && !(flags & DBSCAN_F_NO_QBOUND) &&
+                        (min_pts >= QB_MIN_PTS || (flags & DBSCAN_F_FORCE_QBOUND));
+    if (bounds) {
+      qb_decided = c.alloc<unsigned long long>(1);
+      c.zero(qb_decided, sizeof(unsigned long long));
+      c.zero(core_s, (size_t)n);
+      mark_core_bounds(c, g, cv, Ps, sidx, n, min_pts, core_s, qb_decided);
+      if (min_mode == LABEL_MIN_FIRST) min_mode = LABEL_MIN_SCAN;  // cells are no longer stable
+    }
+    mark_core(c, g, cv, Ps, n, min_pts, wide, core_s, &qtrees, bounds);
     // ---- a7: core-first compaction
     tm.stage(DBSCAN_STAGE_COMPACT);
     compact_core(c, g, cv, Ps, sidx, core_s, n, min_pts, core_cnt, cnt32);
@@ -601,6 +611,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   unsigned long long h64[3];
   const uint32_t* h32_h = c.fetch(cnt32, 4);
   const unsigned long long* h64_h = c.fetch(cnt64, 3);
+  const unsigned long long* hqb = qb_decided ? c.fetch(qb_decided, 1) : nullptr;
   tm.close();  // (the last event; read after the stream is idle)
   c.free_all();
   if (c.tracing) c.mark("final sync");
@@ -645,6 +656,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_BRICK] = so.brick;
   out->stats[DBSCAN_STAT_POINT_BORDER] = so.point_border;
   out->stats[DBSCAN_STAT_SPARSE_PASSES] = so.passes;
+  out->stats[DBSCAN_STAT_QB_DECIDED] = hqb ? (int64_t)*hqb : -1;
   return DBSCAN_OK;
 }
 

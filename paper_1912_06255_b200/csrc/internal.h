@@ -281,8 +281,16 @@ struct QTrees {
 // Orders the points of tree cells by Morton code inside the cell (Ps, idx
 // permuted within each cell) and builds the trees.
 void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx, int64_t n, QTrees* qt);
+// pre: core_s already holds 1 for points proved core by mark_core_bounds
+// (0 elsewhere); those points are skipped.
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
-               int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt = nullptr);
+               int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt = nullptr, bool pre = false);
+// Row f2, large minPts: points proved core by lower bounds from sub-cell
+// counts (qtree.cu; reorders the points of cells with >= 256 points by
+// sub-cell). core_s must be zeroed; *decided (device) += points proved core.
+constexpr int64_t QB_MIN_PTS = 2000;  // minPts from which the bounds run by default
+void mark_core_bounds(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx, int64_t n,
+                      int64_t min_pts, uint8_t* core_s, unsigned long long* decided);
 // core-first stable partition inside each mixed cell (Ps, idx, core_s permuted in
 // place); core_cnt[ncells]; counters[0] += core cells, counters[1] += mixed cells.
 void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32_t* idx,

@@ -100,7 +100,8 @@ def test_random_small_vs_o1(oracle_lib):
                                    pkg.F_RADIX_GROUP, pkg.F_RADIX_GROUP | pkg.F_FORCE_SPARSE,
                                    pkg.F_LATTICE_GROUP, pkg.F_LATTICE_GROUP | pkg.F_FORCE_SPARSE,
                                    pkg.F_LATTICE_GROUP | pkg.F_NO_SPARSE,
-                                   pkg.F_QUADTREE, pkg.F_QUADTREE | pkg.F_RADIX_GROUP | pkg.F_FORCE_TREE])
+                                   pkg.F_QUADTREE, pkg.F_QUADTREE | pkg.F_RADIX_GROUP | pkg.F_FORCE_TREE,
+                                   pkg.F_FORCE_QBOUND, pkg.F_FORCE_QBOUND | pkg.F_RADIX_GROUP | pkg.F_FORCE_WIDE])
 def test_flag_variants_vs_o1(oracle_lib, flags):
     for k, (pts, eps, mp) in enumerate(_instances(200 + flags, 120, dmax=8)):
         r = run_or_erange(pts, eps, mp, flags)
@@ -526,3 +527,24 @@ def test_border_many_labels_vs_o2(oracle_lib, flags):
     rows = np.diff(want.border_off)
     assert rows.max() == 6 and (rows == 6).sum() == 3
     assert_same(np_result(r), want, f"star flags={flags}")
+
+
+@pytest.mark.parametrize("d", [2, 3, 5])
+def test_subcell_bounds_large_minpts_vs_o2(oracle_lib, d):
+    """Row f2 for large minPts: points proved core by lower bounds from
+    sub-cell counts (cells of >= 256 points subdivided, nodes inside the
+    eps-ball of a query sub-cell counted without tests), the rest counted
+    exactly. Seed-spreader clusters with cells of thousands of points,
+    minPts around the neighbourhood sizes (some points decided by the
+    bounds, some counted, some non-core), against O2 and against the path
+    without the bounds."""
+    L = 1e6 if d <= 3 else 1e5
+    pts = datagen.seed_spreader(300_000, d, L / 10, 70 + d, 0.002, noise_frac=0.01)
+    eps = 400 if d <= 3 else 1500
+    for mp in (2000, 8000):
+        r = gpu(pts, eps, mp)
+        assert r.stats["qb_decided"] >= 0, r.stats
+        want = oracle_lib.o2(pts, eps, mp)
+        assert_same(np_result(r), want, f"bounds d={d} mp={mp}")
+        assert_same(np_result(gpu(pts, eps, mp, pkg.F_NO_QBOUND)), want, f"no bounds d={d} mp={mp}")
+    assert r.stats["qb_decided"] > 0 or d == 5
