@@ -99,9 +99,6 @@ struct SpArgs {
   uint32_t* parent;
   uint2* large;
   uint32_t large_cap;
-  uint2* edges;              // ClusterCore: positive pairs (g, h), linked by link_edges_kernel
-  uint32_t* nedges;
-  uint32_t edge_cap;
   uint32_t* bcnt;            // [n] input order
   uint32_t* tmp_lab;         // [n*SP_MAXL] label sets by sorted position (MISS = empty slot)
   uint8_t* tmp_n;            // [n] by sorted position: 0 no label, 1 labels in tmp_lab, 0xff overflowed
@@ -533,40 +530,12 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 // connect, tested directly), then the rest with Find first — on data where
 // most cells join one component the second pass is pruned almost entirely
 // instead of testing and linking every pair against one contended root.
-// Positive pairs are not linked in place: the union-find walks of a link are
-// chains of dependent L2 round trips that ran with 2-3 of 32 lanes active
-// inside the lanes' divergent pair loops (ncu, c5). They go to a per-warp
-// shared buffer, flushed to a global edge list with one atomic per half
-// buffer, and link_edges_kernel links them afterwards with a thread per edge
-// (a buffer or list that is full links in place: correct, only slower).
-constexpr int SP_EB = 128;  // edges buffered per warp
-
-__device__ __forceinline__ void sp_flush_edges(const SpArgs& a, uint2* buf, uint32_t* cntp, int lane) {
-  __syncwarp();
-  const uint32_t cnt = min(*cntp, (uint32_t)SP_EB);
-  uint32_t base = 0;
-  if (lane == 0 && cnt) base = atomicAdd(a.nedges, cnt);
-  base = __shfl_sync(DB_FULL, base, 0);
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const uint2 e = buf[i];
-    if (base + i < a.edge_cap) a.edges[base + i] = e;
-    else uf_link(a.parent, e.x, e.y);
-  }
-  __syncwarp();
-  if (lane == 0) *cntp = 0;
-  __syncwarp();
-}
-
 template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
 __global__ void __launch_bounds__(256, 4) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
                                                        int col_hi, bool find_first) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
-  __shared__ uint2 s_e[8][SP_EB];
-  __shared__ uint32_t s_en[8];
-  uint2* ebuf = s_e[threadIdx.x >> 5];
-  uint32_t* ecnt = s_en + (threadIdx.x >> 5);
-  if ((threadIdx.x & 31) == 0) *ecnt = 0;
+
   const int nb = col_hi - col_lo;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     s_off[i] = a.bcoff[col_lo + i];
@@ -594,7 +563,6 @@ __global__ void __launch_bounds__(256, 4) sp_pairs_kernel(SpArgs a, unsigned lon
     // the h loop issued with ~3 of 32 lanes active (ncu, uniform-3d eps=1000)
     for (uint32_t it0 = 0; it0 < items; it0 += 32) {
       __syncwarp();
-      if (*ecnt >= SP_EB / 2) sp_flush_edges(a, ebuf, ecnt, lane);  // (warp-uniform)
       const uint32_t it = it0 + lane;
       if (it >= items) continue;
       const uint32_t ci = it / nb, col = it - ci * nb;
@@ -630,25 +598,11 @@ __global__ void __launch_bounds__(256, 4) sp_pairs_kernel(SpArgs a, unsigned lon
             }
           }
         }
-        if (hit) {
-          const uint32_t pos = atomicAdd(ecnt, 1u);
-          if (pos < (uint32_t)SP_EB) ebuf[pos] = make_uint2(g, h);
-          else uf_link(a.parent, g, h);
-        }
+        if (hit) uf_link(a.parent, g, h);
       }
     }
   }
-  sp_flush_edges(a, ebuf, ecnt, lane);
   block_add_u64(mine, tested);
-}
-
-__global__ void __launch_bounds__(256) link_edges_kernel(uint32_t* parent, const uint2* __restrict__ edges,
-                                                         const uint32_t* __restrict__ nedges, uint32_t cap) {
-  const uint32_t m = min(*nedges, cap);
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
-    const uint2 e = edges[t];
-    uf_link(parent, e.x, e.y);
-  }
 }
 
 // --------------------------------------------------------- ClusterBorder (a10)
@@ -1151,10 +1105,6 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   a.parent = parent;
   a.large_cap = a.ncore + 4096;
   a.large = c.alloc<uint2>(a.large_cap);
-  a.edge_cap = (uint32_t)std::min<uint64_t>(4ull * a.ncore + 65536, 1ull << 30);
-  a.edges = c.alloc<uint2>(a.edge_cap);
-  a.nedges = c.alloc<uint32_t>(1);
-  c.zero(a.nedges, sizeof(uint32_t));
   uf_init_list(c, parent, a.core_list, a.ncore);  // (Find and Link touch core cells only)
   if (a.nbcols > 0 && a.ncore > 0) {
     const unsigned grid = grid_for(((int64_t)cv.ncells + 31) / 32 * 32, 256, c.sms * 16);
@@ -1173,9 +1123,6 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
         if (g.at) sp_pairs_kernel<DIM, D, W, true, true><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         else sp_pairs_kernel<DIM, D, W, true, false><<<grid, 256, 0, c.st>>>(a, tested, lo, hi, pass > 0);
         c.launched();
-        link_edges_kernel<<<c.sms * 8, 256, 0, c.st>>>(parent, a.edges, a.nedges, a.edge_cap);
-        c.launched();
-        c.zero(a.nedges, sizeof(uint32_t));
         ++o->passes;
         if (two && hi < a.nbcols) uf_flatten(c, parent, a.core_list, a.ncore);
       }

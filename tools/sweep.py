@@ -63,8 +63,11 @@ def main():
         # row f2: minPts sweep where sparse points beside huge cells count long
         # (P:L1473-1477), plain scan vs per-cell trees (F_QUADTREE)
         ss3 = datagen.seed_spreader(a.n, 3, 1e6, 2, 1000 / a.n, noise_frac=1e-4)
-        for mp in (100, 1000, 10_000, 30_000):
+        # default (sub-cell lower bounds from minPts 2000), without them, and
+        # the per-point tree traversal (F_QUADTREE)
+        for mp in (100, 1000, 3000, 10_000, 30_000):
             sets.append(("ss-simden-3d", ss3, 1000, mp))
+            sets.append(("ss-simden-3d+noqb", ss3, 1000, mp))
             sets.append(("ss-simden-3d+qt", ss3, 1000, mp))
     if a.only in ("", "approx"):
         # row f4: rho-approximate DBSCAN on the same configs (rho = 0: exact)
@@ -79,7 +82,7 @@ def main():
             sets.append((f"ss-varden-{d}d", vd, eps, 100))
     for name, pts, eps, mp in sets:
         t = torch.from_numpy(pts).cuda()
-        flags = pkg.F_QUADTREE if name.endswith("+qt") else 0
+        flags = pkg.F_QUADTREE if name.endswith("+qt") else (pkg.F_NO_QBOUND if name.endswith("+noqb") else 0)
         rho = float(name.split("rho=")[1]) if "~rho=" in name else 0.0
         ms, r = timed(t, eps, mp, a.reps, flush, flags, rho or None)
         print(json.dumps({"data": name, "n": len(pts), "d": pts.shape[1], "eps": eps, "min_pts": mp,
