@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256, 4) border_kernel(
 // Counts per non-core point (scattered to input order), then border_off =
 // exclusive scan over all points with core points read as 0 (cluster >= 0),
 // so the counts need no clearing; no border point at all: border_off = 0.
-int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+void border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                      const uint32_t* idx, const uint32_t* core_cnt, const uint32_t* cell_label,
                      const int32_t* cluster, int64_t n, bool wide, int64_t* border_off,
                      unsigned long long* nborder) {
@@ -148,12 +148,8 @@ int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* P
                                                 nullptr, nullptr, nborder);
   });
   c.launched();
-  if (c.read(nborder) == 0) {
-    DB_CUDA(cudaMemsetAsync(border_off, 0, sizeof(int64_t) * (size_t)(n + 1), c.st));
-    return 0;
-  }
-  exclusive_scan_u32_i64_masked(c, bcnt, cluster, border_off, n);
-  return c.read(border_off + n);
+  // (no border point at all: the scan writes zeros without reading the counts)
+  exclusive_scan_u32_i64_masked(c, bcnt, cluster, border_off, n, nborder);
 }
 
 void border_fill(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,

@@ -545,6 +545,15 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   int32_t* cluster_d = dev_io ? out->cluster : c.alloc<int32_t>(n);
   int64_t* off_d = dev_io ? out->border_off : c.alloc<int64_t>((size_t)n + 1);
   int64_t nnz = 0;
+  // final counters (read with the call's last synchronisation)
+  const uint32_t* h32_h = nullptr;
+  const unsigned long long* h64_h = nullptr;
+  const unsigned long long* hqb = nullptr;
+  auto fetch_counters = [&]() {
+    h32_h = c.fetch(cnt32, 4);
+    h64_h = c.fetch(cnt64, 3);
+    hqb = qb_decided ? c.fetch(qb_decided, 1) : nullptr;
+  };
   if (core_cells == 0) {
     // no core point: no cluster, every point is noise
     tm.stage(DBSCAN_STAGE_LABELS);
@@ -578,9 +587,15 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
 
     // ---- a10: ClusterBorder
     tm.stage(DBSCAN_STAGE_BORDER);
-    if (sparse) nnz = sparse_border(c, g, cell_label, cluster_d, n, wide, off_d, cnt64 + 1, &so);
-    else nnz = border_count(c, g, cv, Ps, sidx, core_cnt, cell_label, cluster_d, n, wide, off_d, cnt64 + 1);
-    // (border_count synchronised the stream: border_off is final)
+    if (sparse) sparse_border(c, g, cell_label, cluster_d, n, wide, off_d, cnt64 + 1, &so);
+    else border_count(c, g, cv, Ps, sidx, core_cnt, cell_label, cluster_d, n, wide, off_d, cnt64 + 1);
+    // one synchronisation gives nnz = border_off[n] (the size of border_ids)
+    // and the final counters; with no border point the device work ends here
+    const int64_t* nnz_h = c.fetch(off_d + n, 1);
+    fetch_counters();
+    if (c.tracing) c.mark("border sync");
+    c.sync();
+    nnz = *nnz_h;
     if (!dev_io && nnz == 0) host_fill(out->border_off, 0, sizeof(int64_t) * (size_t)(n + 1));
     else if (!dev_io)
       DB_CUDA(cudaMemcpyAsync(out->border_off, off_d, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost,
@@ -609,9 +624,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   }
   uint32_t h32[4];
   unsigned long long h64[3];
-  const uint32_t* h32_h = c.fetch(cnt32, 4);
-  const unsigned long long* h64_h = c.fetch(cnt64, 3);
-  const unsigned long long* hqb = qb_decided ? c.fetch(qb_decided, 1) : nullptr;
+  if (!h32_h) fetch_counters();
   tm.close();  // (the last event; read after the stream is idle)
   c.free_all();
   if (c.tracing) c.mark("final sync");

@@ -187,10 +187,12 @@ struct DbWorkReg {
 // ---- scan.cu ----
 // out[0..n] = exclusive prefix sums of in[0..n-1]; out[n] = total.
 void exclusive_scan_u32_u64(Ctx& c, const uint32_t* in, uint64_t* out, int64_t n);
-void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n);
+void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n,
+                            const unsigned long long* zero_if = nullptr /* device: 0 => all outputs 0 */);
 void exclusive_scan_u32_u32(Ctx& c, const uint32_t* in, uint32_t* out, int64_t n);
 // same, with in[i] read as 0 where mask[i] >= 0 (in[i] is then never read)
-void exclusive_scan_u32_i64_masked(Ctx& c, const uint32_t* in, const int32_t* mask, int64_t* out, int64_t n);
+void exclusive_scan_u32_i64_masked(Ctx& c, const uint32_t* in, const int32_t* mask, int64_t* out, int64_t n,
+                                   const unsigned long long* zero_if = nullptr);
 
 // ---- radix.cu (a2) ----
 // LSD passes over the low `passes` 8-bit digits; hist = [passes][256] global digit
@@ -325,8 +327,8 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
 void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                     const uint32_t* core_cnt, bool wide, uint32_t* parent,
                     unsigned long long* tested, SparseOut* o);
-int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const int32_t* cluster, int64_t n,
-                      bool wide, int64_t* border_off, unsigned long long* nborder, SparseOut* o);
+void sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const int32_t* cluster, int64_t n,
+                   bool wide, int64_t* border_off, unsigned long long* nborder, SparseOut* o);
 void sparse_border_fill(Ctx& c, const Geo& g, bool wide, const int64_t* border_off,
                         int32_t* border_ids, SparseOut* o);
 void sparse_release(SparseOut* o);
@@ -359,8 +361,9 @@ void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* cor
 
 // ---- border.cu (a10) ----
 // count pass -> border_off (exclusive scan in input order, device int64[n+1],
-// core points read as 0 through cluster[] >= 0); returns nnz (synchronises).
-int64_t border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
+// core points read as 0 through cluster[] >= 0); nnz = border_off[n] (no
+// host synchronisation: the caller reads it).
+void border_count(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps,
                      const uint32_t* idx, const uint32_t* core_cnt, const uint32_t* cell_label,
                      const int32_t* cluster, int64_t n, bool wide, int64_t* border_off,
                      unsigned long long* nborder /*device counter, zeroed*/);

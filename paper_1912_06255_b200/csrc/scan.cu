@@ -14,11 +14,16 @@ constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 // Thread t of a tile owns items [16t, 16t + 16): vector loads and stores
 // straight from registers (a warp's 4 loads / 8 stores of 16 B cover whole
 // sectors), the tile total is published as the aggregate before the look-back.
+// zero_if (optional, device): when *zero_if == 0 every input is known to be 0
+// (e.g. no border point at all): the outputs are written as zeros without
+// reading the input or looking back — the caller need not read the flag on
+// the host first.
 template <typename TOut>
 __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __restrict__ in,
                                                           const int32_t* __restrict__ mask,
                                                           TOut* __restrict__ out, int64_t n,
-                                                          uint64_t* status, uint32_t* tile_ctr) {
+                                                          uint64_t* status, uint32_t* tile_ctr,
+                                                          const unsigned long long* zero_if) {
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_scan[33];
   __shared__ uint64_t s_pref;
@@ -26,6 +31,17 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t j0 = tile * SC_TILE + (int64_t)threadIdx.x * SC_ITEMS;
+  if (zero_if && *zero_if == 0) {
+    if (j0 + SC_ITEMS <= n && (reinterpret_cast<uintptr_t>(out + j0) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < SC_ITEMS * (int)sizeof(TOut) / 16; ++q) reinterpret_cast<uint4*>(out + j0)[q] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (int i = 0; i < SC_ITEMS; ++i)
+        if (j0 + i < n) out[j0 + i] = 0;
+    }
+    if (j0 < n && j0 + SC_ITEMS >= n) out[n] = 0;
+    return;
+  }
   uint32_t v[SC_ITEMS];
   const bool full = j0 + SC_ITEMS <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
                     (!mask || (reinterpret_cast<uintptr_t>(mask) & 15) == 0);
@@ -86,7 +102,8 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
 }
 
 template <typename TOut>
-static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n, const int32_t* mask = nullptr) {
+static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n, const int32_t* mask = nullptr,
+                      const unsigned long long* zero_if = nullptr) {
   if (n == 0) {
     c.zero(out, sizeof(TOut));
     return;
@@ -95,18 +112,20 @@ static void scan_impl(Ctx& c, const uint32_t* in, TOut* out, int64_t n, const in
   uint64_t* status = c.alloc<uint64_t>(tiles + 1);  // [tiles]: the tile counter
   uint32_t* ctr = reinterpret_cast<uint32_t*>(status + tiles);
   c.zero(status, sizeof(uint64_t) * (tiles + 1));
-  scan_kernel<TOut><<<(unsigned)tiles, SC_THREADS, 0, c.st>>>(in, mask, out, n, status, ctr);
+  scan_kernel<TOut><<<(unsigned)tiles, SC_THREADS, 0, c.st>>>(in, mask, out, n, status, ctr, zero_if);
   c.launched();
 }
 
 void exclusive_scan_u32_u64(Ctx& c, const uint32_t* in, uint64_t* out, int64_t n) {
   scan_impl<uint64_t>(c, in, out, n);
 }
-void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n) {
-  scan_impl<int64_t>(c, in, out, n);
+void exclusive_scan_u32_i64(Ctx& c, const uint32_t* in, int64_t* out, int64_t n,
+                            const unsigned long long* zero_if) {
+  scan_impl<int64_t>(c, in, out, n, nullptr, zero_if);
 }
-void exclusive_scan_u32_i64_masked(Ctx& c, const uint32_t* in, const int32_t* mask, int64_t* out, int64_t n) {
-  scan_impl<int64_t>(c, in, out, n, mask);
+void exclusive_scan_u32_i64_masked(Ctx& c, const uint32_t* in, const int32_t* mask, int64_t* out, int64_t n,
+                                   const unsigned long long* zero_if) {
+  scan_impl<int64_t>(c, in, out, n, mask, zero_if);
 }
 
 }  // namespace db

@@ -1131,8 +1131,8 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
   }
 }
 
-int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const int32_t* cluster, int64_t n,
-                      bool wide, int64_t* border_off, unsigned long long* nborder, SparseOut* o) {
+void sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const int32_t* cluster, int64_t n,
+                   bool wide, int64_t* border_off, unsigned long long* nborder, SparseOut* o) {
   SpArgs& a = *(SpArgs*)o->stash;
   a.cell_label = cell_label;
   a.bcnt = c.alloc<uint32_t>(n);
@@ -1157,13 +1157,9 @@ int64_t sparse_border(Ctx& c, const Geo& g, const uint32_t* cell_label, const in
     sp_border_ovf_kernel<DIM, D, W><<<c.sms * 2, 256, 0, c.st>>>(a);
     c.launched();
   });
-  if (c.read(nborder) == 0) {
-    DB_CUDA(cudaMemsetAsync(border_off, 0, sizeof(int64_t) * (size_t)(n + 1), c.st));
-    return 0;
-  }
   (void)cluster;
-  exclusive_scan_u32_i64(c, a.bcnt, border_off, n);
-  return c.read(border_off + n);
+  // (no border point at all: the scan writes zeros without reading the counts)
+  exclusive_scan_u32_i64(c, a.bcnt, border_off, n, nborder);
 }
 
 void sparse_border_fill(Ctx& c, const Geo& g, bool wide, const int64_t* border_off,
