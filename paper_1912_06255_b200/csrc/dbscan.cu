@@ -549,10 +549,12 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   const uint32_t* h32_h = nullptr;
   const unsigned long long* h64_h = nullptr;
   const unsigned long long* hqb = nullptr;
+  const uint64_t* hnbr = nullptr;
   auto fetch_counters = [&]() {
     h32_h = c.fetch(cnt32, 4);
     h64_h = c.fetch(cnt64, 3);
     hqb = qb_decided ? c.fetch(qb_decided, 1) : nullptr;
+    hnbr = c.nbr_total_d ? c.fetch(c.nbr_total_d, 1) : nullptr;
   };
   if (core_cells == 0) {
     // no core point: no cluster, every point is noise
@@ -649,7 +651,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_NCELLS] = ncells;
   out->stats[DBSCAN_STAT_KEY_BITS] = bits;
   out->stats[DBSCAN_STAT_SORT_PASSES] = passes;
-  out->stats[DBSCAN_STAT_NBR_ENTRIES] = (int64_t)nbr_total;
+  out->stats[DBSCAN_STAT_NBR_ENTRIES] = hnbr ? (int64_t)*hnbr : (int64_t)nbr_total;
   out->stats[DBSCAN_STAT_CORE_CELLS] = core_cells == UINT32_MAX ? h32[0] : core_cells;
   out->stats[DBSCAN_STAT_PAIRS] = (int64_t)h64[2];
   out->stats[DBSCAN_STAT_PAIRS_TESTED] = (int64_t)h64[0];

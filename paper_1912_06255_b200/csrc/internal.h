@@ -64,6 +64,7 @@ struct Ctx {
   int64_t launches = 0;
   int sms = 148;
   uint32_t* dense_dir = nullptr;  // dense cell directory, when built
+  const uint64_t* nbr_total_d = nullptr;  // exact neighbour-CSR size (device), when only bounded on the host
   uint64_t dense_lat[3] = {0, 0, 0};
   // Temporaries come out of the call's workspace (one device allocation kept
   // across calls: no allocator call per temporary); past its end they fall
@@ -246,6 +247,7 @@ uint64_t build_hash(Ctx& c, const uint64_t* cell_key, uint32_t ncells, Slot** ta
 // ---- neighbors.cu (a5) ----
 // neighbour-cell CSR excluding the cell itself: nbr_off[ncells+1] (device), nbr list.
 // Both build the CSR and ub[g] = sum of the neighbours' sizes (MarkCore bound).
+// *total: the CSR size, or an upper bound of it (exact count then in c.nbr_total_d).
 // d <= 3 (or forced): builds a dense cell directory or a hash table itself.
 void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                        uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,

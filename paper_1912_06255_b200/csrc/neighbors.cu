@@ -193,6 +193,17 @@ __global__ void dense_fill_kernel(const uint64_t* __restrict__ cell_key, uint32_
   dir[lin] = i;
 }
 
+// Size of the neighbour CSR for the allocations: the exact count (a host read,
+// i.e. a synchronisation) only when the structural bound would be large;
+// otherwise the bound, and the exact count stays on the device (c.nbr_total_d,
+// read with the call's final counters).
+constexpr uint64_t NBR_BOUND_MAX = 1ull << 25;  // entries (128 MB of u32, 256 MB of pairs)
+static uint64_t nbr_total_bound(Ctx& c, const uint64_t* total_d, uint64_t bound) {
+  c.nbr_total_d = total_d;
+  if (bound <= NBR_BOUND_MAX) return bound;
+  return c.read(total_d);
+}
+
 void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                        uint32_t ncells, int64_t n, uint64_t** nbr_off, uint32_t** nbr,
                        uint32_t** ub_out, uint64_t* total, bool* dense_out, const uint32_t** ccls) {
@@ -282,7 +293,7 @@ void neighbors_stencil(Ctx& c, const Geo& g, const uint64_t* cell_key, const uin
   };
   launch(0, nullptr);
   exclusive_scan_u32_u64(c, cnt, off, ncells);
-  *total = c.read(off + ncells);
+  *total = nbr_total_bound(c, off + ncells, (uint64_t)ncells * (uint64_t)noffs);
   uint32_t* list = c.alloc<uint32_t>(*total + 1);
   launch(1, list);
   *nbr_off = off;
@@ -493,7 +504,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   };
   launch(0, nullptr);
   exclusive_scan_u32_u64(c, cnt, off, ncells);
-  *total = c.read(off + ncells);
+  *total = nbr_total_bound(c, off + ncells, (uint64_t)ncells * (uint64_t)ncells);
   uint32_t* list = c.alloc<uint32_t>(*total + 1);
   launch(1, list);
   *nbr_off = off;
