@@ -341,6 +341,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--detail", action="store_true", help="print per-run stage times to stderr")
     ap.add_argument("--no-work", action="store_true", help="skip the work-counting pass (no ALU fractions)")
+    ap.add_argument("--no-small", action="store_true", help="skip the configs[0] (c1) fixed-cost line")
     ap.add_argument("--work-pass", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -533,6 +534,26 @@ def main():
                              f"{','.join(r for r in REF_RUNS if r in runs)} ({npts} points, {dt:.1f} s); c5 runs "
                              "timed in profiles/r2_cpu_baselines.jsonl (O2 16 threads: 17-18 s each)"}
 
+    # ---- configs[0] (c1, 10K points): not part of the 10M-point metric; its
+    # per-call time (fixed cost: launches and synchronisations) reported beside it
+    small = None
+    if rank == 0 and not args.no_small:
+        cfg = datagen.CONFIGS["c1"]
+        t1 = torch.from_numpy(cfg.points()).to(dev)
+        ms1 = []
+        for it in range(25):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pkg.dbscan(t1, cfg.eps, cfg.min_pts)
+            e1.record(stream)
+            e1.synchronize()
+            if it >= 5:
+                ms1.append(e0.elapsed_time(e1))
+        m1 = statistics.median(ms1)
+        small = {"run": "c1", "n": cfg.n, "ms_median": round(m1, 4), "pts_per_s": cfg.n / (m1 / 1e3),
+                 "note": "configs[0], 10K points: per-call fixed cost (device time, CUDA events, median of 20)"}
+
     run_info = []
     for i, (name, cfg, _, _) in enumerate(data):
         m = statistics.median(per_run_ms[i])
@@ -548,7 +569,7 @@ def main():
                        "stage_timing": "stage_ms and rooflines from a second pass of the same steps with the library stage events (F_TIMING), outside the timed region",
                        "parallelism": "replicas" if world > 1 else "single GPU"},
             "roofline": roofline, "rooflines": rooflines, "u1_peak_T_tests_per_s": peaks_out, "stage_ms_per_step": {k: round(v / args.steps, 4) for k, v in stage_tot.items()},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "small_config": small,
             "clocks": clocks, "runs": run_info}
     if args.detail and rank == 0:
         for ri in run_info:
