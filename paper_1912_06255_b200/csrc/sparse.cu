@@ -55,7 +55,7 @@ constexpr int BRK = 16;                  // brick side in cells
 constexpr int BRK_R = 2;                 // halo (R = 2; the usual case for d = 3)
 constexpr int BRK_H = BRK + 2 * BRK_R;   // 20
 constexpr int BRK_COLS = BRK_H * BRK_H;  // halo columns
-constexpr int BRK_CAP = 2200;            // halo points held in shared memory (c5: mean 1,920, sd 44)
+constexpr int BRK_CAP = 2400;            // halo points held in shared memory (c5: mean 1,920)
 constexpr int BRK_THREADS = 512;
 constexpr int BRK_PER = (BRK_COLS + BRK_THREADS - 1) / BRK_THREADS;
 constexpr int BRK_MAXC = (2 * BRK_R + 1) * (2 * BRK_R + 1);  // stencil columns at R = 2: 25
@@ -285,12 +285,8 @@ struct BrickSmem {
   int32_t gdelta[BRK_COLS];              // sorted position - index in pts, per column
   uint32_t obase[BRK_COLS];              // prefix of the own points per column
   uint32_t list[BRK_MAXC][BRK_THREADS];  // phase A: non-empty windows, start | end << 16
-  uint32_t pinfo[BRK_THREADS];           // phase A -> B: index in pts | column << 16
-  uint8_t plen[BRK_THREADS];             // phase A -> B: list length
-  uint16_t perm[BRK_THREADS];            // phase B thread -> phase A slot (longest walks first)
-  uint32_t hist[256];                    // walk lengths (candidates, capped at 255)
   unsigned long long scan[33];
-  uint32_t total, own, nwork;
+  uint32_t total, own;
   uint64_t bar;
 };
 
@@ -411,102 +407,60 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
   }
   __syncthreads();
   mbar_wait(&S.bar, 0);
-  // ---- own points, BRK_THREADS per round: phase A by point, then phase B by
-  // walk length — a warp's walks last as long as its longest, so the round's
-  // points are counting-sorted by their candidate count and consecutive
-  // threads take similar walks (c5: 38.7 steps per warp for 27.6 tests per
-  // point when taken in column order)
+  // ---- a thread per own point
   const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
   const uint16_t* abs_flat = &S.abs[0][0];
-  const int lane = threadIdx.x & 31;
-  for (uint32_t t0 = 0; t0 < nown; t0 += BRK_THREADS) {
-    const uint32_t t = t0 + threadIdx.x;
-    uint32_t key = 0;
-    bool work = false;
-    if (t < nown) {
-      // its column: the last one whose own prefix is <= t (never an empty one)
-      int cc = 0;
+  for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
+    // its column: the last one whose own prefix is <= t (never an empty one)
+    int cc = 0;
 #pragma unroll
-      for (int step = 256; step; step >>= 1)
-        if (cc + step < BRK_COLS && S.obase[cc + step] <= t) cc += step;
-      const uint16_t* col = S.abs[cc];
-      const uint32_t i = t - S.obase[cc] + col[BRK_R];  // index in pts
-      // its cell: the last own z whose start is <= i
-      int hz = BRK_R;
+    for (int step = 256; step; step >>= 1)
+      if (cc + step < BRK_COLS && S.obase[cc + step] <= t) cc += step;
+    const uint16_t* col = S.abs[cc];
+    const uint32_t i = t - S.obase[cc] + col[BRK_R];  // index in pts
+    // its cell: the last own z whose start is <= i
+    int hz = BRK_R;
 #pragma unroll
-      for (int step = 8; step; step >>= 1)
-        if (col[hz + step] <= i) hz += step;
-      if ((int64_t)(col[hz + 1] - col[hz]) >= a.min_pts) {
-        a.core_s[(uint32_t)((int32_t)i + S.gdelta[cc])] = 1;  // dense cell
-      } else {
-        // phase A: non-empty stencil windows, nearest first (32-bit shared
-        // addresses: no 64-bit pointer arithmetic per window)
-        const uint32_t base = smem_addr(abs_flat + cc * (BRK_H + 1) + hz);
-        const uint32_t L = smem_addr(&S.list[0][threadIdx.x]);
-        uint32_t Lw = L, tot = 0;
+    for (int step = 8; step; step >>= 1)
+      if (col[hz + step] <= i) hz += step;
+    const uint32_t j = (uint32_t)((int32_t)i + S.gdelta[cc]);  // sorted position
+    if ((int64_t)(col[hz + 1] - col[hz]) >= a.min_pts) { a.core_s[j] = 1; continue; }  // dense cell
+    const int4 pv = S.pts[i];
+    const int32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
+    // phase A: non-empty stencil windows, nearest first
+    // (32-bit shared-memory addresses: no 64-bit pointer arithmetic per column)
+    const uint32_t base = smem_addr(abs_flat + cc * (BRK_H + 1) + hz);
+    const uint32_t L = smem_addr(&S.list[0][threadIdx.x]);
+    uint32_t Lw = L;
 #pragma unroll
-        for (int k = 0; k < BRK_MAXC; ++k) {
-          if (k < cols.ncols) {
-            const uint32_t lo = lds_u16(base + cols.A[k]), hi = lds_u16(base + cols.B[k]);
-            if (lo < hi) {
-              sts_u32(Lw, __byte_perm(lo, hi, 0x5410));  // lo | hi << 16
-              Lw += 4 * BRK_THREADS;
-              tot += hi - lo;
-            }
-          }
+    for (int k = 0; k < BRK_MAXC; ++k) {
+      if (k < cols.ncols) {
+        const uint32_t lo = lds_u16(base + cols.A[k]), hi = lds_u16(base + cols.B[k]);
+        if (lo < hi) {
+          sts_u32(Lw, __byte_perm(lo, hi, 0x5410));  // lo | hi << 16
+          Lw += 4 * BRK_THREADS;
         }
-        S.pinfo[threadIdx.x] = i | ((uint32_t)cc << 16);
-        S.plen[threadIdx.x] = (uint8_t)((Lw - L) / (4 * BRK_THREADS));
-        key = 255u - min(tot, 255u);  // (longest first)
-        work = true;
       }
     }
-    // counting sort of the round's walks by length
-    if (threadIdx.x < 256) S.hist[threadIdx.x] = 0;
-    __syncthreads();
-    if (work) atomicAdd(&S.hist[key], 1u);
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      uint32_t v[8], sum = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) { v[q] = S.hist[lane * 8 + q]; sum += v[q]; }
-      const uint32_t inc = warp_inclusive_scan(sum);
-      uint32_t ex = inc - sum;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) { S.hist[lane * 8 + q] = ex; ex += v[q]; }
-      if (lane == 31) S.nwork = inc;
-    }
-    __syncthreads();
-    if (work) S.perm[atomicAdd(&S.hist[key], 1u)] = (uint16_t)threadIdx.x;
-    __syncthreads();
+    const uint32_t Lend = Lw;
     // phase B: every step tests one candidate (the own column is never empty)
-    if (threadIdx.x < S.nwork) {
-      const uint32_t o = S.perm[threadIdx.x];
-      const uint32_t info = S.pinfo[o];
-      const uint32_t i = info & 0xffffu, cc = info >> 16;
-      const int4 pv = S.pts[i];
-      const int32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
-      const uint32_t L = smem_addr(&S.list[0][o]);
-      const uint32_t Lend = L + (uint32_t)S.plen[o] * (4 * BRK_THREADS);
-      uint32_t count = 0, u = 0, u1 = 0, Lr = L;
-      for (;;) {
-        if (u >= u1) {
-          if (Lr == Lend) break;
-          const uint32_t w = lds_u32(Lr);
-          Lr += 4 * BRK_THREADS;
-          u = w & 0xffffu;
-          u1 = w >> 16;
-        }
-        DB_WORK(0);
-        const int4 qv = S.pts[u];
-        const int32_t q[4] = {qv.x, qv.y, qv.z, qv.w};
-        count += within<3, WIDE>(p, q, a.g.clampc, a.g.eps2) ? 1u : 0u;
-        ++u;
-        if (count >= need) break;
+    uint32_t count = 0, u = 0, u1 = 0, Lr = L;
+    for (;;) {
+      if (u >= u1) {
+        if (Lr == Lend) break;
+        const uint32_t w = lds_u32(Lr);
+        Lr += 4 * BRK_THREADS;
+        u = w & 0xffffu;
+        u1 = w >> 16;
       }
-      a.core_s[(uint32_t)((int32_t)i + S.gdelta[cc])] = count >= need;
+      DB_WORK(0);
+      const int4 qv = S.pts[u];
+      const int32_t q[4] = {qv.x, qv.y, qv.z, qv.w};
+      count += within<3, WIDE>(p, q, a.g.clampc, a.g.eps2) ? 1u : 0u;
+      ++u;
+      if (count >= need) break;
     }
-    __syncthreads();  // (the lists and the histogram are reused by the next round)
+    a.core_s[j] = count >= need;
   }
 }
 
