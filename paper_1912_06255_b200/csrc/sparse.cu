@@ -55,7 +55,7 @@ constexpr int BRK = 16;                  // brick side in cells
 constexpr int BRK_R = 2;                 // halo (R = 2; the usual case for d = 3)
 constexpr int BRK_H = BRK + 2 * BRK_R;   // 20
 constexpr int BRK_COLS = BRK_H * BRK_H;  // halo columns
-constexpr int BRK_CAP = 2400;            // halo points held in shared memory (c5: mean 1,920)
+constexpr int BRK_CAP = 2400;            // halo points held in shared memory (c5: mean 1,864, sd 43)
 constexpr int BRK_THREADS = 512;
 constexpr int BRK_PER = (BRK_COLS + BRK_THREADS - 1) / BRK_THREADS;
 constexpr int BRK_MAXC = (2 * BRK_R + 1) * (2 * BRK_R + 1);  // stencil columns at R = 2: 25
@@ -1028,12 +1028,13 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   // a6: MarkCore — bricks staged in shared memory (d = 3, R = 2), else a
   // thread per point over the stencil columns (U = 2)
   c.stage(DBSCAN_STAGE_MARKCORE);
-  // bricks hold BRK_CAP / BRK_H^3 = 0.38 points per halo cell: taken when the
-  // mean over the lattice is below 0.3 (denser data would overflow them)
+  // bricks hold BRK_CAP / BRK_H^3 = 0.30 points per halo cell: taken when the
+  // mean over the lattice is at most 0.27 (denser data would overflow them:
+  // at 0.27 a halo holds 2,160 points on average, sd 46)
   // ... and at least 0.15: below it most halo columns are empty and the
   // per-brick staging costs more than it saves (measured: 0.08 points per
   // cell 1.32 ms against 0.93 ms for the thread kernel; 0.23 (c5) 1.04 / 1.07)
-  o->brick = brick_ok && g.d == 3 && g.R == BRK_R && !g.at && (unsigned __int128)n * 10 <= vol * 3 &&
+  o->brick = brick_ok && g.d == 3 && g.R == BRK_R && !g.at && (unsigned __int128)n * 100 <= vol * 27 &&
              (unsigned __int128)n * 20 >= vol * 3;
   if (o->brick) {
     std::vector<int8_t> geom;
