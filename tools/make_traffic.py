@@ -1,11 +1,11 @@
 #!/usr/bin/env python3
-"""Assemble profiles/rN_traffic.json (read by bench.py) from ncu --set full raw
-CSVs of tools/prof.sh, one per config: per-kernel DRAM bytes per launch, the
-dominant MarkCore kernels, and the grouping stage's bytes per call (kernels
-lat_*, group_*, hash_*, radix_*, segment*, sample_collisions; the shared
-scan_kernel is left out since other stages launch it too).
+"""Assemble profiles/r2_traffic.json (read by bench.py) from ncu --set full raw
+CSVs of tools/prof.sh (one call per run, every kernel): DRAM bytes
+(dram__bytes_read.sum + dram__bytes_write.sum) per call of each stage's
+kernels, keyed {run: {stage: bytes}}, plus the per-kernel table. The shared
+scan_kernel is left out (several stages launch it).
 
-usage: python tools/make_traffic.py c5_10=gpurun_out/a_raw.csv c3=... > profiles/r1_traffic.json
+usage: python tools/make_traffic.py c5_10=gpurun_out/a_raw.csv c3=... > profiles/r2_traffic.json
 """
 import json
 import os
@@ -14,18 +14,29 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_traffic import load  # noqa: E402
 
-GROUP = ("lat_", "group_", "hash_", "radix", "segment", "sample_collisions")
-out = {"note": "DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch from ncu --set full "
-               "(cold L2: ncu flushes caches before each replay) on tools/run_one.py; "
-               "see profiles/r1_ncu_*_table.txt", "grouping": {}, "kernels": {}}
+STAGES = [  # (stage, kernel-name prefixes)
+    ("a1 bbox", ("bbox", "sample_collisions")),
+    ("a2-a3 grouping", ("lat_", "group_", "radix", "segment", "keys_kernel")),
+    ("a4-a5 neighbour cells", ("nbr_", "hash_insert", "dense_fill", "tree_", "morton", "decode_cells", "bucket_",
+                               "sort_rows")),
+    ("a6 MarkCore", ("sp_core", "mark_core", "qt_", "qb_")),
+    ("a7 compaction", ("sp_cells", "partition", "core_count", "dir_set", "popc", "dir_pack", "core_list")),
+    ("a8 ClusterCore", ("sp_pairs", "wave_csr", "bcp_large", "uf_")),
+    ("a9 labels", ("label_roots", "cell_label", "write_points", "write_positions", "core_from_cluster")),
+    ("a10 ClusterBorder", ("sp_border", "border_")),
+]
+out = {"note": "DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per call of each stage's kernels, "
+               "ncu --set full (cold L2: ncu flushes caches before each replay, an upper bound for inputs "
+               "that are L2-resident in a real run) on tools/run_one.py; scan_kernel (shared) left out"}
+kern = {}
 for arg in sys.argv[1:]:
     run, path = arg.split("=", 1)
     k = load(path)
-    out["kernels"][run] = k
-    g = sum(v["dram_bytes_per_launch"] * v["launches"] for n, v in k.items() if n.startswith(GROUP))
-    kind = "lattice" if any(n.startswith("lat_") for n in k) else "hash"
-    out["grouping"][f"{run} ({kind})"] = g
-    for name in ("sp_core_brick_kernel", "sp_core_kernel"):
-        if name in k and name not in out:
-            out[name] = k[name]["dram_bytes_per_launch"]
+    kern[run] = k
+    out[run] = {}
+    for stage, pre in STAGES:
+        b = sum(v["dram_bytes_per_launch"] * v["launches"] for n, v in k.items() if n.startswith(pre))
+        if b:
+            out[run][stage] = b
+out["kernels"] = kern
 print(json.dumps(out, indent=1, sort_keys=True))
