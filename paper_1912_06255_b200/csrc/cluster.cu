@@ -291,6 +291,10 @@ __global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, 
         is = kh > 0 && (by_class || nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
         if (is) {
           need = !uf_same(parent, gc, h);
+          if (APX && need && apx_cells_within(cv.cell_key[gc], cv.cell_key[h], g)) {
+            uf_link(parent, gc, h);  // (rho-approximate: no point test needed)
+            need = false;
+          }
           small = need && (uint64_t)kg * kh <= SMALL_PAIR;
         }
       }

@@ -53,6 +53,8 @@ struct Geo {
   uint32_t R;           // max |delta| of lattice coordinates between neighbour cells
   uint64_t eps;         // eps
   uint32_t at;          // rho-approximate DBSCAN (row f4): sub-cell side t >= 2; 0 = exact
+  uint64_t eps2_apx;    // rho-approximate: floor((eps (1 + rho'))^2), rho' <= rho dyadic; 0 = exact
+  uint32_t apxc;        // rho-approximate: per-axis clamp (> sqrt(eps2_apx))
 };
 
 __device__ __forceinline__ uint32_t cell_coord(uint64_t key, const Geo& g, int k) {
@@ -177,6 +179,27 @@ __device__ __forceinline__ bool connect_q(const int32_t* qa, const int32_t* qb, 
     }
   }
   return acc <= g.eps2;
+}
+
+// rho-approximate cell-level cut-off (row f4; the paper's quadtree search
+// "terminates once a node's sub-cell is completely contained in the
+// eps(1+rho)-radius", at the root: the cell): two core cells
+// whose lattice boxes are entirely within eps(1+rho) of each other may be
+// connected without any point test — every pair of their points is within
+// eps(1+rho), so connecting them is allowed, and the pairs within eps are
+// connected as required. Cells differing by delta along an axis have points
+// at most (|delta| + 1) s - 1 apart along it.
+__device__ __forceinline__ bool apx_cells_within(uint64_t ka, uint64_t kb, const Geo& g) {
+  if (!g.eps2_apx) return false;
+  uint64_t acc = 0;
+  for (int k = 0; k < g.d; ++k) {
+    const uint32_t a = cell_coord(ka, g, k), b = cell_coord(kb, g, k);
+    const uint64_t dl = a > b ? a - b : b - a;
+    uint64_t m = (dl + 1) * (uint64_t)g.s - 1;
+    if (m > g.apxc) m = g.apxc;
+    acc += m * m;
+  }
+  return acc <= g.eps2_apx;
 }
 
 template <int D, bool WIDE>

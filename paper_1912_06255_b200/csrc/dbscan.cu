@@ -381,6 +381,19 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     uint64_t m = (uint64_t)mm;
     while (m > 0 && 4.0L * d * (long double)m * (long double)m > er * er) --m;
     if (m >= 1) g.at = (uint32_t)(m + 1);
+    // cell-level cut-off threshold floor((eps (1 + rho'))^2) with the dyadic
+    // rho' = floor(rho 2^40) / 2^40 <= rho, exactly in 128-bit integers:
+    // X = eps (2^40 + M), X = q 2^40 + r, X^2 / 2^80 = q^2 + (2 q r + r^2 / 2^40) / 2^40
+    const long double rr = (long double)rho * 1099511627776.0L;
+    const u128 M = (u128)floorl(rr);
+    const u128 X = (u128)eps * (((u128)1 << 40) + M);
+    const u128 q = X >> 40, r = X & (((u128)1 << 40) - 1);
+    const u128 T = q * q + ((2 * q * r + ((r * r) >> 40)) >> 40);
+    const u128 lim = ((u128)1 << 60) / (u128)d;
+    if (M > 0 && T < lim) {
+      g.eps2_apx = (uint64_t)T;
+      g.apxc = (uint32_t)std::min<u128>(isqrt_u128(T) + 1, 0xffffffffu);
+    }
   }
 
   tm.stage(DBSCAN_STAGE_BBOX);

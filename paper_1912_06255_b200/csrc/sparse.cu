@@ -576,6 +576,10 @@ __global__ void __launch_bounds__(256, 4) sp_pairs_kernel(SpArgs a, unsigned lon
         const uint32_t h = a.core_list[r];
         const uint32_t kh = a.core_cnt[h];
         if (find_first && uf_same_hop(a.parent, g, h)) continue;
+        if (APX && apx_cells_within(a.cell_key[g], a.cell_key[h], a.g)) {
+          uf_link(a.parent, g, h);  // (rho-approximate: no point test needed)
+          continue;
+        }
         if ((uint64_t)kg * kh > SP_SMALL) {
           if (uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
           const uint32_t slot = atomicAdd(a.counters + 2, 1u);

@@ -76,6 +76,14 @@ def main():
             pts = cfg.points()
             for rho in (0.0, 0.01, 0.1, 0.5, 1.0):
                 sets.append((f"{cfgname}~rho={rho}", pts, cfg.eps, cfg.min_pts))
+        # BCP-bound inputs: SS-simden 3D at eps = 4000 (large cells), uniform 3D
+        # at eps = 1000 (sparse path) and 2000 (CSR path), all core
+        ss3 = datagen.seed_spreader(a.n, 3, 1e6, 2, 1000 / a.n, noise_frac=1e-4)
+        uf = datagen.uniform(a.n, 3, 100_000, 4)
+        for rho in (0.0, 0.5, 1.0):
+            sets.append((f"ss-simden-3d~rho={rho}", ss3, 4000, 100))
+            sets.append((f"uniform-3d~rho={rho}", uf, 1000, 10))
+            sets.append((f"uniform-3d~rho={rho}", uf, 2000, 10))
     if a.only in ("", "varden"):
         for d, L, eps in ((2, 1e6, 1000), (3, 1e6, 1000), (5, 1e5, 2000), (7, 1e5, 2000)):
             vd = datagen.seed_spreader(a.n, d, L, 20 + d, 1000 / a.n, varden=True)
