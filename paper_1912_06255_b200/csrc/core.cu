@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
 // consecutive points, so the loads coalesce. The count is warp-uniform, so
 // the exit at minPts is a uniform branch.
 template <int D, bool WIDE>
-__global__ void __launch_bounds__(256, 4) mark_core_warp_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+__global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const int32_t* __restrict__ Ps,
                                                              const uint32_t* __restrict__ queue,
                                                              const uint32_t* __restrict__ qcount,
                                                              int64_t min_pts, uint32_t clampc,

@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
 // most cells join one component the second pass is pruned almost entirely
 // instead of testing and linking every pair against one contended root.
 template <int DIM, int D, bool WIDE, bool BY_CELLS, bool APX>
-__global__ void __launch_bounds__(256, 4) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
+__global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long long* tested, int col_lo,
                                                        int col_hi, bool find_first) {
   __shared__ long long s_off[SP_MAX_COLS];
   __shared__ uint32_t s_mask[SP_MAX_COLS];
