@@ -74,95 +74,17 @@ __device__ __forceinline__ uint64_t gslot_insert(GSlot* T, uint64_t mask, uint64
   return ~0ull;
 }
 
-// Per-warp double-buffered input staging: a warp walks its chunks of GR_CHUNK
-// consecutive points; lane 0 brings the NEXT chunk into shared memory with one
-// TMA bulk copy (cp.async.bulk, completing on the warp's mbarrier) while the
-// lanes process the current one, so every warp keeps GR_CHUNK*DD*4 bytes in
-// flight instead of one 32-point step (the count pass ran at ~2 TB/s on c3,
-// latency-bound). Chunks that are partial or misaligned are read directly.
-constexpr int GR_WARPS = GR_THREADS / 32;
-constexpr uint32_t GR_CHUNK = 256;  // points per warp chunk (several chunks per warp: balance)
-
-template <int DD>
-struct WarpChunks {
-  int32_t* buf;    // [2][GR_CHUNK * DD] of this warp
-  uint64_t* bar;   // [2]
-  uint32_t phase;  // bit b: parity of buffer b's next completion
-  bool tma;        // input 16-byte aligned
-
-  __device__ __forceinline__ bool full(uint32_t ch, uint32_t n) const {
-    return tma && (uint64_t)(ch + 1) * GR_CHUNK <= n;
-  }
-  // (all lanes) start loading chunk ch into buffer b
-  __device__ __forceinline__ void issue(const int32_t* pts, uint32_t ch, uint32_t n, int b) {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0 && full(ch, n)) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (the lanes' reads of b are done)
-      bulk_load(buf + b * GR_CHUNK * DD, pts + (uint64_t)ch * GR_CHUNK * DD, GR_CHUNK * DD * 4, bar + b);
-    }
-  }
-  // (all lanes) wait for buffer b if it holds a bulk copy of chunk ch
-  __device__ __forceinline__ void wait(uint32_t ch, uint32_t n, int b) {
-    if (full(ch, n)) {
-      mbar_wait(bar + b, (phase >> b) & 1u);
-      phase ^= 1u << b;
-    }
-  }
-  __device__ __forceinline__ void load(const int32_t* pts, uint32_t ch, uint32_t n, int b, uint32_t i,
-                                       int32_t* x) const {
-    if (full(ch, n)) {
-      const int32_t* src = buf + b * GR_CHUNK * DD + (i - ch * GR_CHUNK) * DD;
-#pragma unroll
-      for (int k = 0; k < DD; ++k) x[k] = src[k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < DD; ++k) x[k] = __ldg(pts + (uint64_t)i * DD + k);
-    }
-  }
-};
-
-template <int DD>
-__device__ __forceinline__ WarpChunks<DD> warp_chunks(int32_t* sm, uint64_t* bars, const int32_t* pts) {
-  WarpChunks<DD> w;
-  const int wi = threadIdx.x >> 5;
-  w.buf = sm + (size_t)wi * 2 * GR_CHUNK * DD;
-  w.bar = bars + 2 * wi;
-  w.phase = 0;
-  w.tma = (reinterpret_cast<uintptr_t>(pts) & 15) == 0;
-  if ((threadIdx.x & 31) == 0) {
-    mbar_init(w.bar, 1);
-    mbar_init(w.bar + 1, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  return w;
-}
-
-template <int DD>
-__device__ __forceinline__ uint64_t key_of(const int32_t* x, const Geo& g, uint64_t magic) {
-  uint64_t key = 0;
-#pragma unroll
-  for (int k = 0; k < DD; ++k) {
-    const uint32_t off = (uint32_t)x[k] - (uint32_t)g.lo[k];
-    const uint32_t ck = magic ? (uint32_t)__umul64hi((uint64_t)off, magic) : off;
-    key |= (uint64_t)ck << g.shift[k];
-  }
-  return key;
-}
-
 // A: count points per key. A warp walks a contiguous chunk of the input, 32
 // points per step (coalesced). Clustered data keeps one key for long runs:
 // while the whole warp holds the key of the current run, lane 0 only adds to
 // a register; the count is flushed with one atomic when the key changes.
 // Steps with several keys go through __match_any_sync, one atomic per key.
+constexpr uint32_t GR_CHUNK = 256;  // points per warp chunk (several chunks per warp: balance)
 
 template <int DD>
 __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* __restrict__ pts, uint32_t n,
                                                                  Geo g, uint64_t magic, GSlot* T,
                                                                  uint64_t mask, uint32_t* overflow) {
-  extern __shared__ __align__(16) int32_t gc_sm[];
-  __shared__ uint64_t gc_bar[2 * GR_WARPS];
-  WarpChunks<DD> W = warp_chunks<DD>(gc_sm, gc_bar, pts);
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t nchunks = (n + GR_CHUNK - 1) / GR_CHUNK;
@@ -172,28 +94,16 @@ __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* 
     if (run_cnt && run_slot != ~0ull) atomicAdd(&T[run_slot].cnt, run_cnt);
     run_cnt = 0;
   };
-  uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int b = 0;
-  if (ch < nchunks) W.issue(pts, ch, n, 0);
-  for (; ch < nchunks; ch += nwarps, b ^= 1) {
-    if (ch + nwarps < nchunks) W.issue(pts, ch + nwarps, n, b ^ 1);  // the next chunk, in flight meanwhile
-    W.wait(ch, n, b);
+  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nwarps) {
     uint32_t ov = 0;
     if (lane == 0) ov = *(volatile uint32_t*)overflow;
-    if (__shfl_sync(DB_FULL, ov, 0)) {  // warp-uniform; drain the copy in flight
-      if (ch + nwarps < nchunks) W.wait(ch + nwarps, n, b ^ 1);
-      return;
-    }
+    if (__shfl_sync(DB_FULL, ov, 0)) return;  // warp-uniform
     const uint32_t c0 = ch * GR_CHUNK, c1 = min(n, c0 + GR_CHUNK);
     for (uint32_t i0 = c0; i0 < c1; i0 += 32) {
       const uint32_t i = i0 + lane;
       const bool valid = i < c1;
       int32_t x[DD];
-      uint64_t key = ~0ull;
-      if (valid) {
-        W.load(pts, ch, n, b, i, x);
-        key = key_of<DD>(x, g, magic);
-      }
+      const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
       const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
       const uint32_t vmask = __ballot_sync(DB_FULL, valid);
       if (__all_sync(DB_FULL, !valid || key == k0)) {
@@ -280,18 +190,10 @@ __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
     const int32_t* __restrict__ pts, uint32_t n, Geo g, uint64_t magic, const GSlot* __restrict__ T,
     uint64_t mask, uint32_t* __restrict__ cursor, uint32_t* __restrict__ cellmin, int32_t* __restrict__ Ps,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ cell_of) {
-  extern __shared__ __align__(16) int32_t gs_sm[];
-  __shared__ uint64_t gs_bar[2 * GR_WARPS];
-  WarpChunks<DD> W = warp_chunks<DD>(gs_sm, gs_bar, pts);
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t nchunks = (n + GR_CHUNK - 1) / GR_CHUNK;
-  uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int b = 0;
-  if (ch < nchunks) W.issue(pts, ch, n, 0);
-  for (; ch < nchunks; ch += nwarps, b ^= 1) {
-    if (ch + nwarps < nchunks) W.issue(pts, ch + nwarps, n, b ^ 1);
-    W.wait(ch, n, b);
+  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < nchunks; ch += nwarps) {
     const uint32_t c0 = ch * GR_CHUNK, c1 = min(n, c0 + GR_CHUNK);
     uint64_t run_key = ~0ull;
     uint32_t run_id = 0xffffffffu;
@@ -299,11 +201,7 @@ __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
       const uint32_t i = i0 + lane;
       const bool valid = i < c1;
       int32_t x[DD];
-      uint64_t key = ~0ull;
-      if (valid) {
-        W.load(pts, ch, n, b, i, x);
-        key = key_of<DD>(x, g, magic);
-      }
+      const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
       const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
       const bool uniform = __all_sync(DB_FULL, !valid || key == k0);
       uint32_t id = 0xffffffffu;
@@ -383,9 +281,7 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
   const unsigned grid = grid_for(n, GR_THREADS, c.sms * 8);
   by_dim_g(g.d, [&](auto Dd, auto) {
     constexpr int DD = decltype(Dd)::value;
-    const int sm = 2 * GR_WARPS * GR_CHUNK * DD * 4;
-    DB_CUDA(cudaFuncSetAttribute(group_count_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    group_count_kernel<DD><<<grid, GR_THREADS, sm, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, ctr);
+    group_count_kernel<DD><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, ctr);
   });
   c.launched();
   uint32_t* list = c.alloc<uint32_t>(cap);
@@ -431,10 +327,8 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
   DB_CUDA(cudaMemcpyAsync(cursor, cell_start, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, c.st));
   by_dim_g(g.d, [&](auto Dd, auto Dp) {
     constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
-    const int sm = 2 * GR_WARPS * GR_CHUNK * DD * 4;
-    DB_CUDA(cudaFuncSetAttribute(group_scatter_kernel<DD, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    group_scatter_kernel<DD, D><<<grid, GR_THREADS, sm, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, cursor,
-                                                                cellmin, Ps, idx, cell_of);
+    group_scatter_kernel<DD, D><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, cursor,
+                                                               cellmin, Ps, idx, cell_of);
   });
   c.launched();
   *cellmin_out = cellmin;
