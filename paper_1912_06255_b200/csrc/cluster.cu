@@ -517,6 +517,35 @@ __global__ void __launch_bounds__(256) write_positions_kernel(uint32_t n, const 
   if (threadIdx.x == 0 && s_c) atomicAdd(counters + 1, (uint32_t)s_c);
 }
 
+// By input index (the grouping kept the inverse permutation inv): thread i
+// reads its sorted position and cell, and writes cluster[i] and core[i] —
+// coalesced stores instead of a scatter through idx (write_positions), the
+// random reads (cell_of at the sorted position) hitting L2.
+__global__ void __launch_bounds__(256) write_input_kernel(uint32_t n, const uint32_t* __restrict__ inv,
+                                                          const uint32_t* __restrict__ cell_of,
+                                                          const uint32_t* __restrict__ cell_start,
+                                                          const uint32_t* __restrict__ core_cnt,
+                                                          const uint32_t* __restrict__ cell_label,
+                                                          int32_t* __restrict__ cluster_out,
+                                                          uint8_t* __restrict__ core_out, uint32_t* counters) {
+  unsigned long long nc = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t j = inv[i];
+    const uint32_t g = cell_of[j];
+    const bool is_core = j - cell_start[g] < core_cnt[g];
+    cluster_out[i] = is_core ? (int32_t)cell_label[g] : -1;
+    core_out[i] = is_core;
+    nc += is_core;
+  }
+  __shared__ unsigned long long s_c;
+  if (threadIdx.x == 0) s_c = 0;
+  __syncthreads();
+  nc = __reduce_add_sync(DB_FULL, (uint32_t)nc);
+  if ((threadIdx.x & 31) == 0 && nc) atomicAdd(&s_c, nc);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_c) atomicAdd(counters + 1, (uint32_t)s_c);
+}
+
 // (also sets cell_label: the cell's component minimum, ~0 without core points)
 __global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const uint32_t* __restrict__ list,
                                                            const uint32_t* __restrict__ idx,
@@ -578,6 +607,15 @@ void labels(Ctx& c, const CellsView& cv, const uint32_t* idx, const uint8_t* cor
                                                                     min_mode, cellmin, parent, comp_min,
                                                                     counters);
   c.launched();
+  if (!core_list && (int64_t)nc * 32 <= n && c.inv) {
+    cell_label_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(m, core_list, core_cnt, parent, comp_min,
+                                                                    cell_label);
+    c.launched();
+    write_input_kernel<<<grid_for(n, 256, c.sms * 16), 256, 0, c.st>>>(
+        (uint32_t)n, c.inv, cv.cell_of, cv.cell_start, core_cnt, cell_label, cluster_out, core_out, counters);
+    c.launched();
+    return;  // (core[] written too)
+  }
   if (!core_list && (int64_t)nc * 32 <= n) {
     cell_label_kernel<<<grid_for(m, 256, 1 << 30), 256, 0, c.st>>>(m, core_list, core_cnt, parent, comp_min,
                                                                     cell_label);

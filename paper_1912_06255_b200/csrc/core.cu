@@ -301,7 +301,8 @@ template <int D>
 __global__ void partition_kernel(CellsView cv, const uint32_t* __restrict__ mixed,
                                  const uint32_t* __restrict__ nmixed, int32_t* __restrict__ Ps,
                                  uint32_t* __restrict__ idx, uint8_t* __restrict__ core_s,
-                                 int32_t* __restrict__ scratchP, uint32_t* __restrict__ scratchI) {
+                                 int32_t* __restrict__ scratchP, uint32_t* __restrict__ scratchI,
+                                 uint32_t* __restrict__ inv) {
   const uint32_t m = *nmixed;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
     const uint32_t g = mixed[t];
@@ -330,6 +331,7 @@ __global__ void partition_kernel(CellsView cv, const uint32_t* __restrict__ mixe
               else reinterpret_cast<int4*>(Ps)[w] = make_int4(P[q][0], P[q][1], P[q][2], P[q][3]);
               idx[w] = I[q];
               core_s[w] = (uint8_t)pass;
+              if (inv) inv[I[q]] = w;
               ++w;
             }
         continue;
@@ -347,6 +349,7 @@ __global__ void partition_kernel(CellsView cv, const uint32_t* __restrict__ mixe
         for (int k = 0; k < D; ++k) Ps[(size_t)w * D + k] = scratchP[(size_t)u * D + k];
         idx[w] = v & 0x7fffffffu;
         core_s[w] = (uint8_t)pass;
+        if (inv) inv[v & 0x7fffffffu] = w;
         ++w;
       }
   }
@@ -368,7 +371,7 @@ void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* 
   uint32_t* sI = c.alloc<uint32_t>(n);
   auto go = [&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
-    partition_kernel<D><<<c.sms * 16, 256, 0, c.st>>>(cv, mixed, nmixed, Ps, idx, core_s, sP, sI);
+    partition_kernel<D><<<c.sms * 16, 256, 0, c.st>>>(cv, mixed, nmixed, Ps, idx, core_s, sP, sI, c.inv);
   };
   if (g.D == 2) go(std::integral_constant<int, 2>());
   else if (g.D == 4) go(std::integral_constant<int, 4>());

@@ -449,10 +449,12 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
                         (n <= (1 << 19) || lohi[16] >= 16);
   if (try_hash) {
     sidx = c.alloc<uint32_t>(n);
+    c.inv = c.alloc<uint32_t>(n);  // inverse permutation (labels by input index)
     const bool sparse_ok = d <= 3 && !(flags & (DBSCAN_F_NO_SPARSE | DBSCAN_F_FORCE_STENCIL | DBSCAN_F_FORCE_TREE));
     const int sparse_mode = !sparse_ok ? 0 : ((flags & DBSCAN_F_FORCE_SPARSE) ? 2 : 1);
     hash_group = group_by_hash(c, dpts, n, g, sparse_mode, Ps, sidx, cell_of, cell_start, cell_key, &cellmin,
                                &ncells, &key_ordered);
+    if (!hash_group) c.inv = nullptr;
   }
   // many cells, d <= 3, small padded lattice: counting sort over the lattice
   // (group.cu), which also yields the sparse path's rank directory and the

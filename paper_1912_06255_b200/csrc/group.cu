@@ -189,7 +189,7 @@ template <int DD, int D>
 __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
     const int32_t* __restrict__ pts, uint32_t n, Geo g, uint64_t magic, const GSlot* __restrict__ T,
     uint64_t mask, uint32_t* __restrict__ cursor, uint32_t* __restrict__ cellmin, int32_t* __restrict__ Ps,
-    uint32_t* __restrict__ idx, uint32_t* __restrict__ cell_of) {
+    uint32_t* __restrict__ idx, uint32_t* __restrict__ cell_of, uint32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t nchunks = (n + GR_CHUNK - 1) / GR_CHUNK;
@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
       }
       idx[pos] = i;
       cell_of[pos] = id;
+      if (inv) inv[i] = pos;  // (coalesced: lanes hold consecutive i)
     }
   }
 }
@@ -328,7 +329,7 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
   by_dim_g(g.d, [&](auto Dd, auto Dp) {
     constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
     group_scatter_kernel<DD, D><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, cursor,
-                                                               cellmin, Ps, idx, cell_of);
+                                                               cellmin, Ps, idx, cell_of, c.inv);
   });
   c.launched();
   *cellmin_out = cellmin;

@@ -64,6 +64,9 @@ struct Ctx {
   int64_t launches = 0;
   int sms = 148;
   uint32_t* dense_dir = nullptr;  // dense cell directory, when built
+  // inverse permutation (input index -> sorted position) when the grouping
+  // wrote it; the kernels that move points inside cells keep it current
+  uint32_t* inv = nullptr;
   const uint64_t* nbr_total_d = nullptr;  // exact neighbour-CSR size (device), when only bounded on the host
   uint64_t dense_lat[3] = {0, 0, 0};
   // Temporaries come out of the call's workspace (one device allocation kept

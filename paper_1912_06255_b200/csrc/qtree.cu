@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(1024) qt_sort_cells_kernel(int32_t* __restrict
                                                              Geo g, int B, int32_t* __restrict__ Ps2,
                                                              uint32_t* __restrict__ idx2, uint32_t min_size,
                                                              const uint32_t* __restrict__ tidx,
-                                                             uint32_t* __restrict__ qstart) {
+                                                             uint32_t* __restrict__ qstart,
+                                                             uint32_t* __restrict__ inv) {
   __shared__ uint32_t hist[1 << QT_SUB_BITS];
   __shared__ uint32_t s_scan[33];
   const int NB = 1 << (B * g.d);
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(1024) qt_sort_cells_kernel(int32_t* __restrict
 #pragma unroll
       for (int k = 0; k < D; ++k) Ps[(size_t)j * D + k] = Ps2[(size_t)j * D + k];
       idx[j] = idx2[j];
+      if (inv) inv[idx2[j]] = j;
     }
     __syncthreads();
   }
@@ -224,7 +226,7 @@ void build_qtrees(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
   byD([&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
     qt_sort_cells_kernel<D><<<std::min<uint32_t>(nc, (uint32_t)c.sms * 8), 1024, 0, c.st>>>(
-        Ps, idx, cv.cell_start, cv.cell_key, nc, g, B, Ps2, idx2, QT_MIN, nullptr, nullptr);
+        Ps, idx, cv.cell_start, cv.cell_key, nc, g, B, Ps2, idx2, QT_MIN, nullptr, nullptr, c.inv);
   });
   c.launched();
   // 2. node offsets and leaf lists
@@ -491,7 +493,7 @@ void mark_core_bounds(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, ui
   byD([&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
     qt_sort_cells_kernel<D><<<std::min<uint32_t>(nc, (uint32_t)c.sms * 8), 1024, 0, c.st>>>(
-        Ps, idx, cv.cell_start, cv.cell_key, nc, g, B, Ps2, idx2, QB_MIN, tidx, qstart);
+        Ps, idx, cv.cell_start, cv.cell_key, nc, g, B, Ps2, idx2, QB_MIN, tidx, qstart, c.inv);
     c.launched();
     qb_bound_kernel<D><<<c.sms * 16, 256, 0, c.st>>>(A);
     c.launched();

@@ -1,0 +1,3 @@
+timeout 900 python -u -m pytest tests -x -q -m "gpu and not slow" --timeout 300 -p no:cacheprovider > gpurun_out/g13_tests.log 2>&1
+tail -2 gpurun_out/g13_tests.log
+python bench.py --no-cpu --no-e2e --detail > gpurun_out/g13_bench.json 2> gpurun_out/g13_bench.err
