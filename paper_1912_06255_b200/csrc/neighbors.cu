@@ -339,23 +339,26 @@ __global__ void iota_kernel(uint32_t* __restrict__ v, uint32_t n) {
   if (i < n) v[i] = i;
 }
 
-// bucket of a cell: (axis-0, axis-1) coordinates, c0 * B1 + c1 (B1 = 1: axis 0 only)
-__device__ __forceinline__ uint32_t cell_bucket(const uint32_t* __restrict__ cc, uint32_t i, uint32_t B1) {
-  return B1 > 1 ? cc[8 * (size_t)i] * B1 + cc[8 * (size_t)i + 1] : cc[8 * (size_t)i];
+// bucket of a cell: (axis-0, axis-1[, axis-2]) coordinates, (c0 * B1 + c1) * B2 + c2
+// (B1 = 1: axis 0 only; B2 = 1: two axes)
+__device__ __forceinline__ uint32_t cell_bucket(const uint32_t* __restrict__ cc, uint32_t i, uint32_t B1,
+                                                uint32_t B2) {
+  const uint32_t* c = cc + 8 * (size_t)i;
+  return B1 > 1 ? (c[0] * B1 + c[1]) * B2 + (B2 > 1 ? c[2] : 0u) : c[0];
 }
 
-__global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1,
+__global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1, uint32_t B2,
                                     uint32_t* __restrict__ bcnt) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < ncells) atomicAdd(bcnt + cell_bucket(cc, i, B1), 1u);
+  if (i < ncells) atomicAdd(bcnt + cell_bucket(cc, i, B1, B2), 1u);
 }
 
-__global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1,
+__global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1, uint32_t B2,
                                    const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcur,
                                    uint32_t* __restrict__ order) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ncells) return;
-  const uint32_t b = cell_bucket(cc, i, B1);
+  const uint32_t b = cell_bucket(cc, i, B1, B2);
   order[bstart[b] + atomicAdd(bcur + b, 1u)] = i;
 }
 
@@ -363,7 +366,7 @@ template <int DD>
 __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t* __restrict__ cc,
                                                         const uint32_t* __restrict__ order,
                                                         const uint32_t* __restrict__ bstart, uint32_t maxb,
-                                                        uint32_t B1, uint32_t ncells, Geo g,
+                                                        uint32_t B1, uint32_t B2, uint32_t ncells, Geo g,
                                                         const uint64_t* __restrict__ gtab_g, int gmax,
                                                         const uint32_t* __restrict__ cell_start,
                                                         uint32_t* __restrict__ ccount /*[3][ncells]*/,
@@ -394,12 +397,19 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     const uint32_t c0 = maxb ? cq[0] : 0u;  // maxb = 0: a single bucket
     const uint32_t blo = c0 > g.R ? c0 - g.R : 0u, bhi = min(maxb, c0 + g.R);
     // B1 > 1: buckets by (axis 0, axis 1); for each axis-0 bucket the axis-1
-    // window c1 - R .. c1 + R is one contiguous run of `order`
+    // window c1 - R .. c1 + R is one contiguous run of `order`. B2 > 1:
+    // buckets by (axis 0, axis 1, axis 2); a run per (axis-0, axis-1) bucket
+    // over the axis-2 window.
     const uint32_t y0 = B1 > 1 ? (cq[1] > g.R ? cq[1] - g.R : 0u) : 0u;
     const uint32_t y1 = B1 > 1 ? min(B1 - 1, cq[1] + g.R) : 0u;
+    const uint32_t z0 = B2 > 1 ? (cq[2] > g.R ? cq[2] - g.R : 0u) : 0u;
+    const uint32_t z1 = B2 > 1 ? min(B2 - 1, cq[2] + g.R) : 0u;
     for (uint32_t b0 = blo; b0 <= bhi; ++b0) {
-    const uint32_t t1 = bstart[b0 * B1 + y1 + 1];
-    for (uint32_t t0 = bstart[b0 * B1 + y0]; t0 < t1; t0 += 32) {
+    for (uint32_t b1 = y0; b1 <= (B2 > 1 ? y1 : y0); ++b1) {
+    const uint32_t r0 = B2 > 1 ? (b0 * B1 + b1) * B2 + z0 : b0 * B1 + y0;
+    const uint32_t r1 = B2 > 1 ? (b0 * B1 + b1) * B2 + z1 : b0 * B1 + y1;
+    const uint32_t t1 = bstart[r1 + 1];
+    for (uint32_t t0 = bstart[r0]; t0 < t1; t0 += 32) {
       const uint32_t t = t0 + lane;
       const uint32_t h = t < t1 ? order[t] : 0u;
       int cls = -1;
@@ -429,6 +439,7 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
         n3[c] += __popc(b);
       }
       if (!fill && cls >= 0) sum += cell_start[h + 1] - cell_start[h];
+    }
     }
     }
     if (!fill) {
@@ -469,17 +480,24 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
                               ((uint64_t)g.maxc[0] + 1) * ((uint64_t)g.maxc[1] + 1) < 4ull * ncells + 1024
                           ? g.maxc[1] + 1
                           : 1u;
-  const uint64_t nbk = ((uint64_t)maxb + 1) * B1;  // buckets 0 .. nbk - 1
+  // a third bucketed axis when the lattice is crowded (many cells, clustered:
+  // SS-varden 7D has 72K cells and ~1,150 neighbours per cell) and the 3D
+  // bucket grid stays within 32 buckets per cell
+  const uint64_t v3 = ((uint64_t)g.maxc[0] + 1) * ((uint64_t)g.maxc[1] + 1) * ((uint64_t)g.maxc[2] + 1);
+  const uint32_t B2 = B1 > 1 && g.d >= 3 && ncells >= 16384 && v3 <= 32ull * ncells + (1u << 20)
+                          ? g.maxc[2] + 1
+                          : 1u;
+  const uint64_t nbk = ((uint64_t)maxb + 1) * B1 * B2;  // buckets 0 .. nbk - 1
   uint32_t* bcnt = c.alloc<uint32_t>((size_t)nbk + 1);
   uint32_t* bstart = c.alloc<uint32_t>((size_t)nbk + 1);
   uint32_t* order = c.alloc<uint32_t>(ncells);
   c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
   if (maxb) {
-    bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, bcnt);
+    bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bcnt);
     c.launched();
     exclusive_scan_u32_u32(c, bcnt, bstart, (int64_t)nbk);
     c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
-    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, bstart, bcnt, order);
+    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bstart, bcnt, order);
     c.launched();
   } else {
     // one bucket: every cell (cc[0] is then clamped by maxb = 0 -> buckets 0..0)
@@ -495,10 +513,10 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
   auto launch = [&](int fill, uint32_t* list) {
     if (g.d <= 4)
-      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, ncells, g, (const uint64_t*)dgt,
+      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, B2, ncells, g, (const uint64_t*)dgt,
                                                   gmax, cell_start, ccount, cnt, ub, off, list);
     else
-      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, ncells, g, (const uint64_t*)dgt,
+      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, B2, ncells, g, (const uint64_t*)dgt,
                                                   gmax, cell_start, ccount, cnt, ub, off, list);
     c.launched();
   };

@@ -548,3 +548,15 @@ def test_subcell_bounds_large_minpts_vs_o2(oracle_lib, d):
         assert_same(np_result(r), want, f"bounds d={d} mp={mp}")
         assert_same(np_result(gpu(pts, eps, mp, pkg.F_NO_QBOUND)), want, f"no bounds d={d} mp={mp}")
     assert r.stats["qb_decided"] > 0 or d == 5
+
+
+def test_high_d_three_axis_buckets_vs_o2(oracle_lib):
+    """d >= 4 with tens of thousands of clustered cells (SS-varden 7D in a
+    small domain: 52K cells): the all-pairs neighbour search buckets the cells
+    by three lattice axes, a run per (axis-0, axis-1) bucket over the axis-2
+    window; against O2 (all-pairs cell scan, independent code)."""
+    pts = datagen.seed_spreader(300_000, 7, 2e4, 27, 0.02, varden=True)
+    for mp in (20, 300):
+        r = gpu(pts, 600, mp)
+        assert r.stats["tree"] == 1 and 16384 <= r.stats["ncells"] <= 131_072, r.stats
+        assert_same(np_result(r), oracle_lib.o2(pts, 600, mp), f"3-axis buckets mp={mp}")
