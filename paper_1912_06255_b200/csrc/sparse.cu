@@ -568,13 +568,10 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
       const uint32_t ci = it / nb, col = it - ci * nb;
       const uint32_t g = BY_CELLS ? r0 + (uint32_t)__fns(cm, 0, ci + 1) : a.core_list[r0 + ci];
       const uint64_t base = cell_lin<DIM>(a.cell_key[g], a);
-      // g's cell range and first core point, loaded beside the probe
-      const uint32_t kg = a.core_cnt[g], sg = a.cell_start[g];
-      int32_t p0[D];
-      load_pt<D>(a.Ps, sg, p0);
       uint32_t id0;
       const uint32_t nc = dir_probe(a.cdir, base + (uint64_t)s_off[col], s_mask[col], &id0);
       if (!nc) continue;
+      const uint32_t kg = a.core_cnt[g], sg = a.cell_start[g];
       for (uint32_t r = id0; r < id0 + nc; ++r) {
         const uint32_t h = a.core_list[r];
         const uint32_t kh = a.core_cnt[h];
@@ -594,12 +591,7 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
         bool hit = false;
         for (uint32_t u = sg; u < sg + kg && !hit; ++u) {
           int32_t p[D];
-          if (u == sg) {
-#pragma unroll
-            for (int k = 0; k < D; ++k) p[k] = p0[k];
-          } else {
-            load_pt<D>(a.Ps, u, p);
-          }
+          load_pt<D>(a.Ps, u, p);
           for (uint32_t v = sh; v < sh + kh; ++v) {
             int32_t q[D];
             load_pt<D>(a.Ps, v, q);
@@ -744,10 +736,6 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
     const uint64_t base = cell_lin<DIM>(a.cell_key[h], a);
     const uint32_t sh = a.cell_start[h], kh = a.core_cnt[h];
     const uint32_t lab = a.cell_label[h];
-    // the cell's first core point, loaded with the probes (the candidate
-    // loop then tests against registers; most core cells have one)
-    int32_t q0[D];
-    load_pt<D>(a.Ps, sh, q0);
     uint32_t lo = 0, len = 0;
     if (lane < a.ncols) {
       uint32_t id0;
@@ -775,15 +763,11 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
         if (e <= t) k += step;
       }
       const uint32_t u = __shfl_sync(DB_FULL, lo, k) + t - __shfl_sync(DB_FULL, excl, k);
-      if (t >= total) continue;
-      // the candidate's point and core flag are loaded together (92% of the
-      // candidates on c5 are non-core and need the point anyway)
+      if (t >= total || a.core_s[u]) continue;
       int32_t p[D];
       load_pt<D>(a.Ps, u, p);
-      if (a.core_s[u]) continue;
-      DB_WORK(2);
-      bool hit = within_dim<DIM, D, WIDE>(p, q0, a.g);
-      for (uint32_t v = sh + 1; v < sh + kh && !hit; ++v) {
+      bool hit = false;
+      for (uint32_t v = sh; v < sh + kh && !hit; ++v) {
         int32_t q[D];
         load_pt<D>(a.Ps, v, q);
         DB_WORK(2);
