@@ -412,13 +412,6 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   }
   int32_t* lohi_d = c.alloc<int32_t>(17);
   bbox(c, dpts, n, d, g.s, lohi_d);
-  // the hash grouping's count pass goes right behind the bounding box, with
-  // the key layout computed on the device (group.cu group_hash_launch), so
-  // that one synchronisation reads both (it does nothing when the sample
-  // rules the hash table out)
-  HashPre hpre;
-  const bool spec_hash = !(flags & (DBSCAN_F_RADIX_GROUP | DBSCAN_F_LATTICE_GROUP));
-  if (spec_hash) group_hash_launch(c, dpts, n, g, lohi_d, &hpre);
   int32_t lohi[17];
   const int32_t* lohi_h = c.fetch(lohi_d, 17);
   c.sync();
@@ -452,15 +445,15 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   bool key_ordered = true;  // cell ids follow key order (the radix path always)
   // the hash table (<= 2^20 slots) always fits n <= 2^19 cells; beyond that
   // try it only if the sample saw repeated cells
-  // (the same rule as geo_kernel's go-ahead)
-  const bool try_hash = spec_hash && (n <= (1 << 19) || lohi[16] >= 16);
+  const bool try_hash = !(flags & (DBSCAN_F_RADIX_GROUP | DBSCAN_F_LATTICE_GROUP)) &&
+                        (n <= (1 << 19) || lohi[16] >= 16);
   if (try_hash) {
     sidx = c.alloc<uint32_t>(n);
     c.inv = c.alloc<uint32_t>(n);  // inverse permutation (labels by input index)
     const bool sparse_ok = d <= 3 && !(flags & (DBSCAN_F_NO_SPARSE | DBSCAN_F_FORCE_STENCIL | DBSCAN_F_FORCE_TREE));
     const int sparse_mode = !sparse_ok ? 0 : ((flags & DBSCAN_F_FORCE_SPARSE) ? 2 : 1);
     hash_group = group_by_hash(c, dpts, n, g, sparse_mode, Ps, sidx, cell_of, cell_start, cell_key, &cellmin,
-                               &ncells, &key_ordered, &hpre);
+                               &ncells, &key_ordered);
     if (!hash_group) c.inv = nullptr;
   }
   // many cells, d <= 3, small padded lattice: counting sort over the lattice

@@ -56,8 +56,7 @@ __device__ __forceinline__ uint64_t point_key(const int32_t* __restrict__ pts, u
   return key;
 }
 
-__global__ void group_init_kernel(GSlot* T, uint64_t cap, const uint32_t* __restrict__ go) {
-  if (!*go) return;  // (speculative launch that the sample ruled out)
+__global__ void group_init_kernel(GSlot* T, uint64_t cap) {
   const uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (h < cap) reinterpret_cast<uint4*>(T)[h] = make_uint4(0xffffffffu, 0xffffffffu, 0u, 0u);
 }
@@ -82,16 +81,10 @@ __device__ __forceinline__ uint64_t gslot_insert(GSlot* T, uint64_t mask, uint64
 // Steps with several keys go through __match_any_sync, one atomic per key.
 constexpr uint32_t GR_CHUNK = 256;  // points per warp chunk (several chunks per warp: balance)
 
-// (gd, go: the key layout and the go-ahead come from device memory — the pass
-// is launched right after the bounding box, before the host has read it;
-// go = 0: the sample saw few repeated cells or the key is too wide: no work)
 template <int DD>
 __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                                 const Geo* __restrict__ gd,
-                                                                 const uint32_t* __restrict__ go, uint64_t magic,
-                                                                 GSlot* T, uint64_t mask, uint32_t* overflow) {
-  if (!*go) return;
-  const Geo g = *gd;
+                                                                 Geo g, uint64_t magic, GSlot* T,
+                                                                 uint64_t mask, uint32_t* overflow) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t nchunks = (n + GR_CHUNK - 1) / GR_CHUNK;
@@ -137,9 +130,7 @@ __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* 
 // B1: compact the non-empty slots (slot index list; one atomic per block).
 __global__ void __launch_bounds__(GR_THREADS) group_compact_kernel(const GSlot* __restrict__ T, uint64_t cap,
                                                                    uint32_t* __restrict__ list,
-                                                                   uint32_t* __restrict__ nlist,
-                                                                   const uint32_t* __restrict__ go) {
-  if (!*go) return;
+                                                                   uint32_t* __restrict__ nlist) {
   __shared__ uint32_t s_base;
   __shared__ uint32_t s_scan[33];
   const uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -277,65 +268,32 @@ static void by_dim_g(int d, F&& f) {
   }
 }
 
-// Key layout on the device from the bounding box (the host repeats the same
-// arithmetic after its read, dbscan.cu): lo, maxc, width, shift, bits; and the
-// go-ahead of the speculative hash count: key within 63 bits and (n <= 2^19
-// or >= 16 repeated cells in the sample, the host's rule).
-__global__ void geo_kernel(const int32_t* __restrict__ lohi, int64_t n, Geo* gd, uint32_t* go) {
-  Geo g = *gd;
-  uint32_t bits = 0;
-  for (int k = g.d - 1; k >= 0; --k) {
-    const uint64_t span = (uint64_t)((int64_t)lohi[8 + k] - (int64_t)lohi[k]);
-    const uint64_t maxc = span / g.s;
-    g.lo[k] = lohi[k];
-    g.maxc[k] = (uint32_t)maxc;
-    g.width[k] = maxc ? 64u - (uint32_t)__clzll((long long)maxc) : 0u;
-    g.shift[k] = bits;
-    bits += g.width[k];
-  }
-  g.bits = bits;
-  *gd = g;
-  *go = bits <= 63 && (n <= (1 << 19) || lohi[16] >= 16) ? 1u : 0u;
-}
-
-void group_hash_launch(Ctx& c, const int32_t* pts, int64_t n, const Geo& g0, const int32_t* lohi_d, HashPre* h) {
-  h->cap = 1024;
-  while (h->cap < 2ull * (uint64_t)n && h->cap < (1ull << 20)) h->cap <<= 1;
-  const uint64_t magic = g0.s > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + g0.s - 1) / g0.s) : 0;
-  Geo* gd = c.alloc<Geo>(1);
-  uint32_t* go = c.alloc<uint32_t>(1);
-  c.upload(gd, &g0, 1);
-  geo_kernel<<<1, 1, 0, c.st>>>(lohi_d, n, gd, go);
-  c.launched();
-  h->T = c.alloc<GSlot>(h->cap);
-  h->ctr = c.alloc<uint32_t>(2);  // [0] overflow, [1] distinct keys
-  group_init_kernel<<<(unsigned)((h->cap + 255) / 256), 256, 0, c.st>>>(h->T, h->cap, go);
-  c.launched();
-  c.zero(h->ctr, 2 * sizeof(uint32_t));
-  const unsigned grid = grid_for(n, GR_THREADS, c.sms * 8);
-  by_dim_g(g0.d, [&](auto Dd, auto) {
-    constexpr int DD = decltype(Dd)::value;
-    group_count_kernel<DD><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, gd, go, magic, h->T, h->cap - 1, h->ctr);
-  });
-  c.launched();
-  h->list = c.alloc<uint32_t>(h->cap);
-  group_compact_kernel<<<(unsigned)((h->cap + GR_THREADS - 1) / GR_THREADS), GR_THREADS, 0, c.st>>>(
-      h->T, h->cap, h->list, h->ctr + 1, go);
-  c.launched();
-  h->ctr_h = c.fetch(h->ctr, 2);  // (read with the bounding box)
-  h->launched = true;
-}
-
 bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int sparse_mode, int32_t* Ps,
                    uint32_t* idx, uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key,
-                   uint32_t** cellmin_out, uint32_t* ncells_out, bool* ordered, const HashPre* pre) {
-  // (the count pass ran speculatively after the bounding box: group_hash_launch)
-  const uint64_t cap = pre->cap;
+                   uint32_t** cellmin_out, uint32_t* ncells_out, bool* ordered) {
+  uint64_t cap = 1024;
+  while (cap < 2ull * (uint64_t)n && cap < (1ull << 20)) cap <<= 1;
   const uint64_t magic = g.s > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + g.s - 1) / g.s) : 0;
-  GSlot* T = pre->T;
-  uint32_t* list = pre->list;
-  uint32_t h2[2] = {pre->ctr_h[0], pre->ctr_h[1]};
+  GSlot* T = c.alloc<GSlot>(cap);
+  uint32_t* ctr = c.alloc<uint32_t>(2);  // [0] overflow, [1] distinct keys
+  group_init_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, c.st>>>(T, cap);
+  c.launched();
+  c.zero(ctr, 2 * sizeof(uint32_t));
   const unsigned grid = grid_for(n, GR_THREADS, c.sms * 8);
+  by_dim_g(g.d, [&](auto Dd, auto) {
+    constexpr int DD = decltype(Dd)::value;
+    group_count_kernel<DD><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, ctr);
+  });
+  c.launched();
+  uint32_t* list = c.alloc<uint32_t>(cap);
+  group_compact_kernel<<<(unsigned)((cap + GR_THREADS - 1) / GR_THREADS), GR_THREADS, 0, c.st>>>(T, cap, list,
+                                                                                               ctr + 1);
+  c.launched();
+  uint32_t h2[2];
+  const uint32_t* h2_h = c.fetch(ctr, 2);
+  c.sync();
+  h2[0] = h2_h[0];
+  h2[1] = h2_h[1];
   if (h2[0]) return false;  // too many cells for the table: radix path
   const uint32_t m = h2[1];
   // Cell ids in key order are needed by the sparse path's rank directory

@@ -228,23 +228,9 @@ uint32_t segment_and_gather(Ctx& c, const void* sorted_keys, bool key64, const u
 // written) when the keys do not fit its table, and the caller sorts instead.
 // sparse_mode (whether the sparse path, which needs cell ids in key order,
 // may run): 0 no, 1 if the lattice turns out sparse, 2 forced.
-// The count pass of the hash grouping is launched speculatively right after
-// the bounding box (group_hash_launch: the key layout computed on the device;
-// the pass does nothing when the sample or the key width rule it out), and
-// its counters are read with the bounding box; group_by_hash completes it.
-struct HashPre {
-  struct GSlot* T = nullptr;
-  uint64_t cap = 0;
-  uint32_t* ctr = nullptr;
-  uint32_t* list = nullptr;
-  const uint32_t* ctr_h = nullptr;  // host copy of ctr (valid after the caller's sync)
-  bool launched = false;
-};
-void group_hash_launch(Ctx& c, const int32_t* pts, int64_t n, const Geo& g_base, const int32_t* lohi_d, HashPre* h);
 bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int sparse_mode, int32_t* Ps,
                    uint32_t* idx, uint32_t* cell_of, uint32_t* cell_start, uint64_t* cell_key,
-                   uint32_t** cellmin, uint32_t* ncells, bool* ordered /* ids in key order */,
-                   const HashPre* pre);
+                   uint32_t** cellmin, uint32_t* ncells, bool* ordered /* ids in key order */);
 // lattice counting sort for d <= 3 when the padded lattice has at most
 // LAT_PER_POINT cells per point (group.cu): writes Ps, idx, cell_of,
 // cell_start, cell_key (cell ids in key order) and the sparse path's rank
