@@ -353,18 +353,27 @@ __global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t nc
   if (i < ncells) atomicAdd(bcnt + cell_bucket(cc, i, B1, B2), 1u);
 }
 
+// (ccs: the cells' decoded coordinates in bucket order, so that a query
+// streams its candidates' coordinates without the order[] indirection)
 __global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1, uint32_t B2,
                                    const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcur,
-                                   uint32_t* __restrict__ order) {
+                                   uint32_t* __restrict__ order, uint32_t* __restrict__ ccs,
+                                   const uint32_t* __restrict__ cell_start, uint32_t* __restrict__ bsize) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ncells) return;
   const uint32_t b = cell_bucket(cc, i, B1, B2);
-  order[bstart[b] + atomicAdd(bcur + b, 1u)] = i;
+  const uint32_t t = bstart[b] + atomicAdd(bcur + b, 1u);
+  order[t] = i;
+  bsize[t] = cell_start[i + 1] - cell_start[i];
+  reinterpret_cast<uint4*>(ccs)[2 * t] = reinterpret_cast<const uint4*>(cc)[2 * i];
+  reinterpret_cast<uint4*>(ccs)[2 * t + 1] = reinterpret_cast<const uint4*>(cc)[2 * i + 1];
 }
 
 template <int DD>
 __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t* __restrict__ cc,
+                                                        const uint32_t* __restrict__ ccs,
                                                         const uint32_t* __restrict__ order,
+                                                        const uint32_t* __restrict__ bsize,
                                                         const uint32_t* __restrict__ bstart, uint32_t maxb,
                                                         uint32_t B1, uint32_t B2, uint32_t ncells, Geo g,
                                                         const uint64_t* __restrict__ gtab_g, int gmax,
@@ -373,6 +382,10 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
                                                         uint32_t* __restrict__ cnt, uint32_t* __restrict__ ub,
                                                         const uint64_t* __restrict__ off,
                                                         uint32_t* __restrict__ nbr) {
+  // fill: 0 = count (cnt, ccount, ub), 1 = write class-sorted rows at off,
+  // 2 = one pass: write (neighbour | class << 30) in candidate order into a
+  // row of its candidate capacity at off AND the counts (nbr_compact_kernel
+  // then class-sorts the rows into the final CSR)
   __shared__ unsigned long long gt[GT_MAX + 1];
   for (int i = threadIdx.x; i <= gmax; i += blockDim.x) gt[i] = gtab_g[i];
   __syncthreads();
@@ -387,7 +400,9 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
       cq[0] = a.x; cq[1] = a.y; cq[2] = a.z; cq[3] = a.w; cq[4] = b.x; cq[5] = b.y; cq[6] = b.z; cq[7] = b.w;
     }
     uint64_t pos[3] = {0, 0, 0};
-    if (fill) {
+    if (fill == 2) {
+      pos[0] = off[q];
+    } else if (fill) {
       pos[0] = off[q];
       pos[1] = pos[0] + ccount[q];
       pos[2] = pos[1] + ccount[ncells + q];
@@ -411,14 +426,14 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     const uint32_t t1 = bstart[r1 + 1];
     for (uint32_t t0 = bstart[r0]; t0 < t1; t0 += 32) {
       const uint32_t t = t0 + lane;
-      const uint32_t h = t < t1 ? order[t] : 0u;
       int cls = -1;
-      if (t < t1 && h != q) {
+      if (t < t1) {
+        const uint4* CS = reinterpret_cast<const uint4*>(ccs);
         uint32_t ch[8];
-        const uint4 a = C[2 * h];
+        const uint4 a = CS[2 * t];
         ch[0] = a.x; ch[1] = a.y; ch[2] = a.z; ch[3] = a.w;
         if (DD > 4) {
-          const uint4 b = C[2 * h + 1];
+          const uint4 b = CS[2 * t + 1];
           ch[4] = b.x; ch[5] = b.y; ch[6] = b.z; ch[7] = b.w;
         }
         uint64_t acc = 0;
@@ -429,20 +444,26 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
           acc += gt[dl];
           l1 += dl;
         }
-        if (acc <= g.eps2) cls = l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);
+        if (acc <= g.eps2 && l1 > 0) cls = l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);  // (l1 = 0: the query itself)
+      }
+      const uint32_t h = cls >= 0 ? order[t] : 0u;
+      if (fill == 2) {
+        const uint32_t b = __ballot_sync(DB_FULL, cls >= 0);
+        if (cls >= 0) nbr[pos[0] + __popc(b & lt)] = h | ((uint32_t)cls << 30);
+        pos[0] += __popc(b);
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const uint32_t b = __ballot_sync(DB_FULL, cls == c);
-        if (fill && cls == c) nbr[pos[c] + __popc(b & lt)] = h;
-        pos[c] += __popc(b);
+        if (fill == 1 && cls == c) nbr[pos[c] + __popc(b & lt)] = h;
+        if (fill == 1) pos[c] += __popc(b);
         n3[c] += __popc(b);
       }
-      if (!fill && cls >= 0) sum += cell_start[h + 1] - cell_start[h];
+      if (fill != 1 && cls >= 0) sum += bsize[t];
     }
     }
     }
-    if (!fill) {
+    if (fill != 1) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(DB_FULL, sum, o);
       if (lane == 0) {
@@ -454,6 +475,66 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     }
   }
 }
+
+__global__ void cell_size_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
+                                 uint32_t* __restrict__ bsize) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ncells) bsize[i] = cell_start[i + 1] - cell_start[i];
+}
+
+// candidate capacity of each cell's row: the length of its bucket runs (what
+// nbr_brute_kernel scans), no distance tests
+__global__ void nbr_cap_kernel(const uint32_t* __restrict__ cc, const uint32_t* __restrict__ bstart, uint32_t maxb,
+                               uint32_t B1, uint32_t B2, uint32_t ncells, uint32_t R, uint32_t* __restrict__ cap) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ncells) return;
+  const uint32_t c0 = maxb ? cc[8 * q] : 0u, c1 = cc[8 * q + 1], c2 = cc[8 * q + 2];
+  const uint32_t blo = c0 > R ? c0 - R : 0u, bhi = min(maxb, c0 + R);
+  const uint32_t y0 = B1 > 1 ? (c1 > R ? c1 - R : 0u) : 0u, y1 = B1 > 1 ? min(B1 - 1, c1 + R) : 0u;
+  const uint32_t z0 = B2 > 1 ? (c2 > R ? c2 - R : 0u) : 0u, z1 = B2 > 1 ? min(B2 - 1, c2 + R) : 0u;
+  uint32_t sum = 0;
+  for (uint32_t b0 = blo; b0 <= bhi; ++b0)
+    for (uint32_t b1 = y0; b1 <= (B2 > 1 ? y1 : y0); ++b1) {
+      const uint32_t r0 = B2 > 1 ? (b0 * B1 + b1) * B2 + z0 : b0 * B1 + y0;
+      const uint32_t r1 = B2 > 1 ? (b0 * B1 + b1) * B2 + z1 : b0 * B1 + y1;
+      sum += bstart[r1 + 1] - bstart[r0];
+    }
+  cap[q] = sum;
+}
+
+// one warp per cell: the tagged row (candidate order) -> the final row,
+// class-sorted, order kept inside a class (the rows fill == 1 writes)
+__global__ void __launch_bounds__(256) nbr_compact_kernel(const uint32_t* __restrict__ tagged,
+                                                          const uint64_t* __restrict__ toff,
+                                                          const uint32_t* __restrict__ cnt,
+                                                          const uint32_t* __restrict__ ccount,
+                                                          const uint64_t* __restrict__ off, uint32_t ncells,
+                                                          uint32_t* __restrict__ nbr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncells; q += nwarps) {
+    const uint32_t* src = tagged + toff[q];
+    const uint32_t len = cnt[q];
+    uint64_t pos[3];
+    pos[0] = off[q];
+    pos[1] = pos[0] + ccount[q];
+    pos[2] = pos[1] + ccount[ncells + q];
+    for (uint32_t t0 = 0; t0 < len; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      const uint32_t v = t < len ? src[t] : 0xffffffffu;
+      const uint32_t cls = v >> 30;
+#pragma unroll
+      for (uint32_t k = 0; k < 3; ++k) {
+        const uint32_t b = __ballot_sync(DB_FULL, cls == k);
+        if (cls == k) nbr[pos[k] + __popc(b & lt)] = v & 0x3fffffffu;
+        pos[k] += __popc(b);
+      }
+    }
+  }
+}
+
+constexpr uint64_t NBR_ONEPASS_MAX = 1ull << 29;  // tagged-row entries (2 GB)
 
 static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, const uint32_t* cell_start,
                             uint32_t ncells, uint64_t** nbr_off, uint32_t** nbr, uint32_t** ub_out,
@@ -491,13 +572,17 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   uint32_t* bcnt = c.alloc<uint32_t>((size_t)nbk + 1);
   uint32_t* bstart = c.alloc<uint32_t>((size_t)nbk + 1);
   uint32_t* order = c.alloc<uint32_t>(ncells);
+  uint32_t* ccs = cc;  // (one bucket: the cells in their own order)
+  uint32_t* bsize = c.alloc<uint32_t>(ncells);  // points per cell, bucket order
   c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
   if (maxb) {
     bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bcnt);
     c.launched();
     exclusive_scan_u32_u32(c, bcnt, bstart, (int64_t)nbk);
     c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
-    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bstart, bcnt, order);
+    ccs = c.alloc<uint32_t>((size_t)ncells * 8);
+    bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bstart, bcnt, order,
+                                                                         ccs, cell_start, bsize);
     c.launched();
   } else {
     // one bucket: every cell (cc[0] is then clamped by maxb = 0 -> buckets 0..0)
@@ -505,28 +590,56 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
     c.upload(bstart, h2, 2);
     iota_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(order, ncells);
     c.launched();
+    cell_size_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_start, ncells, bsize);
+    c.launched();
   }
   uint32_t* ccount = c.alloc<uint32_t>(2 * (size_t)ncells);
   uint32_t* cnt = c.alloc<uint32_t>(ncells);
   uint32_t* ub = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
   const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
-  auto launch = [&](int fill, uint32_t* list) {
+  auto launch = [&](int fill, uint32_t* list, const uint64_t* lo) {
     if (g.d <= 4)
-      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, B2, ncells, g, (const uint64_t*)dgt,
-                                                  gmax, cell_start, ccount, cnt, ub, off, list);
+      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, ccs, order, bsize, bstart, maxb, B1, B2, ncells, g,
+                                                  (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list);
     else
-      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, order, bstart, maxb, B1, B2, ncells, g, (const uint64_t*)dgt,
-                                                  gmax, cell_start, ccount, cnt, ub, off, list);
+      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, ccs, order, bsize, bstart, maxb, B1, B2, ncells, g,
+                                                  (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list);
     c.launched();
   };
-  launch(0, nullptr);
-  exclusive_scan_u32_u64(c, cnt, off, ncells);
-  *total = nbr_total_bound(c, off + ncells, (uint64_t)ncells * (uint64_t)ncells);
-  uint32_t* list = c.alloc<uint32_t>(*total + 1);
-  launch(1, list);
+  // one test pass when the candidate rows fit: rows of candidate capacity
+  // (bucket runs) take the tagged neighbours and the counts; a compaction
+  // pass class-sorts them into the CSR (two passes of tests otherwise: count,
+  // then fill at the scanned offsets)
+  bool onepass = false;
+  if (maxb && ncells < (1u << 30)) {
+    uint32_t* cap = c.alloc<uint32_t>(ncells);
+    uint64_t* toff = c.alloc<uint64_t>((size_t)ncells + 1);
+    nbr_cap_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, bstart, maxb, B1, B2, ncells, g.R, cap);
+    c.launched();
+    exclusive_scan_u32_u64(c, cap, toff, ncells);
+    const uint64_t tcap = c.read(toff + ncells);
+    if (tcap <= NBR_ONEPASS_MAX) {
+      uint32_t* tagged = c.alloc<uint32_t>(tcap + 1);
+      launch(2, tagged, toff);
+      exclusive_scan_u32_u64(c, cnt, off, ncells);
+      *total = nbr_total_bound(c, off + ncells, tcap);
+      uint32_t* list = c.alloc<uint32_t>(*total + 1);
+      nbr_compact_kernel<<<grid, 256, 0, c.st>>>(tagged, toff, cnt, ccount, off, ncells, list);
+      c.launched();
+      *nbr = list;
+      onepass = true;
+    }
+  }
+  if (!onepass) {
+    launch(0, nullptr, off);
+    exclusive_scan_u32_u64(c, cnt, off, ncells);
+    *total = nbr_total_bound(c, off + ncells, (uint64_t)ncells * (uint64_t)ncells);
+    uint32_t* list = c.alloc<uint32_t>(*total + 1);
+    launch(1, list, off);
+    *nbr = list;
+  }
   *nbr_off = off;
-  *nbr = list;
   *ub_out = ub;
   *ccls = ccount;  // rows are class-sorted: waves read only their class's segment
   return true;
