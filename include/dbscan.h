@@ -65,6 +65,9 @@ extern "C" {
                                       per-cell tree instead of scanning (CSR path)           */
 #define DBSCAN_F_NO_QBOUND  16384u /* never run the sub-cell lower bounds before MarkCore (row f2)  */
 #define DBSCAN_F_FORCE_QBOUND 32768u /* run them whatever minPts (testing; CSR path)              */
+#define DBSCAN_F_NBR_TWO_PASS 65536u /* all-pairs neighbour search (d >= 4) with a counting pass
+                                      and a filling pass even where the one-pass search with
+                                      candidate-capacity rows fits (testing)                  */
 #define DBSCAN_F_NO_BRICK    8192u /* sparse path, d = 3: MarkCore with a thread per point
                                       instead of the shared-memory brick kernel (testing)    */
 

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256, 2) bcp_large_kernel(const uint2* __restri
 // segment of class-sorted rows holds at most 2d cells): each group walks its
 // own cells and the warp runs until all of its groups are done.
 template <int D, bool WIDE, bool APX, int G>
-__global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, CellsView cv, Geo g,
+__global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, bool flat, CellsView cv, Geo g,
                                                        const int32_t* __restrict__ Ps,
                                                        const uint32_t* __restrict__ core_cnt, uint32_t* parent,
                                                        uint2* __restrict__ large, uint32_t* __restrict__ nlarge,
@@ -255,8 +255,13 @@ __global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, 
   const bool by_class = cv.ccls && nwaves == NWAVES;  // class-sorted rows: the wave's segment only
   uint32_t mine = 0, cand = 0;
   uint32_t gc = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NG + lane / G;
-  uint32_t kg = 0;
+  uint32_t kg = 0, rg = 0;
   uint64_t key_g = 0, t0 = 0, r1 = 0;
+  // waves after the first (class-sorted rows; the host flattens the forest
+  // before each): a pair whose h has the ancestor rg of g as its parent is
+  // connected with one load (a cached parent is stale at worst, and then
+  // still an ancestor: components only merge)
+  const bool hop = by_class && wave > 0 && flat;
   // move the group to its next core cell with a non-empty segment
   auto seek = [&]() {
     for (; gc < cv.ncells; gc += gstride) {
@@ -273,6 +278,7 @@ __global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, 
       if (r0 < r1) {
         t0 = r0;
         if (!by_class && nwaves > 1) key_g = cv.cell_key[gc];
+        if (hop) rg = uf_root_cached(parent, gc);
         return;
       }
     }
@@ -286,7 +292,9 @@ __global__ void __launch_bounds__(256, 4) wave_csr_kernel(int wave, int nwaves, 
     if (act && t < r1) {
       const uint32_t h = cv.nbr[t];
       p.y = h;
-      if (h < gc) {
+      if (h < gc && hop && __ldca(parent + h) == rg) {
+        is = true;  // (h is core: a cell without core points is never linked)
+      } else if (h < gc) {
         const uint32_t kh = core_cnt[h];
         is = kh > 0 && (by_class || nwaves == 1 || wave_of(key_g, cv.cell_key[h], g) == wave);
         if (is) {
@@ -407,21 +415,25 @@ void cluster_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, 
   for (int w = 0; w < nw; ++w) {
     // the face segment of class-sorted rows is short (<= 2d cells): groups of 8
     const bool narrow = cv.ccls && nw == NWAVES && w == 0;
+    // long rows (the crowded high-d lattices): flatten the forest before the
+    // later waves, whose pairs then mostly settle with one load
+    const bool flat = cv.ccls && nw == NWAVES && w > 0 && nbr_total >= 256ull * nc;
+    if (flat) uf_flatten(c, parent, nullptr, nc);
     const unsigned wgrid = grid_for((int64_t)nc * (narrow ? 8 : 32), 256, c.sms * 16);
     dispatch(g.D, wide, [&]<int D, bool W>() {
       if (g.at) {
         if (narrow)
-          wave_csr_kernel<D, W, true, 8><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+          wave_csr_kernel<D, W, true, 8><<<wgrid, 256, 0, c.st>>>(w, nw, flat, cv, g, Ps, core_cnt, parent, large,
                                                                   nlarge + w, tested, npairs_out);
         else
-          wave_csr_kernel<D, W, true, 32><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+          wave_csr_kernel<D, W, true, 32><<<wgrid, 256, 0, c.st>>>(w, nw, flat, cv, g, Ps, core_cnt, parent, large,
                                                                    nlarge + w, tested, npairs_out);
       } else {
         if (narrow)
-          wave_csr_kernel<D, W, false, 8><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+          wave_csr_kernel<D, W, false, 8><<<wgrid, 256, 0, c.st>>>(w, nw, flat, cv, g, Ps, core_cnt, parent, large,
                                                                    nlarge + w, tested, npairs_out);
         else
-          wave_csr_kernel<D, W, false, 32><<<wgrid, 256, 0, c.st>>>(w, nw, cv, g, Ps, core_cnt, parent, large,
+          wave_csr_kernel<D, W, false, 32><<<wgrid, 256, 0, c.st>>>(w, nw, flat, cv, g, Ps, core_cnt, parent, large,
                                                                     nlarge + w, tested, npairs_out);
       }
     });

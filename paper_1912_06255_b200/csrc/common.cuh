@@ -233,6 +233,26 @@ __device__ __forceinline__ bool near_box(const int32_t* p, const int64_t* blo, c
   return acc <= g.eps2;
 }
 
+// Squared gap between the box [qlo, qhi] (the bounding box of some query
+// points) and the integer box of a cell with lower corner blo, clamped as in
+// near_box: <= eps^2 unless no point of the cell is within eps of any point
+// in [qlo, qhi].
+template <int D>
+__device__ __forceinline__ bool near_box2(const int32_t* qlo, const int32_t* qhi, const int64_t* blo, const Geo& g) {
+  uint64_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < g.d) {
+      const int64_t lo = blo[k], hi = blo[k] + (int64_t)g.s - 1;
+      const int64_t t = qlo[k] > hi ? qlo[k] - hi : (qhi[k] < lo ? lo - qhi[k] : 0);
+      uint64_t u = (uint64_t)t;
+      if (u > g.clampc) u = g.clampc;
+      acc += u * u;
+    }
+  }
+  return acc <= g.eps2;
+}
+
 template <int D>
 __device__ __forceinline__ void cell_box_lo(uint64_t key, const Geo& g, int64_t* blo) {
 #pragma unroll

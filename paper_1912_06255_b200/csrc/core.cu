@@ -14,6 +14,12 @@ namespace db {
 // Candidate points of one query (sum of neighbour-cell sizes, ub[g]) at or
 // below this are scanned by one thread; above it by one warp.
 constexpr uint32_t WARP_CANDIDATES = 32;
+// Such a cell with at least this many points goes to the cell-tile kernel
+// (a warp per cell, lanes over its points) instead of a warp per point.
+constexpr int64_t TILE_MIN_POINTS = 4;
+// (and the per-point kernel's point-box filter of neighbour cells: both pay
+// from d = 6 on, ncu on SS-varden 5D / 7D and the BASELINE 5D / 7D configs)
+constexpr int TILE_MIN_D = 6;
 
 // Warp per cell (grid-stride), lanes over its points. With cnt = |g| and
 // ub = sum of the neighbours' sizes (from the neighbour stage): cnt >= minPts
@@ -25,7 +31,9 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
                                                         int64_t min_pts, uint32_t clampc, uint64_t eps2,
                                                         uint8_t* __restrict__ core_s,
                                                         uint32_t* __restrict__ queue,
-                                                        uint32_t* __restrict__ qcount, bool pre) {
+                                                        uint32_t* __restrict__ qcount,
+                                                        uint32_t* __restrict__ cqueue,
+                                                        uint32_t* __restrict__ cqcount, bool pre) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < cv.ncells; g += nwarps) {
@@ -35,6 +43,10 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
     if (cnt >= min_pts || cnt + (int64_t)ub < min_pts) {
       const uint8_t v = cnt >= min_pts;
       for (uint32_t u = s + lane; u < e; u += 32) core_s[u] = v;
+      continue;
+    }
+    if (cqueue && ub > WARP_CANDIDATES && cnt >= TILE_MIN_POINTS) {  // the whole cell to the tile kernel
+      if (lane == 0) cqueue[atomicAdd(cqcount, 1u)] = g;
       continue;
     }
     for (uint32_t j0 = s; j0 < e; j0 += 32) {
@@ -80,9 +92,11 @@ template <int D, bool WIDE>
 __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const int32_t* __restrict__ Ps,
                                                              const uint32_t* __restrict__ queue,
                                                              const uint32_t* __restrict__ qcount,
-                                                             int64_t min_pts, uint32_t clampc,
-                                                             uint64_t eps2, uint8_t* __restrict__ core_s) {
+                                                             int64_t min_pts, Geo geo,
+                                                             uint8_t* __restrict__ core_s, bool prune) {
   const int lane = threadIdx.x & 31;
+  const uint32_t clampc = geo.clampc;
+  const uint64_t eps2 = geo.eps2;
   const uint32_t m = *qcount;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < m; w += nwarps) {
@@ -91,14 +105,20 @@ __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const
     int32_t p[D], q[D];
     PtLoad<D>::load(Ps, j, p);
     int64_t count = cv.cell_start[g + 1] - cv.cell_start[g];
-    const uint64_t nb1 = cv.nbr_off[g + 1];
-    for (uint64_t cb = cv.nbr_off[g]; cb < nb1 && count < min_pts; cb += 32) {
+    const uint64_t nb0 = cv.nbr_off[g], nb1 = cv.nbr_off[g + 1];
+    for (uint64_t cb = nb0; cb < nb1 && count < min_pts; cb += 32) {
       const uint64_t t = cb + lane;
       uint32_t sz = 0, st = 0;
       if (t < nb1) {
+        // (a neighbour cell whose box is beyond eps of p holds no candidate)
         const uint32_t h = cv.nbr[t];
         st = cv.cell_start[h];
         sz = cv.cell_start[h + 1] - st;
+        if (prune && cb > nb0) {  // (from the second block of 32 cells: most points stop in the first)
+          int64_t blo[D];
+          cell_box_lo<D>(cv.cell_key[h], geo, blo);
+          if (!near_box<D>(p, blo, geo)) sz = 0;
+        }
       }
       const uint32_t incl = warp_inclusive_scan(sz);
       const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
@@ -123,6 +143,122 @@ __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const
       }
     }
     if (lane == 0) core_s[j] = count >= min_pts;
+  }
+}
+
+// Cell-tile variant (CSR path): a warp per queued cell, a lane per point of
+// the cell (32 at a time). The candidates — the points of the neighbouring
+// cells, 32 cells at a time, flattened by a prefix sum as in the warp kernel
+// — are staged 32 at a time in a per-warp shared-memory tile, one load per
+// lane, and every lane tests its own point against each staged candidate
+// (broadcast reads): a candidate load serves all the cell's points. Counting
+// stops when every lane has reached minPts (Alg 2; reading 13).
+template <int D>
+__device__ __forceinline__ void tile_put(int32_t* t, const int32_t* q) {
+  if constexpr (D == 2) {
+    *reinterpret_cast<int2*>(t) = make_int2(q[0], q[1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < D; k += 4) *reinterpret_cast<int4*>(t + k) = make_int4(q[k], q[k + 1], q[k + 2], q[k + 3]);
+  }
+}
+template <int D>
+__device__ __forceinline__ void tile_get(const int32_t* t, int32_t* q) {
+  if constexpr (D == 2) {
+    const int2 v = *reinterpret_cast<const int2*>(t);
+    q[0] = v.x; q[1] = v.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < D; k += 4) {
+      const int4 v = *reinterpret_cast<const int4*>(t + k);
+      q[k] = v.x; q[k + 1] = v.y; q[k + 2] = v.z; q[k + 3] = v.w;
+    }
+  }
+}
+
+template <int D, bool WIDE>
+__global__ void __launch_bounds__(256, 4) mark_core_tile_kernel(CellsView cv, const int32_t* __restrict__ Ps,
+                                                             const uint32_t* __restrict__ cqueue,
+                                                             const uint32_t* __restrict__ cqcount,
+                                                             int64_t min_pts, Geo geo,
+                                                             uint8_t* __restrict__ core_s, bool pre) {
+  const uint32_t clampc = geo.clampc;
+  const uint64_t eps2 = geo.eps2;
+  __shared__ __align__(16) int32_t tile[8][32 * D];
+  const int lane = threadIdx.x & 31;
+  int32_t* T = tile[threadIdx.x >> 5];
+  const uint32_t m = *cqcount;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t need = (uint32_t)min(min_pts, (int64_t)0xffffffff);
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < m; w += nwarps) {
+    const uint32_t g = cqueue[w];
+    const uint32_t s = cv.cell_start[g], e = cv.cell_start[g + 1];
+    const uint64_t nb0 = cv.nbr_off[g], nb1 = cv.nbr_off[g + 1];
+    for (uint32_t j0 = s; j0 < e; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool live = j < e && !(pre && core_s[j]);
+      if (!__any_sync(DB_FULL, live)) continue;
+      int32_t p[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) p[k] = 0;
+      if (live) PtLoad<D>::load(Ps, j, p);
+      // bounding box of the live points: neighbour cells beyond eps of it are skipped
+      int32_t qlo[D], qhi[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        qlo[k] = __reduce_min_sync(DB_FULL, live ? p[k] : INT32_MAX);
+        qhi[k] = __reduce_max_sync(DB_FULL, live ? p[k] : INT32_MIN);
+      }
+      uint32_t count = e - s;  // its own cell (< minPts: not a dense cell)
+      bool done = !live;
+      for (uint64_t cb = nb0; cb < nb1; cb += 32) {
+        const uint64_t t = cb + lane;
+        uint32_t sz = 0, st = 0;
+        if (t < nb1) {
+          const uint32_t h = cv.nbr[t];
+          int64_t blo[D];
+          cell_box_lo<D>(cv.cell_key[h], geo, blo);
+          if (near_box2<D>(qlo, qhi, blo, geo)) {
+            st = cv.cell_start[h];
+            sz = cv.cell_start[h + 1] - st;
+          }
+        }
+        const uint32_t incl = warp_inclusive_scan(sz);
+        const uint32_t total = __shfl_sync(DB_FULL, incl, 31);
+        const uint32_t excl = incl - sz;
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+          const uint32_t tt = t0 + lane;
+          int lo = 0;
+#pragma unroll
+          for (int sh = 16; sh >= 1; sh >>= 1) {
+            const uint32_t ex = __shfl_sync(DB_FULL, excl, lo + sh);
+            if (ex <= tt) lo += sh;
+          }
+          const uint32_t ost = __shfl_sync(DB_FULL, st, lo);
+          const uint32_t oex = __shfl_sync(DB_FULL, excl, lo);
+          if (tt < total) {
+            int32_t q[D];
+            PtLoad<D>::load(Ps, ost + (tt - oex), q);
+            tile_put<D>(T + lane * D, q);
+          }
+          __syncwarp();
+          const uint32_t nt = min(32u, total - t0);
+          if (!done) {
+            for (uint32_t u = 0; u < nt; ++u) {
+              int32_t q[D];
+              tile_get<D>(T + u * D, q);
+              DB_WORK(0);
+              count += within<D, WIDE>(p, q, clampc, eps2) ? 1u : 0u;
+            }
+            done = count >= need;
+          }
+          __syncwarp();
+          if (__all_sync(DB_FULL, done)) break;
+        }
+        if (__all_sync(DB_FULL, done)) break;
+      }
+      if (live) core_s[j] = count >= need;
+    }
   }
 }
 
@@ -247,17 +383,28 @@ __global__ void __launch_bounds__(256, 4) mark_core_qt_kernel(CellsView cv, cons
 void mark_core(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps, int64_t n,
                int64_t min_pts, bool wide, uint8_t* core_s, const QTrees* qt, bool pre) {
   uint32_t* queue = c.alloc<uint32_t>(n);
-  uint32_t* qcount = c.alloc<uint32_t>(1);
-  c.zero(qcount, sizeof(uint32_t));
+  uint32_t* qcount = c.alloc<uint32_t>(2);  // [0] points, [1] cells
+  const bool use_qt = qt && qt->nodes;
+  // the cell tiles pay where a point needs many candidates to reach minPts:
+  // high d, where the eps-ball fills a small part of its neighbour cells
+  const bool tiles = !use_qt && g.d >= TILE_MIN_D;
+  uint32_t* cqueue = tiles ? c.alloc<uint32_t>(cv.ncells) : nullptr;
+  c.zero(qcount, 2 * sizeof(uint32_t));
   dispatch(g.D, wide, [&]<int D, bool W>() {
     mark_core_kernel<D, W><<<grid_for((int64_t)cv.ncells * 32, 256, c.sms * 16), 256, 0, c.st>>>(
-        cv, Ps, min_pts, g.clampc, g.eps2, core_s, queue, qcount, pre);
+        cv, Ps, min_pts, g.clampc, g.eps2, core_s, queue, qcount, cqueue, qcount + 1, pre);
     c.launched();
-    if (qt && qt->nodes)
+    if (use_qt) {
       mark_core_qt_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts, g, *qt, core_s);
-    else
-      mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts,
-                                                                 g.clampc, g.eps2, core_s);
+    } else {
+      if (tiles) {
+        mark_core_tile_kernel<D, W><<<c.sms * 8, 256, 0, c.st>>>(cv, Ps, cqueue, qcount + 1, min_pts, g, core_s,
+                                                                 pre);
+        c.launched();
+      }
+      mark_core_warp_kernel<D, W><<<c.sms * 16, 256, 0, c.st>>>(cv, Ps, queue, qcount, min_pts, g, core_s,
+                                                                 g.d >= TILE_MIN_D);
+    }
     c.launched();
   });
 }

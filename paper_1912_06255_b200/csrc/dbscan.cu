@@ -301,6 +301,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   c.st = st;
   init_device_once(dev, &c.sms);
   c.ar = &ws.mem;
+  c.flags = flags;
   c.pin = ws.pin.base ? &ws.pin : nullptr;
   static const bool tracing = getenv("DB_TRACE") != nullptr;
   c.tracing = tracing;

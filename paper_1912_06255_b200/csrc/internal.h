@@ -55,6 +55,7 @@ struct Ctx {
   // host-side trace (DB_TRACE=1 in the environment): what the host thread
   // does when, to find where the GPU waits for it
   bool tracing = false;
+  uint32_t flags = 0;  // the call's DBSCAN_F_* flags (path switches read by the stages)
   std::vector<std::pair<std::pair<const char*, int>, double>> trace;
   void mark(const char* what, int v = -1) {
     trace.push_back({{what, v}, std::chrono::duration<double, std::micro>(

@@ -612,7 +612,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   // pass class-sorts them into the CSR (two passes of tests otherwise: count,
   // then fill at the scanned offsets)
   bool onepass = false;
-  if (maxb && ncells < (1u << 30)) {
+  if (maxb && ncells < (1u << 30) && !(c.flags & DBSCAN_F_NBR_TWO_PASS)) {
     uint32_t* cap = c.alloc<uint32_t>(ncells);
     uint64_t* toff = c.alloc<uint64_t>((size_t)ncells + 1);
     nbr_cap_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, bstart, maxb, B1, B2, ncells, g.R, cap);

@@ -550,6 +550,22 @@ def test_subcell_bounds_large_minpts_vs_o2(oracle_lib, d):
     assert r.stats["qb_decided"] > 0 or d == 5
 
 
+@pytest.mark.parametrize("d", [6, 7])
+def test_markcore_cell_tiles_vs_o2(oracle_lib, d):
+    """MarkCore's cell tiles (d >= 6: a warp per sparse cell, a lane per
+    point, candidates staged 32 at a time, neighbour cells beyond eps of the
+    tile's bounding box skipped) and the per-point warp kernel's point-box
+    filter, on variable-density data whose sparse cells hold 1..300 points:
+    minPts 40 (one 32-point slab, mixed cells) and 400 (several slabs), with
+    and without the sub-cell bounds marking points core first."""
+    pts = datagen.seed_spreader(150_000, d, 2e4, 20, 0.02, varden=True)
+    for mp in (40, 400):
+        o = oracle_lib.o2(pts, 500, mp)
+        for flags in (0, pkg.F_FORCE_QBOUND):
+            r = gpu(pts, 500, mp, flags=flags)
+            assert_same(np_result(r), o, f"tiles d={d} mp={mp} flags={flags}")
+
+
 def test_high_d_three_axis_buckets_vs_o2(oracle_lib):
     """d >= 4 with tens of thousands of clustered cells (SS-varden 7D in a
     small domain: 52K cells): the all-pairs neighbour search buckets the cells
@@ -557,6 +573,10 @@ def test_high_d_three_axis_buckets_vs_o2(oracle_lib):
     window; against O2 (all-pairs cell scan, independent code)."""
     pts = datagen.seed_spreader(300_000, 7, 2e4, 27, 0.02, varden=True)
     for mp in (20, 300):
-        r = gpu(pts, 600, mp)
-        assert r.stats["tree"] == 1 and 16384 <= r.stats["ncells"] <= 131_072, r.stats
-        assert_same(np_result(r), oracle_lib.o2(pts, 600, mp), f"3-axis buckets mp={mp}")
+        o = oracle_lib.o2(pts, 600, mp)
+        # one test pass into candidate-capacity rows + compaction (default),
+        # and the counting + filling passes (the fallback for huge rows)
+        for flags in (0, pkg.F_NBR_TWO_PASS):
+            r = gpu(pts, 600, mp, flags=flags)
+            assert r.stats["tree"] == 1 and 16384 <= r.stats["ncells"] <= 131_072, r.stats
+            assert_same(np_result(r), o, f"3-axis buckets mp={mp} flags={flags}")
