@@ -358,22 +358,28 @@ __global__ void bucket_count_kernel(const uint32_t* __restrict__ cc, uint32_t nc
 __global__ void bucket_fill_kernel(const uint32_t* __restrict__ cc, uint32_t ncells, uint32_t B1, uint32_t B2,
                                    const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bcur,
                                    uint32_t* __restrict__ order, uint32_t* __restrict__ ccs,
-                                   const uint32_t* __restrict__ cell_start, uint32_t* __restrict__ bsize) {
+                                   const uint32_t* __restrict__ cell_start, uint32_t* __restrict__ bsize,
+                                   uint32_t* __restrict__ bpos) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ncells) return;
   const uint32_t b = cell_bucket(cc, i, B1, B2);
   const uint32_t t = bstart[b] + atomicAdd(bcur + b, 1u);
   order[t] = i;
+  bpos[i] = t;
   bsize[t] = cell_start[i + 1] - cell_start[i];
   reinterpret_cast<uint4*>(ccs)[2 * t] = reinterpret_cast<const uint4*>(cc)[2 * i];
   reinterpret_cast<uint4*>(ccs)[2 * t + 1] = reinterpret_cast<const uint4*>(cc)[2 * i + 1];
 }
 
-template <int DD>
+// PACK: 32-bit table entries gap^2 | |delta| << 27 (host: d (eps^2 + 1) <
+// 2^27, d gmax < 32), so one add per axis accumulates both the squared gap
+// and the lattice L1 distance that sets the class
+template <int DD, bool PACK>
 __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t* __restrict__ cc,
                                                         const uint32_t* __restrict__ ccs,
                                                         const uint32_t* __restrict__ order,
                                                         const uint32_t* __restrict__ bsize,
+                                                        const uint32_t* __restrict__ bpos,
                                                         const uint32_t* __restrict__ bstart, uint32_t maxb,
                                                         uint32_t B1, uint32_t B2, uint32_t ncells, Geo g,
                                                         const uint64_t* __restrict__ gtab_g, int gmax,
@@ -383,11 +389,17 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
                                                         const uint64_t* __restrict__ off,
                                                         uint32_t* __restrict__ nbr) {
   // fill: 0 = count (cnt, ccount, ub), 1 = write class-sorted rows at off,
-  // 2 = one pass: write (neighbour | class << 30) in candidate order into a
-  // row of its candidate capacity at off AND the counts (nbr_compact_kernel
-  // then class-sorts the rows into the final CSR)
+  // 2 = one symmetric pass: only candidates after q in bucket order are
+  // tested, and a pair found adds (other cell | class << 30) to BOTH rows,
+  // rows of candidate capacity at off filled through the counters cnt[]
+  // (nbr_compact_kernel then class-sorts the rows into the final CSR and
+  // counts the classes and ub)
   __shared__ unsigned long long gt[GT_MAX + 1];
-  for (int i = threadIdx.x; i <= gmax; i += blockDim.x) gt[i] = gtab_g[i];
+  __shared__ uint32_t gtp[GT_MAX + 1];
+  for (int i = threadIdx.x; i <= gmax; i += blockDim.x) {
+    gt[i] = gtab_g[i];
+    if (PACK) gtp[i] = (uint32_t)gtab_g[i] | ((uint32_t)i << 27);
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
@@ -407,8 +419,8 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
       pos[1] = pos[0] + ccount[q];
       pos[2] = pos[1] + ccount[ncells + q];
     }
-    uint32_t n3[3] = {0, 0, 0};
-    uint64_t sum = 0;
+    uint32_t n3[3] = {0, 0, 0};  // fill == 1: warp totals; else per lane, reduced at the end
+    uint32_t sum = 0;            // per lane: < n < 2^32
     const uint32_t c0 = maxb ? cq[0] : 0u;  // maxb = 0: a single bucket
     const uint32_t blo = c0 > g.R ? c0 - g.R : 0u, bhi = min(maxb, c0 + g.R);
     // B1 > 1: buckets by (axis 0, axis 1); for each axis-0 bucket the axis-1
@@ -419,12 +431,14 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     const uint32_t y1 = B1 > 1 ? min(B1 - 1, cq[1] + g.R) : 0u;
     const uint32_t z0 = B2 > 1 ? (cq[2] > g.R ? cq[2] - g.R : 0u) : 0u;
     const uint32_t z1 = B2 > 1 ? min(B2 - 1, cq[2] + g.R) : 0u;
+    const uint32_t tq = fill == 2 ? bpos[q] : 0u;
     for (uint32_t b0 = blo; b0 <= bhi; ++b0) {
     for (uint32_t b1 = y0; b1 <= (B2 > 1 ? y1 : y0); ++b1) {
     const uint32_t r0 = B2 > 1 ? (b0 * B1 + b1) * B2 + z0 : b0 * B1 + y0;
     const uint32_t r1 = B2 > 1 ? (b0 * B1 + b1) * B2 + z1 : b0 * B1 + y1;
     const uint32_t t1 = bstart[r1 + 1];
-    for (uint32_t t0 = bstart[r0]; t0 < t1; t0 += 32) {
+    const uint32_t ts = fill == 2 ? max(bstart[r0], tq + 1) : bstart[r0];
+    for (uint32_t t0 = ts; t0 < t1; t0 += 32) {
       const uint32_t t = t0 + lane;
       int cls = -1;
       if (t < t1) {
@@ -436,36 +450,68 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
           const uint4 b = CS[2 * t + 1];
           ch[4] = b.x; ch[5] = b.y; ch[6] = b.z; ch[7] = b.w;
         }
-        uint64_t acc = 0;
-        uint32_t l1 = 0;
+        uint32_t l1;
+        bool in;
+        if constexpr (PACK) {
+          uint32_t acc = 0;
 #pragma unroll
-        for (int k = 0; k < DD; ++k) {
-          const uint32_t dl = min(__usad(ch[k], cq[k], 0u), (uint32_t)gmax);
-          acc += gt[dl];
-          l1 += dl;
+          for (int k = 0; k < DD; ++k) acc += gtp[min(__usad(ch[k], cq[k], 0u), (uint32_t)gmax)];
+          l1 = acc >> 27;
+          in = (acc & 0x7ffffffu) <= (uint32_t)g.eps2;
+        } else {
+          uint64_t acc = 0;
+          l1 = 0;
+#pragma unroll
+          for (int k = 0; k < DD; ++k) {
+            const uint32_t dl = min(__usad(ch[k], cq[k], 0u), (uint32_t)gmax);
+            acc += gt[dl];
+            l1 += dl;
+          }
+          in = acc <= g.eps2;
         }
-        if (acc <= g.eps2 && l1 > 0) cls = l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);  // (l1 = 0: the query itself)
+        if (in && l1 > 0) cls = l1 <= 1 ? 0 : (l1 == 2 ? 1 : 2);  // (l1 = 0: the query itself)
       }
-      const uint32_t h = cls >= 0 ? order[t] : 0u;
       if (fill == 2) {
         const uint32_t b = __ballot_sync(DB_FULL, cls >= 0);
-        if (cls >= 0) nbr[pos[0] + __popc(b & lt)] = h | ((uint32_t)cls << 30);
-        pos[0] += __popc(b);
+        if (b) {
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(cnt + q, (uint32_t)__popc(b));
+          base = __shfl_sync(DB_FULL, base, 0);
+          if (cls >= 0) {
+            const uint32_t h = order[t];
+            nbr[pos[0] + base + __popc(b & lt)] = h | ((uint32_t)cls << 30);
+            nbr[off[h] + atomicAdd(cnt + h, 1u)] = q | ((uint32_t)cls << 30);
+          }
+        }
+        continue;
       }
+      if (fill == 1) {
+        const uint32_t h = cls >= 0 ? order[t] : 0u;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const uint32_t b = __ballot_sync(DB_FULL, cls == c);
-        if (fill == 1 && cls == c) nbr[pos[c] + __popc(b & lt)] = h;
-        if (fill == 1) pos[c] += __popc(b);
-        n3[c] += __popc(b);
+        for (int c = 0; c < 3; ++c) {
+          const uint32_t b = __ballot_sync(DB_FULL, cls == c);
+          if (cls == c) nbr[pos[c] + __popc(b & lt)] = h;
+          pos[c] += __popc(b);
+        }
+      } else {
+        n3[0] += cls == 0;
+        n3[1] += cls == 1;
+        n3[2] += cls == 2;
+        if (cls >= 0) sum += bsize[t];
       }
-      if (fill != 1 && cls >= 0) sum += bsize[t];
     }
     }
     }
-    if (fill != 1) {
+    if (fill == 0) {
+      uint64_t sum64 = sum;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(DB_FULL, sum, o);
+      for (int o = 16; o; o >>= 1) {
+        sum64 += __shfl_xor_sync(DB_FULL, sum64, o);
+        n3[0] += __shfl_xor_sync(DB_FULL, n3[0], o);
+        n3[1] += __shfl_xor_sync(DB_FULL, n3[1], o);
+        n3[2] += __shfl_xor_sync(DB_FULL, n3[2], o);
+      }
+      const uint64_t sum = sum64;
       if (lane == 0) {
         cnt[q] = n3[0] + n3[1] + n3[2];
         ccount[q] = n3[0];
@@ -507,7 +553,8 @@ __global__ void nbr_cap_kernel(const uint32_t* __restrict__ cc, const uint32_t* 
 __global__ void __launch_bounds__(256) nbr_compact_kernel(const uint32_t* __restrict__ tagged,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ cnt,
-                                                          const uint32_t* __restrict__ ccount,
+                                                          const uint32_t* __restrict__ cell_start,
+                                                          uint32_t* __restrict__ ccount, uint32_t* __restrict__ ub,
                                                           const uint64_t* __restrict__ off, uint32_t ncells,
                                                           uint32_t* __restrict__ nbr) {
   const int lane = threadIdx.x & 31;
@@ -516,10 +563,30 @@ __global__ void __launch_bounds__(256) nbr_compact_kernel(const uint32_t* __rest
   for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncells; q += nwarps) {
     const uint32_t* src = tagged + toff[q];
     const uint32_t len = cnt[q];
+    // class counts and ub (the sum of the neighbours' sizes)
+    uint32_t n0 = 0, n1 = 0;
+    uint64_t sum = 0;
+    for (uint32_t t = lane; t < len; t += 32) {
+      const uint32_t v = src[t], h = v & 0x3fffffffu, cls = v >> 30;
+      n0 += cls == 0;
+      n1 += cls == 1;
+      sum += cell_start[h + 1] - cell_start[h];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      n0 += __shfl_xor_sync(DB_FULL, n0, o);
+      n1 += __shfl_xor_sync(DB_FULL, n1, o);
+      sum += __shfl_xor_sync(DB_FULL, sum, o);
+    }
+    if (lane == 0) {
+      ccount[q] = n0;
+      ccount[ncells + q] = n1;
+      ub[q] = (uint32_t)min(sum, (uint64_t)0xffffffffu);
+    }
     uint64_t pos[3];
     pos[0] = off[q];
-    pos[1] = pos[0] + ccount[q];
-    pos[2] = pos[1] + ccount[ncells + q];
+    pos[1] = pos[0] + n0;
+    pos[2] = pos[1] + n1;
     for (uint32_t t0 = 0; t0 < len; t0 += 32) {
       const uint32_t t = t0 + lane;
       const uint32_t v = t < len ? src[t] : 0xffffffffu;
@@ -574,6 +641,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   uint32_t* order = c.alloc<uint32_t>(ncells);
   uint32_t* ccs = cc;  // (one bucket: the cells in their own order)
   uint32_t* bsize = c.alloc<uint32_t>(ncells);  // points per cell, bucket order
+  uint32_t* bpos = c.alloc<uint32_t>(ncells);   // each cell's position in bucket order
   c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
   if (maxb) {
     bucket_count_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bcnt);
@@ -582,7 +650,7 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
     c.zero(bcnt, sizeof(uint32_t) * ((size_t)nbk + 1));
     ccs = c.alloc<uint32_t>((size_t)ncells * 8);
     bucket_fill_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cc, ncells, B1, B2, bstart, bcnt, order,
-                                                                         ccs, cell_start, bsize);
+                                                                         ccs, cell_start, bsize, bpos);
     c.launched();
   } else {
     // one bucket: every cell (cc[0] is then clamped by maxb = 0 -> buckets 0..0)
@@ -598,13 +666,19 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   uint32_t* ub = c.alloc<uint32_t>(ncells);
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
   const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
+  const bool pack = (uint64_t)g.d * (g.eps2 + 1) < (1ull << 27) && (uint64_t)g.d * gmax < 32;
   auto launch = [&](int fill, uint32_t* list, const uint64_t* lo) {
-    if (g.d <= 4)
-      nbr_brute_kernel<4><<<grid, 256, 0, c.st>>>(fill, cc, ccs, order, bsize, bstart, maxb, B1, B2, ncells, g,
-                                                  (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list);
-    else
-      nbr_brute_kernel<8><<<grid, 256, 0, c.st>>>(fill, cc, ccs, order, bsize, bstart, maxb, B1, B2, ncells, g,
-                                                  (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list);
+    auto go = [&](auto kern) {
+      kern<<<grid, 256, 0, c.st>>>(fill, cc, ccs, order, bsize, bpos, bstart, maxb, B1, B2, ncells, g,
+                                   (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list);
+    };
+    if (g.d <= 4) {
+      if (pack) go(nbr_brute_kernel<4, true>);
+      else go(nbr_brute_kernel<4, false>);
+    } else {
+      if (pack) go(nbr_brute_kernel<8, true>);
+      else go(nbr_brute_kernel<8, false>);
+    }
     c.launched();
   };
   // one test pass when the candidate rows fit: rows of candidate capacity
@@ -621,11 +695,12 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
     const uint64_t tcap = c.read(toff + ncells);
     if (tcap <= NBR_ONEPASS_MAX) {
       uint32_t* tagged = c.alloc<uint32_t>(tcap + 1);
+      c.zero(cnt, sizeof(uint32_t) * ncells);  // the rows' fill counters
       launch(2, tagged, toff);
       exclusive_scan_u32_u64(c, cnt, off, ncells);
       *total = nbr_total_bound(c, off + ncells, tcap);
       uint32_t* list = c.alloc<uint32_t>(*total + 1);
-      nbr_compact_kernel<<<grid, 256, 0, c.st>>>(tagged, toff, cnt, ccount, off, ncells, list);
+      nbr_compact_kernel<<<grid, 256, 0, c.st>>>(tagged, toff, cnt, cell_start, ccount, ub, off, ncells, list);
       c.launched();
       *nbr = list;
       onepass = true;
