@@ -122,7 +122,12 @@ extern "C" {
                                         0 in the product library                              */
 #define DBSCAN_STAT_QB_DECIDED   23  /* MarkCore points proved core by the sub-cell lower bounds
                                         (row f2, minPts >= 2000 on the CSR path); -1: not run  */
-#define DBSCAN_NSTATS            32  /* (24-31 reserved) */
+#define DBSCAN_STAT_MARKCORE_ALG2 24 /* MarkCore work of Alg 2 as written: the tests of
+                                        the cell-level stencil walk, nearest column first, stopping
+                                        at minPts (measurement build only; equals MARKCORE_TESTS
+                                        except where the brick kernel's sub-cell stencils skip
+                                        candidates)                                            */
+#define DBSCAN_NSTATS            32  /* (25-31 reserved) */
 
 typedef struct dbscan_result {
   int64_t  n;

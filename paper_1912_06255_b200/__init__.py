@@ -48,7 +48,7 @@ STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore
           "cluster", "labels", "border", "total"]
 STATS = ["ncells", "key_bits", "sort_passes", "nbr_entries", "core_cells", "pairs", "pairs_tested",
          "launches", "wide", "tree", "cell_side", "dense_dir", "sparse", "hash_group", "markcore_tests", "qt_nodes", "approx_side", "brick", "point_border",
-         "sparse_passes", "bcp_tests", "border_tests", "counting_build", "qb_decided"]
+         "sparse_passes", "bcp_tests", "border_tests", "counting_build", "qb_decided", "markcore_alg2"]
 
 
 class _Result(C.Structure):

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) mark_core_kernel(CellsView cv, const int3
           for (uint32_t u = cv.cell_start[h]; u < he; ++u) {
             PtLoad<D>::load(Ps, u, q);
             DB_WORK(0);
+            DB_WORK(3);
             count += within<D, WIDE>(p, q, clampc, eps2);
             if (count >= min_pts) break;
           }
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(256) mark_core_warp_kernel(CellsView cv, const
         bool hit = false;
         if (tt < total) {
           DB_WORK(0);
+          DB_WORK(3);
           PtLoad<D>::load(Ps, ost + (tt - oex), q);
           hit = within<D, WIDE>(p, q, clampc, eps2);
         }
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(256, 4) mark_core_tile_kernel(CellsView cv, co
               int32_t q[D];
               tile_get<D>(T + u * D, q);
               DB_WORK(0);
+              DB_WORK(3);
               count += within<D, WIDE>(p, q, clampc, eps2) ? 1u : 0u;
             }
             done = count >= need;
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(256, 4) mark_core_qt_kernel(CellsView cv, cons
         if (tt < total) {
           PtLoad<D>::load(Ps, ost + (tt - oex), q);
           DB_WORK(0);
+          DB_WORK(3);
           hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
         }
         count += __popc(__ballot_sync(DB_FULL, hit));
@@ -359,6 +363,7 @@ __global__ void __launch_bounds__(256, 4) mark_core_qt_kernel(CellsView cv, cons
             if (u < e0) {
               PtLoad<D>::load(Ps, u, q);
               DB_WORK(0);
+              DB_WORK(3);
           hit = within<D, WIDE>(p, q, g.clampc, g.eps2);
             }
             count += __popc(__ballot_sync(DB_FULL, hit));

@@ -681,6 +681,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   out->stats[DBSCAN_STAT_MARKCORE_TESTS] = (int64_t)hw[0];
   out->stats[DBSCAN_STAT_BCP_TESTS] = (int64_t)hw[1];
   out->stats[DBSCAN_STAT_BORDER_TESTS] = (int64_t)hw[2];
+  out->stats[DBSCAN_STAT_MARKCORE_ALG2] = (int64_t)hw[3];
   out->stats[DBSCAN_STAT_COUNTING_BUILD] = counting_build();
   out->stats[DBSCAN_STAT_QT_NODES] = (int64_t)qtrees.nodes;
   out->stats[DBSCAN_STAT_APPROX_SIDE] = g.at;

@@ -62,9 +62,30 @@ constexpr int BRK_MAXC = (2 * BRK_R + 1) * (2 * BRK_R + 1);  // stencil columns 
 
 // stencil columns for the brick kernel, nearest first: window of column k of
 // a cell at abs row index i = abs_flat[i + A[k]] .. abs_flat[i + B[k]]
+// (the cell-level stencil; the kernel walks the sub-cell tables below and
+// uses these only to count Alg 2's work in the measurement build)
 struct BrickCols {
   int32_t A[BRK_MAXC], B[BRK_MAXC];  // byte offsets (2 per abs entry)
   int32_t ncols;
+  uint32_t thr[3];                   // sub-cell thresholds t_1..t_3 of a cell offset (BRK_SUB per axis)
+  int32_t nwmax;                     // most windows of a sub-cell stencil
+};
+
+// Sub-cell stencils (DESIGN.md §5 "MarkCore"): a point's offset inside its
+// cell, o_k = x_k - lo_k - c_k s in [0, s), falls in one of BRK_SUB
+// sub-intervals per axis (j_k = #{i : o_k >= t_i}); for each of the
+// BRK_SUB^3 sub-cells the windows are the cells whose box lies within eps of
+// the sub-cell's box (the exact gap of reading 7 between the sub-interval and
+// the cell) — a subset of the cell-level stencil that still holds every point
+// within eps of any point of the sub-cell, so the count is unchanged.
+// Entry (uint16): byte offset A of the window's first abs entry relative to
+// the point's own (column, z) entry, + 2048, in bits 0-11; the window's span
+// in bytes (2 per cell) in bits 12-15. Nearest column first.
+constexpr int BRK_SUB = 4;
+constexpr int BRK_NSUB = BRK_SUB * BRK_SUB * BRK_SUB;
+struct BrickTab {
+  uint16_t w[BRK_NSUB][BRK_MAXC];
+  uint8_t nw[BRK_NSUB];
 };
 
 struct SpArgs {
@@ -252,6 +273,7 @@ __global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, const uint32_t* 
           for (int k = 0; k < U; ++k)
             if (u + k < ue) count += within_dim<DIM, D, WIDE>(p, q[k], a.g);
           DB_WORK_N(0, min((uint32_t)U, ue - u));
+          DB_WORK_N(3, min((uint32_t)U, ue - u));
         }
       }
       a.core_s[j] = count >= need;
@@ -280,11 +302,16 @@ __global__ void __launch_bounds__(256) sp_core_kernel(SpArgs a, const uint32_t* 
 // its points to the thread kernel (core_s stays 0xff for them).
 
 struct BrickSmem {
-  int4 pts[BRK_CAP];
+  union {
+    int4 raw[BRK_CAP];                     // the halo's points as copied (x, y, z, 0)
+    uint32_t list[BRK_MAXC][BRK_THREADS];  // phase A: non-empty windows, start | end << 16
+  };
+  uint2 pts[BRK_CAP];                    // the same points relative to the halo's origin:
+                                         // {x | y << 16, z} (< 2^16: s BRK_H < 2^16 / sqrt 3)
   uint16_t abs[BRK_COLS][BRK_H + 1];     // per column: index in pts of its cell z (z = BRK_H: end)
   int32_t gdelta[BRK_COLS];              // sorted position - index in pts, per column
   uint32_t obase[BRK_COLS];              // prefix of the own points per column
-  uint32_t list[BRK_MAXC][BRK_THREADS];  // phase A: non-empty windows, start | end << 16
+  BrickTab tab;                          // sub-cell stencils
   unsigned long long scan[33];
   uint32_t total, own;
   uint64_t bar;
@@ -315,12 +342,26 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+// ||p - q||^2 <= eps^2 on halo-relative 16-bit coordinates (exact: each
+// squared difference < 2^32 / 3)
+__device__ __forceinline__ bool brick_within(const uint32_t* p, uint2 q, uint32_t eps2) {
+  const uint32_t dx = __sad(p[0], q.x & 0xffffu, 0u), dy = __sad(p[1], q.x >> 16, 0u), dz = __sad(p[2], q.y, 0u);
+  return dx * dx + dy * dy + dz * dz <= eps2;
+}
+
 template <bool WIDE>
 __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a, const BrickCols cols,
+                                                                    const BrickTab* __restrict__ gtab,
                                                                     uint32_t nby, uint32_t nbz,
                                                                     uint32_t* overflow) {
   extern __shared__ __align__(16) uint8_t brick_raw[];
   BrickSmem& S = *reinterpret_cast<BrickSmem*>(brick_raw);
+  {  // sub-cell stencils (read from L2 by every CTA: 3.3 KB)
+    static_assert(sizeof(BrickTab) % 4 == 0, "BrickTab copied by words");
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(gtab);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&S.tab);
+    for (int i = threadIdx.x; i < (int)(sizeof(BrickTab) / 4); i += BRK_THREADS) dst[i] = __ldg(src + i);
+  }
   const uint32_t bid = blockIdx.x;
   const uint32_t bz = bid % nbz, by = (bid / nbz) % nby, bx = bid / (nbz * nby);
   const uint64_t Dx = a.g.maxc[0] + 1 + 2 * BRK_R, Dy = a.g.maxc[1] + 1 + 2 * BRK_R,
@@ -399,7 +440,7 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
   for (int q = 0; q < BRK_PER; ++q) {
     const int cc = threadIdx.x * BRK_PER + q;
     if (cc >= BRK_COLS) continue;
-    if (len[q]) bulk_copy(&S.pts[el], reinterpret_cast<const int4*>(a.Ps) + g0s[q], len[q] * 16u, &S.bar);
+    if (len[q]) bulk_copy(&S.raw[el], reinterpret_cast<const int4*>(a.Ps) + g0s[q], len[q] * 16u, &S.bar);
 #pragma unroll
     for (int z = 0; z <= BRK_H; ++z) S.abs[cc][z] += (uint16_t)el;
     S.gdelta[cc] = (int32_t)(g0s[q] - el);
@@ -407,8 +448,22 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
   }
   __syncthreads();
   mbar_wait(&S.bar, 0);
+  // ---- points relative to the halo's origin (lattice coordinate X0 - R of
+  // halo cell 0): 16 bits per axis, half the shared-memory wavefronts of a
+  // candidate load, squared distances exact in 32 bits
+  {
+    const uint32_t ox = (uint32_t)a.g.lo[0] + (uint32_t)(X0 - BRK_R) * a.g.s;
+    const uint32_t oy = (uint32_t)a.g.lo[1] + (uint32_t)(Y0 - BRK_R) * a.g.s;
+    const uint32_t oz = (uint32_t)a.g.lo[2] + (uint32_t)(Z0 - BRK_R) * a.g.s;
+    for (uint32_t k = threadIdx.x; k < total; k += BRK_THREADS) {
+      const int4 v = S.raw[k];
+      S.pts[k] = make_uint2(((uint32_t)v.x - ox) | (((uint32_t)v.y - oy) << 16), (uint32_t)v.z - oz);
+    }
+  }
+  __syncthreads();  // (phase A's lists overwrite raw)
   // ---- a thread per own point
   const uint32_t need = (uint32_t)min(a.min_pts, (int64_t)0xffffffff);
+  const uint32_t eps2 = (uint32_t)a.g.eps2;
   const uint16_t* abs_flat = &S.abs[0][0];
   for (uint32_t t = threadIdx.x; t < nown; t += blockDim.x) {
     // its column: the last one whose own prefix is <= t (never an empty one)
@@ -425,17 +480,44 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
       if (col[hz + step] <= i) hz += step;
     const uint32_t j = (uint32_t)((int32_t)i + S.gdelta[cc]);  // sorted position
     if ((int64_t)(col[hz + 1] - col[hz]) >= a.min_pts) { a.core_s[j] = 1; continue; }  // dense cell
-    const int4 pv = S.pts[i];
-    const int32_t p[4] = {pv.x, pv.y, pv.z, pv.w};
-    // phase A: non-empty stencil windows, nearest first
-    // (32-bit shared-memory addresses: no 64-bit pointer arithmetic per column)
+    const uint2 pv = S.pts[i];
+    const uint32_t p[3] = {pv.x & 0xffffu, pv.x >> 16, pv.y};
+    // its sub-cell: offsets inside the cell (halo coordinates hx, hy, hz)
+    uint32_t sub = 0;
+    {
+      const uint32_t hxyz[3] = {(uint32_t)cc / BRK_H, (uint32_t)cc % BRK_H, (uint32_t)hz};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t o = p[k] - hxyz[k] * a.g.s;
+        sub = sub * BRK_SUB + (o >= cols.thr[0]) + (o >= cols.thr[1]) + (o >= cols.thr[2]);
+      }
+    }
+    // (32-bit shared-memory addresses: no 64-bit pointer arithmetic per window)
     const uint32_t base = smem_addr(abs_flat + cc * (BRK_H + 1) + hz);
+#ifdef DB_COUNT_WORK
+    {  // Alg 2's work: the tests of the cell-level stencil walk,
+       // nearest column first, stopping at minPts (what slot 0 counts on the
+       // other MarkCore paths)
+      uint32_t alg2 = 0, cnt = 0;
+      for (int k = 0; k < cols.ncols && cnt < need; ++k)
+        for (uint32_t u = lds_u16(base + cols.A[k]), ue = lds_u16(base + cols.B[k]); u < ue && cnt < need; ++u) {
+          cnt += brick_within(p, S.pts[u], eps2) ? 1u : 0u;
+          ++alg2;
+        }
+      DB_WORK_N(3, alg2);
+    }
+#endif
+    // phase A: the non-empty windows of the sub-cell's stencil, nearest first
+    // (table rows are padded with empty windows to nwmax: no per-lane trip count)
     const uint32_t L = smem_addr(&S.list[0][threadIdx.x]);
     uint32_t Lw = L;
+    const uint32_t tw = smem_addr(&S.tab.w[sub][0]);
 #pragma unroll
     for (int k = 0; k < BRK_MAXC; ++k) {
-      if (k < cols.ncols) {
-        const uint32_t lo = lds_u16(base + cols.A[k]), hi = lds_u16(base + cols.B[k]);
+      if (k < cols.nwmax) {
+        const uint32_t e = lds_u16(tw + 2 * k);
+        const uint32_t wa = base + (e & 0xfffu) - 2048u;
+        const uint32_t lo = lds_u16(wa), hi = lds_u16(wa + (e >> 12));
         if (lo < hi) {
           sts_u32(Lw, __byte_perm(lo, hi, 0x5410));  // lo | hi << 16
           Lw += 4 * BRK_THREADS;
@@ -443,7 +525,7 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
       }
     }
     const uint32_t Lend = Lw;
-    // phase B: every step tests one candidate (the own column is never empty)
+    // phase B: every step tests one candidate (the own window is never empty)
     uint32_t count = 0, u = 0, u1 = 0, Lr = L;
     for (;;) {
       if (u >= u1) {
@@ -454,9 +536,7 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
         u1 = w >> 16;
       }
       DB_WORK(0);
-      const int4 qv = S.pts[u];
-      const int32_t q[4] = {qv.x, qv.y, qv.z, qv.w};
-      count += within<3, WIDE>(p, q, a.g.clampc, a.g.eps2) ? 1u : 0u;
+      count += brick_within(p, S.pts[u], eps2) ? 1u : 0u;
       ++u;
       if (count >= need) break;
     }
@@ -932,6 +1012,59 @@ static Cols stencil_columns(const Geo& g, const uint64_t* stride, Cols* back,
   return cols;
 }
 
+// Sub-cell stencils of the brick kernel (d = 3, R = 2): sub-interval j of
+// an axis holds the cell offsets [t_j, t_{j+1}) with t_0 = 0, t_j = j s /
+// BRK_SUB, t_BRK_SUB = s (s < BRK_SUB: one sub-interval, thresholds s). A
+// cell at lattice delta v along an axis is at gap v s - (t_{j+1} - 1) (v > 0),
+// t_j - (v s + s - 1) (v < 0), 0 (v = 0) from the sub-interval: the distance
+// between their closest integer coordinates. Windows keep the cells with
+// sum of squared gaps <= eps^2, per column one z-run (the condition is convex
+// in v), ordered by the column's lateral gap.
+// Rows are padded with empty windows (A = 0, span 0); returns the longest row.
+static int brick_tables(const Geo& g, uint32_t thr[3], BrickTab* tab) {
+  int nwmax = 0;
+  const int64_t s = g.s;
+  const int nsub = s >= BRK_SUB ? BRK_SUB : 1;
+  int64_t t[BRK_SUB + 1];
+  for (int j = 0; j <= BRK_SUB; ++j) t[j] = j < nsub ? j * s / nsub : s;
+  for (int j = 0; j < 3; ++j) thr[j] = (uint32_t)t[j + 1];
+  auto gap = [&](int j, int v) -> int64_t {
+    if (v > 0) return v * s - (t[j + 1] - 1);
+    if (v < 0) return t[j] - (v * s + s - 1);
+    return 0;
+  };
+  const int R = BRK_R;
+  for (int jx = 0; jx < BRK_SUB; ++jx)
+    for (int jy = 0; jy < BRK_SUB; ++jy)
+      for (int jz = 0; jz < BRK_SUB; ++jz) {
+        const int o = (jx * BRK_SUB + jy) * BRK_SUB + jz;
+        std::vector<std::pair<uint64_t, uint16_t>> ws;
+        if (jx < nsub && jy < nsub && jz < nsub) {
+          for (int dx = -R; dx <= R; ++dx)
+            for (int dy = -R; dy <= R; ++dy) {
+              const uint64_t gx = (uint64_t)gap(jx, dx), gy = (uint64_t)gap(jy, dy);
+              const uint64_t lat = gx * gx + gy * gy;
+              int zlo = 1, zhi = 0;
+              for (int dz = -R; dz <= R; ++dz) {
+                const uint64_t gz = (uint64_t)gap(jz, dz);
+                if (lat + gz * gz <= g.eps2) { zlo = std::min(zlo, dz); zhi = std::max(zhi, dz); }
+              }
+              if (zlo > zhi) continue;
+              const int dc = (dx * BRK_H + dy) * (BRK_H + 1);
+              const int A = 2 * (dc + zlo), span = 2 * (zhi - zlo + 1);
+              if (A + 2048 < 0 || A + 2048 > 0xfff || span > 15) throw Error(-4, "brick_tables: entry out of range");
+              ws.push_back({lat, (uint16_t)((A + 2048) | (span << 12))});
+            }
+          std::stable_sort(ws.begin(), ws.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        }
+        if (ws.size() > (size_t)BRK_MAXC) throw Error(-4, "brick_tables: too many windows");
+        tab->nw[o] = (uint8_t)ws.size();
+        nwmax = std::max(nwmax, (int)ws.size());
+        for (int k = 0; k < BRK_MAXC; ++k) tab->w[o][k] = k < (int)ws.size() ? ws[k].second : (uint16_t)2048;
+      }
+  return nwmax;
+}
+
 bool sparse_applicable(const Geo& g, int64_t n, uint32_t ncells, bool forced) {
   if (g.d > 3) return false;
   // 4 bits per lattice cell (two directories of 16 B per 32 cells): keep them
@@ -1038,8 +1171,13 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   // ... and at least 0.15: below it most halo columns are empty and the
   // per-brick staging costs more than it saves (measured: 0.08 points per
   // cell 1.32 ms against 0.93 ms for the thread kernel; 0.23 (c5) 1.04 / 1.07)
+  // (halo-relative coordinates: 3 (s BRK_H)^2 < 2^32 for exact 32-bit squares)
   o->brick = brick_ok && g.d == 3 && g.R == BRK_R && !g.at && (unsigned __int128)n * 100 <= vol * 27 &&
-             (unsigned __int128)n * 20 >= vol * 3;
+             (unsigned __int128)n * 20 >= vol * 3 && 3ull * ((uint64_t)g.s * BRK_H) * ((uint64_t)g.s * BRK_H) < (1ull << 32) &&
+             g.eps2 < (1ull << 32);
+  BrickTab tab{};
+  uint32_t thr[3] = {0, 0, 0};
+  if (o->brick) brick_tables(g, thr, &tab);
   if (o->brick) {
     std::vector<int8_t> geom;
     stencil_columns(g, a.stride, &back, &geom);
@@ -1051,6 +1189,11 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
       bc.A[k] = 2 * (dc - mz);
       bc.B[k] = 2 * (dc + mz + 1);
     }
+    for (int k = 0; k < 3; ++k) bc.thr[k] = thr[k];
+    bc.nwmax = 0;
+    for (int k = 0; k < BRK_NSUB; ++k) bc.nwmax = std::max(bc.nwmax, (int32_t)tab.nw[k]);
+    BrickTab* dtab = c.alloc<BrickTab>(1);
+    c.upload(dtab, &tab, 1);
     const uint32_t nb[3] = {(g.maxc[0] + BRK) / BRK, (g.maxc[1] + BRK) / BRK, (g.maxc[2] + BRK) / BRK};
     const uint64_t nbricks = (uint64_t)nb[0] * nb[1] * nb[2];
     if (nbricks >= (1ull << 31)) throw Error(-4, "sparse path: brick grid too large");
@@ -1062,7 +1205,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
       if constexpr (DIM == 3) {
         auto kern = sp_core_brick_kernel<W>;
         DB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, bc, nb[1], nb[2], a.counters + 1);
+        kern<<<(unsigned)nbricks, BRK_THREADS, smem, c.st>>>(a, bc, dtab, nb[1], nb[2], a.counters + 1);
         c.launched();
         sp_core_kernel<DIM, D, W, 2><<<grid_for(n, 256, 1 << 30), 256, 0, c.st>>>(a, a.counters + 1);
         c.launched();

@@ -266,6 +266,38 @@ def test_brick_markcore_vs_o2(oracle_lib, grouping):
         assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"brick eps={eps}")
 
 
+def test_brick_subcell_edges_vs_o2(oracle_lib):
+    """The brick MarkCore's sub-cell stencils (DESIGN.md §5, 4 sub-intervals
+    per axis of a cell): points snapped to the sub-interval edges of their
+    cells (offsets 0, t_j - 1, t_j, s - 1 from the cell origin lo + c s) and
+    pairs at exactly eps ((300, 400, 0) and (0, 0, 500) apart for eps = 500),
+    where a stencil one cell or one sub-interval too small would miss a
+    neighbour: same result as O2 and as the thread kernel."""
+    eps, mp = 500, 4
+    pts = datagen.uniform(150_000, 3, 25_000, 41)
+    probe = gpu(pts, eps, mp)
+    assert probe.stats["brick"] == 1, probe.stats
+    s = int(probe.stats["cell_side"])
+    lo = pts.min(axis=0).astype(np.int64)
+    edges = np.array(sorted({0, s - 1} | {j * s // 4 for j in (1, 2, 3)} | {j * s // 4 - 1 for j in (1, 2, 3)}))
+    rng = np.random.default_rng(42)
+    k = 60_000
+    rel = pts[:k].astype(np.int64) - lo
+    snapped = (rel // s) * s + edges[rng.integers(0, len(edges), size=rel.shape)]
+    pts[:k] = (snapped + lo).astype(pts.dtype)
+    # exact-eps partners for 20,000 of the snapped points
+    off = np.array([[300, 400, 0], [0, 0, 500], [-400, 0, 300], [0, -300, -400]], dtype=np.int64)
+    m = 20_000
+    pts[k:k + m] = (pts[:m].astype(np.int64) + off[rng.integers(0, 4, size=m)]).astype(pts.dtype)
+    pts[:, :] = np.maximum(pts, lo)   # (keep the bounding box's origin)
+    pts[k + m] = lo
+    r = gpu(pts, eps, mp)
+    assert r.stats["brick"] == 1, r.stats
+    t = gpu(pts, eps, mp, pkg.F_NO_BRICK)
+    assert_same(np_result(r), np_result(t), "brick vs thread at sub-cell edges")
+    assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), "brick at sub-cell edges")
+
+
 def test_point_centric_border_vs_o2(oracle_lib):
     """Sparse lattice where almost every point is core: ClusterBorder runs from
     the few non-core points (domain-boundary points here) instead of from the
