@@ -70,6 +70,9 @@ extern "C" {
                                       candidate-capacity rows fits (testing)                  */
 #define DBSCAN_F_NO_BRICK    8192u /* sparse path, d = 3: MarkCore with a thread per point
                                       instead of the shared-memory brick kernel (testing)    */
+#define DBSCAN_F_NO_PACKED_CORE 131072u /* sparse path: ClusterCore's one-pass pair search on the
+                                      per-cell tables instead of the packed core points
+                                      (testing)                                               */
 
 /* ---- stage timers (indices into stage_ms) -------------------------------- */
 #define DBSCAN_STAGE_BBOX      0  /* a1: bounding box                                  */

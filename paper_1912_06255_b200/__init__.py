@@ -43,6 +43,7 @@ F_FORCE_STENCIL, F_FORCE_TREE, F_FORCE_WIDE, F_NO_WAVES = 8, 16, 32, 64
 F_NO_SPARSE, F_FORCE_SPARSE, F_RADIX_GROUP, F_LATTICE_GROUP, F_COUNT_WORK = 128, 256, 512, 1024, 2048
 F_QUADTREE, F_NO_BRICK, F_NO_QBOUND, F_FORCE_QBOUND = 4096, 8192, 16384, 32768
 F_NBR_TWO_PASS = 65536
+F_NO_PACKED_CORE = 131072
 NSTAGES, NSTATS = 12, 32
 STAGES = ["bbox", "keys+sort", "sort", "segment", "hash", "neighbors", "markcore", "compact",
           "cluster", "labels", "border", "total"]

@@ -126,6 +126,10 @@ struct SpArgs {
   uint32_t* ovf_list;        // sorted positions of overflowed sets (count in ovf_count)
   uint32_t* ovf_count;
   unsigned long long* nborder;
+  const uint32_t* cpre;      // [ncore + 1] core points before each core cell (core_list order)
+  const uint64_t* clin;      // [ncore] padded linear lattice index of each core cell
+  const int4* cpts;          // core points in core_list order: {x, y, z (0 in 2D), cell id}
+  uint64_t ncpts;            // core points
   int64_t n;
 };
 
@@ -689,6 +693,125 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
   block_add_u64(mine, tested);
 }
 
+// Core points packed in core_list order (cells with core points in linear
+// order): the core points of the core cells found by one probe of the core
+// directory (ranks id0 .. id0 + nc) are one contiguous range of cpts, so a
+// pair search reads no per-cell tables for the cells it finds.
+template <int DIM>
+__global__ void sp_core_count_kernel(SpArgs a, uint32_t* __restrict__ ccnt, uint64_t* __restrict__ clin) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < a.ncore; r += gridDim.x * blockDim.x) {
+    const uint32_t g = a.core_list[r];
+    ccnt[r] = a.core_cnt[g];
+    clin[r] = cell_lin<DIM>(a.cell_key[g], a);
+  }
+}
+
+template <int D>
+__global__ void sp_core_pack_kernel(SpArgs a, int4* __restrict__ cpts) {
+  // a warp per 32 core cells, lanes over their core points
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < a.ncore; r0 += nwarps * 32) {
+    const uint32_t r1 = min(r0 + 32, a.ncore);
+    const uint32_t q0 = a.cpre[r0], q1 = a.cpre[r1];
+    for (uint32_t q = q0 + lane; q < q1; q += 32) {
+      // its cell: the last rank in r0 .. r1 whose start is <= q
+      uint32_t r = r0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1)
+        if (r + step < r1 && a.cpre[r + step] <= q) r += step;
+      const uint32_t h = a.core_list[r];
+      int32_t p[D];
+      load_pt<D>(a.Ps, a.cell_start[h] + (q - a.cpre[r]), p);
+      cpts[q] = make_int4(p[0], p[1], D > 2 ? p[2] : 0, (int32_t)h);
+    }
+  }
+}
+
+// ClusterCore on the packed core points (one pass over the back columns, no
+// Find filter; Alg 3): the lanes of a warp take (core cell g,
+// back column) items; a probe of the core directory gives the core cells of
+// the column run and, through cpre, their core points as one range; each is
+// tested against g's core points and a hit links g with the point's cell
+// (pairs are seen once, from the higher id, as in sp_pairs_kernel). Pairs
+// with more than SP_SMALL point pairs go to the warp BCP as before.
+template <int DIM, int D, bool WIDE>
+__global__ void __launch_bounds__(256) sp_pairs_cp_kernel(SpArgs a, unsigned long long* tested) {
+  __shared__ long long s_off[SP_MAX_COLS];
+  __shared__ uint32_t s_mask[SP_MAX_COLS];
+  const int nb = a.nbcols;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    s_off[i] = a.bcoff[i];
+    s_mask[i] = a.bcmask[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t mine = 0;
+  for (uint32_t r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < a.ncore; r0 += nwarps * 32) {
+    const uint32_t k = min(32u, a.ncore - r0);
+    const uint32_t items = k * (uint32_t)nb;
+    for (uint32_t it0 = 0; it0 < items; it0 += 32) {
+      __syncwarp();
+      const uint32_t it = it0 + lane;
+      if (it >= items) continue;
+      const uint32_t ci = it / nb, col = it - ci * nb;
+      const uint32_t r = r0 + ci;
+      uint32_t id0;
+      const uint32_t nc = dir_probe(a.cdir, a.clin[r] + (uint64_t)s_off[col], s_mask[col], &id0);
+      if (!nc) continue;
+      const uint32_t g = a.core_list[r];
+      const uint32_t pb = a.cpre[r], pe = a.cpre[r + 1];
+      const uint32_t qb = a.cpre[id0], qe = a.cpre[id0 + nc];
+      if ((uint64_t)(pe - pb) * (qe - qb) <= SP_SMALL) {
+        uint32_t last = MISS;  // (the cell linked last: its other points need no test)
+        for (uint32_t q = qb; q < qe; ++q) {
+          const int4 qv = __ldg(a.cpts + q);
+          if ((uint32_t)qv.w == last) continue;
+          const int32_t qq[4] = {qv.x, qv.y, qv.z, 0};
+          ++mine;
+          for (uint32_t u = pb; u < pe; ++u) {
+            const int4 pv = __ldg(a.cpts + u);
+            const int32_t pp[4] = {pv.x, pv.y, pv.z, 0};
+            DB_WORK(1);
+            if (within_dim<DIM, 4, WIDE>(pp, qq, a.g)) {
+              uf_link(a.parent, g, (uint32_t)qv.w);
+              last = (uint32_t)qv.w;
+              break;
+            }
+          }
+        }
+        continue;
+      }
+      // larger: per found cell, as sp_pairs_kernel (big pairs to the warp BCP)
+      const uint32_t kg = pe - pb;
+      for (uint32_t rr = id0; rr < id0 + nc; ++rr) {
+        const uint32_t h = a.core_list[rr];
+        const uint32_t hb = a.cpre[rr], he = a.cpre[rr + 1];
+        if ((uint64_t)kg * (he - hb) > SP_SMALL) {
+          if (uf_find(a.parent, g) == uf_find(a.parent, h)) continue;
+          const uint32_t slot = atomicAdd(a.counters + 2, 1u);
+          if (slot < a.large_cap) { a.large[slot] = make_uint2(g, h); continue; }
+        }
+        ++mine;
+        bool hit = false;
+        for (uint32_t u = pb; u < pe && !hit; ++u) {
+          const int4 pv = __ldg(a.cpts + u);
+          const int32_t pp[4] = {pv.x, pv.y, pv.z, 0};
+          for (uint32_t v = hb; v < he; ++v) {
+            const int4 qv = __ldg(a.cpts + v);
+            const int32_t qq[4] = {qv.x, qv.y, qv.z, 0};
+            DB_WORK(1);
+            if (within_dim<DIM, 4, WIDE>(pp, qq, a.g)) { hit = true; break; }
+          }
+        }
+        if (hit) uf_link(a.parent, g, h);
+      }
+    }
+  }
+  block_add_u64(mine, tested);
+}
+
 // --------------------------------------------------------- ClusterBorder (a10)
 // Does core cell h hold a core point within eps of p? Core points are first in
 // their cell (a7), so they are Ps[cell_start[h] .. + core_cnt[h]).
@@ -1237,6 +1360,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.ncore = hc[4];
   if (o->brick && hc[1]) o->brick = 2;
   const uint64_t core_pts = hc[5];
+  a.ncpts = core_pts;
   // ClusterBorder from the side with less work: the non-core points when they
   // are fewer than the core cells (almost every point core), else the cells
   o->point_border = (uint64_t)n - core_pts < (uint64_t)a.ncore;
@@ -1264,6 +1388,26 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
       // cells (c5: 8%) the second probe pass costs more than it prunes)
       // (with two: gap 0, then gap 1, then the rest, flattening in between)
       const bool two = 2ull * a.ncore >= cv.ncells;
+      if (!two && !g.at && !(o->flags & DBSCAN_F_NO_PACKED_CORE)) {
+        // one pass on the packed core points
+        uint32_t* ccnt = c.alloc<uint32_t>(a.ncore);
+        uint32_t* cpre = c.alloc<uint32_t>((size_t)a.ncore + 1);
+        uint64_t* clin = c.alloc<uint64_t>(a.ncore);
+        int4* cpts = c.alloc<int4>(std::max<uint64_t>(a.ncpts, 1));
+        sp_core_count_kernel<DIM><<<grid_for(a.ncore, 256, c.sms * 8), 256, 0, c.st>>>(a, ccnt, clin);
+        a.clin = clin;
+        c.launched();
+        exclusive_scan_u32_u32(c, ccnt, cpre, a.ncore);
+        a.cpre = cpre;
+        a.cpts = cpts;
+        sp_core_pack_kernel<D><<<grid_for(((int64_t)a.ncore + 31) / 32 * 32, 256, c.sms * 16), 256, 0, c.st>>>(a, cpts);
+        c.launched();
+        sp_pairs_cp_kernel<DIM, D, W><<<grid_for(((int64_t)a.ncore + 31) / 32 * 32, 256, c.sms * 16), 256, 0,
+                                        c.st>>>(a, tested);
+        c.launched();
+        o->passes = 1;
+        return;
+      }
       const int cut[4] = {0, two ? a.nbnear : a.nbcols, two ? a.nbmid : a.nbcols, a.nbcols};
       for (int pass = 0; pass < 3; ++pass) {
         const int lo = cut[pass], hi = cut[pass + 1];

@@ -298,6 +298,24 @@ def test_brick_subcell_edges_vs_o2(oracle_lib):
     assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), "brick at sub-cell edges")
 
 
+@pytest.mark.parametrize("mp", [10, 14])
+def test_packed_core_pairs_vs_o2(oracle_lib, mp):
+    """Sparse ClusterCore in one pass on the packed core points (core cells
+    few relative to all cells): a c5-like lattice plus two dense blobs whose
+    core cells hold many core points (pairs above SP_SMALL go to the warp
+    BCP); equal to the pass on the per-cell tables (F_NO_PACKED_CORE) and
+    to O2."""
+    eps = 500
+    pts = datagen.uniform(400_000, 3, 35_000, 60 + mp)
+    pts[:3000] = pts[0] + datagen.uniform(3000, 3, 900, 61)
+    pts[3000:5000] = pts[1] + datagen.uniform(2000, 3, 1500, 62)
+    r = gpu(pts, eps, mp)
+    assert r.stats["sparse"] == 1 and r.stats["sparse_passes"] == 1, r.stats
+    t = gpu(pts, eps, mp, pkg.F_NO_PACKED_CORE)
+    assert_same(np_result(r), np_result(t), f"packed vs tables mp={mp}")
+    assert_same(np_result(r), oracle_lib.o2(pts, eps, mp), f"packed mp={mp}")
+
+
 def test_point_centric_border_vs_o2(oracle_lib):
     """Sparse lattice where almost every point is core: ClusterBorder runs from
     the few non-core points (domain-boundary points here) instead of from the
