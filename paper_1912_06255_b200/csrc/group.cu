@@ -427,75 +427,97 @@ __global__ void __launch_bounds__(LAT_THREADS) lat_words_kernel(const uint32_t* 
   if (threadIdx.x == 0 && s_m) atomicMax(mx, s_m);
 }
 
-// pass 2b: cells in linear order: cell_start, cell_key, and the directory
-// entry {bits w, bits w+1, cells before w, 0} of the sparse path. The 32
-// counters of a word stay in registers; byte prefix sums by shifts; lattice
-// coordinates by multiply-high (exact for lin < 2^32, else 64-bit division).
-__global__ void __launch_bounds__(LAT_THREADS) lat_cells_kernel(const uint32_t* __restrict__ cnt8, LatArgs L,
-                                                                const uint32_t* __restrict__ bm,
-                                                                const uint32_t* __restrict__ cpre,
-                                                                const uint32_t* __restrict__ ppre,
-                                                                uint32_t* __restrict__ cell_start,
-                                                                uint64_t* __restrict__ cell_key,
-                                                                uint4* __restrict__ dir) {
-  const uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (w >= L.words) return;
-  const uint32_t bits = bm[w];
-  dir[w] = make_uint4(bits, w + 1 < L.words ? bm[w + 1] : 0u, cpre[w], 0u);
-  if (!bits) return;
-  const uint4 a = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w);
-  const uint4 b = __ldg(reinterpret_cast<const uint4*>(cnt8) + 2 * w + 1);
-  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  // excl[q]: points in counters 0 .. 4q-1 of the word; inside a u32 the byte
-  // prefix sums come from x * 0x01010101 (<= 4 * 255 would overflow a byte, so
-  // sum in 16-bit halves instead)
-  uint32_t excl[8];
-  uint32_t run = 0;
+// pass 2b, a thread per 4 counters (one u32 of cnt8; 8 threads per 32-cell
+// word): the cells of its counters in linear order — cell_start, cell_key,
+// and cell_of for their points — at the rank and position given by the
+// word's prefixes plus an 8-lane exclusive scan; lane 0 of a word writes its
+// directory entry {bits w, bits w+1, cells before w, 0}. (A thread per word
+// looping over its cells ran at ~17 active lanes.)
+__device__ __forceinline__ uint64_t lat_key(uint64_t lin, const LatArgs& L) {
+  uint64_t key = 0;
+  if (L.small) {
+    uint32_t rem = (uint32_t)lin;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    excl[q] = run;
-    run += (v[q] & 255u) + ((v[q] >> 8) & 255u) + ((v[q] >> 16) & 255u) + (v[q] >> 24);
-  }
-  uint32_t r = cpre[w];
-  const uint32_t p = ppre[w];
-  for (uint32_t bb = bits; bb; bb &= bb - 1) {
-    const int k = __ffs(bb) - 1;
-    const int q = k >> 2, sub = k & 3;
-    uint32_t before = excl[0];
-#pragma unroll
-    for (int qq = 1; qq < 8; ++qq)
-      if (qq == q) before = excl[qq];
-    uint32_t vq = v[0];
-#pragma unroll
-    for (int qq = 1; qq < 8; ++qq)
-      if (qq == q) vq = v[qq];
-    for (int s = 0; s < sub; ++s) before += (vq >> (8 * s)) & 255u;
-    const uint64_t lin = 32 * w + (uint64_t)k;
-    uint64_t key = 0;
-    if (L.small) {
-      uint32_t rem = (uint32_t)lin;
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        if (ax < L.g.d) {
-          const uint32_t ca = L.smagic[ax] ? (uint32_t)__umul64hi((uint64_t)rem, L.smagic[ax]) : rem;
-          rem -= ca * (uint32_t)L.stride[ax];
-          key |= (uint64_t)(ca - L.g.R) << L.g.shift[ax];
-        }
+    for (int ax = 0; ax < 3; ++ax) {
+      if (ax < L.g.d) {
+        const uint32_t ca = L.smagic[ax] ? (uint32_t)__umul64hi((uint64_t)rem, L.smagic[ax]) : rem;
+        rem -= ca * (uint32_t)L.stride[ax];
+        key |= (uint64_t)(ca - L.g.R) << L.g.shift[ax];
       }
-    } else {
-      uint64_t rem = lin;
+    }
+  } else {
+    uint64_t rem = lin;
 #pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        if (ax < L.g.d) {
-          const uint64_t ca = rem / L.stride[ax];
-          rem -= ca * L.stride[ax];
-          key |= (ca - L.g.R) << L.g.shift[ax];
+    for (int ax = 0; ax < 3; ++ax) {
+      if (ax < L.g.d) {
+        const uint64_t ca = rem / L.stride[ax];
+        rem -= ca * L.stride[ax];
+        key |= (ca - L.g.R) << L.g.shift[ax];
+      }
+    }
+  }
+  return key;
+}
+
+__global__ void __launch_bounds__(LAT_THREADS) lat_cells4_kernel(const uint32_t* __restrict__ cnt8, LatArgs L,
+                                                                 const uint32_t* __restrict__ bm,
+                                                                 const uint32_t* __restrict__ cpre,
+                                                                 const uint32_t* __restrict__ ppre,
+                                                                 uint32_t* __restrict__ cell_start,
+                                                                 uint64_t* __restrict__ cell_key,
+                                                                 uint4* __restrict__ dir,
+                                                                 uint32_t* __restrict__ cell_of) {
+  // the warp's (<= 128) cells, compacted: {offset in the warp's 128 lattice
+  // cells | points << 8, rank, first position}
+  __shared__ uint3 s_cell[LAT_THREADS / 32][128];
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t w = t >> 3;
+  const uint32_t q = (uint32_t)t & 7u;
+  const bool valid = w < L.words;
+  const uint32_t v = valid ? __ldg(cnt8 + t) : 0u;
+  const uint32_t bw = valid ? __ldg(bm + w) : 0u;
+  const uint32_t nib = (bw >> (4 * q)) & 15u;
+  const uint32_t cx = __popc(nib);
+  const uint32_t px = (v & 255u) + ((v >> 8) & 255u) + ((v >> 16) & 255u) + (v >> 24);
+  // exclusive scans over the 8 lanes of the word (ranks, positions) and over
+  // the warp (compacted slot)
+  uint32_t ci = cx, pi = px, mi = cx;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t m2 = __shfl_up_sync(DB_FULL, mi, d);
+    if (lane >= (uint32_t)d) mi += m2;
+    if (d < 8) {
+      const uint32_t c2 = __shfl_up_sync(DB_FULL, ci, d, 8), p2 = __shfl_up_sync(DB_FULL, pi, d, 8);
+      if (q >= (uint32_t)d) { ci += c2; pi += p2; }
+    }
+  }
+  const uint32_t M = __shfl_sync(DB_FULL, mi, 31);
+  uint3* sc = s_cell[threadIdx.x >> 5];
+  if (valid) {
+    if (q == 0) dir[w] = make_uint4(bw, w + 1 < L.words ? __ldg(bm + w + 1) : 0u, __ldg(cpre + w), 0u);
+    if (nib) {
+      uint32_t m = mi - cx, r = __ldg(cpre + w) + ci - cx, p = __ldg(ppre + w) + pi - px;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c = (v >> (8 * k)) & 255u;
+        if (c) {
+          sc[m] = make_uint3((lane * 4 + k) | (c << 8), r, p);
+          ++m;
+          ++r;
+          p += c;
         }
       }
     }
-    cell_start[r] = p + before;
-    cell_key[r] = key;
-    ++r;
+  }
+  __syncwarp();
+  const uint64_t lin0 = 4 * (t - lane);
+  for (uint32_t m = lane; m < M; m += 32) {
+    const uint3 e = sc[m];
+    const uint32_t c = e.x >> 8;
+    cell_start[e.y] = e.z;
+    cell_key[e.y] = lat_key(lin0 + (e.x & 255u), L);
+    for (uint32_t s = 0; s < c; ++s) cell_of[e.z + s] = e.y;
   }
 }
 
@@ -656,17 +678,6 @@ __global__ void __launch_bounds__(PL_THREADS) lat_place_kernel(uint32_t n, const
   idx[pos] = i;
 }
 
-// cell_of from the cell ranges: a thread per cell writes its positions, so
-// consecutive threads write consecutive words (in 3b they would be a fourth
-// scattered partial-sector stream)
-__global__ void lat_cell_of_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
-                                   uint32_t* __restrict__ cell_of) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < ncells; r += gridDim.x * blockDim.x) {
-    const uint32_t e = cell_start[r + 1];
-    for (uint32_t p = cell_start[r]; p < e; ++p) cell_of[p] = r;
-  }
-}
-
 bool lattice_applicable(const Geo& g, int64_t n) {
   if (g.d > 3 || n == 0 || n > LAT_MAX_N) return false;
   unsigned __int128 vol = 1;
@@ -727,7 +738,8 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
   exclusive_scan_u32_u32(c, wcells, cpre, (int64_t)L.words);
   exclusive_scan_u32_u32(c, wpts, ppre, (int64_t)L.words);
   uint4* dir = c.alloc<uint4>(L.words);
-  lat_cells_kernel<<<wgrid, LAT_THREADS, 0, c.st>>>(cnt8, L, bm, cpre, ppre, cell_start, cell_key, dir);
+  lat_cells4_kernel<<<grid_for((int64_t)L.words * 8, LAT_THREADS, 1 << 30), LAT_THREADS, 0, c.st>>>(
+      cnt8, L, bm, cpre, ppre, cell_start, cell_key, dir, cell_of);
   c.launched();
   const uint32_t ncells = c.read(cpre + L.words);
   DB_CUDA(cudaMemcpyAsync(cell_start + ncells, ppre + L.words, sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.st));
@@ -756,8 +768,6 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
     c.launched();
     lat_place_kernel<D><<<nchunks, PL_THREADS, 0, c.st>>>((uint32_t)n, rec, reci, dir, cell_start, ppre, ws,
                                                           L.words, nbk, chunk_bucket, Ps, idx, cell_of);
-    c.launched();
-    lat_cell_of_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cell_start, ncells, cell_of);
     c.launched();
   });
   *dir_out = dir;
