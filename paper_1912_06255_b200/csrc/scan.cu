@@ -32,14 +32,18 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
   const int64_t tile = s_tile;
   const int64_t j0 = tile * SC_TILE + (int64_t)threadIdx.x * SC_ITEMS;
   if (zero_if && *zero_if == 0) {
-    if (j0 + SC_ITEMS <= n && (reinterpret_cast<uintptr_t>(out + j0) & 15) == 0) {
+    // the tile's outputs as 16-byte stores, consecutive threads on
+    // consecutive 16 bytes (each warp store covers 512 contiguous bytes)
+    const int64_t t0 = tile * SC_TILE;
+    constexpr int PER16 = 16 / sizeof(TOut);
+    if (t0 + SC_TILE <= n && (reinterpret_cast<uintptr_t>(out + t0) & 15) == 0) {
+      uint4* o4 = reinterpret_cast<uint4*>(out + t0);
 #pragma unroll
-      for (int q = 0; q < SC_ITEMS * (int)sizeof(TOut) / 16; ++q) reinterpret_cast<uint4*>(out + j0)[q] = make_uint4(0, 0, 0, 0);
+      for (int q = 0; q < SC_TILE / PER16 / SC_THREADS; ++q) o4[q * SC_THREADS + threadIdx.x] = make_uint4(0, 0, 0, 0);
     } else {
-      for (int i = 0; i < SC_ITEMS; ++i)
-        if (j0 + i < n) out[j0 + i] = 0;
+      for (int64_t j = t0 + threadIdx.x; j < min(n, t0 + SC_TILE); j += SC_THREADS) out[j] = 0;
     }
-    if (j0 < n && j0 + SC_ITEMS >= n) out[n] = 0;
+    if (t0 + SC_TILE >= n && threadIdx.x == 0) out[n] = 0;
     return;
   }
   uint32_t v[SC_ITEMS];
@@ -80,19 +84,28 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const uint32_t* __rest
 #pragma unroll
   for (int i = 0; i < SC_ITEMS; ++i) { o[i] = (TOut)run; run += v[i]; }
   constexpr int PER16 = 16 / sizeof(TOut);  // outputs per 16-byte store
-  const bool ofull = j0 + SC_ITEMS <= n && (reinterpret_cast<uintptr_t>(out + j0) & 15) == 0;
-  if (ofull) {
+  const int64_t t0 = tile * SC_TILE;
+  const bool tfull = t0 + SC_TILE <= n && (reinterpret_cast<uintptr_t>(out + t0) & 15) == 0;
+  if (tfull) {
+    // through shared memory, a warp's store instruction then covers 512
+    // contiguous bytes (straight from registers, lanes were 64-128 B apart)
+    __shared__ uint4 s_out[SC_THREADS / 32][32 * SC_ITEMS / PER16];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < SC_ITEMS / PER16; ++q) {
-      uint4 w;
+      uint4 x;
       if constexpr (PER16 == 4) {
-        w = make_uint4((uint32_t)o[4 * q], (uint32_t)o[4 * q + 1], (uint32_t)o[4 * q + 2], (uint32_t)o[4 * q + 3]);
+        x = make_uint4((uint32_t)o[4 * q], (uint32_t)o[4 * q + 1], (uint32_t)o[4 * q + 2], (uint32_t)o[4 * q + 3]);
       } else {
         const uint64_t a = (uint64_t)o[2 * q], b = (uint64_t)o[2 * q + 1];
-        w = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+        x = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
       }
-      reinterpret_cast<uint4*>(out + j0)[q] = w;
+      s_out[w][lane * (SC_ITEMS / PER16) + q] = x;
     }
+    __syncwarp();
+    uint4* o4 = reinterpret_cast<uint4*>(out + t0) + (int64_t)w * (32 * SC_ITEMS / PER16);
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS / PER16; ++q) o4[q * 32 + lane] = s_out[w][q * 32 + lane];
   } else {
 #pragma unroll
     for (int i = 0; i < SC_ITEMS; ++i)
