@@ -503,7 +503,7 @@ def main():
                          "ms_per_launch": top["ms"], "ms_share": top["ms_share"],
                          "algorithmic_per_launch": top["algorithmic"], "peak_kind": top["peak_kind"],
                          "traffic_note": "DRAM bytes (read + write) of the stage's kernels per call, ncu --set full "
-                                         "(cold L2), profiles/r2_traffic.json"})
+                                         "(cold L2), profiles/r2_traffic.json (current build; r2a_traffic.json: the earlier round-2 build)"})
     peaks_out = {f"d{d}_{'i64' if v else 'u32'}": round(p / 1e12, 4) for (d, v), p in peaks_u1.items()}
 
     # ---- e2e through the C ABI with pinned host buffers
