@@ -334,17 +334,21 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
     *slot = p;
     return p;
   };
-  if (!caller_out) {
+  // (for n > 0 allocated right after the bounding-box launch, so the GPU
+  // starts while the host allocates)
+  auto alloc_outputs = [&]() {
+    if (caller_out) return;
     out->core = (uint8_t*)out_alloc((size_t)n, &priv->core);
     out->cluster = (int32_t*)out_alloc(sizeof(int32_t) * (size_t)n, &priv->cluster);
     out->border_off = (int64_t*)out_alloc(sizeof(int64_t) * (size_t)(n + 1), &priv->border_off);
-  }
+  };
   // border_ids: the caller's buffer (F_CALLER_OUT with capacity) when it fits
   auto ids_alloc = [&](int64_t nnz) -> int32_t* {
     if (caller_out && uids && nnz <= ucap) return uids;
     return (int32_t*)out_alloc(sizeof(int32_t) * (size_t)nnz, &priv->border_ids);
   };
   if (n == 0) {
+    alloc_outputs();
     out->border_ids = ids_alloc(0);
     if (dev_io) DB_CUDA(cudaMemsetAsync(out->border_off, 0, sizeof(int64_t), st));
     else out->border_off[0] = 0;
@@ -413,6 +417,7 @@ static int run(const int32_t* pts, int64_t n, int32_t d, int64_t eps, int64_t mi
   }
   int32_t* lohi_d = c.alloc<int32_t>(17);
   bbox(c, dpts, n, d, g.s, lohi_d);
+  alloc_outputs();
   int32_t lohi[17];
   const int32_t* lohi_h = c.fetch(lohi_d, 17);
   c.sync();
