@@ -425,16 +425,38 @@ __global__ void __launch_bounds__(256) core_count_kernel(CellsView cv, const uin
   __shared__ uint32_t s_base;
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   bool is_core_cell = false, is_mixed = false;
+  uint32_t s = 0, e = 0, k = 0;
+  bool big = false;  // more than 64 points below minPts: counted by the whole warp
   if (g < cv.ncells) {
-    const uint32_t s = cv.cell_start[g], e = cv.cell_start[g + 1];
-    uint32_t k;
+    s = cv.cell_start[g];
+    e = cv.cell_start[g + 1];
     if ((int64_t)(e - s) >= min_pts) {
       k = e - s;
+    } else if (e - s > 64) {
+      big = true;
     } else {
-      k = 0;
       for (uint32_t u = s; u < e; ++u) k += core_s[u];
-      is_mixed = k > 0 && k < e - s;
     }
+  }
+  // the block's large cells, spread over its warps (a warp per cell)
+  __shared__ uint32_t s_nbig, s_big[256], s_k[256];
+  if (threadIdx.x == 0) s_nbig = 0;
+  __syncthreads();
+  if (big) s_big[atomicAdd(&s_nbig, 1u)] = threadIdx.x;
+  __syncthreads();
+  for (uint32_t q = threadIdx.x >> 5; q < s_nbig; q += blockDim.x >> 5) {
+    const uint32_t gg = blockIdx.x * blockDim.x + s_big[q];
+    const uint32_t cs = cv.cell_start[gg], ce = cv.cell_start[gg + 1];
+    uint32_t part = 0;
+    for (uint32_t u = cs + (threadIdx.x & 31u); u < ce; u += 32) part += core_s[u];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(DB_FULL, part, o);
+    if ((threadIdx.x & 31u) == 0) s_k[s_big[q]] = part;
+  }
+  __syncthreads();
+  if (big) k = s_k[threadIdx.x];
+  if (g < cv.ncells) {
+    if ((int64_t)(e - s) < min_pts) is_mixed = k > 0 && k < e - s;
     core_cnt[g] = k;
     is_core_cell = k > 0;
   }
@@ -447,20 +469,37 @@ __global__ void __launch_bounds__(256) core_count_kernel(CellsView cv, const uin
   if (is_mixed) mixed[s_base + ex] = g;
 }
 
-// Stable partition of one mixed cell: core points first, each group in its
-// original (input-index) order. Thread per mixed cell via a scratch copy.
+// Stable partition of the mixed cells: core points first, each group in its
+// original (input-index) order. A warp takes 32 mixed cells: a cell of <= 8
+// points is partitioned by its lane in registers (sparse lattices); the
+// larger ones by the whole warp, one after the other — 32 points per step
+// to their places in a scratch copy (ballot ranks: the core ones from the
+// cell start, the others after its core_cnt core points), then copied back
+// coalesced. (A thread per large cell made SS-simden 3D at minPts 3e4 spend
+// 11.5 ms here: cells of tens of thousands of points done serially.)
 template <int D>
 __global__ void partition_kernel(CellsView cv, const uint32_t* __restrict__ mixed,
-                                 const uint32_t* __restrict__ nmixed, int32_t* __restrict__ Ps,
-                                 uint32_t* __restrict__ idx, uint8_t* __restrict__ core_s,
-                                 int32_t* __restrict__ scratchP, uint32_t* __restrict__ scratchI,
-                                 uint32_t* __restrict__ inv) {
+                                 const uint32_t* __restrict__ nmixed, const uint32_t* __restrict__ core_cnt,
+                                 int32_t* __restrict__ Ps, uint32_t* __restrict__ idx,
+                                 uint8_t* __restrict__ core_s, int32_t* __restrict__ scratchP,
+                                 uint32_t* __restrict__ scratchI, uint32_t* __restrict__ inv) {
   const uint32_t m = *nmixed;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
-    const uint32_t g = mixed[t];
-    const uint32_t s = cv.cell_start[g], e = cv.cell_start[g + 1];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  // the small cells (<= 8 points, D <= 4), a lane per cell over chunks of 32
+  if constexpr (D <= 4)
+  for (uint32_t t0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; t0 < m; t0 += nwarps * 32) {
+    const uint32_t t = t0 + lane;
+    uint32_t g = 0, s = 0, e = 0;
+    if (t < m) {
+      g = mixed[t];
+      s = cv.cell_start[g];
+      e = cv.cell_start[g + 1];
+    }
     if constexpr (D <= 4) {
-      if (e - s <= 8) {  // small cell (sparse lattices): in registers, no scratch round trip
+      const bool big = t < m && e - s > 8;
+      if (t < m && !big) {  // small cell: in registers, no scratch round trip
         constexpr int SM = 8;
         int32_t P[SM][D];
         uint32_t I[SM];
@@ -486,24 +525,48 @@ __global__ void partition_kernel(CellsView cv, const uint32_t* __restrict__ mixe
               if (inv) inv[I[q]] = w;
               ++w;
             }
-        continue;
       }
     }
-    for (uint32_t u = s; u < e; ++u) {
-      for (int k = 0; k < D; ++k) scratchP[(size_t)u * D + k] = Ps[(size_t)u * D + k];
-      scratchI[u] = idx[u] | ((uint32_t)core_s[u] << 31);
-    }
-    uint32_t w = s;
-    for (int pass = 1; pass >= 0; --pass)
-      for (uint32_t u = s; u < e; ++u) {
-        uint32_t v = scratchI[u];
-        if ((v >> 31) != (uint32_t)pass) continue;
-        for (int k = 0; k < D; ++k) Ps[(size_t)w * D + k] = scratchP[(size_t)u * D + k];
-        idx[w] = v & 0x7fffffffu;
-        core_s[w] = (uint8_t)pass;
-        if (inv) inv[v & 0x7fffffffu] = w;
-        ++w;
+  }
+  // the large cells (> 8 points; all of them for D = 8), a warp per cell
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < m; t += nwarps) {
+    {
+      const uint32_t gs = mixed[t];
+      const uint32_t cs = cv.cell_start[gs], ce = cv.cell_start[gs + 1];
+      if (D <= 4 && ce - cs <= 8) continue;  // (warp-uniform)
+      const uint32_t kc = core_cnt[gs];
+      uint32_t nc = 0, nn = 0;  // core / other points placed so far
+      for (uint32_t u0 = cs; u0 < ce; u0 += 32) {
+        const uint32_t u = u0 + lane;
+        const bool valid = u < ce;
+        const uint32_t c = valid ? core_s[u] : 0u;
+        int32_t P[D];
+        uint32_t I = 0;
+        if (valid) {
+          PtLoad<D>::load(Ps, u, P);
+          I = idx[u];
+        }
+        const uint32_t bc = __ballot_sync(DB_FULL, valid && c), bn = __ballot_sync(DB_FULL, valid && !c);
+        if (valid) {
+          const uint32_t pos = c ? cs + nc + __popc(bc & lt) : cs + kc + nn + __popc(bn & lt);
+#pragma unroll
+          for (int k = 0; k < D; ++k) scratchP[(size_t)pos * D + k] = P[k];
+          scratchI[pos] = I | (c << 31);
+        }
+        nc += __popc(bc);
+        nn += __popc(bn);
       }
+      __syncwarp();
+      for (uint32_t u = cs + lane; u < ce; u += 32) {
+        const uint32_t v = scratchI[u];
+#pragma unroll
+        for (int k = 0; k < D; ++k) Ps[(size_t)u * D + k] = scratchP[(size_t)u * D + k];
+        idx[u] = v & 0x7fffffffu;
+        core_s[u] = (uint8_t)(v >> 31);
+        if (inv) inv[v & 0x7fffffffu] = u;
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -514,16 +577,17 @@ void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
   core_count_kernel<<<grid_for(cv.ncells, 256, 1 << 30), 256, 0, c.st>>>(cv, core_s, min_pts,
                                                                           core_cnt, mixed, counters);
   c.launched();
-  partition_mixed(c, g, cv, mixed, counters + 1, Ps, idx, core_s, n);
+  partition_mixed(c, g, cv, mixed, counters + 1, core_cnt, Ps, idx, core_s, n);
 }
 
 void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* mixed,
-                     const uint32_t* nmixed, int32_t* Ps, uint32_t* idx, uint8_t* core_s, int64_t n) {
+                     const uint32_t* nmixed, const uint32_t* core_cnt, int32_t* Ps, uint32_t* idx,
+                     uint8_t* core_s, int64_t n) {
   int32_t* sP = c.alloc<int32_t>((size_t)n * g.D);
   uint32_t* sI = c.alloc<uint32_t>(n);
   auto go = [&](auto Dc) {
     constexpr int D = decltype(Dc)::value;
-    partition_kernel<D><<<c.sms * 16, 256, 0, c.st>>>(cv, mixed, nmixed, Ps, idx, core_s, sP, sI, c.inv);
+    partition_kernel<D><<<c.sms * 16, 256, 0, c.st>>>(cv, mixed, nmixed, core_cnt, Ps, idx, core_s, sP, sI, c.inv);
   };
   if (g.D == 2) go(std::integral_constant<int, 2>());
   else if (g.D == 4) go(std::integral_constant<int, 4>());

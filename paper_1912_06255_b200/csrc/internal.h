@@ -307,7 +307,8 @@ void compact_core(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps, uint32
 
 // stable core-first partition of the listed cells (count on the device)
 void partition_mixed(Ctx& c, const Geo& g, const CellsView& cv, const uint32_t* mixed,
-                     const uint32_t* nmixed, int32_t* Ps, uint32_t* idx, uint8_t* core_s, int64_t n);
+                     const uint32_t* nmixed, const uint32_t* core_cnt, int32_t* Ps, uint32_t* idx,
+                     uint8_t* core_s, int64_t n);
 
 // ---- sparse.cu (cell-centric path for sparse lattices, d <= 3) ----
 constexpr uint64_t SPARSE_MEAN_PER_CELL = 4;  // n / ncells at or below: sparse path

@@ -1348,7 +1348,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.core_tmp = c.alloc<uint32_t>(cv.ncells);
   sp_cells_kernel<<<grid_for(((int64_t)cv.ncells + SC_CELLS - 1) / SC_CELLS, 256, 1 << 30), 256, 0, c.st>>>(a);
   c.launched();
-  partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, Ps, idx, core_s, n);
+  partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, core_cnt, Ps, idx, core_s, n);
   // directory of the cells holding core points, and their list in linear order
   a.cdir = build_dir(c, a, words, a.core_tmp, a.counters + 4);
   uint32_t* core_list = c.alloc<uint32_t>(cv.ncells);
