@@ -567,18 +567,33 @@ __global__ void __launch_bounds__(256) write_points_kernel(uint32_t nc, const ui
                                                            uint32_t* __restrict__ cell_label,
                                                            int32_t* __restrict__ cluster_out, uint32_t* counters) {
   unsigned long long ncore = 0;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += gridDim.x * blockDim.x) {
-    const uint32_t g = cell_at(list, t);
-    const uint32_t k = core_cnt[g];
-    if (!k) {
-      cell_label[g] = 0xffffffffu;
-      continue;
+  const uint32_t lane = threadIdx.x & 31u;
+  // (warp-uniform trip count: the cells with more than 32 core points are
+  // written by the whole warp)
+  for (uint32_t t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; t0 < nc; t0 += gridDim.x * blockDim.x) {
+    const uint32_t t = t0 + lane;
+    uint32_t k = 0, s = 0;
+    int32_t lab = -1;
+    if (t < nc) {
+      const uint32_t g = cell_at(list, t);
+      k = core_cnt[g];
+      if (!k) {
+        cell_label[g] = 0xffffffffu;
+      } else {
+        lab = (int32_t)comp_min[uf_find(parent, g)];
+        cell_label[g] = (uint32_t)lab;
+        s = cell_start[g];
+        if (k <= 32)
+          for (uint32_t u = s; u < s + k; ++u) cluster_out[idx[u]] = lab;
+        ncore += k;
+      }
     }
-    const int32_t lab = (int32_t)comp_min[uf_find(parent, g)];
-    cell_label[g] = (uint32_t)lab;
-    const uint32_t s = cell_start[g];
-    for (uint32_t u = s; u < s + k; ++u) cluster_out[idx[u]] = lab;
-    ncore += k;
+    for (uint32_t bm = __ballot_sync(DB_FULL, k > 32); bm; bm &= bm - 1) {
+      const int src = __ffs(bm) - 1;
+      const uint32_t bs = __shfl_sync(DB_FULL, s, src), bk = __shfl_sync(DB_FULL, k, src);
+      const int32_t bl = __shfl_sync(DB_FULL, lab, src);
+      for (uint32_t u = bs + lane; u < bs + bk; u += 32) cluster_out[idx[u]] = bl;
+    }
   }
   __shared__ unsigned long long s_part[32];
 #pragma unroll
