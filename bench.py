@@ -105,7 +105,8 @@ def measure_peaks(pkg, dims, wide_dims):
     """U1 peak_dist per (d, path): max over register tiles qt = 1, 2, 4."""
     out = {}
     for d in sorted(dims):
-        for v in ([0] + ([1] if d in wide_dims else [])):
+        # (variant 3: the brick MarkCore's predicate on packed rows, d = 3)
+        for v in ([0] + ([1] if d in wide_dims else []) + ([3] if d == 3 else [])):
             best = max(pkg.peak_dist(d, v, qt, reps=60)["tests_per_s"] for qt in (1, 2, 4))
             out[(d, v)] = best
     return out
@@ -472,7 +473,10 @@ def main():
                 e.update({"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                           "algorithmic": amount, "peak_kind": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"})
             else:
-                pk = peaks_u1.get((cfg.d, 1 if st["wide"] else 0))
+                # the predicate the stage's kernel ran: the brick MarkCore's
+                # packed-row test, else the shipped uint32 / 64-bit one
+                brick = row == "a6 MarkCore" and st.get("brick", 0) >= 1
+                pk = peaks_u1.get((cfg.d, 3)) if brick else peaks_u1.get((cfg.d, 1 if st["wide"] else 0))
                 if not amount or not pk:
                     e["frac"] = None
                     rooflines.append(e)
@@ -483,7 +487,8 @@ def main():
                     e.update({"executed_tests": ex, "executed_frac": ex / (e["ms"] / 1e3) / pk})
                 e.update({"achieved": ach / 1e12, "peak": pk / 1e12, "unit": "T distance tests/s",
                           "frac": ach / pk, "algorithmic": amount,
-                          "peak_kind": f"U1 peak_dist measured live (d={cfg.d}, {'64-bit' if st['wide'] else 'uint32'} predicate)"})
+                          "peak_kind": f"U1 peak_dist measured live (d={cfg.d}, "
+                                       f"{'brick packed-row' if brick else ('64-bit' if st['wide'] else 'uint32')} predicate)"})
             e["traffic"] = traffic.get(name, {}).get(row)
             rooflines.append(e)
     # the headline: the stage with the largest share of the step (a single
@@ -504,7 +509,7 @@ def main():
                          "algorithmic_per_launch": top["algorithmic"], "peak_kind": top["peak_kind"],
                          "traffic_note": "DRAM bytes (read + write) of the stage's kernels per call, ncu --set full "
                                          "(cold L2), profiles/r2_traffic.json (current build; r2a_traffic.json: the earlier round-2 build)"})
-    peaks_out = {f"d{d}_{'i64' if v else 'u32'}": round(p / 1e12, 4) for (d, v), p in peaks_u1.items()}
+    peaks_out = {f"d{d}_{ {0: 'u32', 1: 'i64', 3: 'brick'}[v] }": round(p / 1e12, 4) for (d, v), p in peaks_u1.items()}
 
     # ---- e2e through the C ABI with pinned host buffers
     e2e = None

@@ -219,7 +219,8 @@ const char *dbscan_stage_name(int i);
  * the a6/a8 roofline fractions that bench.py reports. Not part of DBSCAN.
  *   d        dimension 1..8 (candidates stored D-padded as the stage kernels do)
  *   variant  0: the shipped uint32 `__sad` predicate; 1: the shipped 64-bit
- *            clamped predicate; 2: an fp64 FMA predicate (north_star's fp64 pipe)
+ *            clamped predicate; 2: an fp64 FMA predicate (north_star's fp64 pipe);
+ *            3: the brick MarkCore's predicate on 8-byte packed rows (d = 3 only)
  *   qt       queries held in registers per thread (1, 2 or 4) against a
  *            1024-point shared-memory tile of candidates (one tile load per
  *            candidate serves qt tests)

@@ -142,7 +142,8 @@ class _DeviceBuffer:
 def peak_dist(d: int, variant: int = 0, qt: int = 1, reps: int = 200, stream=None) -> dict:
     """U1 microbenchmark (dbscan_peak_dist): measured distance tests per second
     of the exact predicate on the current CUDA device. variant 0 = shipped
-    uint32 path, 1 = shipped 64-bit path, 2 = fp64."""
+    uint32 path, 1 = shipped 64-bit path, 2 = fp64, 3 = the brick MarkCore's
+    predicate on packed 8-byte rows (d = 3)."""
     lib = load()
     tps, ms = C.c_double(), C.c_double()
     tests, hits = C.c_int64(), C.c_int64()
@@ -152,7 +153,7 @@ def peak_dist(d: int, variant: int = 0, qt: int = 1, reps: int = 200, stream=Non
     rc = lib.dbscan_peak_dist(int(d), int(variant), int(qt), int(reps), st, C.byref(tps), C.byref(ms),
                               C.byref(tests), C.byref(hits))
     _check(lib, rc)
-    return {"d": d, "variant": ("u32", "i64", "f64")[variant], "qt": qt, "tests_per_s": tps.value,
+    return {"d": d, "variant": ("u32", "i64", "f64", "brick")[variant], "qt": qt, "tests_per_s": tps.value,
             "ms": ms.value, "tests": tests.value, "hits": hits.value}
 
 

@@ -145,6 +145,14 @@ __device__ __forceinline__ bool within(const int32_t* a, const int32_t* b, uint3
   }
 }
 
+// The brick MarkCore's predicate (sparse.cu): ||p - q||^2 <= eps^2 on 3D
+// coordinates relative to the halo's origin, q packed {x | y << 16, z} (exact:
+// each squared difference < 2^32 / 3). Also run by U1 (peak.cu, variant 3).
+__device__ __forceinline__ bool brick_within(const uint32_t* p, uint2 q, uint32_t eps2) {
+  const uint32_t dx = __sad(p[0], q.x & 0xffffu, 0u), dy = __sad(p[1], q.x >> 16, 0u), dz = __sad(p[2], q.y, 0u);
+  return dx * dx + dy * dy + dz * dz <= eps2;
+}
+
 // Connectivity test of two core points in ClusterCore (Alg 3, the BCP).
 // Exact DBSCAN: ||a-b|| <= eps. rho-approximate DBSCAN (row f4, Gan and Tao,
 // PAPER.md P:L225-235): the points are snapped to sub-cells of integer side

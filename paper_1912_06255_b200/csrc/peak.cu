@@ -13,8 +13,10 @@
 // QT = 2, 4. Variants: 0 = uint32 `__sad` path (shipped for every BASELINE
 // config), 1 = the 64-bit clamped path (shipped for wide inputs), 2 = fp64
 // (north_star's "int64/fp64 pipe peak"; exact here because coordinates are
-// < 2^12). Coordinates come from a counter-based hash on the device (no
-// upload); about half the pairs pass, so the compare is data-dependent.
+// < 2^12), 3 = the brick MarkCore's predicate (d = 3: candidates packed
+// {x | y << 16, z} in an 8-byte shared-memory row, `brick_within`).
+// Coordinates come from a counter-based hash on the device (no upload);
+// about half the pairs pass, so the compare is data-dependent.
 #include "internal.h"
 
 namespace db {
@@ -58,6 +60,41 @@ __device__ __forceinline__ void pk_load(const int32_t* tile, int m, int32_t* x) 
   }
 }
 
+// variant 3: the brick kernel's packed rows and predicate (d = 3)
+template <int QT>
+__global__ void __launch_bounds__(PK_THREADS) peak_brick_kernel(int64_t reps, uint32_t eps2,
+                                                                unsigned long long* hits) {
+  __shared__ uint2 tile[PK_M];
+  for (int m = threadIdx.x; m < PK_M; m += blockDim.x) {
+    const uint32_t x = pk_hash(blockIdx.x * 7919u + m * 131u) & 4095u,
+                   y = pk_hash(blockIdx.x * 7919u + m * 131u + 1) & 4095u,
+                   z = pk_hash(blockIdx.x * 7919u + m * 131u + 2) & 4095u;
+    tile[m] = make_uint2(x | (y << 16), z);
+  }
+  uint32_t q[QT][3];
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < QT; ++j)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q[j][k] = pk_hash(0x9e3779b9u ^ (tid * QT + j) * 17u + k) & 4095u;
+  __syncthreads();
+  uint32_t cnt[QT];
+#pragma unroll
+  for (int j = 0; j < QT; ++j) cnt[j] = 0;
+  for (int64_t r = 0; r < reps; ++r) {
+#pragma unroll 4
+    for (int m = 0; m < PK_M; ++m) {
+      const uint2 c = tile[m];
+#pragma unroll
+      for (int j = 0; j < QT; ++j) cnt[j] += brick_within(q[j], c, eps2) ? 1u : 0u;
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < QT; ++j) s += cnt[j];
+  block_add_u64(s, hits);
+}
+
 template <int DIM, int V, int QT>
 __global__ void __launch_bounds__(PK_THREADS) peak_dist_kernel(int64_t reps, uint32_t clampc, uint64_t eps2,
                                                                unsigned long long* hits) {
@@ -98,8 +135,8 @@ using namespace db;
 
 extern "C" int dbscan_peak_dist(int32_t d, int32_t variant, int32_t qt, int64_t reps, void* stream,
                                 double* tests_per_s, double* ms_out, int64_t* tests_out, int64_t* hits_out) {
-  if (d < 1 || d > 8 || variant < 0 || variant > 2 || !(qt == 1 || qt == 2 || qt == 4) || reps < 1 ||
-      !tests_per_s)
+  if (d < 1 || d > 8 || variant < 0 || variant > 3 || (variant == 3 && d != 3) || !(qt == 1 || qt == 2 || qt == 4) ||
+      reps < 1 || !tests_per_s)
     return DBSCAN_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0, sms = 148;
@@ -136,8 +173,20 @@ extern "C" int dbscan_peak_dist(int32_t d, int32_t variant, int32_t qt, int64_t 
     else if (qt == 2) go(dimc, vc, std::integral_constant<int, 2>());
     else go(dimc, vc, std::integral_constant<int, 4>());
   };
+  auto brick = [&](auto qc) {
+    constexpr int QT = decltype(qc)::value;
+    peak_brick_kernel<QT><<<blocks, PK_THREADS, 0, st>>>(1, (uint32_t)(eps * eps), dh);  // warm-up
+    cudaMemsetAsync(dh, 0, sizeof(unsigned long long), st);
+    cudaEventRecord(e0, st);
+    peak_brick_kernel<QT><<<blocks, PK_THREADS, 0, st>>>(reps, (uint32_t)(eps * eps), dh);
+    cudaEventRecord(e1, st);
+  };
   auto by_v = [&](auto dimc) {
-    if (variant == 0) by_q(dimc, std::integral_constant<int, 0>());
+    if (variant == 3) {
+      if (qt == 1) brick(std::integral_constant<int, 1>());
+      else if (qt == 2) brick(std::integral_constant<int, 2>());
+      else brick(std::integral_constant<int, 4>());
+    } else if (variant == 0) by_q(dimc, std::integral_constant<int, 0>());
     else if (variant == 1) by_q(dimc, std::integral_constant<int, 1>());
     else by_q(dimc, std::integral_constant<int, 2>());
   };

@@ -346,12 +346,6 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-// ||p - q||^2 <= eps^2 on halo-relative 16-bit coordinates (exact: each
-// squared difference < 2^32 / 3)
-__device__ __forceinline__ bool brick_within(const uint32_t* p, uint2 q, uint32_t eps2) {
-  const uint32_t dx = __sad(p[0], q.x & 0xffffu, 0u), dy = __sad(p[1], q.x >> 16, 0u), dz = __sad(p[2], q.y, 0u);
-  return dx * dx + dy * dy + dz * dz <= eps2;
-}
 
 template <bool WIDE>
 __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a, const BrickCols cols,

@@ -68,7 +68,7 @@ def test_einval_before_cuda(lib, args):
     assert not res.border_ids and not res.priv
 
 
-@pytest.mark.parametrize("args", [(0, 0, 1, 1), (9, 0, 1, 1), (3, 3, 1, 1), (3, 0, 3, 1), (3, 0, 1, 0)])
+@pytest.mark.parametrize("args", [(0, 0, 1, 1), (9, 0, 1, 1), (3, 4, 1, 1), (2, 3, 1, 1), (3, 0, 3, 1), (3, 0, 1, 0)])
 def test_peak_dist_einval(lib, args):
     """U1 rejects bad arguments before touching CUDA."""
     v = C.c_double()
