@@ -316,6 +316,8 @@ struct BrickSmem {
   int32_t gdelta[BRK_COLS];              // sorted position - index in pts, per column
   uint32_t obase[BRK_COLS];              // prefix of the own points per column
   BrickTab tab;                          // sub-cell stencils
+  uint32_t cbits[BRK_COLS];              // per column: occupancy of its BRK_H cells
+  uint32_t crank[BRK_COLS];              // per column: id of its first occupied cell
   unsigned long long scan[33];
   uint32_t total, own;
   uint64_t bar;
@@ -399,6 +401,8 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
       if ((bits >> z) & 1u) run = __ldg(a.cell_start + r + __popc(bits & ((2u << z) - 1u))) - g0;
     }
     S.abs[cc][BRK_H] = (uint16_t)min(run, 65535u);
+    S.cbits[cc] = bits;
+    S.crank[cc] = r;
     len[q] = run;
     g0s[q] = g0;
     own[q] = (hx >= BRK_R && hx < BRK_R + BRK && hy >= BRK_R && hy < BRK_R + BRK) ? o1 - o0 : 0u;
@@ -477,7 +481,14 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
     for (int step = 8; step; step >>= 1)
       if (col[hz + step] <= i) hz += step;
     const uint32_t j = (uint32_t)((int32_t)i + S.gdelta[cc]);  // sorted position
-    if ((int64_t)(col[hz + 1] - col[hz]) >= a.min_pts) { a.core_s[j] = 1; continue; }  // dense cell
+    // (a core point adds one to its cell's core count, core_cnt zeroed before
+    // the kernel: a7's sp_cells then reads the counts instead of the flags)
+    const uint32_t cell = S.crank[cc] + __popc(S.cbits[cc] & ((1u << hz) - 1u));
+    if ((int64_t)(col[hz + 1] - col[hz]) >= a.min_pts) {  // dense cell
+      a.core_s[j] = 1;
+      atomicAdd(a.core_cnt + cell, 1u);
+      continue;
+    }
     const uint2 pv = S.pts[i];
     const uint32_t p[3] = {pv.x & 0xffffu, pv.x >> 16, pv.y};
     // its sub-cell: offsets inside the cell (halo coordinates hx, hy, hz)
@@ -539,13 +550,17 @@ __global__ void __launch_bounds__(BRK_THREADS, 2) sp_core_brick_kernel(SpArgs a,
       if (count >= need) break;
     }
     a.core_s[j] = count >= need;
+    if (count >= need) atomicAdd(a.core_cnt + cell, 1u);
   }
 }
 
 // Thread per cell: core count (a7); mixed cells are listed for the partition.
 constexpr int SC_CELLS = 8;  // consecutive cells per thread in sp_cells (fewer blocks, fewer atomics)
 
-__global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
+// counted (after the brick kernel): core_cnt already holds the counts unless a
+// brick overflowed (its points went to the thread kernel)
+__global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a, const uint32_t* counted) {
+  const bool have = counted && *counted == 0;
   const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) * SC_CELLS;
   uint32_t ncc = 0, nmx = 0, kpts = 0;
   uint8_t flags[SC_CELLS];  // bit 0 core cell, bit 1 mixed
@@ -557,9 +572,10 @@ __global__ void __launch_bounds__(256) sp_cells_kernel(SpArgs a) {
       const uint32_t s = a.cell_start[g], e = a.cell_start[g + 1], m = e - s;
       uint32_t k = 0;
       if ((int64_t)m >= a.min_pts) k = m;
+      else if (have) k = a.core_cnt[g];
       else
         for (uint32_t u = s; u < e; ++u) k += a.core_s[u];
-      a.core_cnt[g] = k;
+      if (!have) a.core_cnt[g] = k;
       flags[q] = (k > 0 ? 1 : 0) | (k > 0 && k < m ? 2 : 0);
       ncc += k > 0;
       nmx += k > 0 && k < m;
@@ -1315,6 +1331,7 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
     const uint64_t nbricks = (uint64_t)nb[0] * nb[1] * nb[2];
     if (nbricks >= (1ull << 31)) throw Error(-4, "sparse path: brick grid too large");
     DB_CUDA(cudaMemsetAsync(core_s, 0xff, (size_t)n, c.st));
+    c.zero(core_cnt, sizeof(uint32_t) * cv.ncells);  // (the brick kernel counts core points per cell)
     const size_t smem = sizeof(BrickSmem);
     by_dim_sp(g.d, wide, [&](auto Dm, auto Dp, auto Wd) {
       constexpr int DIM = decltype(Dm)::value, D = decltype(Dp)::value;
@@ -1340,7 +1357,8 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   c.stage(DBSCAN_STAGE_COMPACT);
   a.mixed_list = c.alloc<uint32_t>(cv.ncells);
   a.core_tmp = c.alloc<uint32_t>(cv.ncells);
-  sp_cells_kernel<<<grid_for(((int64_t)cv.ncells + SC_CELLS - 1) / SC_CELLS, 256, 1 << 30), 256, 0, c.st>>>(a);
+  sp_cells_kernel<<<grid_for(((int64_t)cv.ncells + SC_CELLS - 1) / SC_CELLS, 256, 1 << 30), 256, 0, c.st>>>(
+      a, o->brick ? a.counters + 1 : nullptr);
   c.launched();
   partition_mixed(c, g, cv, a.mixed_list, a.counters + 3, core_cnt, Ps, idx, core_s, n);
   // directory of the cells holding core points, and their list in linear order
