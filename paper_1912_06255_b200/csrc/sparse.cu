@@ -979,6 +979,7 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
       if (t >= total || a.core_s[u]) continue;
       int32_t p[D];
       load_pt<D>(a.Ps, u, p);
+      const uint32_t iu = __ldg(a.idx + u);  // (issued with the point: no wait after the CAS)
       bool hit = false;
       for (uint32_t v = sh; v < sh + kh && !hit; ++v) {
         int32_t q[D];
@@ -1002,7 +1003,7 @@ __global__ void __launch_bounds__(256) sp_border_emit_kernel(SpArgs a) {
             flag_or(a.tmp_n, u, 1u);
             ++nb;
           }
-          atomicAdd(a.bcnt + a.idx[u], 1u);
+          atomicAdd(a.bcnt + iu, 1u);
         }
         if (old == MISS || old == lab) { placed = true; break; }
       }
