@@ -42,15 +42,43 @@ struct __align__(16) GSlot {
 
 __device__ __forceinline__ uint64_t gslot(uint64_t key, uint64_t mask) { return mix64(key) & mask; }
 
+// floor(off / s) for the cell coordinate (s = the cell side): a 32-bit
+// multiply-high and a shift when every offset is below 2^31 (m32 = ceil(2^(32+r)
+// / s), r = ceil(log2 s) - 1: the product's error off (m32 s - 2^(32+r)) stays
+// below 2^(32+r), so the quotient is exact), else a 64-bit multiply-high by
+// ceil(2^64 / s); s = 1: the offset itself.
+struct CDiv {
+  uint64_t m64;
+  uint32_t m32, r32;
+};
+__device__ __forceinline__ uint32_t cdiv(uint32_t off, const CDiv& v) {
+  if (v.m32) return __umulhi(off, v.m32) >> v.r32;
+  return v.m64 ? (uint32_t)__umul64hi((uint64_t)off, v.m64) : off;
+}
+static CDiv make_cdiv(const Geo& g) {
+  CDiv v{0, 0, 0};
+  if (g.s <= 1) return v;
+  uint64_t span = 0;  // largest offset x - lo: below (maxc + 1) s
+  for (int k = 0; k < g.d; ++k) span = std::max<uint64_t>(span, ((uint64_t)g.maxc[k] + 1) * g.s);
+  if (span <= (1ull << 31)) {
+    const int r = 63 - __builtin_clzll((unsigned long long)g.s - 1);  // ceil(log2 s) - 1
+    v.m32 = (uint32_t)((((unsigned __int128)1 << (32 + r)) + g.s - 1) / g.s);
+    v.r32 = (uint32_t)r;
+  } else {
+    v.m64 = (uint64_t)((((unsigned __int128)1 << 64) + g.s - 1) / g.s);
+  }
+  return v;
+}
+
 template <int DD>
 __device__ __forceinline__ uint64_t point_key(const int32_t* __restrict__ pts, uint32_t i, const Geo& g,
-                                              uint64_t magic, int32_t* x) {
+                                              const CDiv& dv, int32_t* x) {
   uint64_t key = 0;
 #pragma unroll
   for (int k = 0; k < DD; ++k) {
     x[k] = __ldg(pts + (uint64_t)i * DD + k);
     const uint32_t off = (uint32_t)x[k] - (uint32_t)g.lo[k];
-    const uint32_t ck = magic ? (uint32_t)__umul64hi((uint64_t)off, magic) : off;
+    const uint32_t ck = cdiv(off, dv);
     key |= (uint64_t)ck << g.shift[k];
   }
   return key;
@@ -83,7 +111,7 @@ constexpr uint32_t GR_CHUNK = 256;  // points per warp chunk (several chunks per
 
 template <int DD>
 __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                                 Geo g, uint64_t magic, GSlot* T,
+                                                                 Geo g, CDiv dv, GSlot* T,
                                                                  uint64_t mask, uint32_t* overflow) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -103,7 +131,7 @@ __global__ void __launch_bounds__(GR_THREADS) group_count_kernel(const int32_t* 
       const uint32_t i = i0 + lane;
       const bool valid = i < c1;
       int32_t x[DD];
-      const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
+      const uint64_t key = valid ? point_key<DD>(pts, i, g, dv, x) : ~0ull;
       const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
       const uint32_t vmask = __ballot_sync(DB_FULL, valid);
       if (__all_sync(DB_FULL, !valid || key == k0)) {
@@ -187,7 +215,7 @@ __global__ void group_cells_kernel(GSlot* T, const uint32_t* __restrict__ rank_s
 // without a table probe and its run minimum is already recorded.
 template <int DD, int D>
 __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
-    const int32_t* __restrict__ pts, uint32_t n, Geo g, uint64_t magic, const GSlot* __restrict__ T,
+    const int32_t* __restrict__ pts, uint32_t n, Geo g, CDiv dv, const GSlot* __restrict__ T,
     uint64_t mask, uint32_t* __restrict__ cursor, uint32_t* __restrict__ cellmin, int32_t* __restrict__ Ps,
     uint32_t* __restrict__ idx, uint32_t* __restrict__ cell_of, uint32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
@@ -201,7 +229,7 @@ __global__ void __launch_bounds__(GR_THREADS) group_scatter_kernel(
       const uint32_t i = i0 + lane;
       const bool valid = i < c1;
       int32_t x[DD];
-      const uint64_t key = valid ? point_key<DD>(pts, i, g, magic, x) : ~0ull;
+      const uint64_t key = valid ? point_key<DD>(pts, i, g, dv, x) : ~0ull;
       const uint64_t k0 = __shfl_sync(DB_FULL, key, 0);
       const bool uniform = __all_sync(DB_FULL, !valid || key == k0);
       uint32_t id = 0xffffffffu;
@@ -273,7 +301,7 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
                    uint32_t** cellmin_out, uint32_t* ncells_out, bool* ordered) {
   uint64_t cap = 1024;
   while (cap < 2ull * (uint64_t)n && cap < (1ull << 20)) cap <<= 1;
-  const uint64_t magic = g.s > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + g.s - 1) / g.s) : 0;
+  const CDiv dv = make_cdiv(g);
   GSlot* T = c.alloc<GSlot>(cap);
   uint32_t* ctr = c.alloc<uint32_t>(2);  // [0] overflow, [1] distinct keys
   group_init_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, c.st>>>(T, cap);
@@ -282,7 +310,7 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
   const unsigned grid = grid_for(n, GR_THREADS, c.sms * 8);
   by_dim_g(g.d, [&](auto Dd, auto) {
     constexpr int DD = decltype(Dd)::value;
-    group_count_kernel<DD><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, ctr);
+    group_count_kernel<DD><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, dv, T, cap - 1, ctr);
   });
   c.launched();
   uint32_t* list = c.alloc<uint32_t>(cap);
@@ -328,7 +356,7 @@ bool group_by_hash(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, int spar
   DB_CUDA(cudaMemcpyAsync(cursor, cell_start, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, c.st));
   by_dim_g(g.d, [&](auto Dd, auto Dp) {
     constexpr int DD = decltype(Dd)::value, D = decltype(Dp)::value;
-    group_scatter_kernel<DD, D><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, magic, T, cap - 1, cursor,
+    group_scatter_kernel<DD, D><<<grid, GR_THREADS, 0, c.st>>>(pts, (uint32_t)n, g, dv, T, cap - 1, cursor,
                                                                cellmin, Ps, idx, cell_of, c.inv);
   });
   c.launched();
@@ -355,13 +383,13 @@ constexpr int LAT_THREADS = 256;
 
 template <int DD>
 __device__ __forceinline__ uint64_t point_lin(const int32_t* __restrict__ pts, uint32_t i, const Geo& g,
-                                              uint64_t magic, const uint64_t* stride, int32_t* x) {
+                                              const CDiv& dv, const uint64_t* stride, int32_t* x) {
   uint64_t lin = 0;
 #pragma unroll
   for (int k = 0; k < DD; ++k) {
     x[k] = __ldg(pts + (uint64_t)i * DD + k);
     const uint32_t off = (uint32_t)x[k] - (uint32_t)g.lo[k];
-    const uint32_t ck = magic ? (uint32_t)__umul64hi((uint64_t)off, magic) : off;
+    const uint32_t ck = cdiv(off, dv);
     lin += (uint64_t)(ck + g.R) * stride[k];
   }
   return lin;
@@ -369,7 +397,7 @@ __device__ __forceinline__ uint64_t point_lin(const int32_t* __restrict__ pts, u
 
 struct LatArgs {
   Geo g;
-  uint64_t magic;
+  CDiv dv;             // floor(offset / s)
   uint64_t stride[3];
   uint64_t dims[3];    // padded lattice extent per axis
   uint64_t words;      // 32-cell words
@@ -385,7 +413,7 @@ __global__ void __launch_bounds__(LAT_THREADS) lat_count_kernel(const int32_t* _
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t x[DD];
-  const uint64_t lin = point_lin<DD>(pts, i, L.g, L.magic, L.stride, x);
+  const uint64_t lin = point_lin<DD>(pts, i, L.g, L.dv, L.stride, x);
   const uint32_t sh = ((uint32_t)lin & 3u) * 8u;
   const uint32_t old = (atomicAdd(cnt8 + (lin >> 2), 1u << sh) >> sh) & 255u;
   if (old == 255u) *overflow = 1u;  // the add carried into the next counter
@@ -590,7 +618,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2) lat_stage_kernel(const int32_t*
       for (int k = 0; k < DD; ++k) {
         xx[k] = src[k];
         const uint32_t off = (uint32_t)xx[k] - (uint32_t)L.g.lo[k];
-        const uint32_t ck = L.magic ? (uint32_t)__umul64hi((uint64_t)off, L.magic) : off;
+        const uint32_t ck = cdiv(off, L.dv);
         lin += (uint64_t)(ck + L.g.R) * L.stride[k];
       }
 #pragma unroll
@@ -690,7 +718,7 @@ int lattice_group(Ctx& c, const int32_t* pts, int64_t n, const Geo& g, uint64_t 
                   uint64_t* cell_key, const uint4** dir_out, uint32_t* ncells_out) {
   LatArgs L{};
   L.g = g;
-  L.magic = g.s > 1 ? (uint64_t)((((unsigned __int128)1 << 64) + g.s - 1) / g.s) : 0;
+  L.dv = make_cdiv(g);
   unsigned __int128 vol = 1;
   for (int k = g.d - 1; k >= 0; --k) {
     L.stride[k] = (uint64_t)vol;
