@@ -432,6 +432,12 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     const uint32_t z0 = B2 > 1 ? (cq[2] > g.R ? cq[2] - g.R : 0u) : 0u;
     const uint32_t z1 = B2 > 1 ? min(B2 - 1, cq[2] + g.R) : 0u;
     const uint32_t tq = fill == 2 ? bpos[q] : 0u;
+    // fill == 2: a lane's mirror entry (q into the found cell h's row) is
+    // written one step after its counter atomic is issued, so the atomic's
+    // round trip overlaps the next step's tests
+    uint64_t pend_at = 0;      // off[h] of the pending entry
+    uint32_t pend_slot = 0, pend_val = 0;
+    bool pend = false;
     for (uint32_t b0 = blo; b0 <= bhi; ++b0) {
     for (uint32_t b1 = y0; b1 <= (B2 > 1 ? y1 : y0); ++b1) {
     const uint32_t r0 = B2 > 1 ? (b0 * B1 + b1) * B2 + z0 : b0 * B1 + y0;
@@ -480,7 +486,11 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
           if (cls >= 0) {
             const uint32_t h = order[t];
             nbr[pos[0] + base + __popc(b & lt)] = h | ((uint32_t)cls << 30);
-            nbr[off[h] + atomicAdd(cnt + h, 1u)] = q | ((uint32_t)cls << 30);
+            if (pend) nbr[pend_at + pend_slot] = pend_val;
+            pend_slot = atomicAdd(cnt + h, 1u);
+            pend_at = off[h];
+            pend_val = q | ((uint32_t)cls << 30);
+            pend = true;
           }
         }
         continue;
@@ -502,6 +512,7 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     }
     }
     }
+    if (pend) nbr[pend_at + pend_slot] = pend_val;
     if (fill == 0) {
       uint64_t sum64 = sum;
 #pragma unroll
