@@ -387,11 +387,14 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
                                                         uint32_t* __restrict__ ccount /*[3][ncells]*/,
                                                         uint32_t* __restrict__ cnt, uint32_t* __restrict__ ub,
                                                         const uint64_t* __restrict__ off,
-                                                        uint32_t* __restrict__ nbr) {
+                                                        uint32_t* __restrict__ nbr, uint32_t* __restrict__ ownc) {
   // fill: 0 = count (cnt, ccount, ub), 1 = write class-sorted rows at off,
   // 2 = one symmetric pass: only candidates after q in bucket order are
-  // tested, and a pair found adds (other cell | class << 30) to BOTH rows,
-  // rows of candidate capacity at off filled through the counters cnt[]
+  // tested, and a pair found adds (other cell | class << 30) to BOTH rows of
+  // candidate capacity at off: q's own entries forward from the row start
+  // (the warp's running count, ownc[q]), the mirror entries backward from
+  // the row end through the counter cnt[] of the found cell (mirror entries
+  // only; nbr_add_kernel then adds the own ones)
   // (nbr_compact_kernel then class-sorts the rows into the final CSR and
   // counts the classes and ub)
   __shared__ unsigned long long gt[GT_MAX + 1];
@@ -435,8 +438,8 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     // fill == 2: a lane's mirror entry (q into the found cell h's row) is
     // written one step after its counter atomic is issued, so the atomic's
     // round trip overlaps the next step's tests
-    uint64_t pend_at = 0;      // off[h] of the pending entry
-    uint32_t pend_slot = 0, pend_val = 0;
+    uint64_t pend_at = 0;      // last slot of the found cell's row (off[h + 1] - 1)
+    uint32_t pend_slot = 0, pend_val = 0, own = 0;
     bool pend = false;
     for (uint32_t b0 = blo; b0 <= bhi; ++b0) {
     for (uint32_t b1 = y0; b1 <= (B2 > 1 ? y1 : y0); ++b1) {
@@ -480,18 +483,16 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
       if (fill == 2) {
         const uint32_t b = __ballot_sync(DB_FULL, cls >= 0);
         if (b) {
-          uint32_t base = 0;
-          if (lane == 0) base = atomicAdd(cnt + q, (uint32_t)__popc(b));
-          base = __shfl_sync(DB_FULL, base, 0);
           if (cls >= 0) {
             const uint32_t h = order[t];
-            nbr[pos[0] + base + __popc(b & lt)] = h | ((uint32_t)cls << 30);
-            if (pend) nbr[pend_at + pend_slot] = pend_val;
+            nbr[pos[0] + own + __popc(b & lt)] = h | ((uint32_t)cls << 30);
+            if (pend) nbr[pend_at - pend_slot] = pend_val;
             pend_slot = atomicAdd(cnt + h, 1u);
-            pend_at = off[h];
+            pend_at = off[h + 1] - 1;
             pend_val = q | ((uint32_t)cls << 30);
             pend = true;
           }
+          own += __popc(b);
         }
         continue;
       }
@@ -512,7 +513,8 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
     }
     }
     }
-    if (pend) nbr[pend_at + pend_slot] = pend_val;
+    if (pend) nbr[pend_at - pend_slot] = pend_val;
+    if (fill == 2 && lane == 0) ownc[q] = own;  // (cnt[] holds the mirror entries only, their slots)
     if (fill == 0) {
       uint64_t sum64 = sum;
 #pragma unroll
@@ -531,6 +533,11 @@ __global__ void __launch_bounds__(256) nbr_brute_kernel(int fill, const uint32_t
       }
     }
   }
+}
+
+__global__ void nbr_add_kernel(uint32_t* __restrict__ cnt, const uint32_t* __restrict__ ownc, uint32_t ncells) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ncells) cnt[i] += ownc[i];
 }
 
 __global__ void cell_size_kernel(const uint32_t* __restrict__ cell_start, uint32_t ncells,
@@ -564,6 +571,7 @@ __global__ void nbr_cap_kernel(const uint32_t* __restrict__ cc, const uint32_t* 
 __global__ void __launch_bounds__(256) nbr_compact_kernel(const uint32_t* __restrict__ tagged,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ cnt,
+                                                          const uint32_t* __restrict__ ownc,
                                                           const uint32_t* __restrict__ cell_start,
                                                           uint32_t* __restrict__ ccount, uint32_t* __restrict__ ub,
                                                           const uint64_t* __restrict__ off, uint32_t ncells,
@@ -572,13 +580,15 @@ __global__ void __launch_bounds__(256) nbr_compact_kernel(const uint32_t* __rest
   const uint32_t lt = lanemask_lt();
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ncells; q += nwarps) {
+    // the row: own entries [0, own), mirror entries at its end
     const uint32_t* src = tagged + toff[q];
-    const uint32_t len = cnt[q];
+    const uint32_t len = cnt[q], own = ownc[q], skip = (uint32_t)(toff[q + 1] - toff[q]) - len;
+    auto at = [&](uint32_t t) { return src[t < own ? t : t + skip]; };
     // class counts and ub (the sum of the neighbours' sizes)
     uint32_t n0 = 0, n1 = 0;
     uint64_t sum = 0;
     for (uint32_t t = lane; t < len; t += 32) {
-      const uint32_t v = src[t], h = v & 0x3fffffffu, cls = v >> 30;
+      const uint32_t v = at(t), h = v & 0x3fffffffu, cls = v >> 30;
       n0 += cls == 0;
       n1 += cls == 1;
       sum += cell_start[h + 1] - cell_start[h];
@@ -600,7 +610,7 @@ __global__ void __launch_bounds__(256) nbr_compact_kernel(const uint32_t* __rest
     pos[2] = pos[1] + n1;
     for (uint32_t t0 = 0; t0 < len; t0 += 32) {
       const uint32_t t = t0 + lane;
-      const uint32_t v = t < len ? src[t] : 0xffffffffu;
+      const uint32_t v = t < len ? at(t) : 0xffffffffu;
       const uint32_t cls = v >> 30;
 #pragma unroll
       for (uint32_t k = 0; k < 3; ++k) {
@@ -678,10 +688,11 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
   uint64_t* off = c.alloc<uint64_t>((size_t)ncells + 1);
   const unsigned grid = grid_for((int64_t)ncells * 32, 256, c.sms * 16);
   const bool pack = (uint64_t)g.d * (g.eps2 + 1) < (1ull << 27) && (uint64_t)g.d * gmax < 32;
+  uint32_t* ownc = nullptr;  // (one pass: own entries per row)
   auto launch = [&](int fill, uint32_t* list, const uint64_t* lo) {
     auto go = [&](auto kern) {
       kern<<<grid, 256, 0, c.st>>>(fill, cc, ccs, order, bsize, bpos, bstart, maxb, B1, B2, ncells, g,
-                                   (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list);
+                                   (const uint64_t*)dgt, gmax, cell_start, ccount, cnt, ub, lo, list, ownc);
     };
     if (g.d <= 4) {
       if (pack) go(nbr_brute_kernel<4, true>);
@@ -706,12 +717,16 @@ static bool neighbors_brute(Ctx& c, const Geo& g, const uint64_t* cell_key, cons
     const uint64_t tcap = c.read(toff + ncells);
     if (tcap <= NBR_ONEPASS_MAX) {
       uint32_t* tagged = c.alloc<uint32_t>(tcap + 1);
+      ownc = c.alloc<uint32_t>(ncells);
       c.zero(cnt, sizeof(uint32_t) * ncells);  // the rows' fill counters
       launch(2, tagged, toff);
+      nbr_add_kernel<<<grid_for(ncells, 256, 1 << 30), 256, 0, c.st>>>(cnt, ownc, ncells);
+      c.launched();
       exclusive_scan_u32_u64(c, cnt, off, ncells);
       *total = nbr_total_bound(c, off + ncells, tcap);
       uint32_t* list = c.alloc<uint32_t>(*total + 1);
-      nbr_compact_kernel<<<grid, 256, 0, c.st>>>(tagged, toff, cnt, cell_start, ccount, ub, off, ncells, list);
+      nbr_compact_kernel<<<grid, 256, 0, c.st>>>(tagged, toff, cnt, ownc, cell_start, ccount, ub, off, ncells,
+                                                 list);
       c.launched();
       *nbr = list;
       onepass = true;
