@@ -127,7 +127,8 @@ struct SpArgs {
   uint32_t* ovf_count;
   unsigned long long* nborder;
   const uint32_t* cpre;      // [ncore + 1] core points before each core cell (core_list order)
-  const uint64_t* clin;      // [ncore] padded linear lattice index of each core cell
+  const uint64_t* clin;      // [ncore] padded linear lattice index of each core cell (by rank)
+  const uint32_t* ccnt;      // [ncore] core points of each core cell (by rank)
   const int4* cpts;          // core points in core_list order: {x, y, z (0 in 2D), cell id}
   uint64_t ncpts;            // core points
   int64_t n;
@@ -202,14 +203,20 @@ __global__ void dir_pack_kernel(const uint32_t* __restrict__ bm, const uint32_t*
 
 // core_list[rank in cdir] = cell id, for every cell holding core points
 // (from the unordered list core_tmp[0 .. counters[4]))
-__global__ void core_list_kernel(SpArgs a, uint32_t* __restrict__ core_list) {
+// (also, by rank, each core cell's core count and padded lattice index: the
+// packed core points of the one-pass ClusterCore are built from them)
+__global__ void core_list_kernel(SpArgs a, uint32_t* __restrict__ core_list, uint32_t* __restrict__ ccnt,
+                                 uint64_t* __restrict__ clin) {
   const uint32_t m = a.counters[4];
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
     const uint32_t g = a.core_tmp[t];
     uint64_t lin = 0;
     const uint64_t key = a.cell_key[g];
     for (int k = 0; k < a.g.d; ++k) lin += (uint64_t)(cell_coord(key, a.g, k) + a.g.R) * a.stride[k];
-    core_list[dir_rank(a.cdir, lin)] = g;
+    const uint32_t r = dir_rank(a.cdir, lin);
+    core_list[r] = g;
+    ccnt[r] = a.core_cnt[g];
+    clin[r] = lin;
   }
 }
 
@@ -707,15 +714,6 @@ __global__ void __launch_bounds__(256) sp_pairs_kernel(SpArgs a, unsigned long l
 // order): the core points of the core cells found by one probe of the core
 // directory (ranks id0 .. id0 + nc) are one contiguous range of cpts, so a
 // pair search reads no per-cell tables for the cells it finds.
-template <int DIM>
-__global__ void sp_core_count_kernel(SpArgs a, uint32_t* __restrict__ ccnt, uint64_t* __restrict__ clin) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < a.ncore; r += gridDim.x * blockDim.x) {
-    const uint32_t g = a.core_list[r];
-    ccnt[r] = a.core_cnt[g];
-    clin[r] = cell_lin<DIM>(a.cell_key[g], a);
-  }
-}
-
 template <int D>
 __global__ void sp_core_pack_kernel(SpArgs a, int4* __restrict__ cpts) {
   // a warp per 32 core cells, lanes over their core points
@@ -1366,7 +1364,11 @@ uint32_t sparse_pipeline(Ctx& c, const Geo& g, const CellsView& cv, int32_t* Ps,
   a.cdir = build_dir(c, a, words, a.core_tmp, a.counters + 4);
   uint32_t* core_list = c.alloc<uint32_t>(cv.ncells);
   a.core_list = core_list;
-  core_list_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a, core_list);
+  uint32_t* ccnt = c.alloc<uint32_t>(cv.ncells);
+  uint64_t* clin = c.alloc<uint64_t>(cv.ncells);
+  core_list_kernel<<<grid_for(cv.ncells, 256, c.sms * 8), 256, 0, c.st>>>(a, core_list, ccnt, clin);
+  a.ccnt = ccnt;
+  a.clin = clin;
   c.launched();
   const uint32_t* hc = c.fetch(a.counters, 6);  // [1] brick overflow, [4] core cells, [5] core points
   c.sync();
@@ -1403,14 +1405,9 @@ void sparse_cluster(Ctx& c, const Geo& g, const CellsView& cv, const int32_t* Ps
       const bool two = 2ull * a.ncore >= cv.ncells;
       if (!two && !g.at && !(o->flags & DBSCAN_F_NO_PACKED_CORE)) {
         // one pass on the packed core points
-        uint32_t* ccnt = c.alloc<uint32_t>(a.ncore);
         uint32_t* cpre = c.alloc<uint32_t>((size_t)a.ncore + 1);
-        uint64_t* clin = c.alloc<uint64_t>(a.ncore);
         int4* cpts = c.alloc<int4>(std::max<uint64_t>(a.ncpts, 1));
-        sp_core_count_kernel<DIM><<<grid_for(a.ncore, 256, c.sms * 8), 256, 0, c.st>>>(a, ccnt, clin);
-        a.clin = clin;
-        c.launched();
-        exclusive_scan_u32_u32(c, ccnt, cpre, a.ncore);
+        exclusive_scan_u32_u32(c, a.ccnt, cpre, a.ncore);  // (counts by rank: core_list_kernel)
         a.cpre = cpre;
         a.cpts = cpts;
         sp_core_pack_kernel<D><<<grid_for(((int64_t)a.ncore + 31) / 32 * 32, 256, c.sms * 16), 256, 0, c.st>>>(a, cpts);

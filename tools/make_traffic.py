@@ -21,7 +21,7 @@ STAGES = [  # (stage, kernel-name prefixes)
                                "sort_rows")),
     ("a6 MarkCore", ("sp_core_brick", "sp_core_kernel", "mark_core", "qt_", "qb_")),
     ("a7 compaction", ("sp_cells", "partition", "core_count", "dir_set", "popc", "dir_pack", "core_list")),
-    ("a8 ClusterCore", ("sp_pairs", "sp_core_count", "sp_core_pack", "wave_csr", "bcp_large", "uf_")),
+    ("a8 ClusterCore", ("sp_pairs", "sp_core_pack", "wave_csr", "bcp_large", "uf_")),
     ("a9 labels", ("label_roots", "cell_label", "write_points", "write_positions", "core_from_cluster")),
     ("a10 ClusterBorder", ("sp_border", "border_")),
 ]
